@@ -1,0 +1,185 @@
+"""ctypes mirror of include/treeserve_b200.h and the status → exception map.
+
+The shared library is built in-tree by ``__graft_entry__.build()`` into
+``paper_2604_00510_b200/lib/libtreeserve_b200.so``.  There is no fallback:
+if the library is missing, :func:`load_library` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+TS_MAX_DEPTH = 32
+TS_MAX_WIDTH = 32
+TS_ABI_VERSION = 1
+
+TS_OK = 0
+TS_INVALID_ARGUMENT = 1
+TS_TREE_STRUCTURE = 2
+TS_EXHAUSTED = 3
+TS_ACCOUNTING = 4
+TS_UNSUPPORTED_SCHEME = 5
+TS_POOL_OVERFLOW = 6
+TS_CUDA = 7
+
+EXIT_NONE, EXIT_POSITIVE, EXIT_NEGATIVE, EXIT_BUDGET = 0, 1, 2, 3
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libtreeserve_b200.so")
+
+
+class TsProblem(ctypes.Structure):
+    _fields_ = [
+        ("seed", ctypes.c_uint64),
+        ("branching", ctypes.c_int32),
+        ("base_depth", ctypes.c_int32),
+        ("golden_len", ctypes.c_int32),
+        ("hidden_until_depth", ctypes.c_int32),
+        ("has_shared", ctypes.c_int32),
+        ("arrival_step", ctypes.c_int32),
+        ("off_lo", ctypes.c_double),
+        ("off_hi", ctypes.c_double),
+        ("shared_lo", ctypes.c_double),
+        ("shared_hi", ctypes.c_double),
+        ("golden_path", ctypes.c_uint8 * TS_MAX_DEPTH),
+        ("golden_rewards", ctypes.c_double * TS_MAX_DEPTH),
+    ]
+
+
+class TsConfig(ctypes.Structure):
+    _fields_ = [
+        ("scheme", ctypes.c_int32),
+        ("futility_bound", ctypes.c_int32),
+        ("strict_negative_exit", ctypes.c_int32),
+        ("positive_exit", ctypes.c_int32),
+        ("negative_exit", ctypes.c_int32),
+        ("rollout_budget", ctypes.c_int32),
+        ("depth_cap", ctypes.c_int32),
+        ("expand_width", ctypes.c_int32),
+        ("max_concurrency", ctypes.c_int32),
+        ("obs_threshold", ctypes.c_int32),
+        ("boosting_enabled", ctypes.c_int32),
+        ("_pad0", ctypes.c_int32),
+        ("accept_threshold", ctypes.c_double),
+        ("positive_exit_threshold", ctypes.c_double),
+        ("first_step_threshold", ctypes.c_double),
+        ("c_puct", ctypes.c_double),
+        ("beta", ctypes.c_double),
+        ("proximity", ctypes.c_double),
+    ]
+
+
+class TsOutcome(ctypes.Structure):
+    _fields_ = [
+        ("exit_kind", ctypes.c_int32),
+        ("rollouts_completed", ctypes.c_int32),
+        ("tokens_generated", ctypes.c_int64),
+        ("best_score", ctypes.c_double),
+        ("best_len", ctypes.c_int32),
+        ("solved", ctypes.c_int32),
+        ("exit_step", ctypes.c_int32),
+        ("admit_step", ctypes.c_int32),
+        ("launched", ctypes.c_int32),
+        ("cancelled", ctypes.c_int32),
+        ("nodes", ctypes.c_int32),
+        ("status", ctypes.c_int32),
+        ("best_path", ctypes.c_uint8 * TS_MAX_DEPTH),
+    ]
+
+
+class TsRunStats(ctypes.Structure):
+    _fields_ = [
+        ("steps", ctypes.c_int32),
+        ("finished", ctypes.c_int32),
+        ("rollouts", ctypes.c_int64),
+        ("launched", ctypes.c_int64),
+        ("nodes", ctypes.c_int64),
+        ("tokens", ctypes.c_int64),
+        ("children_scored", ctypes.c_int64),
+        ("select_levels", ctypes.c_int64),
+        ("path_nodes", ctypes.c_int64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+# Every symbol include/treeserve_b200.h declares (checked by tests/test_abi.py).
+EXPORTED = (
+    "ts_engine_create", "ts_engine_destroy", "ts_last_error", "ts_abi_version",
+    "ts_load_problems", "ts_wave", "ts_sched_records", "ts_sched_targets", "ts_admit",
+    "ts_local_counts", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_run_batch_host",
+    "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
+)
+
+_lib = None
+
+
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """Load the in-tree CUDA extension; raises if it has not been built."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise ImportError(
+            f"{p} is missing: build the CUDA extension first (python -c 'import __graft_entry__ as g; g.build()')"
+        )
+    lib = ctypes.CDLL(p)
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    i32 = ctypes.c_int32
+    sig = {
+        "ts_engine_create": (ctypes.c_int, [P(TsConfig), i32, i32, P(vp)]),
+        "ts_engine_destroy": (ctypes.c_int, [vp]),
+        "ts_last_error": (ctypes.c_char_p, [vp]),
+        "ts_abi_version": (ctypes.c_int, []),
+        "ts_load_problems": (ctypes.c_int, [vp, P(TsProblem), i32, i32, i32, vp]),
+        "ts_wave": (ctypes.c_int, [vp, i32, vp]),
+        "ts_sched_records": (ctypes.c_int, [vp, i32, vp, vp]),
+        "ts_sched_targets": (ctypes.c_int, [vp, i32, vp, i32, i32, i32, vp]),
+        "ts_admit": (ctypes.c_int, [vp, i32, vp, vp]),
+        "ts_local_counts": (ctypes.c_int, [vp, vp, vp]),
+        "ts_run": (ctypes.c_int, [vp, i32, P(TsRunStats), vp]),
+        "ts_read_outcomes": (ctypes.c_int, [vp, P(TsOutcome), i32, vp]),
+        "ts_read_stats": (ctypes.c_int, [vp, P(TsRunStats), vp]),
+        "ts_run_batch_host": (ctypes.c_int, [vp, P(TsProblem), i32, i32, P(TsOutcome), P(TsRunStats), vp]),
+        "ts_tree_size": (ctypes.c_int, [vp, i32, P(i32)]),
+        "ts_dump_tree": (ctypes.c_int, [vp, i32] + [vp] * 9),
+        "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.ts_abi_version() != TS_ABI_VERSION:
+        raise ImportError("treeserve_b200 ABI version mismatch")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def raise_for_status(code: int, where: str, detail: str = "") -> None:
+    """Map a ts_status to the reference's exception classes."""
+    if code == TS_OK:
+        return
+    from .scoring import UnsupportedSchemeError
+    from .tree import AccountingError, NoExpandableLeafError, TreeStructureError
+
+    msg = f"{where}: {detail}" if detail else where
+    if code == TS_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if code == TS_TREE_STRUCTURE:
+        raise TreeStructureError(msg)
+    if code == TS_EXHAUSTED:
+        raise NoExpandableLeafError(msg)
+    if code == TS_ACCOUNTING:
+        raise AccountingError(msg)
+    if code == TS_UNSUPPORTED_SCHEME:
+        raise UnsupportedSchemeError(msg)
+    if code == TS_POOL_OVERFLOW:
+        raise MemoryError(msg)
+    raise RuntimeError(f"CUDA error in {msg}")

@@ -1,0 +1,343 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+Every value written here comes from reference calls (``/root/reference/pkg/src``)
+or from ``wave_ref.run_waves``, which is composed only of reference calls.  The
+fixtures pin the C oracle (``oracle/``) and, through it and directly, the CUDA
+engine.  Floats are stored with ``repr`` (shortest round-trip), so equality
+checks against them are bit-exact.
+"""
+
+from __future__ import annotations
+
+import gzip
+import json
+import os
+import random
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+import wave_ref  # noqa: E402  (puts the reference on sys.path)
+from treeserve import rng  # noqa: E402
+from treeserve.backend import (  # noqa: E402
+    Difficulty,
+    RewardProfile,
+    generate_steps,
+    golden_step_rewards,
+    make_problem,
+    make_workload,
+)
+from treeserve.scheduler import Job, SchedulerConfig, SchedulerState, JobState, compute_targets  # noqa: E402
+from treeserve.scoring import AggregationScheme, FutilityBound, ScoringConfig  # noqa: E402
+from treeserve.search import run_tree_search  # noqa: E402
+from treeserve.tree import SearchTree  # noqa: E402
+
+SEED = 0
+MIX = (0.6, 0.25, 0.15)
+
+# Config-4 "heavy-tailed stagnation" profile (BASELINE.json configs[3]); the
+# reference has no such profile, so it is defined here and in
+# paper_2604_00510_b200/backend.py (stagnation_profile) with identical values.
+STAGNATION = RewardProfile(
+    golden_range=(0.93, 0.99),
+    off_path_range=(0.22, 0.75),
+    hidden_until_depth=6,
+    shared_range=(0.80, 0.97),
+    target_aggregate=0.55,
+)
+
+
+def dump(name, obj):
+    path = os.path.join(HERE, name + ".json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as f:
+        json.dump(obj, f, separators=(",", ":"), sort_keys=True)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+def problem_record(p):
+    prof = p.reward_profile
+    return {
+        "problem_id": p.problem_id,
+        "seed": p.seed,
+        "difficulty": p.difficulty.value,
+        "depth_range": list(p.depth_range),
+        "branching": p.branching,
+        "base_depth": p.base_depth,
+        "golden_path": list(p.golden_path) if p.golden_path is not None else None,
+        "golden_rewards": list(golden_step_rewards(p)) if p.golden_path is not None else None,
+        "profile": {
+            "golden_range": list(prof.golden_range),
+            "off_path_range": list(prof.off_path_range),
+            "hidden_until_depth": prof.hidden_until_depth,
+            "shared_range": list(prof.shared_range) if prof.shared_range else None,
+            "target_aggregate": prof.target_aggregate,
+        },
+    }
+
+
+def tree_record(tree: SearchTree):
+    d = tree.to_dict()
+    # children order is creation order (ids ascending); keep the dump compact
+    return {
+        "completed_rollouts": d["completed_rollouts"],
+        "rollout_budget": d["rollout_budget"],
+        "parent": [n["parent"] if n["parent"] is not None else -1 for n in d["nodes"]],
+        "reward": [n["reward"] for n in d["nodes"]],
+        "prior": [n["prior"] for n in d["nodes"]],
+        "N": [n["N"] for n in d["nodes"]],
+        "O": [n["O"] for n in d["nodes"]],
+        "W": [n["W"] for n in d["nodes"]],
+        "terminal": [int(n["terminal"]) for n in d["nodes"]],
+        "depth": [n["depth"] for n in d["nodes"]],
+        "step_ref": [tree.nodes[n["id"]].step_ref if n["parent"] is not None else -1 for n in d["nodes"]],
+    }
+
+
+def outcome_record(o):
+    return {
+        "problem_id": o.problem_id,
+        "exit_kind": o.exit_kind.value,
+        "best_score": o.best_score,
+        "best_path": list(o.best_path),
+        "rollouts_completed": o.rollouts_completed,
+        "tokens_generated": o.tokens_generated,
+        "solved": o.solved,
+    }
+
+
+def scoring_record(s: ScoringConfig):
+    return {
+        "scheme": s.scheme.value,
+        "accept_threshold": s.accept_threshold,
+        "positive_exit_threshold": s.positive_exit_threshold,
+        "first_step_threshold": s.first_step_threshold,
+        "strict_negative_exit": s.strict_negative_exit,
+        "futility_bound": s.futility_bound.value,
+    }
+
+
+def serial_tree(problem, scoring, budget, cap, width, pe, ne):
+    """run_tree_search, but keeping the tree (same loop as search.py:79-119)."""
+    out, _ = wave_ref.run_waves(
+        [problem], scoring=scoring, sched=SchedulerConfig(max_concurrency=1, boosting_enabled=False),
+        rollout_budget=budget, depth_cap=cap, expand_width=width, positive_exit=pe,
+        negative_exit=ne, keep_trees=True,
+    )
+    return out[0]["tree"]
+
+
+def gen_rng():
+    r = random.Random(1234)
+    kats = []
+    for _ in range(300):
+        n = r.randint(0, 36)
+        keys = [r.choice([r.randint(0, 40), r.getrandbits(64), r.getrandbits(20)]) for _ in range(n)]
+        lo = r.randint(0, 100)
+        hi = lo + r.randint(0, 200)
+        kats.append({
+            "keys": keys,
+            "mix": rng.mix(*keys),
+            "uniform": rng.uniform(*keys),
+            "uniform_in": [0.05, 0.28, rng.uniform_in(0.05, 0.28, *keys)],
+            "randint": [lo, hi, rng.randint_in(lo, hi, *keys)],
+            "exponential": [2.5, rng.exponential(2.5, *keys)],
+        })
+    dump("rng_kats", kats)
+
+
+def gen_workloads():
+    D7 = {d: (7, 7) for d in Difficulty}
+    D15 = {d: (15, 15) for d in Difficulty}
+    wl = {
+        "c1": [problem_record(p) for p in make_workload(64, MIX, SEED, branching=4, depth_ranges=D7)],
+        "c2": [problem_record(p) for p in make_workload(4096, MIX, SEED, branching=4, depth_ranges=D15)],
+        "cli_default": [problem_record(p) for p in make_workload(500, MIX, 20260810)],
+        "mixed_b3": [problem_record(p) for p in make_workload(
+            97, (0.5, 0.3, 0.2), 77, branching=3,
+            depth_ranges={Difficulty.EASY: (3, 9), Difficulty.HARD_SOLVABLE: (4, 10), Difficulty.UNSOLVABLE: (2, 6)},
+            accept_threshold=0.35)],
+        "c4_stagnation": [problem_record(make_problem(f"s{i:04d}", rng.mix(SEED, 8, i), Difficulty.HARD_SOLVABLE,
+                                                      (31, 31), 8, STAGNATION)) for i in range(16)],
+    }
+    dump("workloads", wl)
+
+
+def gen_steps():
+    r = random.Random(99)
+    kats = []
+    specs = list(make_workload(40, MIX, 5, branching=4, depth_ranges={d: (3, 12) for d in Difficulty}))
+    specs += [make_problem(f"s{i}", rng.mix(3, 8, i), Difficulty.HARD_SOLVABLE, (31, 31), 8, STAGNATION) for i in range(4)]
+    for p in specs:
+        for _ in range(12):
+            # random non-terminal context: walk down random children until terminal
+            path = []
+            depth_target = r.randint(0, p.max_depth)
+            while len(path) < depth_target:
+                cands = generate_steps(p, path, p.branching)
+                j = r.randrange(len(cands))
+                if cands[j].is_terminal:
+                    break
+                path.append(cands[j].step_ref)
+            width = r.randint(1, p.branching)
+            cands = generate_steps(p, path, width)
+            kats.append({
+                "problem": problem_record(p),
+                "path": path,
+                "width": width,
+                "candidates": [[c.step_ref, c.token_count, c.prior, c.prm_reward, int(c.is_terminal)] for c in cands],
+            })
+    dump("steps_kats", kats)
+
+
+def gen_serial():
+    """run_tree_search outcomes (search.py:79) for several scoring variants + tree dumps."""
+    D7 = {d: (7, 7) for d in Difficulty}
+    c1 = make_workload(64, MIX, SEED, branching=4, depth_ranges=D7)
+    mixed = make_workload(97, (0.5, 0.3, 0.2), 77, branching=3,
+                          depth_ranges={Difficulty.EASY: (3, 9), Difficulty.HARD_SOLVABLE: (4, 10), Difficulty.UNSOLVABLE: (2, 6)},
+                          accept_threshold=0.35)
+    cases = []
+    variants = [
+        ("c1_default", c1, ScoringConfig(), 32, 8, 4, True, True),
+        ("c1_exits_off", c1, ScoringConfig(), 32, 8, 4, False, False),
+        ("c1_pe_only", c1, ScoringConfig(), 32, 8, 4, True, False),
+        ("mixed_strict_prefix", mixed, ScoringConfig(strict_negative_exit=True, futility_bound=FutilityBound.PREFIX_AGGREGATE, accept_threshold=0.35), 48, 7, 3, True, True),
+        ("mixed_min_scheme", mixed, ScoringConfig(scheme=AggregationScheme.MINIMUM, positive_exit_threshold=0.6, first_step_threshold=0.3), 40, 12, 2, True, True),
+        ("mixed_cap5", mixed, ScoringConfig(), 24, 5, 3, True, True),
+    ]
+    for name, wl, sc, budget, cap, width, pe, ne in variants:
+        outs = [outcome_record(run_tree_search(p, sc, None, budget, cap, width, pe, ne)) for p in wl]
+        trees = {}
+        for idx in (0, 1, 2, 5, 11, 40):
+            if idx < len(wl):
+                trees[str(idx)] = tree_record(serial_tree(wl[idx], sc, budget, cap, width, pe, ne))
+        cases.append({
+            "name": name, "workload": "c1" if wl is c1 else "mixed_b3", "scoring": scoring_record(sc),
+            "budget": budget, "depth_cap": cap, "expand_width": width, "positive_exit": pe,
+            "negative_exit": ne, "outcomes": outs, "trees": trees,
+        })
+    dump("serial", cases)
+
+
+def gen_deep():
+    """Exits-off deep trees (C2 shape, budget 128) and config-4 stagnation shape."""
+    D15 = {d: (15, 15) for d in Difficulty}
+    c2 = make_workload(4096, MIX, SEED, branching=4, depth_ranges=D15)
+    cases = []
+    for idx in (0, 3):
+        t0 = time.time()
+        tree = serial_tree(c2[idx], ScoringConfig(), 128, 16, 4, False, False)
+        cases.append({"name": f"c2_exits_off_{idx}", "workload": "c2", "index": idx, "budget": 128,
+                      "depth_cap": 16, "expand_width": 4, "positive_exit": False, "negative_exit": False,
+                      "tree": tree_record(tree)})
+        print("deep", idx, len(tree.nodes), time.time() - t0)
+    s = make_problem("s0000", rng.mix(SEED, 8, 0), Difficulty.HARD_SOLVABLE, (31, 31), 8, STAGNATION)
+    tree = serial_tree(s, ScoringConfig(), 48, 32, 8, False, False)
+    cases.append({"name": "c4_exits_off_0", "workload": "c4_stagnation", "index": 0, "budget": 48,
+                  "depth_cap": 32, "expand_width": 8, "positive_exit": False, "negative_exit": False,
+                  "tree": tree_record(tree)})
+    print("deep c4", len(tree.nodes))
+    dump("deep_trees", cases)
+
+
+def wave_case(name, wl_name, problems, sched, budget, cap, width, pe, ne, scoring=None,
+              arrival_steps=None, tree_idx=()):
+    t0 = time.time()
+    out, info = wave_ref.run_waves(problems, scoring=scoring, sched=sched, rollout_budget=budget,
+                                   depth_cap=cap, expand_width=width, positive_exit=pe,
+                                   negative_exit=ne, arrival_steps=arrival_steps,
+                                   keep_trees=bool(tree_idx))
+    trees = {str(i): tree_record(out[i]["tree"]) for i in tree_idx}
+    for o in out:
+        o.pop("tree", None)
+    print(name, "steps", info["steps"], "rollouts", sum(o["rollouts_completed"] for o in out),
+          f"{time.time() - t0:.1f}s")
+    return {
+        "name": name, "workload": wl_name, "scoring": scoring_record(scoring or ScoringConfig()),
+        "sched": {"max_concurrency": sched.max_concurrency, "beta": sched.beta, "proximity": sched.proximity,
+                  "obs_threshold": sched.obs_threshold, "boosting_enabled": sched.boosting_enabled},
+        "budget": budget, "depth_cap": cap, "expand_width": width, "positive_exit": pe,
+        "negative_exit": ne, "arrival_steps": arrival_steps, "steps": info["steps"],
+        "targets_trace": info["targets_trace"], "outcomes": out, "trees": trees,
+    }
+
+
+def serving_arrivals(n, rate, seed, steps_per_unit):
+    """Config-5 arrivals: the reference generator (simulator.py:193-200) quantised to steps."""
+    t = 0.0
+    steps = []
+    for i in range(n):
+        t += rng.exponential(rate, seed, 21, i)
+        steps.append(int(t * steps_per_unit))
+    return steps
+
+
+def gen_waves():
+    D7 = {d: (7, 7) for d in Difficulty}
+    D15 = {d: (15, 15) for d in Difficulty}
+    c1 = make_workload(64, MIX, SEED, branching=4, depth_ranges=D7)
+    c2 = make_workload(4096, MIX, SEED, branching=4, depth_ranges=D15)
+    cli = make_workload(500, MIX, 20260810)
+    mixed = make_workload(97, (0.5, 0.3, 0.2), 77, branching=3,
+                          depth_ranges={Difficulty.EASY: (3, 9), Difficulty.HARD_SOLVABLE: (4, 10), Difficulty.UNSOLVABLE: (2, 6)},
+                          accept_threshold=0.35)
+    cases = [
+        wave_case("c1_M64", "c1", c1, SchedulerConfig(max_concurrency=64), 32, 8, 4, True, True, tree_idx=(0, 7)),
+        wave_case("c1_M256", "c1", c1, SchedulerConfig(max_concurrency=256), 32, 8, 4, True, True, tree_idx=(0, 7)),
+        wave_case("c1_M256_pe", "c1", c1, SchedulerConfig(max_concurrency=256), 32, 8, 4, True, False),
+        wave_case("c1_M48_admission", "c1", c1, SchedulerConfig(max_concurrency=48), 32, 8, 4, True, True),
+        wave_case("mixed_M200_obs3", "mixed_b3", mixed,
+                  SchedulerConfig(max_concurrency=200, beta=1.5, proximity=0.8, obs_threshold=3), 40, 9, 3, True, True,
+                  scoring=ScoringConfig(accept_threshold=0.35), tree_idx=(4,)),
+        wave_case("c2_M4096", "c2", c2, SchedulerConfig(max_concurrency=4096), 128, 16, 4, True, True, tree_idx=(1, 2)),
+        wave_case("c2_s512_M2048", "c2", c2[:512], SchedulerConfig(max_concurrency=2048), 128, 16, 4, True, True),
+        wave_case("c3_s256_M1024_exits_off", "c2", c2[:256], SchedulerConfig(max_concurrency=1024), 24, 16, 4, False, False,
+                  tree_idx=(0,)),
+        wave_case("cli_serving_pe_ne_boost", "cli_default", cli, SchedulerConfig(max_concurrency=16), 32, 16, 4, True, True,
+                  arrival_steps=serving_arrivals(500, 5.0, 20260810, 20.0)),
+        wave_case("cli_serving_pe", "cli_default", cli, SchedulerConfig(max_concurrency=16, boosting_enabled=False), 32, 16, 4,
+                  True, False, arrival_steps=serving_arrivals(500, 5.0, 20260810, 20.0)),
+    ]
+    dump("waves", cases)
+
+
+def gen_targets():
+    """compute_targets (scheduler.py:143-187) on random pools, incl. equal-score lock-step pools."""
+    r = random.Random(7)
+    kats = []
+    for t in range(400):
+        n = r.randint(1, 60) if t % 4 else r.randint(100, 700)
+        M = n + r.randint(0, 5 * n)
+        cfg = SchedulerConfig(max_concurrency=M, beta=r.choice([2.0, 1.0, 0.5]), proximity=r.choice([0.9, 0.5]),
+                              obs_threshold=r.choice([1, 2, 3]), boosting_enabled=r.random() > 0.05)
+        lockstep = t % 3 == 0
+        now_step = r.randint(0, 40)
+        state = SchedulerState(now=float(now_step))
+        rows = []
+        arr = 0
+        for i in range(n):
+            if not lockstep:
+                arr = min(now_step, arr + (r.randint(0, 2) if r.random() < 0.5 else 0))
+            job = Job(job_id=i, arrival_time=float(0 if lockstep else arr), tree=SearchTree(8))
+            job.completed_rollouts = r.randint(0, 5)
+            job.best_score = r.choice([0.0, r.random(), 0.46, 0.44, 0.5 * 0.9, r.random() * 0.6])
+            job.state = JobState.RUNNING
+            state.run_queue.append(job)
+            rows.append([int(job.arrival_time), job.completed_rollouts, job.best_score])
+        targets = compute_targets(state, cfg, 0.5)
+        kats.append({"now_step": now_step, "M": M, "beta": cfg.beta, "proximity": cfg.proximity,
+                     "obs_threshold": cfg.obs_threshold, "boosting": cfg.boosting_enabled,
+                     "theta_pos": 0.5, "jobs": rows, "targets": [targets[i] for i in range(n)]})
+    dump("targets_kats", kats)
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets"]
+    for w in which:
+        globals()["gen_" + w]()
