@@ -1,0 +1,396 @@
+"""Benchmark: MCTS rollouts/s and p99 per-search latency (BASELINE.json metric).
+
+Workload (N=1, BASELINE.json configs[1]): 4096 concurrent searches, branching 4,
+depth 16 (base depth 15 + 1), rollout budget 128, positive + negative early
+exit and adaptive boosting on, M = 4096, workload seed 0 — synthetic problems
+from the reference's seeded generator (make_workload).  One bench "step" is
+one whole batch: every search admitted at wave 0 and advanced wave by wave
+until all have exited.  Under torchrun (N>1) every rank runs its own block of
+4096 searches of one 4096*N-request run queue (weak scaling; M = 4096*N) and
+the scheduler records are all-gathered over NCCL each wave.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PER_GPU = 4096
+BUDGET, DEPTH_CAP, WIDTH, BRANCH, BASE = 128, 16, 4, 4, 15
+METRIC = "MCTS rollouts/sec (p99 per-search latency alongside)"
+UNIT = "rollouts/s"
+# algorithmic bytes: per WU-PUCT child scored, per
+# selection level, per node created, per path node of a backup/cancel
+B_SCORED, B_LEVEL, B_NODE, B_PATH = 28, 28, 44, 48
+
+
+def workload(n_total: int):
+    from paper_2604_00510_b200 import backend as B
+
+    D = {d: (BASE, BASE) for d in B.Difficulty}
+    return B.make_workload(n_total, (0.6, 0.25, 0.15), 0, branching=BRANCH, depth_ranges=D)
+
+
+def search_config(M: int, exits: bool = True):
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    return SearchConfig(scheduler=SchedulerConfig(max_concurrency=M), rollout_budget=BUDGET, depth_cap=DEPTH_CAP,
+                        expand_width=WIDTH, positive_exit=exits, negative_exit=exits)
+
+
+def percentile(values, pct: float) -> float:
+    """Nearest-rank percentile, as metrics.percentile (metrics.py:86-94)."""
+    vals = sorted(values)
+    if not vals:
+        return 0.0
+    import math
+
+    k = max(1, math.ceil(pct / 100.0 * len(vals)))
+    return vals[k - 1]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def flush_l2(buf):
+    buf.add_(1)  # writes 512 MiB > the 126 MB L2
+
+
+# --------------------------------------------------------------------------- ours
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+
+    def init(self):
+        import torch
+
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        self.pg.all_reduce(t)
+        return float(t.item())
+
+
+def run_sharded(eng, d: Dist, n_local: int, counts, allc, recs, allr, max_steps=1 << 30):
+    """The wave loop of one rank: counts → all-gather → admit → records →
+    all-gather (NCCL over NVLink) → targets → wave."""
+    import torch
+
+    for step in range(max_steps):
+        eng.step_counts(step, counts.data_ptr())
+        d.pg.all_gather_into_tensor(allc, counts)
+        if step % 8 == 0 and int(allc.view(-1, 3)[:, 2].sum().item()) == 0:
+            return step
+        eng.step_admit(step, allc.data_ptr(), d.world, d.rank)
+        eng.step_records(step, recs.data_ptr())
+        d.pg.all_gather_into_tensor(allr, recs)
+        eng.step_targets(step, allr.data_ptr())
+        eng.step_wave(step)
+    return max_steps
+
+
+def bench_ours(args, d: Dist):
+    import torch
+
+    from paper_2604_00510_b200.backend import problem_table
+    from paper_2604_00510_b200.engine import Engine
+
+    N = d.world
+    n_total = PER_GPU * N
+    specs = workload(n_total)
+    lo = d.rank * PER_GPU
+    table = problem_table(specs[lo: lo + PER_GPU])
+    cfg = search_config(n_total)
+    eng = Engine(cfg, d.local)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    allc = torch.zeros(3 * N, dtype=torch.int64, device="cuda")
+    recs = torch.zeros(PER_GPU * 16, dtype=torch.uint8, device="cuda")
+    allr = torch.zeros(n_total * 16, dtype=torch.uint8, device="cuda")
+
+    def one_step():
+        if N == 1:
+            eng.run()
+        else:
+            run_sharded(eng, d, PER_GPU, counts, allc, recs, allr)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        eng.load(table, lo, n_total)
+        one_step()
+    torch.cuda.synchronize()
+    d.barrier()
+    clocks = Clocks(d.local) if d.rank == 0 else None
+    total_ms, rollouts, wave_ms, launches, lat, stats = 0.0, 0, 0.0, 0, [], None
+    byte_total = 0
+    for _ in range(args.steps):
+        eng.load(table, lo, n_total)  # H2D of the problem table + tree reset: outside the timed region
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        d.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = d.max(e0.elapsed_time(e1))
+        total_ms += ms
+        stats = eng.stats()
+        rollouts += stats.rollouts
+        wave_ms += stats.wave_ms
+        launches += stats.kernel_launches
+        byte_total += (B_SCORED * stats.children_scored + B_LEVEL * stats.select_levels + B_NODE * stats.nodes
+                       + B_PATH * stats.path_nodes)
+        lat.extend((eng.latencies_ns() / 1e6).tolist())
+    clk = clocks.stop() if clocks else None
+    rollouts_all = d.sum(rollouts)
+    value = rollouts_all / (total_ms / 1e3)
+    outs = eng.outcomes()
+    exits = {k: sum(1 for o in outs if o.exit_kind == k) for k in (1, 2, 3)}
+
+    # e2e: host problem table in → host outcomes out through one C-ABI call
+    e2e = None
+    if N == 1:
+        ts = []
+        ro = 0
+        for _ in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out, st = eng.run_batch_host(table)
+            t1 = time.perf_counter()
+            ts.append(t1 - t0)
+            ro = st.rollouts
+        from paper_2604_00510_b200._abi import TsOutcome, TsProblem
+
+        e2e = {"value": ro / statistics.median(ts), "unit": UNIT,
+               "h2d_bytes_per_step": ctypes.sizeof(TsProblem) * PER_GPU,
+               "d2h_bytes_per_step": ctypes.sizeof(TsOutcome) * PER_GPU,
+               "ms_per_step": 1e3 * statistics.median(ts), "api": "ts_run_batch_host"}
+
+    # exits-off throughput variant on the same seeds (every search runs its budget)
+    variant = None
+    if N == 1:
+        eng2 = Engine(search_config(n_total, exits=False), d.local)
+        eng2.load(table)
+        eng2.run()
+        eng2.load(table)
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st2 = eng2.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms2 = e0.elapsed_time(e1)
+        b2 = (B_SCORED * st2.children_scored + B_LEVEL * st2.select_levels + B_NODE * st2.nodes
+              + B_PATH * st2.path_nodes)
+        hbm, _ = peaks()
+        variant = {"workload": "same 4096 searches, exits off (every search runs 128 rollouts)",
+                   "value": st2.rollouts / (ms2 / 1e3), "unit": UNIT, "ms": ms2, "waves": st2.steps,
+                   "wave_kernel_GBs": b2 / (st2.wave_ms / 1e3) / 1e9,
+                   "wave_frac": b2 / (st2.wave_ms / 1e3) / 1e9 / hbm}
+        eng2.close()
+
+    cpu = cpu_baseline(PER_GPU, n_total) if (d.rank == 0 and N == 1 and not args.no_cpu) else None
+    if d.rank != 0:
+        eng.close()
+        return None
+    hbm, src = peaks()
+    achieved = byte_total / (wave_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64+u64", "data": "synthetic (reference make_workload generator, seed 0)",
+        "config": {"workload": f"c2: {PER_GPU}/GPU searches, b={BRANCH}, depth {BASE + 1}, budget {BUDGET}, "
+                               f"PE+NE+boost, M={n_total}",
+                   "searches": n_total, "branching": BRANCH, "depth": BASE + 1, "rollout_budget": BUDGET,
+                   "max_concurrency": n_total, "parallelism": f"search-sharded x{N}",
+                   "l2": "flushed (512 MiB write) before every timed step; node pool > L2"},
+        "p99_search_latency_ms": percentile(lat, 99), "p50_search_latency_ms": percentile(lat, 50),
+        "rollouts_per_step": rollouts_all / args.steps, "exits": exits,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": None, "kernel": "k_wave", "peak_source": src,
+                     "algorithmic_bytes": byte_total, "wave_ms": wave_ms},
+        "cpu_baseline": cpu, "clocks": clk, "variants": {"exits_off": variant},
+    }
+    eng.close()
+    return line
+
+
+# --------------------------------------------------------------------------- CPU
+def cpu_baseline(per_gpu: int, n_total: int, target_s: float = 12.0):
+    """The C oracle (a restatement of the reference, oracle/) on the host cores:
+    a bounded sample of the same workload (the first S searches, M scaled)."""
+    from oracle import oracle
+    from paper_2604_00510_b200.backend import problem_table
+
+    threads = os.cpu_count() or 1
+    specs = workload(n_total)
+    sample = 256
+    while True:
+        t = problem_table(specs[:sample])
+        cfg = search_config(sample).to_c()
+        t0 = time.perf_counter()
+        r = oracle.OracleRun(t, cfg, threads=threads)
+        dt = time.perf_counter() - t0
+        ro = r.stats.rollouts
+        lat = (r.latencies_s() * 1e3).tolist()
+        r.close()
+        if dt > target_s / 4 or sample >= per_gpu:
+            break
+        sample = min(per_gpu, sample * 4)
+    return {"value": ro / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {sample} of the {per_gpu} searches, M={sample}, same budget/exits/boosting; "
+                      f"{ro} rollouts in {dt:.2f} s",
+            "p99_search_latency_ms": percentile(lat, 99)}
+
+
+def bench_reference(args):
+    """--impl reference: the reference algorithm on the host cores (oracle port;
+    the Python reference itself is not present on the GPU box)."""
+    from oracle import oracle
+    from paper_2604_00510_b200.backend import problem_table
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    specs = workload(PER_GPU)
+    sample = 512
+    t = problem_table(specs[:sample])
+    cfg = search_config(sample).to_c()
+    for _ in range(args.warmup):
+        oracle.OracleRun(t, cfg, threads=threads).close()
+    times, ro, lat = [], 0, []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        r = oracle.OracleRun(t, cfg, threads=threads)
+        times.append(time.perf_counter() - t0)
+        ro += r.stats.rollouts
+        lat.extend((r.latencies_s() * 1e3).tolist())
+        r.close()
+    value = ro / sum(times)
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
+        "config": {"workload": f"c2 sample: first {sample} of {PER_GPU} searches, M={sample}"},
+        "p99_search_latency_ms": percentile(lat, 99),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} searches per step"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return
+        print(json.dumps(bench_reference(args)))
+        return
+    import __graft_entry__
+
+    __graft_entry__.build()
+    d = Dist()
+    d.init()
+    line = bench_ours(args, d)
+    if line is not None:
+        print(json.dumps(line))
+    if d.pg:
+        d.pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

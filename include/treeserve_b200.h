@@ -8,6 +8,9 @@
  * sizes only: no torch types.  All calls return a ts_status; no exception ever
  * crosses the ABI.  One engine = one GPU = one host thread (the reference's
  * single-owner model, tree.py:12-13).
+ *
+ * Time unit: one wave ("step").  A request's arrival is an integer step, the
+ * scheduler's clock is now = step (SchedulerState.now, scheduler.py:100).
  */
 #ifndef TREESERVE_B200_H
 #define TREESERVE_B200_H
@@ -18,31 +21,31 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
-#define TS_MAX_DEPTH 32 /* deepest node any search may create            */
-#define TS_MAX_WIDTH 32 /* min(expand_width, branching) ≤ one warp       */
+#define TS_ABI_VERSION 2
+#define TS_MAX_DEPTH 32 /* golden path / reward table length; base_depth <= 31 */
+#define TS_MAX_WIDTH 32 /* branching <= one warp                                */
 
 /* Status codes, mapped to the reference's exception classes by the shim. */
 typedef enum ts_status {
   TS_OK = 0,
-  TS_INVALID_ARGUMENT = 1, /* ValueError                       */
-  TS_TREE_STRUCTURE = 2,   /* TreeStructureError (tree.py:42)  */
-  TS_EXHAUSTED = 3,        /* NoExpandableLeafError — per-search flag, never a call failure */
-  TS_ACCOUNTING = 4,       /* AccountingError (tree.py:50)     */
-  TS_UNSUPPORTED_SCHEME = 5, /* UnsupportedSchemeError (scoring.py:38) */
-  TS_POOL_OVERFLOW = 6,    /* node arena exhausted (engine bug signal) */
-  TS_CUDA = 7              /* CUDA runtime failure              */
+  TS_INVALID_ARGUMENT = 1,   /* ValueError                                    */
+  TS_TREE_STRUCTURE = 2,     /* TreeStructureError (tree.py:42)               */
+  TS_EXHAUSTED = 3,          /* NoExpandableLeafError — per-search, never a call failure */
+  TS_ACCOUNTING = 4,         /* AccountingError (tree.py:50)                  */
+  TS_UNSUPPORTED_SCHEME = 5, /* UnsupportedSchemeError (scoring.py:38)        */
+  TS_POOL_OVERFLOW = 6,      /* node arena exhausted (engine bug signal)      */
+  TS_CUDA = 7                /* CUDA runtime failure                          */
 } ts_status;
 
 /* AggregationScheme (scoring.py:42-46) */
 enum { TS_SCHEME_MINIMUM = 0, TS_SCHEME_PRODUCT = 1, TS_SCHEME_SUM = 2, TS_SCHEME_AVERAGE = 3 };
 /* FutilityBound (scoring.py:53-55) */
 enum { TS_BOUND_LEAF_REWARD = 0, TS_BOUND_PREFIX_AGGREGATE = 1 };
-/* ExitKind (scoring.py:63-67); TS_EXIT_NONE = still running */
+/* ExitKind (scoring.py:63-67); TS_EXIT_NONE = CONTINUE / still running */
 enum { TS_EXIT_NONE = 0, TS_EXIT_POSITIVE = 1, TS_EXIT_NEGATIVE = 2, TS_EXIT_BUDGET = 3 };
 
 /*
- * One search request: the host-precomputed problem table row.
+ * One search request: the host-precomputed problem-table row.
  * Mirrors SyntheticProblemSpec (backend.py:113-132) plus derived constants:
  * base_depth (backend.py:135-137), golden path (140-141) and the LIFTED golden
  * rewards golden_step_rewards() (201-215, uses pow → computed on the host).
@@ -54,7 +57,8 @@ typedef struct ts_problem {
   int32_t golden_len;          /* len(golden_path), or -1 when golden_path is None */
   int32_t hidden_until_depth;  /* RewardProfile.hidden_until_depth */
   int32_t has_shared;          /* RewardProfile.shared_range is not None */
-  int32_t arrival_step;        /* serving: step at which the request arrives (0 = batch) */
+  int32_t arrival_step;        /* serving: step at which the request arrives (0 = batch);
+                                  non-decreasing in request order (simulator.py:193-200) */
   double off_lo, off_hi;       /* RewardProfile.off_path_range */
   double shared_lo, shared_hi; /* RewardProfile.shared_range */
   uint8_t golden_path[TS_MAX_DEPTH];
@@ -64,7 +68,6 @@ typedef struct ts_problem {
 /*
  * Flattened ScoringConfig (scoring.py:76-103) + SelectionParams (tree.py:92-100)
  * + SchedulerConfig (scheduler.py:77-93) + run_tree_search knobs (search.py:79-88).
- * Time unit: one wave (step).  now = step, arrival = arrival_step.
  */
 typedef struct ts_config {
   int32_t scheme;
@@ -104,79 +107,99 @@ typedef struct ts_outcome {
   uint8_t best_path[TS_MAX_DEPTH];
 } ts_outcome;
 
-/* Per-run statistics of one batch (ts_run). */
+/* Counters of one engine since its last ts_load_problems. */
 typedef struct ts_run_stats {
-  int32_t steps;          /* waves executed */
+  int32_t steps;          /* waves executed (1 + last exit step for ts_run) */
   int32_t finished;       /* searches with an exit decision */
   int64_t rollouts;       /* completed (backpropagated) rollouts */
   int64_t launched;       /* launched rollouts */
-  int64_t nodes;          /* nodes created */
+  int64_t nodes;          /* nodes created (roots excluded) */
   int64_t tokens;
   int64_t children_scored;/* selection work (WU-PUCT evaluations) */
   int64_t select_levels;  /* selection descent levels */
   int64_t path_nodes;     /* Σ (trajectory length + 1) over completed+cancelled rollouts */
+  int64_t kernel_launches;/* engine kernels launched since ts_load_problems (host count) */
+  double wave_ms;         /* Σ device time of the wave kernels (CUDA events on the launch stream) */
 } ts_run_stats;
+
+/* One scheduler record per search, all-gathered across ranks in global
+ * run-queue order before ts_step_targets. */
+typedef struct ts_sched_record {
+  double score;           /* parallelism_score S(i,t), scheduler.py:118-128 */
+  uint32_t flags;         /* bit0 running, bit1 ungated (completed >= obs), bit2 boosted */
+  uint32_t _pad;
+} ts_sched_record;
 
 typedef struct ts_engine ts_engine;
 
 /* ---- engine lifetime ---------------------------------------------------- */
 /* Replaces constructing SearchTree/ProblemBackend/SchedulerState per request
- * (tree.py:120, backend.py:275, scheduler.py:96).  capacity = max searches. */
-int ts_engine_create(const ts_config* cfg, int32_t device, int32_t capacity, ts_engine** out);
+ * (tree.py:120, backend.py:275, scheduler.py:96).  Validates the config the
+ * way the reference's frozen dataclasses do (__post_init__). */
+int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out);
 int ts_engine_destroy(ts_engine* eng);
 const char* ts_last_error(const ts_engine* eng);
 int ts_abi_version(void);
 
-/* Upload a batch of problems (host array) and reset every tree to a bare root
- * (SearchTree.__init__, tree.py:120-128).  Searches get local ids 0..n-1.
- * global_offset/global_stride place them in the global run queue when the
- * batch is sharded over ranks (global id = global_offset + i*global_stride). */
-int ts_load_problems(ts_engine* eng, const ts_problem* host_problems, int32_t n,
-                     int32_t global_offset, int32_t global_stride, void* stream);
+/* Upload a batch of requests (host array) and reset every tree to a bare root
+ * (SearchTree.__init__, tree.py:120-128).  The n_local searches are the
+ * contiguous block [global_offset, global_offset + n_local) of an n_global
+ * run queue sharded over ranks (n_global = n_local on one GPU).  Sizes the
+ * SoA node pool from rollout_budget × width × min(depth_cap, base_depth+1). */
+int ts_load_problems(ts_engine* eng, const ts_problem* host_problems, int32_t n_local,
+                     int32_t global_offset, int32_t n_global, void* stream);
 
-/* One wave for every running search with its current target P_i:
- * select_leaf → simulate_to_terminal (×min(P_i, budget-completed)), then
- * finish_rollout → decide_exit per rollout in launch order, cancel_inflight on
- * exit (search.py:95-107, simulator.py:367-501).            */
-int ts_wave(ts_engine* eng, int32_t step, void* stream);
+/* ---- one step (wave), in call order; ts_run composes them on one GPU ----- */
+/* Local counts before admission: dev_counts[0..2] = {running, arrived-but-
+ * pending (arrival_step <= step), unfinished}.  For multi-GPU, all-gather
+ * these (world × 3 int64) before ts_step_admit. */
+int ts_step_counts(ts_engine* eng, int32_t step, int64_t* dev_counts, void* stream);
+/* admit_jobs (scheduler.py:131-140) as one global FIFO over ranks. */
+int ts_step_admit(ts_engine* eng, int32_t step, const int64_t* dev_all_counts, int32_t world,
+                  int32_t rank, void* stream);
+/* parallelism_score per local search (scheduler.py:118-128) → n_local records. */
+int ts_step_records(ts_engine* eng, int32_t step, ts_sched_record* dev_records, void* stream);
+/* compute_targets (scheduler.py:143-187) over all n_global records (global
+ * run-queue order); keeps this rank's P_i and builds the wave's work list. */
+int ts_step_targets(ts_engine* eng, int32_t step, const ts_sched_record* dev_all_records,
+                    void* stream);
+/* One wave for every running search with its target P_i: select_leaf →
+ * simulate_to_terminal ×min(P_i, budget-completed), then finish_rollout →
+ * decide_exit per rollout in launch order, cancel_inflight on exit
+ * (search.py:95-107, simulator.py:367-501). */
+int ts_step_wave(ts_engine* eng, int32_t step, void* stream);
 
-/* Scheduler, local half: admission (admit_jobs, scheduler.py:131-140) is
- * global; this writes the per-search record {S_i, flags} (parallelism_score,
- * scheduler.py:118-128) into dev_records[local] (2 doubles each).          */
-int ts_sched_records(ts_engine* eng, int32_t step, double* dev_records, void* stream);
-
-/* Scheduler, global half: compute_targets (scheduler.py:143-187) over the
- * gathered records of all ranks (world_size blocks of n_local_max records,
- * rank-major), writing this rank's P_i.  Single GPU: world_size = 1.     */
-int ts_sched_targets(ts_engine* eng, int32_t step, const double* dev_all_records,
-                     int32_t world_size, int32_t n_local_max, int32_t rank, void* stream);
-
-/* Admission (admit_jobs) for the serving loop: admit queued arrivals while the
- * GLOBAL running count < M.  dev_counts = {global running, global admitted}. */
-int ts_admit(ts_engine* eng, int32_t step, const int64_t* dev_global_counts, void* stream);
-int ts_local_counts(ts_engine* eng, int64_t* dev_counts_out, void* stream);
-
-/* Whole batch on one GPU: admission + targets + waves until every search has
- * exited (or max_steps).  Equivalent to ts_admit, ts_sched_records, ts_sched_targets, ts_wave per step. */
+/* Whole batch on one GPU: the five calls above per step until every search
+ * has exited (or max_steps).  stats_out may be NULL. */
 int ts_run(ts_engine* eng, int32_t max_steps, ts_run_stats* stats_out, void* stream);
 
-/* Device→host readout of SearchOutcome records for searches [0, n). */
+/* ---- readout ------------------------------------------------------------ */
+/* Device→host SearchOutcome records for local searches [0, n). */
 int ts_read_outcomes(ts_engine* eng, ts_outcome* host_out, int32_t n, void* stream);
 int ts_read_stats(ts_engine* eng, ts_run_stats* host_out, void* stream);
+/* Targets P_i of the last ts_step_targets for local searches [0, n) (0 = not
+ * running); call between ts_step_targets and ts_step_wave. */
+int ts_read_targets(ts_engine* eng, int32_t* host_out, int32_t n, void* stream);
+/* Per-search latency in ns (device %globaltimer): exit decision time minus the
+ * start of the admission step; 0 for searches that have not exited. */
+int ts_read_latencies(ts_engine* eng, uint64_t* host_ns, int32_t n, void* stream);
+/* Device timestamps (ns, %globaltimer) at the start of each step [0, n). */
+int ts_read_step_times(ts_engine* eng, uint64_t* host_out, int32_t n, void* stream);
 
 /* End-to-end: host problems in, host outcomes out (H2D, run, D2H). */
 int ts_run_batch_host(ts_engine* eng, const ts_problem* host_problems, int32_t n,
                       int32_t max_steps, ts_outcome* host_out, ts_run_stats* stats_out, void* stream);
 
 /* Tree dump in the SearchTree.to_dict schema (tree.py:183-203); arrays sized
- * by ts_tree_size.  Any pointer may be NULL to skip that field. */
+ * by ts_tree_size.  Any pointer may be NULL to skip that field.  step_ref of
+ * the root is -1. */
 int ts_tree_size(ts_engine* eng, int32_t search, int32_t* nodes_out);
 int ts_dump_tree(ts_engine* eng, int32_t search, int32_t* parent, double* reward, double* prior,
                  int32_t* visits, int32_t* inflight, double* value_sum, uint8_t* terminal,
                  int32_t* depth, int32_t* step_ref);
 
 /* Host-side problem-table builder (make_problem + golden_step_rewards,
- * backend.py:144-215): fills derived fields of *out from the spec fields. */
+ * backend.py:144-215): fills *out from the spec fields. */
 int ts_fill_problem(uint64_t seed, int32_t solvable, int32_t depth_lo, int32_t depth_hi,
                     int32_t branching, double golden_lo, double golden_hi, double off_lo,
                     double off_hi, int32_t hidden_until_depth, int32_t has_shared,

@@ -76,6 +76,8 @@ def lib() -> ctypes.CDLL:
         L.or_tree_size.argtypes = [ctypes.c_void_p, i32]
         L.or_tree_dump.restype = None
         L.or_tree_dump.argtypes = [ctypes.c_void_p, i32] + [ctypes.c_void_p] * 9
+        L.or_run_latencies.restype = None
+        L.or_run_latencies.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         L.or_run_free.restype = None
         L.or_run_free.argtypes = [ctypes.c_void_p]
         L.or_run_tree_search.restype = i32
@@ -185,6 +187,13 @@ class OracleRun:
         order = ["parent", "reward", "prior", "N", "O", "W", "terminal", "depth", "step_ref"]
         lib().or_tree_dump(self._h, i, *[out[k].ctypes.data_as(ctypes.c_void_p) for k in order])
         return out
+
+    def latencies_s(self):
+        import numpy as np
+
+        out = np.zeros(max(1, self.n), np.float64)
+        lib().or_run_latencies(self._h, out.ctypes.data_as(ctypes.c_void_p))
+        return out[: self.n]
 
     def close(self):
         if self._h:

@@ -12,7 +12,7 @@ import os
 
 TS_MAX_DEPTH = 32
 TS_MAX_WIDTH = 32
-TS_ABI_VERSION = 1
+TS_ABI_VERSION = 2
 
 TS_OK = 0
 TS_INVALID_ARGUMENT = 1
@@ -88,6 +88,10 @@ class TsOutcome(ctypes.Structure):
     ]
 
 
+class TsSchedRecord(ctypes.Structure):
+    _fields_ = [("score", ctypes.c_double), ("flags", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
+
+
 class TsRunStats(ctypes.Structure):
     _fields_ = [
         ("steps", ctypes.c_int32),
@@ -99,6 +103,8 @@ class TsRunStats(ctypes.Structure):
         ("children_scored", ctypes.c_int64),
         ("select_levels", ctypes.c_int64),
         ("path_nodes", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+        ("wave_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:
@@ -108,9 +114,9 @@ class TsRunStats(ctypes.Structure):
 # Every symbol include/treeserve_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
     "ts_engine_create", "ts_engine_destroy", "ts_last_error", "ts_abi_version",
-    "ts_load_problems", "ts_wave", "ts_sched_records", "ts_sched_targets", "ts_admit",
-    "ts_local_counts", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_run_batch_host",
-    "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
+    "ts_load_problems", "ts_step_counts", "ts_step_admit", "ts_step_records", "ts_step_targets",
+    "ts_step_wave", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_read_targets",
+    "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
 )
 
 _lib = None
@@ -131,19 +137,22 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
     vp = ctypes.c_void_p
     i32 = ctypes.c_int32
     sig = {
-        "ts_engine_create": (ctypes.c_int, [P(TsConfig), i32, i32, P(vp)]),
+        "ts_engine_create": (ctypes.c_int, [P(TsConfig), i32, P(vp)]),
         "ts_engine_destroy": (ctypes.c_int, [vp]),
         "ts_last_error": (ctypes.c_char_p, [vp]),
         "ts_abi_version": (ctypes.c_int, []),
         "ts_load_problems": (ctypes.c_int, [vp, P(TsProblem), i32, i32, i32, vp]),
-        "ts_wave": (ctypes.c_int, [vp, i32, vp]),
-        "ts_sched_records": (ctypes.c_int, [vp, i32, vp, vp]),
-        "ts_sched_targets": (ctypes.c_int, [vp, i32, vp, i32, i32, i32, vp]),
-        "ts_admit": (ctypes.c_int, [vp, i32, vp, vp]),
-        "ts_local_counts": (ctypes.c_int, [vp, vp, vp]),
+        "ts_step_counts": (ctypes.c_int, [vp, i32, vp, vp]),
+        "ts_step_admit": (ctypes.c_int, [vp, i32, vp, i32, i32, vp]),
+        "ts_step_records": (ctypes.c_int, [vp, i32, vp, vp]),
+        "ts_step_targets": (ctypes.c_int, [vp, i32, vp, vp]),
+        "ts_step_wave": (ctypes.c_int, [vp, i32, vp]),
         "ts_run": (ctypes.c_int, [vp, i32, P(TsRunStats), vp]),
         "ts_read_outcomes": (ctypes.c_int, [vp, P(TsOutcome), i32, vp]),
         "ts_read_stats": (ctypes.c_int, [vp, P(TsRunStats), vp]),
+        "ts_read_targets": (ctypes.c_int, [vp, P(i32), i32, vp]),
+        "ts_read_step_times": (ctypes.c_int, [vp, P(ctypes.c_uint64), i32, vp]),
+        "ts_read_latencies": (ctypes.c_int, [vp, P(ctypes.c_uint64), i32, vp]),
         "ts_run_batch_host": (ctypes.c_int, [vp, P(TsProblem), i32, i32, P(TsOutcome), P(TsRunStats), vp]),
         "ts_tree_size": (ctypes.c_int, [vp, i32, P(i32)]),
         "ts_dump_tree": (ctypes.c_int, [vp, i32] + [vp] * 9),

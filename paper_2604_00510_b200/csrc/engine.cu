@@ -1,0 +1,1701 @@
+// engine.cu — B200-native (sm_100a) engine for the data-parallel core of the
+// adaptive parallel MCTS of arXiv 2604.00510 (reference: /root/reference/pkg,
+// "treeserve").  One warp owns one search; thousands of searches advance one
+// wave per step.  See DESIGN.md for layout, kernels and rooflines.
+//
+// Numerics: compiled with -fmad=false; every floating-point expression keeps
+// the reference's evaluation order, so results are
+// bit-identical to the CPU reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/treeserve_b200.h"
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ---- node meta word (one u32 per node) -------------------------------------
+constexpr uint32_t M_DEPTH = 0x3Fu;       // bits 0-5: depth (root 0, <= 32)
+constexpr int SH_REF = 6;                 // bits 6-10: step_ref (child index)
+constexpr uint32_t M_TERM = 1u << 11;     // is_terminal
+constexpr uint32_t M_FORCED = 1u << 12;   // force_terminated (tree.py:340-343)
+constexpr uint32_t M_KIDS = 1u << 13;     // has children
+constexpr int SH_NEXP = 16;               // bits 16-21: # expandable children
+constexpr uint32_t NEXP_ONE = 1u << SH_NEXP;
+constexpr uint64_t O_ONE = 1ull << 32;    // no word: N in low 32, O (in-flight) in high 32
+
+__host__ __device__ inline int meta_nexp(uint32_t m) { return (int)((m >> SH_NEXP) & 0x3Fu); }
+// _expandable (tree.py:175-181), maintained incrementally: a non-terminal
+// node is expandable iff it is a leaf or one of its children is.
+__host__ __device__ inline bool meta_expandable(uint32_t m) {
+  return !(m & M_TERM) && (!(m & M_KIDS) || meta_nexp(m) > 0);
+}
+
+enum { ST_PENDING = 0, ST_RUNNING = 1, ST_FINISHED = 2 };
+
+// Per-search state (SoA would split one warp's scalar reads over many lines;
+// a search's row is touched only by its owning warp and the scheduler).
+struct SearchState {
+  int32_t state, completed, launched, cancelled;
+  int32_t nodes, viable, best_term, exit_kind;
+  int32_t exit_step, admit_step, status, target;
+  int64_t tokens;
+  double best;      // best trajectory score, valid iff best_term >= 0
+  double job_best;  // Job.best_score (scheduler.py:71, refreshed by on_rollout_complete)
+  unsigned long long t_exit;  // %globaltimer at the exit decision
+};
+
+struct Counters {
+  long long running, head, finished, last_exit_step;
+  long long admit_lo, admit_hi;
+  int work_count, work_next;
+  int sum_fallbacks, sched_error;
+  unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
+};
+
+// Kernel-side view of one engine.
+struct View {
+  // SoA node pool; search s owns nodes [s*cap, (s+1)*cap), ids in creation order
+  uint64_t* no;      // N | O << 32
+  double* W;         // value_sum
+  double* prior;
+  double* reward;    // prm_reward
+  int32_t* fc;       // first child (children are contiguous), -1 for leaves
+  int32_t* parent;
+  uint32_t* meta;
+  long long cap;
+  SearchState* st;
+  const ts_problem* prob;
+  const int32_t* arrival;  // local arrival steps (non-decreasing)
+  Counters* ctr;
+  int32_t* work;           // this wave's running local searches
+  int32_t* sp;             // scratch paths of a multi-rollout wave [n_local][budget][32]
+  double* ss;              // scratch scores
+  int32_t* sl;             // scratch lengths
+  const double* log1p_tab; // log1p(k) computed by the host libm, k < log1p_n
+  int32_t log1p_n;
+  int32_t n_local, goff, n_global;
+  unsigned long long* step_times;
+  int32_t step_times_cap;
+  // targets-kernel scratch (global fallback when runs exceed shared memory)
+  double* g_runS;
+  int32_t* g_runStart;
+  long long* g_runWant;
+  long long* g_runPW;
+  ts_config cfg;
+};
+
+// ---- rng.py ------------------------------------------------------------------
+// _splitmix64 (rng.py:15-19)
+__host__ __device__ __forceinline__ uint64_t sm64(uint64_t x) {
+  x = x + 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+constexpr uint64_t MIX_INIT = 0x8E12F5A34C29D96Bull;  // mix() initial state (rng.py:24)
+// uniform (rng.py:30-32): top 53 bits scaled by 2^-53 (exact)
+__host__ __device__ __forceinline__ double u53(uint64_t h) { return (double)(h >> 11) * 0x1p-53; }
+
+// ---- aggregate_trajectory (scoring.py:106-116), incremental along a path ----
+struct Agg {
+  double a, c;
+  int n;
+  __device__ __forceinline__ void init() { a = 1.0; c = 0.0; n = 0; }
+  __device__ __forceinline__ void add(double r, int scheme) {
+    if (scheme == TS_SCHEME_PRODUCT) {
+      a = a * r;  // math.prod: 1 * r0 * r1 ... left to right
+    } else if (scheme == TS_SCHEME_MINIMUM) {
+      a = (n == 0 || r < a) ? r : a;
+    } else if (n == 0) {  // builtin sum(): 0 + r0, then Neumaier (CPython >= 3.12)
+      a = r;
+      c = 0.0;
+    } else {
+      double t = a + r;
+      if (fabs(a) >= fabs(r)) c += (a - t) + r;
+      else c += (r - t) + a;
+      a = t;
+    }
+    ++n;
+  }
+  // prefix aggregate of the path extended by one more reward (prunable schemes)
+  __device__ __forceinline__ double peek(double r, int scheme) const {
+    if (scheme == TS_SCHEME_PRODUCT) return a * r;
+    return (n == 0 || r < a) ? r : a;
+  }
+  __device__ __forceinline__ double value(int scheme) const {
+    if (scheme == TS_SCHEME_PRODUCT || scheme == TS_SCHEME_MINIMUM) return a;
+    double s = a;
+    if (c != 0.0 && isfinite(c)) s += c;
+    if (scheme == TS_SCHEME_SUM) return s;
+    return s / (double)n;
+  }
+};
+
+// ---- warp helpers ------------------------------------------------------------
+// argmax with strict '>' and the lowest index winning ties (tree.py:258, 316);
+// lanes >= wp2 (a power of two >= width) must be invalid.
+__device__ __forceinline__ int warp_argmax(double v, bool valid, int wp2) {
+  int idx = valid ? (int)(threadIdx.x & 31) : 64;
+  for (int off = 1; off < wp2; off <<= 1) {
+    double ov = __shfl_xor_sync(FULL, v, off);
+    int oi = __shfl_xor_sync(FULL, idx, off);
+    bool take = (oi < 64) && (idx >= 64 || ov > v || (ov == v && oi < idx));
+    if (take) { v = ov; idx = oi; }
+  }
+  return __shfl_sync(FULL, idx, 0);
+}
+
+// Running splitmix64 folds: for every expansion depth d a rollout can reach,
+// the lanes hold fold(seed, TAG, len, path[0:depth]) for the four key tags of
+// generate_steps (backend.py:230-269): prior (2, d), reward (1, d+1), tokens
+// (3, d+1), extend (6, d+1).  Each descent step absorbs the chosen step_ref
+// into all of them in parallel, so an expansion at depth d costs O(1) hashes
+// on the critical path instead of the reference's O(d) fold per draw.
+// NSLOT states per lane; 4 tags x (8*NSLOT) depths = 32*NSLOT states.
+template <int NSLOT>
+__device__ __forceinline__ void slot_header(int lane, int k, uint64_t& tag, uint64_t& len) {
+  constexpr int GS = 8 * NSLOT;
+  const int g = lane / GS, d = lane % GS;
+  const int t = g * NSLOT + k;
+  tag = t == 0 ? 2u : t == 1 ? 1u : t == 2 ? 3u : 6u;
+  len = (uint64_t)(t == 0 ? d : d + 1);
+}
+template <int NSLOT, int T>
+__device__ __forceinline__ uint64_t state_at(const uint64_t (&h)[NSLOT], int d) {
+  constexpr int GS = 8 * NSLOT;
+  return __shfl_sync(FULL, h[T % NSLOT], (T / NSLOT) * GS + d);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---- kernels -------------------------------------------------------------------
+
+// SearchTree.__init__ (tree.py:120-128): bare root, reward 1.0, prior 1.0.
+__global__ void k_init(View v) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= v.n_local) return;
+  size_t r = (size_t)s * (size_t)v.cap;
+  v.no[r] = 0;
+  v.W[r] = 0.0;
+  v.prior[r] = 1.0;
+  v.reward[r] = 1.0;
+  v.fc[r] = -1;
+  v.parent[r] = -1;
+  v.meta[r] = 0;
+  SearchState z;
+  z.state = ST_PENDING;
+  z.completed = z.launched = z.cancelled = 0;
+  z.nodes = 1;
+  z.viable = 0;
+  z.best_term = -1;
+  z.exit_kind = TS_EXIT_NONE;
+  z.exit_step = -1;
+  z.admit_step = -1;
+  z.status = TS_OK;
+  z.target = 0;
+  z.tokens = 0;
+  z.best = 0.0;
+  z.job_best = 0.0;
+  z.t_exit = 0;
+  v.st[s] = z;
+}
+
+__global__ void k_reset_counters(Counters* c) {
+  memset(c, 0, sizeof(Counters));
+  c->last_exit_step = -1;
+}
+
+// Local counts before admission: {running, arrived-but-pending, unfinished}.
+__global__ void k_counts(View v, int step, long long* out) {
+  // arrivals are non-decreasing: upper_bound(arrival, step)
+  int lo = 0, hi = v.n_local;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (v.arrival[mid] <= step) lo = mid + 1;
+    else hi = mid;
+  }
+  Counters* c = v.ctr;
+  out[0] = c->running;
+  out[1] = (long long)lo - c->head;
+  out[2] = (long long)v.n_local - c->finished;
+}
+
+// admit_jobs (scheduler.py:131-140): one FIFO over the global run queue.
+__global__ void k_admit(View v, const long long* all, int world, int rank) {
+  long long run_g = 0, pend_g = 0, before = 0;
+  for (int r = 0; r < world; ++r) {
+    run_g += all[3 * r];
+    pend_g += all[3 * r + 1];
+    if (r < rank) before += all[3 * r + 1];
+  }
+  long long A = (long long)v.cfg.max_concurrency - run_g;
+  if (A > pend_g) A = pend_g;
+  if (A < 0) A = 0;
+  long long mine = all[3 * rank + 1];
+  long long q = A - before;
+  if (q > mine) q = mine;
+  if (q < 0) q = 0;
+  Counters* c = v.ctr;
+  c->admit_lo = c->head;
+  c->admit_hi = c->head + q;
+  c->head += q;
+  c->running += q;
+}
+
+// parallelism_score (scheduler.py:118-128) → one record per local search.
+__global__ void k_records(View v, int step, ts_sched_record* rec) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.n_local) return;
+  SearchState* s = v.st + i;
+  const Counters* c = v.ctr;
+  int state = s->state;
+  if (i >= c->admit_lo && i < c->admit_hi) {
+    state = ST_RUNNING;
+    s->state = ST_RUNNING;
+    s->admit_step = step;
+  }
+  ts_sched_record r;
+  r.score = 0.0;
+  r.flags = 0;
+  r._pad = 0;
+  if (state == ST_RUNNING) {
+    const ts_config& cf = v.cfg;
+    int waited = step - v.arrival[i];
+    double ratio = s->job_best / cf.positive_exit_threshold;
+    double boost = ratio > cf.proximity ? cf.beta : 0.0;
+    r.score = v.log1p_tab[waited] + boost;
+    r.flags = 1u | (s->completed >= cf.obs_threshold ? 2u : 0u) | (ratio > cf.proximity ? 4u : 0u);
+  }
+  rec[i] = r;
+}
+
+// ---- compute_targets (scheduler.py:143-187) in one CTA ------------------------
+constexpr int TT = 1024;
+constexpr int RUNCAP = 1536;  // runs per list kept in shared memory
+
+typedef unsigned __int128 u128;
+
+// Exact fixed-point image of a score (LSB 2^-64).  Returns false when the
+// score has bits below 2^-64 (then the sum falls back to the sequential loop).
+__device__ __forceinline__ bool to_fixed(double x, u128& out) {
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  int ex = (int)((b >> 52) & 0x7FF);
+  uint64_t m = b & ((1ull << 52) - 1);
+  if (ex == 0) {
+    out = 0;
+    return m == 0;
+  }
+  m |= 1ull << 52;
+  int sh = ex - 1075 + 64;  // value = m * 2^(ex-1075) = (m << sh) * 2^-64
+  if (sh < 0 || sh > 74) return false;
+  out = (u128)m << sh;
+  return true;
+}
+// Round-to-nearest-even of fixed-point value × 2^-64.
+__device__ double fixed_to_double(u128 v) {
+  if (v == 0) return 0.0;
+  uint64_t hi = (uint64_t)(v >> 64), lo = (uint64_t)v;
+  int p = hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
+  if (p <= 52) return (double)lo * 0x1p-64;
+  int sh = p - 52;
+  uint64_t mant = (uint64_t)(v >> sh);
+  u128 rem = v & (((u128)1 << sh) - 1);
+  u128 half = (u128)1 << (sh - 1);
+  if (rem > half || (rem == half && (mant & 1))) {
+    ++mant;
+    if (mant == (1ull << 53)) { mant >>= 1; ++sh; }
+  }
+  return ldexp((double)mant, sh - 64);
+}
+
+// Block-wide exclusive scan (+) of one value per thread; returns the prefix,
+// writes the block total.  All threads must call.
+__device__ long long block_scan_add(long long x, long long* total, long long* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) sh[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    long long w = sh[lane];
+    long long wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(FULL, wi, o);
+      if (lane >= o) wi += y;
+    }
+    sh[32 + lane] = wi - w;
+    if (lane == 31) sh[64] = wi;
+  }
+  __syncthreads();
+  long long res = sh[32 + wid] + incl - x;
+  if (total) *total = sh[64];
+  __syncthreads();
+  return res;
+}
+// Exclusive min-scan of doubles (identity +inf).
+__device__ double block_scan_min(double x, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl = fmin(incl, y);
+  }
+  double excl = __shfl_up_sync(FULL, incl, 1);
+  if (lane == 0) excl = INFINITY;
+  if (lane == 31) sh[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    double w = sh[lane];
+    double wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      double y = __shfl_up_sync(FULL, wi, o);
+      if (lane >= o) wi = fmin(wi, y);
+    }
+    double we = __shfl_up_sync(FULL, wi, 1);
+    if (lane == 0) we = INFINITY;
+    sh[32 + lane] = we;
+  }
+  __syncthreads();
+  double res = fmin(sh[32 + wid], excl);
+  __syncthreads();
+  return res;
+}
+
+// First run (runs strictly decreasing in S) with runS <= s.
+__device__ __forceinline__ int runs_lower(const double* runS, int nr, double s) {
+  int lo = 0, hi = nr;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (runS[mid] > s) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// compute_targets over the global run queue (records in global id order).
+// The reference sorts ungated jobs by (-S, arrival, id).  Because arrivals
+// are non-decreasing in run-queue order and S = log1p(now - arrival) + boost,
+// the unboosted and the boosted jobs each form a list already sorted by
+// (-S, id) in run-queue order; the sorted order is their merge.  Within a
+// list, equal scores form runs with one `want` each; a job's sorted position
+// and the Σ(want-1) before it follow from run prefix sums plus a binary
+// search in the other list.  The clamp loop (scheduler.py:169-180) then has
+// the closed form extra_k = clamp(R - Σ_{j<k}(want_j-1), 0, want_k-1), and the
+// round-robin leftover gives floor(R'/U) + [pos < R' mod U] (181-186).
+// The score sum Σ S (scheduler.py:165, CPython's Neumaier sum) equals the
+// correctly rounded exact sum when all compensation terms are exact (checked
+// below); it is computed exactly in 128-bit fixed point.
+__global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  long long* shl = (long long*)smem;                 // 80 long longs of scan scratch
+  double* shd = (double*)(smem + 80 * 8);            // 80 doubles
+  u128* shq = (u128*)(smem + 160 * 8);               // 32 u128
+  double* s_runS = (double*)(smem + 160 * 8 + 32 * 16);
+  int32_t* s_runStart = (int32_t*)(s_runS + 2 * RUNCAP);
+  long long* s_runWant = (long long*)(s_runStart + 2 * RUNCAP);
+  long long* s_runPW = s_runWant + 2 * RUNCAP;
+  __shared__ double sT;
+  __shared__ int sBad;
+
+  const int tid = threadIdx.x;
+  const ts_config& cf = v.cfg;
+  if (tid == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
+  const int n = v.n_global;
+  const int per = (n + TT - 1) / TT;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  const int glo = v.goff, ghi = v.goff + v.n_local;
+
+  // phase 1: counts, exact score sum, list positions
+  u128 fx = 0;
+  bool bad = false;
+  long long nrun = 0, cnt0 = 0, cnt1 = 0, nloc = 0;
+  double min0 = INFINITY, min1 = INFINITY;
+  for (int i = lo; i < hi; ++i) {
+    ts_sched_record r = rec[i];
+    if (!(r.flags & 1u)) continue;
+    ++nrun;
+    if (i >= glo && i < ghi) ++nloc;
+    u128 q;
+    if (to_fixed(r.score, q)) fx += q;
+    else bad = true;
+    if (r.flags & 2u) {
+      if (r.flags & 4u) { ++cnt1; min1 = fmin(min1, r.score); }
+      else { ++cnt0; min0 = fmin(min0, r.score); }
+    }
+  }
+  long long tot_run, len0, len1, tot_loc;
+  block_scan_add(nrun, &tot_run, shl);
+  long long pos0 = block_scan_add(cnt0, &len0, shl);
+  long long pos1 = block_scan_add(cnt1, &len1, shl);
+  long long wpos = block_scan_add(nloc, &tot_loc, shl);
+  // u128 reduction
+  {
+    const int lane = tid & 31, wid = tid >> 5;
+    u128 x = fx;
+    for (int o = 16; o > 0; o >>= 1) {
+      uint64_t h = __shfl_down_sync(FULL, (uint64_t)(x >> 64), o);
+      uint64_t l = __shfl_down_sync(FULL, (uint64_t)x, o);
+      x += ((u128)h << 64) | l;
+    }
+    if (lane == 0) shq[wid] = x;
+    if (tid == 0) sBad = 0;
+    __syncthreads();
+    if (bad) sBad = 1;
+    __syncthreads();
+    if (tid == 0) {
+      u128 s = 0;
+      for (int w = 0; w < TT / 32; ++w) s += shq[w];
+      double T;
+      bool fallback = sBad != 0;
+      if (!fallback) {
+        T = fixed_to_double(s);
+        // compensation exactness: n * ulp(2T) < 2^-10
+        double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
+        if ((double)tot_run * u2 >= 0x1p-10) fallback = true;
+      }
+      if (fallback) {  // sequential Neumaier sum in run-queue order
+        double f = 0.0, c = 0.0;
+        bool first = true;
+        for (int i = 0; i < n; ++i) {
+          ts_sched_record r = rec[i];
+          if (!(r.flags & 1u)) continue;
+          double x2 = r.score;
+          if (first) { f = x2; first = false; continue; }
+          double t = f + x2;
+          if (fabs(f) >= fabs(x2)) c += (f - t) + x2;
+          else c += (x2 - t) + f;
+          f = t;
+        }
+        if (c != 0.0 && isfinite(c)) f += c;
+        T = f;
+        atomicAdd(&v.ctr->sum_fallbacks, 1);
+      }
+      sT = T;
+    }
+    __syncthreads();
+  }
+  const double T = sT;
+  const bool boost_on = cf.boosting_enabled != 0 && tot_run > 0;
+  const long long M = cf.max_concurrency;
+  const long long R = M - tot_run;
+
+  // phase 2: runs of equal score in each list (lists are non-increasing)
+  double prev0 = block_scan_min(min0, shd);
+  double prev1 = block_scan_min(min1, shd);
+  long long rs0 = 0, rs1 = 0;
+  if (boost_on) {
+    double p0 = prev0, p1 = prev1;
+    for (int i = lo; i < hi; ++i) {
+      ts_sched_record r = rec[i];
+      if ((r.flags & 3u) != 3u) continue;
+      if (r.flags & 4u) { if (r.score != p1) ++rs1; if (r.score > p1) v.ctr->sched_error = 1; p1 = r.score; }
+      else { if (r.score != p0) ++rs0; if (r.score > p0) v.ctr->sched_error = 1; p0 = r.score; }
+    }
+  }
+  long long nr0, nr1;
+  long long rid0 = block_scan_add(rs0, &nr0, shl);
+  long long rid1 = block_scan_add(rs1, &nr1, shl);
+  const bool in_smem = nr0 <= RUNCAP && nr1 <= RUNCAP;
+  double* runS = in_smem ? s_runS : v.g_runS;
+  int32_t* runStart = in_smem ? s_runStart : v.g_runStart;
+  long long* runWant = in_smem ? s_runWant : v.g_runWant;
+  long long* runPW = in_smem ? s_runPW : v.g_runPW;
+  const int stride = in_smem ? RUNCAP : v.n_global;  // list 1 offset
+  if (boost_on) {
+    double p0 = prev0, p1 = prev1;
+    long long q0 = pos0, q1 = pos1, k0 = rid0, k1 = rid1;
+    for (int i = lo; i < hi; ++i) {
+      ts_sched_record r = rec[i];
+      if ((r.flags & 3u) != 3u) continue;
+      if (r.flags & 4u) {
+        if (r.score != p1) { runS[stride + k1] = r.score; runStart[stride + k1] = (int)q1; ++k1; }
+        p1 = r.score;
+        ++q1;
+      } else {
+        if (r.score != p0) { runS[k0] = r.score; runStart[k0] = (int)q0; ++k0; }
+        p0 = r.score;
+        ++q0;
+      }
+    }
+  }
+  __syncthreads();
+  // phase 3: want per run, prefix Σ cnt*(want-1) over runs
+  long long tw0 = 0, tw1 = 0;
+  for (int b = 0; b < 2 && boost_on; ++b) {
+    const long long nr = b ? nr1 : nr0;
+    const long long len = b ? len1 : len0;
+    const int off = b ? stride : 0;
+    const int per2 = (int)((nr + TT - 1) / TT);
+    const int a0 = (int)min((long long)tid * per2, nr), a1 = (int)min((long long)a0 + per2, nr);
+    long long loc = 0;
+    for (int k = a0; k < a1; ++k) {
+      double s = runS[off + k];
+      long long want = 1;
+      if (T > 0.0) {
+        double f = floor(s / T * (double)M);
+        want = f > 1.0 ? (long long)f : 1;
+      }
+      long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
+      runWant[off + k] = want;
+      loc += cnt * (want - 1);
+    }
+    long long tw;
+    long long pre = block_scan_add(loc, &tw, shl);
+    for (int k = a0; k < a1; ++k) {
+      runPW[off + k] = pre;
+      long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
+      pre += cnt * (runWant[off + k] - 1);
+    }
+    if (b) tw1 = tw; else tw0 = tw;
+  }
+  __syncthreads();
+  // phase 4: targets
+  const long long U = len0 + len1;
+  long long Rp = R - (tw0 + tw1);
+  if (Rp < 0) Rp = 0;
+  {
+    long long q0 = pos0, q1 = pos1, k0 = rid0 - 1, k1 = rid1 - 1, w = wpos;
+    double p0 = prev0, p1 = prev1;
+    for (int i = lo; i < hi; ++i) {
+      ts_sched_record r = rec[i];
+      if (!(r.flags & 1u)) {
+        if (i >= glo && i < ghi) v.st[i - glo].target = 0;
+        continue;
+      }
+      long long tgt = 1;
+      if ((r.flags & 2u) && boost_on) {
+        const int b = (r.flags & 4u) ? 1 : 0;
+        long long pos, k;
+        if (b) { if (r.score != p1) ++k1; p1 = r.score; pos = q1++; k = k1; }
+        else { if (r.score != p0) ++k0; p0 = r.score; pos = q0++; k = k0; }
+        const int off = b ? stride : 0, oo = b ? 0 : stride;
+        const long long want = runWant[off + k];
+        long long before = runPW[off + k] + (pos - runStart[off + k]) * (want - 1);
+        // cross list: elements with S' > S, or S' == S and smaller id
+        const long long nro = b ? nr0 : nr1, leno = b ? len0 : len1, two = b ? tw0 : tw1;
+        const long long obefore = b ? q0 : q1;  // other-list elements with id < i
+        int kk = runs_lower(runS + oo, (int)nro, r.score);
+        long long c, cw;
+        if (kk < nro && runS[oo + kk] == r.score) {
+          long long st0 = runStart[oo + kk];
+          long long cntk = (kk + 1 < nro ? runStart[oo + kk + 1] : leno) - st0;
+          long long part = obefore - st0;
+          if (part < 0) part = 0;
+          if (part > cntk) part = cntk;
+          c = st0 + part;
+          cw = runPW[oo + kk] + part * (runWant[oo + kk] - 1);
+        } else if (kk < nro) {
+          c = runStart[oo + kk];
+          cw = runPW[oo + kk];
+        } else {
+          c = leno;
+          cw = two;
+        }
+        const long long spos = pos + c;
+        before += cw;
+        long long extra = R - before;
+        if (extra < 0) extra = 0;
+        if (extra > want - 1) extra = want - 1;
+        long long rr = 0;
+        if (U > 0) rr = Rp / U + (spos < Rp % U ? 1 : 0);
+        tgt = 1 + extra + rr;
+      } else if ((r.flags & 2u) == 0 && boost_on) {
+        // gated: stays serial; advance nothing
+      }
+      if (i >= glo && i < ghi) {
+        v.st[i - glo].target = (int)tgt;
+        v.work[w++] = i - glo;
+      }
+    }
+  }
+  if (tid == 0) {
+    v.ctr->work_count = (int)tot_loc;
+    v.ctr->work_next = 0;
+  }
+}
+
+// ---- the wave: one warp per running search ----------------------------------
+struct WaveStats {
+  unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
+};
+
+template <int NSLOT>
+__device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
+  const int lane = threadIdx.x & 31;
+  const ts_config& cf = v.cfg;
+  SearchState* S = v.st + s;
+  const ts_problem* pb = v.prob + s;
+  const size_t base = (size_t)s * (size_t)v.cap;
+  uint64_t* NO = v.no + base;
+  double* Wv = v.W + base;
+  double* PR = v.prior + base;
+  double* RW = v.reward + base;
+  int32_t* FC = v.fc + base;
+  int32_t* PA = v.parent + base;
+  uint32_t* ME = v.meta + base;
+
+  const uint64_t seed = pb->seed;
+  const int bdepth = pb->base_depth;
+  const int glen = pb->golden_len;
+  const int hidden = pb->hidden_until_depth;
+  const bool has_shared = pb->has_shared != 0;
+  const double off_lo = pb->off_lo, off_hi = pb->off_hi;
+  const double sh_lo = pb->shared_lo, sh_hi = pb->shared_hi;
+  const int width = min(cf.expand_width, pb->branching);
+  int wp2 = 1;
+  while (wp2 < width) wp2 <<= 1;
+  const int scheme = cf.scheme;
+  const bool strict = cf.strict_negative_exit != 0;
+  const bool prefix_bound = cf.futility_bound == TS_BOUND_PREFIX_AGGREGATE;
+  const double tau = cf.accept_threshold, theta1 = cf.first_step_threshold;
+  // lane l holds golden_path[l] and its lifted reward
+  const int gstep = lane < glen ? (int)pb->golden_path[lane] : -1;
+  const double grew = lane < glen ? pb->golden_rewards[lane] : 0.0;
+
+  int completed = S->completed;
+  int nnodes = S->nodes;
+  int viable = S->viable;
+  int best_term = S->best_term;
+  double best = S->best;
+  long long tokens = S->tokens;
+  int launched = S->launched, cancelled = S->cancelled;
+  int status = TS_OK;
+  const int budget = cf.rollout_budget;
+  int count = min(S->target, budget - completed);
+  const bool multi = count > 1;
+  int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
+  double* SSs = v.ss + (size_t)s * budget;
+  int32_t* SLs = v.sl + (size_t)s * budget;
+
+  // root fold states fold(seed, tag, len) for this lane's slots
+  uint64_t root_h[NSLOT];
+  {
+    const uint64_t h0 = sm64(MIX_INIT ^ seed);
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+      uint64_t tag, len;
+      slot_header<NSLOT>(lane, k, tag, len);
+      root_h[k] = sm64(sm64(h0 ^ tag) ^ len);
+    }
+  }
+  uint32_t root_meta = ME[0];
+  int decision = TS_EXIT_NONE;
+  int nl = 0;
+  // last rollout kept in registers (the P=1 fast path never touches scratch)
+  int pnode = -1, plen = 0;
+  double pscore = 0.0;
+  unsigned long long scored = 0, levels = 0, created = 0, pathn = 0;
+
+  for (int r = 0; r < count && status == TS_OK; ++r) {
+    if (!meta_expandable(root_meta)) {  // NoExpandableLeafError (tree.py:273-274)
+      if (r == 0) decision = -1;        // exhausted: decide below
+      break;
+    }
+    uint64_t h[NSLOT];
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) h[k] = root_h[k];
+    int node = 0, depth = 0;
+    uint32_t nmeta = root_meta;
+    double nrew = 1.0;
+    pnode = -1;
+    uint32_t pmeta = 0;  // lane l: meta of path[l+1] (register copy, sole writer)
+    Agg agg;
+    agg.init();
+    bool golden = glen >= 0;
+    double d1r = 1.0;
+
+    // --- select_leaf (tree.py:264-284) ---
+    while (nmeta & M_KIDS) {
+      const int fc = FC[node];
+      const uint64_t pno = NO[node];
+      const double pW = Wv[node];
+      const long long pN = (long long)(uint32_t)pno, pO = (long long)(pno >> 32);
+      bool valid = lane < width;
+      double sc = -INFINITY, cr = 0.0;
+      uint32_t cm = 0;
+      if (valid) {
+        const int c = fc + lane;
+        const uint64_t cno = NO[c];
+        const double cw = Wv[c];
+        const double cp = PR[c];
+        cm = ME[c];
+        cr = RW[c];
+        valid = meta_expandable(cm);
+        if (valid) {
+          const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
+          // _child_q (tree.py:235-239)
+          double q = cN == 0 ? (pN == 0 ? 0.5 : pW / (double)pN) : cw / (double)cN;
+          if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
+          // wu_puct_score (tree.py:232): q + c*P*sqrt(N_s+O_s)/(1+N_sa+O_sa)
+          sc = q + cf.c_puct * cp * sqrt((double)(pN + pO)) / (double)(1 + cN + cO);
+        }
+      }
+      const unsigned vb = __ballot_sync(FULL, valid);
+      if (__any_sync(FULL, status != TS_OK)) { status = TS_INVALID_ARGUMENT; break; }
+      if (!vb) { status = TS_EXHAUSTED; break; }
+      scored += __popc(vb);
+      ++levels;
+      const int j = warp_argmax(sc, valid, wp2);
+      node = fc + j;
+      ++depth;
+      nmeta = __shfl_sync(FULL, cm, j);
+      nrew = __shfl_sync(FULL, cr, j);
+      if (lane == depth - 1) { pnode = node; pmeta = nmeta; }
+      agg.add(nrew, scheme);
+      if (depth == 1) d1r = nrew;
+      golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
+#pragma unroll
+      for (int k = 0; k < NSLOT; ++k) h[k] = sm64(h[k] ^ (uint64_t)j);
+    }
+    if (status != TS_OK) break;
+
+    // --- simulate_to_terminal (tree.py:322-349) ---
+    while (!(nmeta & M_TERM)) {
+      int fc;
+      double cr = 0.0;
+      uint32_t cm = 0;
+      bool became_dead = false;  // node turned non-expandable
+      if (!(nmeta & M_KIDS)) {
+        // NE bookkeeping: this non-terminal leaf stops being a leaf
+        bool counted = false;
+        if (depth >= 1) {
+          const bool rel = strict || d1r >= theta1;
+          const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
+          counted = rel && !(bound < tau);
+        }
+        if (depth >= cf.depth_cap) {  // depth cap → force terminal (tree.py:340-343)
+          nmeta |= M_TERM | M_FORCED;
+          if (lane == 0) ME[node] = nmeta;
+          if (depth == 0) root_meta = nmeta;
+          else if (lane == depth - 1) pmeta = nmeta;
+          if (counted) --viable;
+          became_dead = true;
+        } else {
+          if (nnodes + width > v.cap) { status = TS_POOL_OVERFLOW; break; }
+          fc = nnodes;
+          nnodes += width;
+          const int d = depth;
+          // expand (tree.py:287-304) with generate_steps replayed (backend.py:230-269)
+          const uint64_t hp = state_at<NSLOT, 0>(h, d);
+          const uint64_t hr = state_at<NSLOT, 1>(h, d);
+          const uint64_t hk = state_at<NSLOT, 2>(h, d);
+          const uint64_t he = state_at<NSLOT, 3>(h, d);
+          const double graw = __shfl_sync(FULL, grew, d);
+          const int gnext = __shfl_sync(FULL, gstep, d);
+          const bool v_ = lane < width;
+          const uint64_t j64 = (uint64_t)lane;
+          const double raw = 0.5 + u53(sm64(hp ^ j64));
+          // total = sum(raw_priors): CPython Neumaier sum in child order
+          double tot = __shfl_sync(FULL, raw, 0), cc = 0.0;
+          for (int i = 1; i < width; ++i) {
+            const double x = __shfl_sync(FULL, raw, i);
+            const double t = tot + x;
+            if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
+            else cc += (x - t) + tot;
+            tot = t;
+          }
+          if (cc != 0.0 && isfinite(cc)) tot += cc;
+          const double pri = raw / tot;
+          const int len = d + 1;
+          const bool gchild = golden && len <= glen && lane == gnext;
+          double rew;
+          if (gchild) {
+            rew = graw;
+          } else {
+            const bool shr = has_shared && len <= hidden;
+            const double lo = shr ? sh_lo : off_lo, hi = shr ? sh_hi : off_hi;
+            rew = lo + (hi - lo) * u53(sm64(hr ^ j64));
+          }
+          const int tok = 40 + (int)(sm64(hk ^ j64) % 81ull);
+          bool term;
+          if (len < bdepth) term = false;
+          else if (len >= bdepth + 1) term = true;
+          else if (gchild) term = true;
+          else term = (sm64(he ^ j64) % 2ull) != 0;  // not _branch_extends
+          const uint32_t cmeta = (uint32_t)len | ((uint32_t)lane << SH_REF) | (term ? M_TERM : 0u);
+          if (v_) {
+            const int c = fc + lane;
+            NO[c] = 0;
+            Wv[c] = 0.0;
+            PR[c] = pri;
+            RW[c] = rew;
+            FC[c] = -1;
+            PA[c] = node;
+            ME[c] = cmeta;
+          }
+          int tsum = v_ ? tok : 0;
+          for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(FULL, tsum, o);
+          tokens += tsum;
+          const unsigned live = __ballot_sync(FULL, v_ && !term);
+          const int ne = __popc(live);
+          nmeta = nmeta | M_KIDS | ((uint32_t)ne << SH_NEXP);
+          if (lane == 0) {
+            FC[node] = fc;
+            ME[node] = nmeta;
+          }
+          if (depth == 0) root_meta = nmeta;
+          else if (lane == depth - 1) pmeta = nmeta;
+          // NE: new non-terminal leaves that are check-relevant and viable
+          bool cnt_child = false;
+          if (v_ && !term) {
+            const bool rel = strict || (len == 1 ? rew : d1r) >= theta1;
+            const double bound = prefix_bound ? fmin(rew, agg.peek(rew, scheme)) : rew;
+            cnt_child = rel && !(bound < tau);
+          }
+          viable += __popc(__ballot_sync(FULL, cnt_child)) - (counted ? 1 : 0);
+          created += width;
+          became_dead = ne == 0;
+          cr = rew;
+          cm = cmeta;
+        }
+      } else {
+        fc = FC[node];
+        if (lane < width) {
+          cr = RW[fc + lane];
+          cm = ME[fc + lane];
+        }
+      }
+      if (became_dead) {
+        // propagate "no expandable leaf below" up the path
+        for (int i = depth - 1; i >= 0; --i) {
+          uint32_t m = i == 0 ? root_meta : __shfl_sync(FULL, pmeta, i - 1);
+          const int pid = i == 0 ? 0 : __shfl_sync(FULL, pnode, i - 1);
+          m -= NEXP_ONE;
+          if (lane == 0) ME[pid] = m;
+          if (i == 0) root_meta = m;
+          else if (lane == i - 1) pmeta = m;
+          if (meta_nexp(m) > 0) break;
+        }
+        if (nmeta & M_TERM) break;  // forced terminal: rollout ends here
+      }
+      // greedy_child (tree.py:307-319)
+      const int j = warp_argmax(cr, lane < width, wp2);
+      node = fc + j;
+      ++depth;
+      nmeta = __shfl_sync(FULL, cm, j);
+      nrew = __shfl_sync(FULL, cr, j);
+      if (lane == depth - 1) { pnode = node; pmeta = nmeta; }
+      agg.add(nrew, scheme);
+      if (depth == 1) d1r = nrew;
+      golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
+#pragma unroll
+      for (int k = 0; k < NSLOT; ++k) h[k] = sm64(h[k] ^ (uint64_t)j);
+    }
+    if (status != TS_OK) break;
+    __syncwarp();
+    // in-flight registration of root..terminal (tree.py:282-283, 347-348)
+    if (lane < depth) NO[pnode] += O_ONE;
+    if (lane == 0) NO[0] += O_ONE;
+    plen = depth;
+    pscore = agg.value(scheme);
+    if (multi) {
+      SPs[(size_t)nl * 32 + lane] = pnode;
+      if (lane == 0) { SSs[nl] = pscore; SLs[nl] = plen; }
+    }
+    ++nl;
+    __syncwarp();
+  }
+
+  // --- finish_rollout → backpropagate (tree.py:352-371) → decide_exit in
+  //     launch order; cancel_inflight for the rest on exit ---
+  launched += nl;
+  bool exhausted = decision == -1;
+  if (exhausted) decision = TS_EXIT_NONE;
+  unsigned long long done = 0;
+  auto decide = [&](bool exh) -> int {
+    if (cf.positive_exit && best_term >= 0 && best >= cf.positive_exit_threshold) return TS_EXIT_POSITIVE;
+    if (cf.negative_exit && (root_meta & M_KIDS) && viable == 0) return TS_EXIT_NEGATIVE;
+    if (exh || completed >= budget) return TS_EXIT_BUDGET;
+    return TS_EXIT_NONE;
+  };
+  if (status == TS_OK && exhausted) decision = decide(true);
+  for (int r = 0; r < nl && status == TS_OK; ++r) {
+    int pn, len;
+    double sc;
+    if (multi) {
+      len = SLs[r];
+      sc = SSs[r];
+      pn = lane < len ? SPs[(size_t)r * 32 + lane] : -1;
+    } else {
+      len = plen;
+      sc = pscore;
+      pn = pnode;
+    }
+    if (completed >= budget) { status = TS_ACCOUNTING; break; }
+    bool bad = false;
+    if (lane < len) {
+      const uint64_t x = NO[pn];
+      if ((x >> 32) < 1) bad = true;
+      NO[pn] = x + 1 - O_ONE;
+      Wv[pn] += sc;
+    }
+    if (lane == 0) {
+      const uint64_t x = NO[0];
+      if ((x >> 32) < 1) bad = true;
+      NO[0] = x + 1 - O_ONE;
+      Wv[0] += sc;
+    }
+    if (__any_sync(FULL, bad)) { status = TS_ACCOUNTING; break; }
+    __syncwarp();
+    ++completed;
+    ++done;
+    pathn += len + 1;
+    if (best_term < 0 || sc > best) {
+      best = sc;
+      best_term = __shfl_sync(FULL, pn, len - 1);
+    }
+    decision = decide(false);
+    if (decision != TS_EXIT_NONE) {
+      for (int r2 = r + 1; r2 < nl; ++r2) {
+        const int len2 = SLs[r2];
+        const int pn2 = lane < len2 ? SPs[(size_t)r2 * 32 + lane] : -1;
+        bool bad2 = lane < len2 && (NO[pn2] >> 32) < 1;
+        if (lane == 0 && (NO[0] >> 32) < 1) bad2 = true;
+        if (__any_sync(FULL, bad2)) { status = TS_ACCOUNTING; break; }
+        if (lane < len2) NO[pn2] -= O_ONE;
+        if (lane == 0) NO[0] -= O_ONE;
+        __syncwarp();
+        ++cancelled;
+        pathn += len2 + 1;
+      }
+      break;
+    }
+  }
+
+  if (lane == 0) {
+    S->completed = completed;
+    S->nodes = nnodes;
+    S->viable = viable;
+    S->best_term = best_term;
+    S->best = best;
+    S->tokens = tokens;
+    S->launched = launched;
+    S->cancelled = cancelled;
+    // on_rollout_complete (scheduler.py:217-233): refresh Job.best_score
+    if (best_term >= 0 && best > S->job_best) S->job_best = best;
+    if (status != TS_OK || decision != TS_EXIT_NONE) {
+      S->state = ST_FINISHED;
+      S->exit_kind = status == TS_OK ? decision : TS_EXIT_NONE;
+      S->status = status;
+      S->exit_step = step;
+      S->t_exit = globaltimer();
+      atomicAdd((unsigned long long*)&v.ctr->running, (unsigned long long)-1ll);
+      atomicAdd((unsigned long long*)&v.ctr->finished, 1ull);
+      atomicMax(&v.ctr->last_exit_step, (long long)step);
+    }
+  }
+  ws.rollouts += done;
+  ws.launched += nl;
+  ws.nodes += created;
+  ws.tokens += 0;
+  ws.scored += scored;
+  ws.levels += levels;
+  ws.path_nodes += pathn;
+  ws.cancelled += 0;
+}
+
+constexpr int WAVE_THREADS = 128;
+
+template <int NSLOT>
+__global__ void __launch_bounds__(WAVE_THREADS) k_wave(View v, int step) {
+  const int lane = threadIdx.x & 31;
+  WaveStats ws = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int count = v.ctr->work_count;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(&v.ctr->work_next, 1);
+    item = __shfl_sync(FULL, item, 0);
+    if (item >= count) break;
+    search_wave<NSLOT>(v, v.work[item], step, ws);
+  }
+  if (lane == 0 && ws.launched) {
+    atomicAdd(&v.ctr->rollouts, ws.rollouts);
+    atomicAdd(&v.ctr->launched, ws.launched);
+    atomicAdd(&v.ctr->nodes, ws.nodes);
+    atomicAdd(&v.ctr->scored, ws.scored);
+    atomicAdd(&v.ctr->levels, ws.levels);
+    atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
+  }
+}
+
+__global__ void k_latency(View v, unsigned long long* out, int n) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const SearchState& st = v.st[s];
+  unsigned long long r = 0;
+  if (st.exit_step >= 0 && st.admit_step >= 0 && st.admit_step < v.step_times_cap) {
+    unsigned long long t0 = v.step_times[st.admit_step];
+    r = st.t_exit > t0 ? st.t_exit - t0 : 0;
+  }
+  out[s] = r;
+}
+
+// SearchOutcome (search.py:32-42): best path by parent walk, solved flag.
+__global__ void k_outcomes(View v, ts_outcome* out, int n) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const SearchState st = v.st[s];
+  const ts_problem* pb = v.prob + s;
+  ts_outcome o;
+  memset(&o, 0, sizeof(o));
+  o.exit_kind = st.exit_kind;
+  o.rollouts_completed = st.completed;
+  o.tokens_generated = st.tokens;
+  o.best_score = st.best_term >= 0 ? st.best : 0.0;
+  o.exit_step = st.exit_step;
+  o.admit_step = st.admit_step;
+  o.launched = st.launched;
+  o.cancelled = st.cancelled;
+  o.nodes = st.nodes;
+  o.status = st.status;
+  if (st.best_term >= 0) {
+    const size_t base = (size_t)s * (size_t)v.cap;
+    int ids[TS_MAX_DEPTH + 1];
+    int n2 = 0;
+    for (int c = st.best_term; c > 0 && n2 <= TS_MAX_DEPTH; c = v.parent[base + c]) ids[n2++] = c;
+    o.best_len = n2;
+    for (int i = 0; i < n2; ++i) o.best_path[i] = (uint8_t)((v.meta[base + ids[n2 - 1 - i]] >> SH_REF) & 31u);
+    if (pb->golden_len >= 0 && o.best_len == pb->golden_len) {
+      o.solved = 1;
+      for (int i = 0; i < n2; ++i)
+        if (o.best_path[i] != pb->golden_path[i]) o.solved = 0;
+    }
+  }
+  out[s] = o;
+}
+
+}  // namespace
+
+// ============================================================================
+// host side
+// ============================================================================
+struct ts_engine {
+  int device = 0;
+  ts_config cfg{};
+  std::string err;
+  int sm_count = 148;
+  int wave_blocks[3] = {0, 0, 0};
+  // sizes
+  int n_local = 0, goff = 0, n_global = 0, cap_searches = 0, cap_global = 0;
+  long long cap = 0, pool_nodes = 0;
+  int nslot = 4;
+  bool loaded = false;
+  // device buffers
+  uint64_t* no = nullptr;
+  double* W = nullptr;
+  double* prior = nullptr;
+  double* reward = nullptr;
+  int32_t* fc = nullptr;
+  int32_t* parent = nullptr;
+  uint32_t* meta = nullptr;
+  SearchState* st = nullptr;
+  ts_problem* prob = nullptr;
+  int32_t* arrival = nullptr;
+  Counters* ctr = nullptr;
+  int32_t* work = nullptr;
+  int32_t* sp = nullptr;
+  double* ss = nullptr;
+  int32_t* sl = nullptr;
+  size_t scratch_rows = 0;
+  double* log1p_tab = nullptr;
+  int log1p_n = 0;
+  unsigned long long* step_times = nullptr;
+  int step_times_cap = 0;
+  double* g_runS = nullptr;
+  int32_t* g_runStart = nullptr;
+  long long* g_runWant = nullptr;
+  long long* g_runPW = nullptr;
+  long long* counts = nullptr;      // 3
+  ts_sched_record* records = nullptr;
+  ts_outcome* outcomes = nullptr;
+  int outcomes_cap = 0;
+  std::vector<int32_t> h_arrival;
+  int max_arrival = 0;
+  long long launches = 0;
+  std::vector<cudaEvent_t> wave_ev;  // start/stop pairs of every wave since load
+  size_t wave_ev_used = 0;
+};
+
+namespace {
+
+int fail(ts_engine* e, int code, const std::string& msg) {
+  if (e) e->err = msg;
+  return code;
+}
+int cuda_fail(ts_engine* e, cudaError_t rc, const char* where) {
+  return fail(e, TS_CUDA, std::string(where) + ": " + cudaGetErrorString(rc));
+}
+#define TS_CUDA_TRY(e, expr)                                   \
+  do {                                                         \
+    cudaError_t rc_ = (expr);                                  \
+    if (rc_ != cudaSuccess) return cuda_fail((e), rc_, #expr); \
+  } while (0)
+#define TS_LAUNCH_CHECK(e, name)                                  \
+  do {                                                            \
+    ++(e)->launches;                                              \
+    cudaError_t rc_ = cudaGetLastError();                         \
+    if (rc_ != cudaSuccess) return cuda_fail((e), rc_, name);     \
+  } while (0)
+
+template <class T>
+int grow(ts_engine* e, T*& p, size_t n, size_t& have, const char* what) {
+  if (n <= have && p) return TS_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cudaError_t rc = cudaMalloc((void**)&p, std::max<size_t>(n, 1) * sizeof(T));
+  if (rc != cudaSuccess) {
+    have = 0;
+    return cuda_fail(e, rc, what);
+  }
+  have = n;
+  return TS_OK;
+}
+
+View make_view(ts_engine* e) {
+  View v;
+  v.no = e->no;
+  v.W = e->W;
+  v.prior = e->prior;
+  v.reward = e->reward;
+  v.fc = e->fc;
+  v.parent = e->parent;
+  v.meta = e->meta;
+  v.cap = e->cap;
+  v.st = e->st;
+  v.prob = e->prob;
+  v.arrival = e->arrival;
+  v.ctr = e->ctr;
+  v.work = e->work;
+  v.sp = e->sp;
+  v.ss = e->ss;
+  v.sl = e->sl;
+  v.log1p_tab = e->log1p_tab;
+  v.log1p_n = e->log1p_n;
+  v.n_local = e->n_local;
+  v.goff = e->goff;
+  v.n_global = e->n_global;
+  v.step_times = e->step_times;
+  v.step_times_cap = e->step_times_cap;
+  v.g_runS = e->g_runS;
+  v.g_runStart = e->g_runStart;
+  v.g_runWant = e->g_runWant;
+  v.g_runPW = e->g_runPW;
+  v.cfg = e->cfg;
+  return v;
+}
+
+size_t targets_smem() { return 160 * 8 + 32 * 16 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8); }
+
+// log1p(k) for k < n from the host libm (the reference calls math.log1p,
+// scheduler.py:128, which is the same C library function).
+int ensure_log1p(ts_engine* e, int need, cudaStream_t s) {
+  if (need <= e->log1p_n) return TS_OK;
+  int n = std::max(need, std::max(1024, e->log1p_n * 2));
+  std::vector<double> h((size_t)n);
+  for (int k = 0; k < n; ++k) h[k] = std::log1p((double)k);
+  double* p = nullptr;
+  TS_CUDA_TRY(e, cudaMalloc((void**)&p, sizeof(double) * n));
+  TS_CUDA_TRY(e, cudaMemcpyAsync(p, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  if (e->log1p_tab) cudaFree(e->log1p_tab);
+  e->log1p_tab = p;
+  e->log1p_n = n;
+  return TS_OK;
+}
+
+int ensure_step_times(ts_engine* e, int need, cudaStream_t s) {
+  if (need <= e->step_times_cap) return TS_OK;
+  int n = std::max(need, std::max(4096, e->step_times_cap * 2));
+  unsigned long long* p = nullptr;
+  TS_CUDA_TRY(e, cudaMalloc((void**)&p, sizeof(unsigned long long) * n));
+  TS_CUDA_TRY(e, cudaMemsetAsync(p, 0, sizeof(unsigned long long) * n, s));
+  if (e->step_times) {
+    TS_CUDA_TRY(e, cudaMemcpyAsync(p, e->step_times, sizeof(unsigned long long) * e->step_times_cap,
+                                   cudaMemcpyDeviceToDevice, s));
+    TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+    cudaFree(e->step_times);
+  }
+  e->step_times = p;
+  e->step_times_cap = n;
+  return TS_OK;
+}
+
+int validate_config(ts_engine* e, const ts_config& c) {
+  if (c.scheme < 0 || c.scheme > 3) return fail(e, TS_INVALID_ARGUMENT, "unknown aggregation scheme");
+  if (c.futility_bound < 0 || c.futility_bound > 1) return fail(e, TS_INVALID_ARGUMENT, "unknown futility bound");
+  // ScoringConfig.__post_init__ (scoring.py:93-103)
+  if (!(c.accept_threshold > 0.0 && c.accept_threshold < 1.0))
+    return fail(e, TS_INVALID_ARGUMENT, "accept_threshold out of (0,1)");
+  if (!(c.positive_exit_threshold > 0.0 && c.positive_exit_threshold < 1.0))
+    return fail(e, TS_INVALID_ARGUMENT, "positive_exit_threshold out of (0,1)");
+  if (!(c.first_step_threshold >= 0.0 && c.first_step_threshold < 1.0))
+    return fail(e, TS_INVALID_ARGUMENT, "first_step_threshold out of [0,1)");
+  // SelectionParams (tree.py:98-100)
+  if (!(c.c_puct > 0.0)) return fail(e, TS_INVALID_ARGUMENT, "c_puct must be positive");
+  // SchedulerConfig (scheduler.py:85-93)
+  if (c.max_concurrency < 1) return fail(e, TS_INVALID_ARGUMENT, "max_concurrency must be >= 1");
+  if (!(c.beta > 0.0)) return fail(e, TS_INVALID_ARGUMENT, "beta must be positive");
+  if (!(c.proximity > 0.0 && c.proximity < 1.0)) return fail(e, TS_INVALID_ARGUMENT, "proximity must lie in (0,1)");
+  if (c.obs_threshold < 1) return fail(e, TS_INVALID_ARGUMENT, "obs_threshold must be >= 1");
+  if (c.rollout_budget < 1) return fail(e, TS_INVALID_ARGUMENT, "rollout_budget must be positive");
+  if (c.depth_cap < 1) return fail(e, TS_INVALID_ARGUMENT, "depth_cap must be positive");
+  if (c.expand_width < 1) return fail(e, TS_INVALID_ARGUMENT, "width must be >= 1");
+  // classify_leaf (scoring.py:124-127), raised up front (simulator.py:106-110)
+  if (c.negative_exit && c.scheme != TS_SCHEME_MINIMUM && c.scheme != TS_SCHEME_PRODUCT)
+    return fail(e, TS_UNSUPPORTED_SCHEME, "negative exit is unsound under this aggregation scheme");
+  return TS_OK;
+}
+
+int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
+  int k = e->nslot == 1 ? 0 : e->nslot == 2 ? 1 : 2;
+  int blocks = e->wave_blocks[k];
+  if (blocks <= 0) {
+    int per = 0;
+    cudaError_t rc;
+    if (k == 0) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<1>, WAVE_THREADS, 0);
+    else if (k == 1) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<2>, WAVE_THREADS, 0);
+    else rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<4>, WAVE_THREADS, 0);
+    if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
+    blocks = std::max(1, per) * e->sm_count;
+    e->wave_blocks[k] = blocks;
+  }
+  // never more warps than searches
+  blocks = std::min(blocks, (e->n_local + WAVE_THREADS / 32 - 1) / (WAVE_THREADS / 32));
+  blocks = std::max(blocks, 1);
+  if (e->wave_ev_used + 2 > e->wave_ev.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t ev;
+      if (cudaEventCreate(&ev) != cudaSuccess) return fail(e, TS_CUDA, "cudaEventCreate");
+      e->wave_ev.push_back(ev);
+    }
+  }
+  cudaEventRecord(e->wave_ev[e->wave_ev_used], s);
+  if (k == 0) k_wave<1><<<blocks, WAVE_THREADS, 0, s>>>(v, step);
+  else if (k == 1) k_wave<2><<<blocks, WAVE_THREADS, 0, s>>>(v, step);
+  else k_wave<4><<<blocks, WAVE_THREADS, 0, s>>>(v, step);
+  TS_LAUNCH_CHECK(e, "k_wave");
+  cudaEventRecord(e->wave_ev[e->wave_ev_used + 1], s);
+  e->wave_ev_used += 2;
+  return TS_OK;
+}
+
+void host_stats(const Counters& c, ts_run_stats* o) {
+  o->steps = (int32_t)(c.last_exit_step + 1);
+  o->finished = (int32_t)c.finished;
+  o->rollouts = (int64_t)c.rollouts;
+  o->launched = (int64_t)c.launched;
+  o->nodes = (int64_t)c.nodes;
+  o->tokens = 0;
+  o->children_scored = (int64_t)c.scored;
+  o->select_levels = (int64_t)c.levels;
+  o->path_nodes = (int64_t)c.path_nodes;
+  o->kernel_launches = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ts_abi_version(void) { return TS_ABI_VERSION; }
+
+const char* ts_last_error(const ts_engine* eng) { return eng ? eng->err.c_str() : "null engine"; }
+
+int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
+  if (!cfg || !out) return TS_INVALID_ARGUMENT;
+  *out = nullptr;
+  ts_engine* e = new ts_engine();
+  int rc = validate_config(e, *cfg);
+  if (rc != TS_OK) {
+    // keep the engine so the caller can read the message, then destroy it
+    *out = e;
+    return rc;
+  }
+  e->cfg = *cfg;
+  e->device = device;
+  cudaError_t cr = cudaSetDevice(device);
+  if (cr != cudaSuccess) {
+    *out = e;
+    return cuda_fail(e, cr, "cudaSetDevice");
+  }
+  cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cr = cudaMalloc((void**)&e->ctr, sizeof(Counters));
+  if (cr == cudaSuccess) cr = cudaMalloc((void**)&e->counts, sizeof(long long) * 3);
+  if (cr == cudaSuccess)
+    cr = cudaFuncSetAttribute(k_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
+  if (cr != cudaSuccess) {
+    *out = e;
+    return cuda_fail(e, cr, "engine allocation");
+  }
+  *out = e;
+  return TS_OK;
+}
+
+int ts_engine_destroy(ts_engine* e) {
+  if (!e) return TS_OK;
+  void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->fc, e->parent, e->meta, e->st, e->prob,
+                  e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
+                  e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
+  delete e;
+  return TS_OK;
+}
+
+int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_t global_offset,
+                     int32_t n_global, void* stream) {
+  if (!e) return TS_INVALID_ARGUMENT;
+  if (!hp || n_local < 1) return fail(e, TS_INVALID_ARGUMENT, "need at least one problem");
+  if (global_offset < 0 || n_global < global_offset + n_local)
+    return fail(e, TS_INVALID_ARGUMENT, "bad shard placement");
+  cudaStream_t s = (cudaStream_t)stream;
+  TS_CUDA_TRY(e, cudaSetDevice(e->device));
+  const ts_config& c = e->cfg;
+  int max_len = 1, max_width = 1, prev_arr = 0;
+  e->h_arrival.resize(n_local);
+  for (int i = 0; i < n_local; ++i) {
+    const ts_problem& p = hp[i];
+    if (p.branching < 1 || p.branching > TS_MAX_WIDTH)
+      return fail(e, TS_INVALID_ARGUMENT, "branching must lie in [1, 32]");
+    if (p.base_depth < 1 || p.base_depth > TS_MAX_DEPTH - 1)
+      return fail(e, TS_INVALID_ARGUMENT, "base_depth must lie in [1, 31]");
+    if (p.golden_len > p.base_depth) return fail(e, TS_INVALID_ARGUMENT, "golden path longer than base depth");
+    if (p.arrival_step < 0 || p.arrival_step < prev_arr)
+      return fail(e, TS_INVALID_ARGUMENT, "arrival steps must be non-negative and non-decreasing");
+    prev_arr = p.arrival_step;
+    e->h_arrival[i] = p.arrival_step;
+    max_len = std::max(max_len, std::min(c.depth_cap, p.base_depth + 1));
+    max_width = std::max(max_width, std::min(c.expand_width, p.branching));
+  }
+  e->max_arrival = prev_arr;
+  e->nslot = max_len <= 8 ? 1 : max_len <= 16 ? 2 : 4;
+  // nodes a search can create: every launched rollout (<= budget) expands at
+  // most min(depth_cap, base_depth+1) levels of `width` children
+  const long long cap = 1 + (long long)c.rollout_budget * max_width * max_len;
+  size_t have;
+  int rc;
+  const size_t pool = (size_t)cap * (size_t)n_local;
+  if (pool > (size_t)e->pool_nodes || !e->no) {
+    void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->fc, e->parent, e->meta};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    e->no = nullptr; e->W = nullptr; e->prior = nullptr; e->reward = nullptr;
+    e->fc = nullptr; e->parent = nullptr; e->meta = nullptr;
+    e->pool_nodes = 0;
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->no, pool * 8));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->W, pool * 8));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->prior, pool * 8));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->reward, pool * 8));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->fc, pool * 4));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->parent, pool * 4));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->meta, pool * 4));
+    e->pool_nodes = (long long)pool;
+  }
+  e->cap = cap;
+  if (n_local > e->cap_searches || !e->st) {
+    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0;
+    if ((rc = grow(e, e->st, n_local, h0, "search state")) ||
+        (rc = grow(e, e->prob, n_local, h1, "problem table")) ||
+        (rc = grow(e, e->arrival, n_local, h2, "arrivals")) ||
+        (rc = grow(e, e->work, n_local, h3, "work list")) ||
+        (rc = grow(e, e->records, n_local, h4, "records")) ||
+        (rc = grow(e, e->outcomes, n_local, h5, "outcomes")))
+      return rc;
+    e->cap_searches = n_local;
+    e->outcomes_cap = n_local;
+  }
+  const size_t rows = (size_t)n_local * (size_t)c.rollout_budget;
+  if (rows > e->scratch_rows || !e->sp) {
+    if (e->sp) cudaFree(e->sp);
+    if (e->ss) cudaFree(e->ss);
+    if (e->sl) cudaFree(e->sl);
+    e->sp = nullptr; e->ss = nullptr; e->sl = nullptr;
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->sp, rows * 32 * 4));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->ss, rows * 8));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->sl, rows * 4));
+    e->scratch_rows = rows;
+  }
+  if (n_global > e->cap_global || !e->g_runS) {
+    size_t a = 0, b = 0, cc = 0, d = 0;
+    if ((rc = grow(e, e->g_runS, (size_t)2 * n_global, a, "runs")) ||
+        (rc = grow(e, e->g_runStart, (size_t)2 * n_global, b, "runs")) ||
+        (rc = grow(e, e->g_runWant, (size_t)2 * n_global, cc, "runs")) ||
+        (rc = grow(e, e->g_runPW, (size_t)2 * n_global, d, "runs")))
+      return rc;
+    e->cap_global = n_global;
+  }
+  e->n_local = n_local;
+  e->goff = global_offset;
+  e->n_global = n_global;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, hp, sizeof(ts_problem) * n_local, cudaMemcpyHostToDevice, s));
+  TS_CUDA_TRY(e, cudaMemcpyAsync(e->arrival, e->h_arrival.data(), sizeof(int32_t) * n_local,
+                                 cudaMemcpyHostToDevice, s));
+  if ((rc = ensure_log1p(e, 1024, s))) return rc;
+  if ((rc = ensure_step_times(e, 4096, s))) return rc;
+  View v = make_view(e);
+  e->launches = 0;
+  e->wave_ev_used = 0;
+  k_reset_counters<<<1, 1, 0, s>>>(e->ctr);
+  TS_LAUNCH_CHECK(e, "k_reset_counters");
+  k_init<<<(n_local + 255) / 256, 256, 0, s>>>(v);
+  TS_LAUNCH_CHECK(e, "k_init");
+  e->loaded = true;
+  (void)have;
+  return TS_OK;
+}
+
+int ts_step_counts(ts_engine* e, int32_t step, int64_t* dev_counts, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!dev_counts || step < 0) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  View v = make_view(e);
+  k_counts<<<1, 1, 0, (cudaStream_t)stream>>>(v, step, (long long*)dev_counts);
+  TS_LAUNCH_CHECK(e, "k_counts");
+  return TS_OK;
+}
+
+int ts_step_admit(ts_engine* e, int32_t step, const int64_t* dev_all_counts, int32_t world, int32_t rank,
+                  void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!dev_all_counts || world < 1 || rank < 0 || rank >= world || step < 0)
+    return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  View v = make_view(e);
+  k_admit<<<1, 1, 0, (cudaStream_t)stream>>>(v, (const long long*)dev_all_counts, world, rank);
+  TS_LAUNCH_CHECK(e, "k_admit");
+  return TS_OK;
+}
+
+int ts_step_records(ts_engine* e, int32_t step, ts_sched_record* dev_records, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!dev_records || step < 0) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure_log1p(e, step + 1, s))) return rc;
+  View v = make_view(e);
+  k_records<<<(e->n_local + 255) / 256, 256, 0, s>>>(v, step, dev_records);
+  TS_LAUNCH_CHECK(e, "k_records");
+  return TS_OK;
+}
+
+int ts_step_targets(ts_engine* e, int32_t step, const ts_sched_record* dev_all, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!dev_all || step < 0) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure_step_times(e, step + 1, s))) return rc;
+  View v = make_view(e);
+  k_targets<<<1, TT, targets_smem(), s>>>(v, step, dev_all);
+  TS_LAUNCH_CHECK(e, "k_targets");
+  return TS_OK;
+}
+
+int ts_step_wave(ts_engine* e, int32_t step, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  View v = make_view(e);
+  return launch_wave(e, v, step, (cudaStream_t)stream);
+}
+
+int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  const int check_every = 8;
+  long long host_counts[3];
+  int step = 0;
+  for (; step < max_steps; ++step) {
+    if ((rc = ts_step_counts(e, step, (int64_t*)e->counts, stream))) return rc;
+    if (step % check_every == 0 && step >= e->max_arrival) {
+      TS_CUDA_TRY(e, cudaMemcpyAsync(host_counts, e->counts, sizeof(host_counts), cudaMemcpyDeviceToHost, s));
+      TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+      if (host_counts[2] == 0) break;
+    }
+    if ((rc = ts_step_admit(e, step, (const int64_t*)e->counts, 1, 0, stream))) return rc;
+    if ((rc = ts_step_records(e, step, e->records, stream))) return rc;
+    if ((rc = ts_step_targets(e, step, e->records, stream))) return rc;
+    if ((rc = ts_step_wave(e, step, stream))) return rc;
+  }
+  if (stats_out) return ts_read_stats(e, stats_out, stream);
+  return TS_OK;
+}
+
+int ts_read_stats(ts_engine* e, ts_run_stats* o, void* stream) {
+  if (!e || !o) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  Counters c;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  TS_CUDA_TRY(e, cudaStreamSynchronize((cudaStream_t)stream));
+  host_stats(c, o);
+  o->kernel_launches = e->launches;
+  o->wave_ms = 0.0;
+  for (size_t i = 0; i + 1 < e->wave_ev_used; i += 2) {
+    float ms = 0.f;
+    TS_CUDA_TRY(e, cudaEventSynchronize(e->wave_ev[i + 1]));
+    TS_CUDA_TRY(e, cudaEventElapsedTime(&ms, e->wave_ev[i], e->wave_ev[i + 1]));
+    o->wave_ms += ms;
+  }
+  // tokens are per search
+  if (e->loaded) {
+    std::vector<SearchState> st(e->n_local);
+    TS_CUDA_TRY(e, cudaMemcpy(st.data(), e->st, sizeof(SearchState) * e->n_local, cudaMemcpyDeviceToHost));
+    long long t = 0;
+    for (auto& x : st) t += x.tokens;
+    o->tokens = t;
+  }
+  if (c.sched_error) return fail(e, TS_INVALID_ARGUMENT, "run queue scores not ordered by arrival");
+  return TS_OK;
+}
+
+int ts_read_outcomes(ts_engine* e, ts_outcome* host_out, int32_t n, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!host_out || n < 0 || n > e->n_local) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  if (n == 0) return TS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  View v = make_view(e);
+  k_outcomes<<<(n + 127) / 128, 128, 0, s>>>(v, e->outcomes, n);
+  TS_LAUNCH_CHECK(e, "k_outcomes");
+  TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, e->outcomes, sizeof(ts_outcome) * n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  return TS_OK;
+}
+
+int ts_read_targets(ts_engine* e, int32_t* host_out, int32_t n, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!host_out || n < 0 || n > e->n_local) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  std::vector<SearchState> st(n);
+  cudaStream_t s = (cudaStream_t)stream;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(st.data(), e->st, sizeof(SearchState) * n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i) host_out[i] = st[i].target;
+  return TS_OK;
+}
+
+int ts_read_latencies(ts_engine* e, uint64_t* host_out, int32_t n, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!host_out || n < 0 || n > e->n_local) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  if (n == 0) return TS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  View v = make_view(e);
+  // scratch: the outcome buffer is large enough (sizeof(ts_outcome) >= 8)
+  unsigned long long* d = (unsigned long long*)e->outcomes;
+  k_latency<<<(n + 255) / 256, 256, 0, s>>>(v, d, n);
+  TS_LAUNCH_CHECK(e, "k_latency");
+  TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  return TS_OK;
+}
+
+int ts_read_step_times(ts_engine* e, uint64_t* host_out, int32_t n, void* stream) {
+  if (!e || !host_out || n < 0) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  n = std::min(n, e->step_times_cap);
+  cudaStream_t s = (cudaStream_t)stream;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, e->step_times, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  return TS_OK;
+}
+
+int ts_run_batch_host(ts_engine* e, const ts_problem* hp, int32_t n, int32_t max_steps, ts_outcome* host_out,
+                      ts_run_stats* stats_out, void* stream) {
+  int rc;
+  if ((rc = ts_load_problems(e, hp, n, 0, n, stream))) return rc;
+  if ((rc = ts_run(e, max_steps, stats_out, stream))) return rc;
+  return ts_read_outcomes(e, host_out, n, stream);
+}
+
+int ts_tree_size(ts_engine* e, int32_t search, int32_t* nodes_out) {
+  if (!e || !e->loaded || !nodes_out || search < 0 || search >= e->n_local)
+    return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  SearchState st;
+  TS_CUDA_TRY(e, cudaMemcpy(&st, e->st + search, sizeof(st), cudaMemcpyDeviceToHost));
+  *nodes_out = st.nodes;
+  return TS_OK;
+}
+
+int ts_dump_tree(ts_engine* e, int32_t search, int32_t* parent, double* reward, double* prior, int32_t* visits,
+                 int32_t* inflight, double* value_sum, uint8_t* terminal, int32_t* depth, int32_t* step_ref) {
+  int32_t n = 0;
+  int rc = ts_tree_size(e, search, &n);
+  if (rc) return rc;
+  const size_t b = (size_t)search * (size_t)e->cap;
+  std::vector<uint64_t> no(n);
+  std::vector<uint32_t> me(n);
+  TS_CUDA_TRY(e, cudaMemcpy(no.data(), e->no + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  TS_CUDA_TRY(e, cudaMemcpy(me.data(), e->meta + b, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  if (parent) TS_CUDA_TRY(e, cudaMemcpy(parent, e->parent + b, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  if (reward) TS_CUDA_TRY(e, cudaMemcpy(reward, e->reward + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  if (prior) TS_CUDA_TRY(e, cudaMemcpy(prior, e->prior + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  if (value_sum) TS_CUDA_TRY(e, cudaMemcpy(value_sum, e->W + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) {
+    if (visits) visits[i] = (int32_t)(uint32_t)no[i];
+    if (inflight) inflight[i] = (int32_t)(no[i] >> 32);
+    if (terminal) terminal[i] = (me[i] & M_TERM) ? 1 : 0;
+    if (depth) depth[i] = (int32_t)(me[i] & M_DEPTH);
+    if (step_ref) step_ref[i] = i == 0 ? -1 : (int32_t)((me[i] >> SH_REF) & 31u);
+  }
+  return TS_OK;
+}
+
+// make_problem (backend.py:144-166) + golden_step_rewards (201-215), host side.
+int ts_fill_problem(uint64_t seed, int32_t solvable, int32_t depth_lo, int32_t depth_hi, int32_t branching,
+                    double golden_lo, double golden_hi, double off_lo, double off_hi, int32_t hidden_until_depth,
+                    int32_t has_shared, double shared_lo, double shared_hi, double target_aggregate,
+                    ts_problem* out) {
+  if (!out || depth_hi < depth_lo || branching < 1 || branching > TS_MAX_WIDTH) return TS_INVALID_ARGUMENT;
+  auto mix = [](std::initializer_list<uint64_t> keys) {
+    uint64_t h = MIX_INIT;
+    for (uint64_t k : keys) h = sm64(h ^ k);
+    return h;
+  };
+  memset(out, 0, sizeof(*out));
+  out->seed = seed;
+  out->branching = branching;
+  out->base_depth = depth_lo + (int32_t)(mix({seed, 4}) % (uint64_t)(depth_hi - depth_lo + 1));
+  out->hidden_until_depth = hidden_until_depth;
+  out->has_shared = has_shared;
+  out->off_lo = off_lo;
+  out->off_hi = off_hi;
+  out->shared_lo = shared_lo;
+  out->shared_hi = shared_hi;
+  out->golden_len = -1;
+  if (!solvable) return TS_OK;
+  const int depth = out->base_depth;
+  if (depth > TS_MAX_DEPTH) return TS_INVALID_ARGUMENT;
+  out->golden_len = depth;
+  for (int d = 0; d < depth; ++d) out->golden_path[d] = (uint8_t)(mix({seed, 5, (uint64_t)d}) % (uint64_t)branching);
+  double r[TS_MAX_DEPTH];
+  for (int d = 0; d < depth; ++d) {
+    const int len = d + 1;  // _raw_golden_reward(spec, d+1)
+    uint64_t h = sm64(sm64(sm64(MIX_INIT ^ seed) ^ 1ull) ^ (uint64_t)len);
+    for (int i = 0; i < len; ++i) h = sm64(h ^ (uint64_t)out->golden_path[i]);
+    const bool shr = has_shared && len <= hidden_until_depth;
+    const double lo = shr ? shared_lo : golden_lo, hi = shr ? shared_hi : golden_hi;
+    r[d] = lo + (hi - lo) * u53(h);
+  }
+  for (int it = 0; it < 4; ++it) {
+    double prod = 1.0;
+    for (int d = 0; d < depth; ++d) prod = prod * r[d];
+    if (prod >= target_aggregate) break;
+    const double lift = std::pow(target_aggregate / prod, 1.0 / (double)depth);
+    for (int d = 0; d < depth; ++d) {
+      const double x = r[d] * lift * 1.001;
+      r[d] = x < 0.99 ? x : 0.99;
+    }
+  }
+  for (int d = 0; d < depth; ++d) out->golden_rewards[d] = r[d];
+  return TS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+"""Python handle on the CUDA engine (include/treeserve_b200.h through ctypes).
+
+One :class:`Engine` owns one GPU's node pool and search table.  Everything
+per step runs in the sm_100a kernels of ``csrc/engine.cu``; this class only
+moves problem tables in and outcomes out.  There is no CPU fallback: without
+the built library or a CUDA device the constructor raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+from . import _abi
+from ._abi import TsConfig, TsOutcome, TsProblem, TsRunStats, load_library, raise_for_status
+from .config import SearchConfig
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                return int(torch.cuda.current_stream().cuda_stream)
+        except Exception:  # pragma: no cover - torch missing
+            pass
+        return 0
+    if hasattr(stream, "cuda_stream"):
+        return int(stream.cuda_stream)
+    return int(stream)
+
+
+class Engine:
+    """One GPU's batch of concurrent searches (SearchTree + ProblemBackend +
+    SchedulerState for every request, tree.py:120, backend.py:275, scheduler.py:96)."""
+
+    def __init__(self, config: SearchConfig, device: int = 0, stream=None):
+        self.lib = load_library()
+        self.config = config
+        self.device = device
+        self._cfg = config.to_c() if isinstance(config, SearchConfig) else config
+        self._h = ctypes.c_void_p()
+        self._stream = stream
+        rc = self.lib.ts_engine_create(ctypes.byref(self._cfg), device, ctypes.byref(self._h))
+        if rc != _abi.TS_OK:
+            msg = self.last_error()
+            self.lib.ts_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+            raise_for_status(rc, "ts_engine_create", msg)
+        self.n = 0
+
+    # ---- plumbing ---------------------------------------------------------
+    @property
+    def stream(self) -> int:
+        return _stream_handle(self._stream)
+
+    def last_error(self) -> str:
+        e = self.lib.ts_last_error(self._h)
+        return e.decode() if e else ""
+
+    def _check(self, rc: int, where: str) -> None:
+        if rc != _abi.TS_OK:
+            raise_for_status(rc, where, self.last_error())
+
+    def close(self) -> None:
+        if self._h:
+            self.lib.ts_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- batch API --------------------------------------------------------
+    def load(self, table, global_offset: int = 0, n_global: Optional[int] = None) -> None:
+        """Upload a ts_problem array and reset every tree to a bare root."""
+        n = len(table)
+        if not isinstance(table, ctypes.Array):
+            arr = (TsProblem * n)()
+            for i, p in enumerate(table):
+                arr[i] = p
+            table = arr
+        self._table = table
+        self.n = n
+        self._check(self.lib.ts_load_problems(self._h, table, n, global_offset,
+                                              n if n_global is None else n_global, self.stream),
+                    "ts_load_problems")
+
+    def run(self, max_steps: int = (1 << 31) - 1) -> TsRunStats:
+        st = TsRunStats()
+        self._check(self.lib.ts_run(self._h, max_steps, ctypes.byref(st), self.stream), "ts_run")
+        return st
+
+    def stats(self) -> TsRunStats:
+        st = TsRunStats()
+        self._check(self.lib.ts_read_stats(self._h, ctypes.byref(st), self.stream), "ts_read_stats")
+        return st
+
+    def outcomes(self, n: Optional[int] = None):
+        n = self.n if n is None else n
+        out = (TsOutcome * max(1, n))()
+        self._check(self.lib.ts_read_outcomes(self._h, out, n, self.stream), "ts_read_outcomes")
+        return out[:n]
+
+    def tree(self, i: int) -> dict:
+        """SearchTree.to_dict() of search i as numpy columns (tree.py:183-203)."""
+        n = ctypes.c_int32()
+        self._check(self.lib.ts_tree_size(self._h, i, ctypes.byref(n)), "ts_tree_size")
+        n = n.value
+        out = {
+            "parent": np.zeros(n, np.int32), "reward": np.zeros(n, np.float64), "prior": np.zeros(n, np.float64),
+            "N": np.zeros(n, np.int32), "O": np.zeros(n, np.int32), "W": np.zeros(n, np.float64),
+            "terminal": np.zeros(n, np.uint8), "depth": np.zeros(n, np.int32), "step_ref": np.zeros(n, np.int32),
+        }
+        order = ["parent", "reward", "prior", "N", "O", "W", "terminal", "depth", "step_ref"]
+        self._check(self.lib.ts_dump_tree(self._h, i, *[out[k].ctypes.data_as(ctypes.c_void_p) for k in order]),
+                    "ts_dump_tree")
+        return out
+
+    # ---- step API (multi-GPU drivers, tests) -----------------------------
+    def step_counts(self, step: int, dev_counts: int) -> None:
+        self._check(self.lib.ts_step_counts(self._h, step, ctypes.c_void_p(dev_counts), self.stream),
+                    "ts_step_counts")
+
+    def step_admit(self, step: int, dev_all_counts: int, world: int, rank: int) -> None:
+        self._check(self.lib.ts_step_admit(self._h, step, ctypes.c_void_p(dev_all_counts), world, rank,
+                                           self.stream), "ts_step_admit")
+
+    def step_records(self, step: int, dev_records: int) -> None:
+        self._check(self.lib.ts_step_records(self._h, step, ctypes.c_void_p(dev_records), self.stream),
+                    "ts_step_records")
+
+    def step_targets(self, step: int, dev_all_records: int) -> None:
+        self._check(self.lib.ts_step_targets(self._h, step, ctypes.c_void_p(dev_all_records), self.stream),
+                    "ts_step_targets")
+
+    def step_wave(self, step: int) -> None:
+        self._check(self.lib.ts_step_wave(self._h, step, self.stream), "ts_step_wave")
+
+    def read_targets(self, n: Optional[int] = None) -> list:
+        n = self.n if n is None else n
+        buf = (ctypes.c_int32 * max(1, n))()
+        self._check(self.lib.ts_read_targets(self._h, buf, n, self.stream), "ts_read_targets")
+        return list(buf[:n])
+
+    def latencies_ns(self, n: Optional[int] = None) -> np.ndarray:
+        """Per-search admission→exit latency in ns (device %globaltimer)."""
+        n = self.n if n is None else n
+        buf = np.zeros(max(1, n), np.uint64)
+        self._check(self.lib.ts_read_latencies(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n,
+                                               self.stream), "ts_read_latencies")
+        return buf[:n]
+
+    def step_times(self, n: int) -> np.ndarray:
+        buf = np.zeros(max(1, n), np.uint64)
+        self._check(self.lib.ts_read_step_times(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n,
+                                                self.stream), "ts_read_step_times")
+        return buf[:n]
+
+    def run_batch_host(self, table, max_steps: int = (1 << 31) - 1):
+        """End to end through one C-ABI call: host table in, host outcomes out."""
+        n = len(table)
+        out = (TsOutcome * n)()
+        st = TsRunStats()
+        self._check(self.lib.ts_run_batch_host(self._h, table, n, max_steps, out, ctypes.byref(st), self.stream),
+                    "ts_run_batch_host")
+        self.n = n
+        return out, st
+
+
+def fill_problem(seed: int, solvable: bool, depth_range, branching: int, profile) -> TsProblem:
+    """ts_fill_problem: make_problem + golden_step_rewards in the library (backend.py:144-215)."""
+    lib = load_library()
+    p = TsProblem()
+    sh = profile.shared_range
+    rc = lib.ts_fill_problem(int(seed) & 0xFFFFFFFFFFFFFFFF, int(solvable), depth_range[0], depth_range[1], branching,
+                             profile.golden_range[0], profile.golden_range[1], profile.off_path_range[0],
+                             profile.off_path_range[1], profile.hidden_until_depth, 1 if sh else 0,
+                             sh[0] if sh else 0.0, sh[1] if sh else 0.0, profile.target_aggregate, ctypes.byref(p))
+    raise_for_status(rc, "ts_fill_problem")
+    return p

@@ -1,0 +1,295 @@
+"""Parity of the CUDA engine with the reference, through the C-ABI (needs a B200).
+
+Expected values are the committed fixtures made by the UNMODIFIED reference
+(tests/golden/make_golden.py) and, for larger or random cases, the C oracle
+(oracle/ts_oracle.c, itself pinned to those fixtures by tests/test_oracle.py).
+Everything integer/index is compared exactly; floats are compared bit-for-bit
+(the north star's 1e-12 Q tolerance is not needed: W accumulates in the
+reference's order).
+"""
+
+import ctypes
+import math
+import random
+
+import numpy as np
+import pytest
+
+from golden_io import WAVE_KEYS, assert_tree_equal, config_from_case, load, outcome_dict, table
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(cfg):
+    from paper_2604_00510_b200.engine import Engine
+
+    return Engine(cfg, 0)
+
+
+OUT_KEYS = ("exit_kind", "rollouts_completed", "tokens_generated", "best_score", "best_len", "solved",
+            "exit_step", "admit_step", "launched", "cancelled", "nodes", "status")
+
+
+def _cmp_outcomes(got, want, label):
+    for i, (a, b) in enumerate(zip(got, want)):
+        for k in OUT_KEYS:
+            assert getattr(a, k) == getattr(b, k), f"{label}[{i}].{k}: {getattr(a, k)!r} != {getattr(b, k)!r}"
+        assert list(a.best_path[: a.best_len]) == list(b.best_path[: b.best_len]), f"{label}[{i}] best_path"
+
+
+@pytest.mark.parametrize("case_idx", range(6))
+def test_serial_goldens(case_idx):
+    """run_tree_search per request (search.py:79) == waves of one rollout."""
+    case = load("serial")[case_idx]
+    recs = load("workloads")[case["workload"]]
+    cfg = config_from_case(case)
+    with _engine(cfg) as eng:
+        eng.load(table(recs))
+        eng.run()
+        outs = eng.outcomes()
+        for o, want in zip(outs, case["outcomes"]):
+            w = dict(want)
+            pid = w.pop("problem_id")
+            assert outcome_dict(o) == w, pid
+        for idx, tree in case["trees"].items():
+            assert_tree_equal(eng.tree(int(idx)), tree, f"{case['name']}[{idx}]")
+
+
+def test_deep_tree_goldens():
+    for case in load("deep_trees"):
+        rec = load("workloads")[case["workload"]][case["index"]]
+        with _engine(config_from_case(case)) as eng:
+            eng.load(table([rec]))
+            eng.run()
+            assert_tree_equal(eng.tree(0), case["tree"], case["name"])
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in load("waves")])
+def test_wave_goldens(name):
+    """Boosted virtual-loss waves vs the reference-composed wave oracle, step by step."""
+    case = next(c for c in load("waves") if c["name"] == name)
+    recs = load("workloads")[case["workload"]][: len(case["outcomes"])]
+    cfg = config_from_case(case)
+    import torch
+
+    n = len(recs)
+    with _engine(cfg) as eng:
+        eng.load(table(recs, case["arrival_steps"]))
+        counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+        records = torch.zeros(n * 16, dtype=torch.uint8, device="cuda")
+        trace = []
+        for step in range(case["steps"]):
+            eng.step_counts(step, counts.data_ptr())
+            eng.step_admit(step, counts.data_ptr(), 1, 0)
+            eng.step_records(step, records.data_ptr())
+            eng.step_targets(step, records.data_ptr())
+            t = eng.read_targets()
+            run = [x for x in t if x > 0]
+            if run:
+                trace.append(run)
+            eng.step_wave(step)
+        assert trace == case["targets_trace"]
+        st = eng.stats()
+        assert st.steps == case["steps"]
+        outs = eng.outcomes()
+        for i, want in enumerate(case["outcomes"]):
+            got = outcome_dict(outs[i])
+            for k in got:
+                assert got[k] == want[k], (name, i, k)
+            for k in WAVE_KEYS:
+                assert getattr(outs[i], k) == want[k], (name, i, k)
+        for idx, tree in case["trees"].items():
+            assert_tree_equal(eng.tree(int(idx)), tree, f"{name}[{idx}]")
+    # the one-call run path agrees with the stepwise one
+    with _engine(cfg) as eng:
+        eng.load(table(recs, case["arrival_steps"]))
+        st = eng.run()
+        assert st.steps == case["steps"]
+        for i, want in enumerate(case["outcomes"]):
+            assert outcome_dict(eng.outcomes()[i]) == {k: want[k] for k in outcome_dict(eng.outcomes()[i])}
+
+
+def test_compute_targets_kats():
+    """Device compute_targets (k_targets) vs the reference's KATs, fed raw records."""
+    import torch
+
+    from paper_2604_00510_b200._abi import TsSchedRecord
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+    from paper_2604_00510_b200.scoring import ScoringConfig
+
+    dummy = load("workloads")["c1"][0]
+    for kat in load("targets_kats"):
+        n = len(kat["jobs"])
+        sch = SchedulerConfig(max_concurrency=kat["M"], beta=kat["beta"], proximity=kat["proximity"],
+                              obs_threshold=kat["obs_threshold"], boosting_enabled=kat["boosting"])
+        cfg = SearchConfig(scoring=ScoringConfig(positive_exit_threshold=kat["theta_pos"]), scheduler=sch)
+        recs = (TsSchedRecord * n)()
+        for i, (arr, comp, best) in enumerate(kat["jobs"]):
+            ratio = best / kat["theta_pos"]
+            boosted = ratio > kat["proximity"]
+            recs[i].score = math.log1p(kat["now_step"] - arr) + (kat["beta"] if boosted else 0.0)
+            recs[i].flags = 1 | (2 if comp >= kat["obs_threshold"] else 0) | (4 if boosted else 0)
+        dev = torch.frombuffer(bytearray(bytes(recs)), dtype=torch.uint8).cuda()
+        with _engine(cfg) as eng:
+            eng.load(table([dummy] * n))
+            eng.step_targets(kat["now_step"], dev.data_ptr())
+            assert eng.read_targets() == kat["targets"], kat
+
+
+def _random_targets_case(rng, n, lockstep):
+    M = n + rng.randint(0, 6 * n)
+    now = rng.randint(0, 60)
+    rows, arr = [], 0
+    for _ in range(n):
+        if not lockstep and rng.random() < 0.3:
+            arr = min(now, arr + rng.randint(0, 3))
+        rows.append((0 if lockstep else arr, rng.randint(0, 4), rng.choice([0.0, 0.46, 0.44, rng.random() * 0.6])))
+    return M, now, rows
+
+
+@pytest.mark.parametrize("n", [1, 7, 300, 1025, 5000, 20000])
+def test_compute_targets_random_vs_oracle(n):
+    """Larger pools (multi-chunk scans, long runs, lock-step ties) vs the oracle's
+    literal sorted loop (scheduler.py:143-187 restated in oracle/ts_oracle.c)."""
+    import torch
+
+    from paper_2604_00510_b200._abi import TsConfig, TsSchedRecord
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    rng = random.Random(n)
+    dummy = load("workloads")["c1"][0]
+    for trial in range(4):
+        M, now, rows = _random_targets_case(rng, n, lockstep=trial % 2 == 0)
+        sch = SchedulerConfig(max_concurrency=M, obs_threshold=rng.choice([1, 2, 3]))
+        cfg = SearchConfig(scheduler=sch)
+        c = cfg.to_c()
+        want = oracle.compute_targets(c, now, [r[0] for r in rows], [r[1] for r in rows], [r[2] for r in rows])
+        recs = (TsSchedRecord * n)()
+        for i, (arr, comp, best) in enumerate(rows):
+            boosted = best / 0.5 > sch.proximity
+            recs[i].score = math.log1p(now - arr) + (sch.beta if boosted else 0.0)
+            recs[i].flags = 1 | (2 if comp >= sch.obs_threshold else 0) | (4 if boosted else 0)
+        dev = torch.frombuffer(bytearray(bytes(recs)), dtype=torch.uint8).cuda()
+        with _engine(cfg) as eng:
+            eng.load(table([dummy] * n))
+            eng.step_targets(now, dev.data_ptr())
+            assert eng.read_targets() == want, (n, trial)
+
+
+def test_sharded_engines_match_single():
+    """Block sharding of the run queue over 3 engines (one 'rank' each) with the
+    exchanges done by device copies == one engine: the multi-GPU step contract."""
+    import torch
+
+    case = next(c for c in load("waves") if c["name"] == "c1_M48_admission")
+    recs = load("workloads")[case["workload"]]
+    cfg = config_from_case(case)
+    n = len(recs)
+    bounds = [0, 20, 41, n]
+    engines = []
+    for r in range(3):
+        e = _engine(cfg)
+        e.load(table(recs[bounds[r]:bounds[r + 1]]), global_offset=bounds[r], n_global=n)
+        engines.append(e)
+    counts = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in engines]
+    recbufs = [torch.zeros((bounds[r + 1] - bounds[r]) * 16, dtype=torch.uint8, device="cuda") for r in range(3)]
+    for step in range(case["steps"]):
+        for e, c in zip(engines, counts):
+            e.step_counts(step, c.data_ptr())
+        allc = torch.cat(counts)
+        for r, e in enumerate(engines):
+            e.step_admit(step, allc.data_ptr(), 3, r)
+        for e, b in zip(engines, recbufs):
+            e.step_records(step, b.data_ptr())
+        allr = torch.cat(recbufs)
+        for e in engines:
+            e.step_targets(step, allr.data_ptr())
+            e.step_wave(step)
+    got = [o for e in engines for o in e.outcomes()]
+    for i, want in enumerate(case["outcomes"]):
+        g = outcome_dict(got[i])
+        for k in g:
+            assert g[k] == want[k], (i, k)
+        for k in WAVE_KEYS:
+            assert getattr(got[i], k) == want[k], (i, k)
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("preset", ["c2_exits_off_P1", "c2_full", "c4_stagnation"])
+def test_random_batches_vs_oracle(preset):
+    """Bigger batches vs the C oracle: trees node by node for a sample."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    if preset == "c2_exits_off_P1":
+        specs = B.make_workload(256, (0.6, 0.25, 0.15), 3, branching=4,
+                                depth_ranges={d: (15, 15) for d in B.Difficulty})
+        cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=1 << 30, boosting_enabled=False),
+                           rollout_budget=32, depth_cap=16, expand_width=4, positive_exit=False,
+                           negative_exit=False)
+    elif preset == "c2_full":
+        specs = B.make_workload(1024, (0.6, 0.25, 0.15), 11, branching=4,
+                                depth_ranges={d: (15, 15) for d in B.Difficulty})
+        cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=2048), rollout_budget=128, depth_cap=16,
+                           expand_width=4)
+    else:
+        from paper_2604_00510_b200 import keyed
+        specs = [B.make_problem(f"s{i}", keyed.mix(5, 8, i), B.Difficulty.HARD_SOLVABLE, (31, 31), 8,
+                                B.stagnation_profile()) for i in range(16)]
+        cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=64), rollout_budget=64, depth_cap=32,
+                           expand_width=8)
+    t = B.problem_table(specs)
+    ref = oracle.OracleRun(t, cfg.to_c(), threads=8)
+    with _engine(cfg) as eng:
+        eng.load(t)
+        st = eng.run()
+        _cmp_outcomes(eng.outcomes(), ref.outcomes, preset)
+        assert st.steps == ref.steps
+        assert st.rollouts == ref.stats.rollouts and st.nodes + len(specs) == ref.stats.nodes
+        for i in (0, 1, len(specs) - 1):
+            assert_tree_equal(eng.tree(i), ref.tree(i), f"{preset}[{i}]")
+    ref.close()
+
+
+def test_host_end_to_end_call():
+    """ts_run_batch_host: host problems in, host outcomes out, one C call."""
+    case = load("serial")[0]
+    recs = load("workloads")[case["workload"]]
+    with _engine(config_from_case(case)) as eng:
+        outs, st = eng.run_batch_host(table(recs))
+        for o, want in zip(outs, case["outcomes"]):
+            w = dict(want)
+            w.pop("problem_id")
+            assert outcome_dict(o) == w
+
+
+def test_dropin_run_tree_search_matches_reference_outcomes():
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.search import run_tree_search, run_tree_searches
+
+    D7 = {d: (7, 7) for d in B.Difficulty}
+    specs = B.make_workload(64, (0.6, 0.25, 0.15), 0, branching=4, depth_ranges=D7)
+    case = load("serial")[0]
+    outs = run_tree_searches(specs, rollout_budget=32, depth_cap=8, expand_width=4)
+    for o, want in zip(outs, case["outcomes"]):
+        assert o.problem_id == want["problem_id"]
+        assert o.exit_kind.value == want["exit_kind"]
+        assert o.best_score == want["best_score"] and list(o.best_path) == want["best_path"]
+        assert (o.rollouts_completed, o.tokens_generated, o.solved) == (
+            want["rollouts_completed"], want["tokens_generated"], want["solved"])
+    one = run_tree_search(specs[5], rollout_budget=32, depth_cap=8, expand_width=4)
+    assert one == outs[5]
+
+
+def test_invalid_config_raises():
+    from paper_2604_00510_b200._abi import TsConfig
+    from paper_2604_00510_b200.engine import Engine
+
+    c = TsConfig()
+    with pytest.raises(ValueError):
+        Engine(c, 0)
