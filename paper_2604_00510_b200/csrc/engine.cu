@@ -126,11 +126,6 @@ struct Agg {
     }
     ++n;
   }
-  // prefix aggregate of the path extended by one more reward (prunable schemes)
-  __device__ __forceinline__ double peek(double r, int scheme) const {
-    if (scheme == TS_SCHEME_PRODUCT) return a * r;
-    return (n == 0 || r < a) ? r : a;
-  }
   __device__ __forceinline__ double value(int scheme) const {
     if (scheme == TS_SCHEME_PRODUCT || scheme == TS_SCHEME_MINIMUM) return a;
     double s = a;
@@ -632,12 +627,29 @@ __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched
 
 // ---- the wave: one warp per running search ----------------------------------
 struct WaveStats {
-  unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
+  unsigned long long rollouts, launched, nodes, scored, levels, path_nodes;
 };
 
+// One wave of one search, executed by one warp.
+//
+// Per rollout the warp walks root→leaf (select_leaf) and leaf→terminal
+// (simulate_to_terminal).  Only the descent's critical path runs per level:
+// in selection one round of child loads + WU-PUCT + argmax; in simulation the
+// children's rewards/terminal flags (needed by greedy_child) and the fold
+// absorb.  Everything else an expansion produces — priors (with CPython's
+// Neumaier sum), tokens, node records, parent links, negative-exit counts — is
+// generated after the descent in one lane-parallel batch: lane l owns the
+// expansion at depth l, using the fold states frozen at that depth.
+//
+// Lane l also keeps path node l+1 in registers (id, meta, N|O word, W, reward,
+// prefix aggregate, golden flag, chosen child index), so registration and a
+// single-rollout backup are pure stores, and subtree-exhaustion propagates up
+// the path without loads.
 template <int NSLOT>
 __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
+  constexpr int GS = 8 * NSLOT;
   const int lane = threadIdx.x & 31;
+  const int dl = lane % GS;  // depth index of this lane's fold states
   const ts_config& cf = v.cfg;
   SearchState* S = v.st + s;
   const ts_problem* pb = v.prob + s;
@@ -664,6 +676,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
   const bool strict = cf.strict_negative_exit != 0;
   const bool prefix_bound = cf.futility_bound == TS_BOUND_PREFIX_AGGREGATE;
   const double tau = cf.accept_threshold, theta1 = cf.first_step_threshold;
+  const double c_puct = cf.c_puct;
   // lane l holds golden_path[l] and its lifted reward
   const int gstep = lane < glen ? (int)pb->golden_path[lane] : -1;
   const double grew = lane < glen ? pb->golden_rewards[lane] : 0.0;
@@ -673,11 +686,10 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
   int viable = S->viable;
   int best_term = S->best_term;
   double best = S->best;
-  long long tokens = S->tokens;
   int launched = S->launched, cancelled = S->cancelled;
   int status = TS_OK;
   const int budget = cf.rollout_budget;
-  int count = min(S->target, budget - completed);
+  const int count = min(S->target, budget - completed);
   const bool multi = count > 1;
   int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
   double* SSs = v.ss + (size_t)s * budget;
@@ -694,12 +706,20 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
       root_h[k] = sm64(sm64(h0 ^ tag) ^ len);
     }
   }
+  // the root's record lives in registers for the whole wave (sole writer)
   uint32_t root_meta = ME[0];
+  uint64_t rno = NO[0];
+  double rW = Wv[0];
+  int rfc = FC[0];
   int decision = TS_EXIT_NONE;
   int nl = 0;
-  // last rollout kept in registers (the P=1 fast path never touches scratch)
-  int pnode = -1, plen = 0;
-  double pscore = 0.0;
+  long long tok_acc = 0;  // per-lane token tally, reduced once per wave
+  // last rollout's path registers (the P=1 backup uses them directly)
+  int pnode = -1, plen = 0, pj = 0;
+  uint32_t pmeta = 0;
+  uint64_t pno = 0;
+  double pW = 0.0, prew = 0.0, pagg = 1.0, pscore = 0.0;
+  bool pgold = false;
   unsigned long long scored = 0, levels = 0, created = 0, pathn = 0;
 
   for (int r = 0; r < count && status == TS_OK; ++r) {
@@ -710,40 +730,43 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
     uint64_t h[NSLOT];
 #pragma unroll
     for (int k = 0; k < NSLOT; ++k) h[k] = root_h[k];
-    int node = 0, depth = 0;
+    int node = 0, depth = 0, nfc = rfc;
     uint32_t nmeta = root_meta;
-    double nrew = 1.0;
+    uint64_t nno = rno;
+    double nW = rW, nrew = 1.0;
     pnode = -1;
-    uint32_t pmeta = 0;  // lane l: meta of path[l+1] (register copy, sole writer)
     Agg agg;
     agg.init();
     bool golden = glen >= 0;
     double d1r = 1.0;
 
-    // --- select_leaf (tree.py:264-284) ---
+    // --- select_leaf (tree.py:264-284): one round of child loads per level ---
     while (nmeta & M_KIDS) {
-      const int fc = FC[node];
-      const uint64_t pno = NO[node];
-      const double pW = Wv[node];
-      const long long pN = (long long)(uint32_t)pno, pO = (long long)(pno >> 32);
+      const long long pN = (long long)(uint32_t)nno, pO = (long long)(nno >> 32);
+      const double psq = sqrt((double)(pN + pO));
+      const double pq = pN == 0 ? 0.5 : nW / (double)pN;
+      const int fc = nfc;
       bool valid = lane < width;
-      double sc = -INFINITY, cr = 0.0;
+      double sc = -INFINITY, cr = 0.0, cw = 0.0;
       uint32_t cm = 0;
+      uint64_t cno = 0;
+      int cfc = -1;
       if (valid) {
         const int c = fc + lane;
-        const uint64_t cno = NO[c];
-        const double cw = Wv[c];
+        cno = NO[c];
+        cw = Wv[c];
         const double cp = PR[c];
         cm = ME[c];
         cr = RW[c];
+        cfc = FC[c];
         valid = meta_expandable(cm);
         if (valid) {
           const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
           // _child_q (tree.py:235-239)
-          double q = cN == 0 ? (pN == 0 ? 0.5 : pW / (double)pN) : cw / (double)cN;
+          const double q = cN == 0 ? pq : cw / (double)cN;
           if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
           // wu_puct_score (tree.py:232): q + c*P*sqrt(N_s+O_s)/(1+N_sa+O_sa)
-          sc = q + cf.c_puct * cp * sqrt((double)(pN + pO)) / (double)(1 + cN + cO);
+          sc = q + c_puct * cp * psq / (double)(1 + cN + cO);
         }
       }
       const unsigned vb = __ballot_sync(FULL, valid);
@@ -756,166 +779,225 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
       ++depth;
       nmeta = __shfl_sync(FULL, cm, j);
       nrew = __shfl_sync(FULL, cr, j);
-      if (lane == depth - 1) { pnode = node; pmeta = nmeta; }
+      nno = __shfl_sync(FULL, cno, j);
+      nW = __shfl_sync(FULL, cw, j);
+      nfc = __shfl_sync(FULL, cfc, j);
       agg.add(nrew, scheme);
       if (depth == 1) d1r = nrew;
       golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
+      if (lane == depth - 1) {
+        pnode = node; pmeta = nmeta; pno = nno; pW = nW; prew = nrew; pagg = agg.a; pgold = golden; pj = j;
+      }
 #pragma unroll
-      for (int k = 0; k < NSLOT; ++k) h[k] = sm64(h[k] ^ (uint64_t)j);
+      for (int k = 0; k < NSLOT; ++k)
+        if (dl >= depth) h[k] = sm64(h[k] ^ (uint64_t)j);
     }
     if (status != TS_OK) break;
+    const int d0 = depth;  // the selected non-terminal leaf
+    const int fc0 = nnodes;
 
-    // --- simulate_to_terminal (tree.py:322-349) ---
-    while (!(nmeta & M_TERM)) {
-      int fc;
-      double cr = 0.0;
-      uint32_t cm = 0;
-      bool became_dead = false;  // node turned non-expandable
-      if (!(nmeta & M_KIDS)) {
-        // NE bookkeeping: this non-terminal leaf stops being a leaf
-        bool counted = false;
-        if (depth >= 1) {
-          const bool rel = strict || d1r >= theta1;
-          const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
-          counted = rel && !(bound < tau);
-        }
-        if (depth >= cf.depth_cap) {  // depth cap → force terminal (tree.py:340-343)
-          nmeta |= M_TERM | M_FORCED;
-          if (lane == 0) ME[node] = nmeta;
-          if (depth == 0) root_meta = nmeta;
-          else if (lane == depth - 1) pmeta = nmeta;
-          if (counted) --viable;
-          became_dead = true;
-        } else {
-          if (nnodes + width > v.cap) { status = TS_POOL_OVERFLOW; break; }
-          fc = nnodes;
-          nnodes += width;
-          const int d = depth;
-          // expand (tree.py:287-304) with generate_steps replayed (backend.py:230-269)
-          const uint64_t hp = state_at<NSLOT, 0>(h, d);
-          const uint64_t hr = state_at<NSLOT, 1>(h, d);
-          const uint64_t hk = state_at<NSLOT, 2>(h, d);
-          const uint64_t he = state_at<NSLOT, 3>(h, d);
-          const double graw = __shfl_sync(FULL, grew, d);
-          const int gnext = __shfl_sync(FULL, gstep, d);
-          const bool v_ = lane < width;
-          const uint64_t j64 = (uint64_t)lane;
-          const double raw = 0.5 + u53(sm64(hp ^ j64));
-          // total = sum(raw_priors): CPython Neumaier sum in child order
-          double tot = __shfl_sync(FULL, raw, 0), cc = 0.0;
-          for (int i = 1; i < width; ++i) {
-            const double x = __shfl_sync(FULL, raw, i);
-            const double t = tot + x;
-            if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
-            else cc += (x - t) + tot;
-            tot = t;
-          }
-          if (cc != 0.0 && isfinite(cc)) tot += cc;
-          const double pri = raw / tot;
-          const int len = d + 1;
-          const bool gchild = golden && len <= glen && lane == gnext;
-          double rew;
-          if (gchild) {
-            rew = graw;
-          } else {
-            const bool shr = has_shared && len <= hidden;
-            const double lo = shr ? sh_lo : off_lo, hi = shr ? sh_hi : off_hi;
-            rew = lo + (hi - lo) * u53(sm64(hr ^ j64));
-          }
-          const int tok = 40 + (int)(sm64(hk ^ j64) % 81ull);
-          bool term;
-          if (len < bdepth) term = false;
-          else if (len >= bdepth + 1) term = true;
-          else if (gchild) term = true;
-          else term = (sm64(he ^ j64) % 2ull) != 0;  // not _branch_extends
-          const uint32_t cmeta = (uint32_t)len | ((uint32_t)lane << SH_REF) | (term ? M_TERM : 0u);
-          if (v_) {
-            const int c = fc + lane;
-            NO[c] = 0;
-            Wv[c] = 0.0;
-            PR[c] = pri;
-            RW[c] = rew;
-            FC[c] = -1;
-            PA[c] = node;
-            ME[c] = cmeta;
-          }
-          int tsum = v_ ? tok : 0;
-          for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(FULL, tsum, o);
-          tokens += tsum;
-          const unsigned live = __ballot_sync(FULL, v_ && !term);
-          const int ne = __popc(live);
-          nmeta = nmeta | M_KIDS | ((uint32_t)ne << SH_NEXP);
-          if (lane == 0) {
-            FC[node] = fc;
-            ME[node] = nmeta;
-          }
-          if (depth == 0) root_meta = nmeta;
-          else if (lane == depth - 1) pmeta = nmeta;
-          // NE: new non-terminal leaves that are check-relevant and viable
-          bool cnt_child = false;
-          if (v_ && !term) {
-            const bool rel = strict || (len == 1 ? rew : d1r) >= theta1;
-            const double bound = prefix_bound ? fmin(rew, agg.peek(rew, scheme)) : rew;
-            cnt_child = rel && !(bound < tau);
-          }
-          viable += __popc(__ballot_sync(FULL, cnt_child)) - (counted ? 1 : 0);
-          created += width;
-          became_dead = ne == 0;
-          cr = rew;
-          cm = cmeta;
-        }
+    // --- simulate_to_terminal (tree.py:322-349): critical path only ---
+    bool forced = false;
+    while (true) {
+      if (depth >= cf.depth_cap) { forced = true; break; }  // tree.py:340-343
+      if (nnodes + width > v.cap) { status = TS_POOL_OVERFLOW; break; }
+      const int d = depth;
+      const int len = d + 1;
+      const uint64_t hr = state_at<NSLOT, 1>(h, d);
+      const double graw = __shfl_sync(FULL, grew, d);
+      const int gnext = __shfl_sync(FULL, gstep, d);
+      const bool gchild = golden && len <= glen && lane == gnext;
+      double rew;
+      if (gchild) {
+        rew = graw;
       } else {
-        fc = FC[node];
-        if (lane < width) {
-          cr = RW[fc + lane];
-          cm = ME[fc + lane];
-        }
+        const bool shr = has_shared && len <= hidden;
+        const double lo = shr ? sh_lo : off_lo, hi = shr ? sh_hi : off_hi;
+        rew = lo + (hi - lo) * u53(sm64(hr ^ (uint64_t)lane));
       }
-      if (became_dead) {
-        // propagate "no expandable leaf below" up the path
-        for (int i = depth - 1; i >= 0; --i) {
-          uint32_t m = i == 0 ? root_meta : __shfl_sync(FULL, pmeta, i - 1);
-          const int pid = i == 0 ? 0 : __shfl_sync(FULL, pnode, i - 1);
-          m -= NEXP_ONE;
-          if (lane == 0) ME[pid] = m;
-          if (i == 0) root_meta = m;
-          else if (lane == i - 1) pmeta = m;
-          if (meta_nexp(m) > 0) break;
-        }
-        if (nmeta & M_TERM) break;  // forced terminal: rollout ends here
+      bool term;
+      if (len < bdepth) {
+        term = false;
+      } else if (len >= bdepth + 1) {
+        term = true;
+      } else {
+        const uint64_t he = state_at<NSLOT, 3>(h, d);
+        term = gchild || (sm64(he ^ (uint64_t)lane) & 1ull) != 0;  // not _branch_extends
       }
-      // greedy_child (tree.py:307-319)
-      const int j = warp_argmax(cr, lane < width, wp2);
-      node = fc + j;
+      const int j = warp_argmax(rew, lane < width, wp2);  // greedy_child (tree.py:307-319)
+      const bool jterm = __shfl_sync(FULL, term, j);
+      node = nnodes + j;
+      nnodes += width;
       ++depth;
-      nmeta = __shfl_sync(FULL, cm, j);
-      nrew = __shfl_sync(FULL, cr, j);
-      if (lane == depth - 1) { pnode = node; pmeta = nmeta; }
+      nrew = __shfl_sync(FULL, rew, j);
+      nmeta = (uint32_t)depth | ((uint32_t)j << SH_REF) | (jterm ? M_TERM : 0u);
       agg.add(nrew, scheme);
       if (depth == 1) d1r = nrew;
-      golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
+      golden = golden && depth <= glen && gnext == j;
+      if (lane == depth - 1) {
+        pnode = node; pmeta = nmeta; pno = O_ONE; pW = 0.0; prew = nrew; pagg = agg.a; pgold = golden; pj = j;
+      }
 #pragma unroll
-      for (int k = 0; k < NSLOT; ++k) h[k] = sm64(h[k] ^ (uint64_t)j);
+      for (int k = 0; k < NSLOT; ++k)
+        if (dl >= depth) h[k] = sm64(h[k] ^ (uint64_t)j);
+      if (jterm) break;
     }
     if (status != TS_OK) break;
-    __syncwarp();
-    // in-flight registration of root..terminal (tree.py:282-283, 347-348)
-    if (lane < depth) NO[pnode] += O_ONE;
-    if (lane == 0) NO[0] += O_ONE;
-    plen = depth;
+    const int dend = depth;        // terminal (or force-terminated) node depth
+    const int nlev = dend - d0;    // expansions happened at depths d0 .. dend-1
+    plen = dend;
     pscore = agg.value(scheme);
+
+    // --- deferred expansion batch: lane l writes the children of depth l ---
+    // values of path node l (the expanded node) come from lane l-1
+    const int up_node = __shfl_up_sync(FULL, pnode, 1);
+    const uint32_t up_meta = __shfl_up_sync(FULL, pmeta, 1);
+    const double up_rew = __shfl_up_sync(FULL, prew, 1);
+    const double up_agg = __shfl_up_sync(FULL, pagg, 1);
+    const bool up_gold = __shfl_up_sync(FULL, pgold, 1);
+    const int node_l = lane == 0 ? 0 : up_node;
+    const uint32_t leaf_meta = lane == 0 ? root_meta : up_meta;
+    const double rew_l = lane == 0 ? 1.0 : up_rew;
+    const double agg_l = lane == 0 ? 1.0 : up_agg;
+    const bool gold_l = lane == 0 ? (glen >= 0) : up_gold;
+    // frozen fold states of depth `lane` for the four tags
+    const uint64_t st_prior = __shfl_sync(FULL, h[0], (0 / NSLOT) * GS + dl);
+    const uint64_t st_rew = __shfl_sync(FULL, h[1 % NSLOT], (1 / NSLOT) * GS + dl);
+    const uint64_t st_tok = __shfl_sync(FULL, h[2 % NSLOT], (2 / NSLOT) * GS + dl);
+    const uint64_t st_ext = __shfl_sync(FULL, h[3 % NSLOT], (3 / NSLOT) * GS + dl);
+    const bool act = lane >= d0 && lane < d0 + nlev;
+    int live = 0;       // non-terminal children of this level
+    int ne_cnt = 0;     // NE: check-relevant viable new leaves
+    uint32_t meta_l = 0;
+    if (act) {
+      const int l = lane;
+      const int len = l + 1;
+      const int fcl = fc0 + (l - d0) * width;
+      // total = sum(raw_priors): CPython Neumaier sum in child order
+      double tot = 0.5 + u53(sm64(st_prior)), cc = 0.0;
+      for (int i = 1; i < width; ++i) {
+        const double x = 0.5 + u53(sm64(st_prior ^ (uint64_t)i));
+        const double t = tot + x;
+        if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
+        else cc += (x - t) + tot;
+        tot = t;
+      }
+      if (cc != 0.0 && isfinite(cc)) tot += cc;
+      const bool shr = has_shared && len <= hidden;
+      const double lo = shr ? sh_lo : off_lo, hi = shr ? sh_hi : off_hi;
+      const bool last = l == dend - 1;
+      for (int j = 0; j < width; ++j) {
+        const bool gch = gold_l && len <= glen && j == gstep;
+        const double rew = gch ? grew : lo + (hi - lo) * u53(sm64(st_rew ^ (uint64_t)j));
+        bool term;
+        if (len < bdepth) term = false;
+        else if (len >= bdepth + 1) term = true;
+        else term = gch || (sm64(st_ext ^ (uint64_t)j) & 1ull) != 0;
+        tok_acc += 40 + (long long)(sm64(st_tok ^ (uint64_t)j) % 81ull);
+        const int c = fcl + j;
+        const bool onpath = j == pj;
+        NO[c] = onpath ? O_ONE : 0ull;
+        Wv[c] = 0.0;
+        PR[c] = (0.5 + u53(sm64(st_prior ^ (uint64_t)j))) / tot;
+        RW[c] = rew;
+        PA[c] = node_l;
+        // the on-path child expanded at the next level gets its fc/meta from lane l+1
+        if (!onpath || last) {
+          FC[c] = -1;
+          uint32_t m = (uint32_t)len | ((uint32_t)j << SH_REF) | (term ? M_TERM : 0u);
+          if (onpath && forced) m |= M_TERM | M_FORCED;
+          ME[c] = m;
+        }
+        if (!term) {
+          ++live;
+          // NE: a new non-terminal leaf, check-relevant and viable (scoring.py:119-175)
+          const bool rel = strict || (len == 1 ? rew : d1r) >= theta1;
+          const double bound = prefix_bound ? fmin(rew, l == 0 ? rew : (scheme == TS_SCHEME_PRODUCT ? agg_l * rew
+                                                                         : (rew < agg_l ? rew : agg_l)))
+                                            : rew;
+          if (rel && !(bound < tau)) ++ne_cnt;
+        }
+      }
+      // the expanded node (path node l) stops being a leaf
+      if (l >= 1) {
+        const bool rel = strict || d1r >= theta1;
+        const double bound = prefix_bound ? fmin(rew_l, agg_l) : rew_l;
+        if (rel && !(bound < tau)) --ne_cnt;
+      }
+    }
+    // meta of path node l: leaf meta (l == d0) or the fresh node's own fields
+    {
+      const int upj = __shfl_up_sync(FULL, pj, 1);
+      if (act) {
+        const int l = lane;
+        uint32_t m = l == d0 ? leaf_meta : ((uint32_t)l | ((uint32_t)upj << SH_REF));
+        meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
+        FC[node_l] = fc0 + (l - d0) * width;
+        ME[node_l] = meta_l;
+      }
+    }
+    // refresh the path meta registers (lane l-1 holds path node l)
+    {
+      const uint32_t dn = __shfl_down_sync(FULL, meta_l, 1);
+      const bool dn_act = (lane + 1) >= d0 && (lane + 1) < d0 + nlev;
+      if (dn_act) pmeta = dn;
+      if (d0 == 0 && nlev > 0) root_meta = __shfl_sync(FULL, meta_l, 0);
+      if (forced && lane == dend - 1) pmeta |= M_TERM | M_FORCED;
+    }
+    if (forced && nlev == 0) {
+      // the selected leaf itself hit the depth cap (d0 >= 1 since depth_cap >= 1)
+      const uint32_t m = __shfl_sync(FULL, pmeta, dend - 1);
+      const int lid = __shfl_sync(FULL, pnode, dend - 1);
+      if (lane == 0) ME[lid] = m;
+    }
+    viable += __reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
+    if (forced) {
+      // NE: the force-terminated leaf leaves the leaf set
+      const bool rel = strict || d1r >= theta1;
+      const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
+      if (rel && !(bound < tau)) --viable;
+    }
+    created += (unsigned long long)nlev * width;
+    if (nlev > 0 && d0 == 0) rfc = fc0;
+    __syncwarp();
+    // subtree exhaustion: forced node, or a last expansion with no live child
+    int dead_from = -1;
+    if (forced) dead_from = dend;
+    else if (nlev > 0 && __shfl_sync(FULL, live, dend - 1) == 0) dead_from = dend - 1;
+    if (dead_from >= 0) {
+      for (int i = dead_from - 1; i >= 0; --i) {
+        uint32_t m = i == 0 ? root_meta : __shfl_sync(FULL, pmeta, i - 1);
+        const int pid = i == 0 ? 0 : __shfl_sync(FULL, pnode, i - 1);
+        m -= NEXP_ONE;
+        if (lane == 0) ME[pid] = m;
+        if (i == 0) root_meta = m;
+        else if (lane == i - 1) pmeta = m;
+        if (meta_nexp(m) > 0) break;
+      }
+    }
+    // in-flight registration of root..leaf (tree.py:282-283); the simulated
+    // path was written with O = 1 above (tree.py:347-348)
+    rno += O_ONE;
+    if (lane < d0) pno += O_ONE;
     if (multi) {
+      if (lane < d0) NO[pnode] = pno;
+      if (lane == 0) NO[0] = rno;
       SPs[(size_t)nl * 32 + lane] = pnode;
       if (lane == 0) { SSs[nl] = pscore; SLs[nl] = plen; }
     }
     ++nl;
     __syncwarp();
   }
+  {
+    long long t = tok_acc;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+    tok_acc = t;
+  }
 
   // --- finish_rollout → backpropagate (tree.py:352-371) → decide_exit in
   //     launch order; cancel_inflight for the rest on exit ---
   launched += nl;
-  bool exhausted = decision == -1;
+  const bool exhausted = decision == -1;
   if (exhausted) decision = TS_EXIT_NONE;
   unsigned long long done = 0;
   auto decide = [&](bool exh) -> int {
@@ -928,29 +1010,33 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
   for (int r = 0; r < nl && status == TS_OK; ++r) {
     int pn, len;
     double sc;
+    bool bad = false;
+    if (completed >= budget) { status = TS_ACCOUNTING; break; }
     if (multi) {
       len = SLs[r];
       sc = SSs[r];
       pn = lane < len ? SPs[(size_t)r * 32 + lane] : -1;
+      if (lane < len) {
+        const uint64_t x = NO[pn];
+        if ((x >> 32) < 1) bad = true;
+        NO[pn] = x + 1 - O_ONE;
+        Wv[pn] += sc;
+      }
     } else {
+      // single rollout: the path's N|O and W are still the registers' values
       len = plen;
       sc = pscore;
       pn = pnode;
+      if (lane < len) {
+        if ((pno >> 32) < 1) bad = true;
+        NO[pn] = pno + 1 - O_ONE;
+        Wv[pn] = pW + sc;
+      }
     }
-    if (completed >= budget) { status = TS_ACCOUNTING; break; }
-    bool bad = false;
-    if (lane < len) {
-      const uint64_t x = NO[pn];
-      if ((x >> 32) < 1) bad = true;
-      NO[pn] = x + 1 - O_ONE;
-      Wv[pn] += sc;
-    }
-    if (lane == 0) {
-      const uint64_t x = NO[0];
-      if ((x >> 32) < 1) bad = true;
-      NO[0] = x + 1 - O_ONE;
-      Wv[0] += sc;
-    }
+    if ((rno >> 32) < 1) bad = true;
+    rno = rno + 1 - O_ONE;
+    rW += sc;
+    if (lane == 0) { NO[0] = rno; Wv[0] = rW; }
     if (__any_sync(FULL, bad)) { status = TS_ACCOUNTING; break; }
     __syncwarp();
     ++completed;
@@ -966,10 +1052,11 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
         const int len2 = SLs[r2];
         const int pn2 = lane < len2 ? SPs[(size_t)r2 * 32 + lane] : -1;
         bool bad2 = lane < len2 && (NO[pn2] >> 32) < 1;
-        if (lane == 0 && (NO[0] >> 32) < 1) bad2 = true;
+        if ((rno >> 32) < 1) bad2 = true;
         if (__any_sync(FULL, bad2)) { status = TS_ACCOUNTING; break; }
         if (lane < len2) NO[pn2] -= O_ONE;
-        if (lane == 0) NO[0] -= O_ONE;
+        rno -= O_ONE;
+        if (lane == 0) NO[0] = rno;
         __syncwarp();
         ++cancelled;
         pathn += len2 + 1;
@@ -984,7 +1071,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
     S->viable = viable;
     S->best_term = best_term;
     S->best = best;
-    S->tokens = tokens;
+    S->tokens += tok_acc;
     S->launched = launched;
     S->cancelled = cancelled;
     // on_rollout_complete (scheduler.py:217-233): refresh Job.best_score
@@ -1003,19 +1090,18 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
   ws.rollouts += done;
   ws.launched += nl;
   ws.nodes += created;
-  ws.tokens += 0;
   ws.scored += scored;
   ws.levels += levels;
   ws.path_nodes += pathn;
-  ws.cancelled += 0;
 }
+
 
 constexpr int WAVE_THREADS = 128;
 
 template <int NSLOT>
 __global__ void __launch_bounds__(WAVE_THREADS) k_wave(View v, int step) {
   const int lane = threadIdx.x & 31;
-  WaveStats ws = {0, 0, 0, 0, 0, 0, 0, 0};
+  WaveStats ws = {0, 0, 0, 0, 0, 0};
   const int count = v.ctr->work_count;
   for (;;) {
     int item = 0;
