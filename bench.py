@@ -174,6 +174,44 @@ def run_sharded(eng, d: Dist, n_local: int, counts, allc, recs, allr, max_steps=
     return max_steps
 
 
+def algorithmic_bytes(st) -> int:
+    return (B_SCORED * st.children_scored + B_LEVEL * st.select_levels + B_NODE * st.nodes
+            + B_PATH * st.path_nodes)
+
+
+def profile_waves(eng, table, lo, n_total, d: Dist):
+    """Σ k_wave time (CUDA events on the launch stream) and algorithmic bytes of one batch."""
+    import torch
+
+    if d.world > 1:
+        return 0.0, 0
+    n = len(table)
+    eng.load(table, lo, n_total)
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    recs = torch.zeros(n * 16, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    evs = []
+    step = 0
+    while True:
+        eng.step_counts(step, counts.data_ptr())
+        if step % 4 == 0:
+            torch.cuda.synchronize()
+            if int(counts[2].item()) == 0:
+                break
+        eng.step_admit(step, counts.data_ptr(), 1, 0)
+        eng.step_records(step, recs.data_ptr())
+        eng.step_targets(step, recs.data_ptr())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        eng.step_wave(step)
+        e1.record()
+        evs.append((e0, e1))
+        step += 1
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    return ms, algorithmic_bytes(eng.stats())
+
+
 def bench_ours(args, d: Dist):
     import torch
 
@@ -206,8 +244,7 @@ def bench_ours(args, d: Dist):
     torch.cuda.synchronize()
     d.barrier()
     clocks = Clocks(d.local) if d.rank == 0 else None
-    total_ms, rollouts, wave_ms, launches, lat, stats = 0.0, 0, 0.0, 0, [], None
-    byte_total = 0
+    total_ms, rollouts, launches, lat, stats = 0.0, 0, 0, [], None
     for _ in range(args.steps):
         eng.load(table, lo, n_total)  # H2D of the problem table + tree reset: outside the timed region
         flush_l2(flush)
@@ -222,16 +259,18 @@ def bench_ours(args, d: Dist):
         total_ms += ms
         stats = eng.stats()
         rollouts += stats.rollouts
-        wave_ms += stats.wave_ms
         launches += stats.kernel_launches
-        byte_total += (B_SCORED * stats.children_scored + B_LEVEL * stats.select_levels + B_NODE * stats.nodes
-                       + B_PATH * stats.path_nodes)
         lat.extend((eng.latencies_ns() / 1e6).tolist())
     clk = clocks.stop() if clocks else None
     rollouts_all = d.sum(rollouts)
     value = rollouts_all / (total_ms / 1e3)
     outs = eng.outcomes()
     exits = {k: sum(1 for o in outs if o.exit_kind == k) for k in (1, 2, 3)}
+
+    # roofline: one extra batch through the step API with CUDA events around
+    # every k_wave launch on the launch stream (the graph path above has no
+    # per-kernel events); algorithmic bytes from the engine counters
+    wave_ms, byte_total = profile_waves(eng, table, lo, n_total, d)
 
     # e2e: host problem table in → host outcomes out through one C-ABI call
     e2e = None
@@ -267,13 +306,12 @@ def bench_ours(args, d: Dist):
         e1.record(stream)
         torch.cuda.synchronize()
         ms2 = e0.elapsed_time(e1)
-        b2 = (B_SCORED * st2.children_scored + B_LEVEL * st2.select_levels + B_NODE * st2.nodes
-              + B_PATH * st2.path_nodes)
+        wms2, b2 = profile_waves(eng2, table, 0, n_total, d)
         hbm, _ = peaks()
         variant = {"workload": "same 4096 searches, exits off (every search runs 128 rollouts)",
                    "value": st2.rollouts / (ms2 / 1e3), "unit": UNIT, "ms": ms2, "waves": st2.steps,
-                   "wave_kernel_GBs": b2 / (st2.wave_ms / 1e3) / 1e9,
-                   "wave_frac": b2 / (st2.wave_ms / 1e3) / 1e9 / hbm}
+                   "wave_ms": wms2, "wave_kernel_GBs": b2 / (wms2 / 1e3) / 1e9,
+                   "wave_frac": b2 / (wms2 / 1e3) / 1e9 / hbm}
         eng2.close()
 
     cpu = cpu_baseline(PER_GPU, n_total) if (d.rank == 0 and N == 1 and not args.no_cpu) else None

@@ -55,6 +55,8 @@ struct SearchState {
 
 struct Counters {
   long long running, head, finished, last_exit_step;
+  long long step, max_steps;  // device-side step counter of ts_run's graph loop
+  int cur_step, _pad;
   long long admit_lo, admit_hi;
   int work_count, work_next;
   int sum_fallbacks, sched_error;
@@ -138,15 +140,18 @@ struct Agg {
 // ---- warp helpers ------------------------------------------------------------
 // argmax with strict '>' and the lowest index winning ties (tree.py:258, 316);
 // lanes >= wp2 (a power of two >= width) must be invalid.
-__device__ __forceinline__ int warp_argmax(double v, bool valid, int wp2) {
-  int idx = valid ? (int)(threadIdx.x & 31) : 64;
-  for (int off = 1; off < wp2; off <<= 1) {
-    double ov = __shfl_xor_sync(FULL, v, off);
-    int oi = __shfl_xor_sync(FULL, idx, off);
-    bool take = (oi < 64) && (idx >= 64 || ov > v || (ov == v && oi < idx));
-    if (take) { v = ov; idx = oi; }
-  }
-  return __shfl_sync(FULL, idx, 0);
+// The double is mapped to an order-preserving u64 key (-0.0 folded into +0.0,
+// so equal values tie) and reduced with two REDUX steps; the lowest winning
+// lane is the first child among equals.  Invalid lanes never win.
+__device__ __forceinline__ int warp_argmax(double v, bool valid, int /*wp2*/) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v + 0.0);
+  const uint64_t key = (b >> 63) ? ~b : (b | (1ull << 63));
+  const unsigned hi = valid ? (unsigned)(key >> 32) : 0u;
+  const unsigned lo = valid ? (unsigned)key : 0u;
+  const unsigned mh = __reduce_max_sync(FULL, hi);
+  const unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+  const unsigned win = __ballot_sync(FULL, valid && hi == mh && lo == ml);
+  return __ffs(win) - 1;
 }
 
 // Running splitmix64 folds: for every expansion depth d a rollout can reach,
@@ -212,6 +217,8 @@ __global__ void k_reset_counters(Counters* c) {
   memset(c, 0, sizeof(Counters));
   c->last_exit_step = -1;
 }
+
+__global__ void k_set_max_steps(Counters* c, int max_steps) { c->max_steps = max_steps; }
 
 // Local counts before admission: {running, arrived-but-pending, unfinished}.
 __global__ void k_counts(View v, int step, long long* out) {
@@ -396,7 +403,7 @@ __device__ __forceinline__ int runs_lower(const double* runS, int nr, double s) 
 // The score sum Σ S (scheduler.py:165, CPython's Neumaier sum) equals the
 // correctly rounded exact sum when all compensation terms are exact (checked
 // below); it is computed exactly in 128-bit fixed point.
-__global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
+__device__ void targets_block(const View& v, int step, const ts_sched_record* rec) {
   extern __shared__ __align__(16) unsigned char smem[];
   long long* shl = (long long*)smem;                 // 80 long longs of scan scratch
   double* shd = (double*)(smem + 80 * 8);            // 80 doubles
@@ -622,7 +629,74 @@ __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched
   if (tid == 0) {
     v.ctr->work_count = (int)tot_loc;
     v.ctr->work_next = 0;
+    v.ctr->cur_step = step;
   }
+}
+
+__global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
+  targets_block(v, step, rec);
+}
+
+// One scheduler pass of a single-GPU run, fused: the loop test of the wave
+// driver, admit_jobs, parallelism_score records and compute_targets.  The
+// step counter lives on the device, so a CUDA-graph while-loop of
+// {k_sched, k_wave} runs a whole batch without host round trips.
+__global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cudaGraphConditionalHandle cond,
+                                              int use_cond) {
+  __shared__ int s_go;
+  Counters* c = v.ctr;
+  const int step = (int)c->step;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = v.n_local;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (v.arrival[mid] <= step) lo = mid + 1;
+      else hi = mid;
+    }
+    const long long unfinished = (long long)v.n_local - c->finished;
+    const bool go = unfinished > 0 && step < c->max_steps && step < v.log1p_n;
+    if (go) {
+      long long q = (long long)v.cfg.max_concurrency - c->running;
+      if (q > (long long)lo - c->head) q = (long long)lo - c->head;
+      if (q < 0) q = 0;
+      c->admit_lo = c->head;
+      c->admit_hi = c->head + q;
+      c->head += q;
+      c->running += q;
+    } else {
+      c->work_count = 0;
+      c->work_next = 0;
+      if (use_cond) cudaGraphSetConditional(cond, 0);
+    }
+    s_go = go;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const long long alo = c->admit_lo, ahi = c->admit_hi;
+  const ts_config& cf = v.cfg;
+  for (int i = threadIdx.x; i < v.n_local; i += TT) {
+    SearchState* st = v.st + i;
+    int state = st->state;
+    if (i >= alo && i < ahi) {
+      state = ST_RUNNING;
+      st->state = ST_RUNNING;
+      st->admit_step = step;
+    }
+    ts_sched_record r;
+    r.score = 0.0;
+    r.flags = 0;
+    r._pad = 0;
+    if (state == ST_RUNNING) {
+      const double ratio = st->job_best / cf.positive_exit_threshold;
+      const bool boosted = ratio > cf.proximity;
+      r.score = v.log1p_tab[step - v.arrival[i]] + (boosted ? cf.beta : 0.0);
+      r.flags = 1u | (st->completed >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
+    }
+    rec[i] = r;
+  }
+  __syncthreads();
+  targets_block(v, step, rec);
+  if (threadIdx.x == 0) c->step = step + 1;
 }
 
 // ---- the wave: one warp per running search ----------------------------------
@@ -1103,6 +1177,7 @@ __global__ void __launch_bounds__(WAVE_THREADS) k_wave(View v, int step) {
   const int lane = threadIdx.x & 31;
   WaveStats ws = {0, 0, 0, 0, 0, 0};
   const int count = v.ctr->work_count;
+  if (step < 0) step = v.ctr->cur_step;
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(&v.ctr->work_next, 1);
@@ -1216,6 +1291,11 @@ struct ts_engine {
   long long launches = 0;
   std::vector<cudaEvent_t> wave_ev;  // start/stop pairs of every wave since load
   size_t wave_ev_used = 0;
+  // ts_run: CUDA graph with a device-driven while loop over {k_sched, k_wave}
+  cudaGraph_t run_graph = nullptr;
+  cudaGraphExec_t run_exec = nullptr;
+  View run_view;
+  bool graph_failed = false;
 };
 
 namespace {
@@ -1255,6 +1335,7 @@ int grow(ts_engine* e, T*& p, size_t n, size_t& have, const char* what) {
 
 View make_view(ts_engine* e) {
   View v;
+  memset(&v, 0, sizeof(v));
   v.no = e->no;
   v.W = e->W;
   v.prior = e->prior;
@@ -1348,6 +1429,82 @@ int validate_config(ts_engine* e, const ts_config& c) {
   return TS_OK;
 }
 
+int wave_grid(ts_engine* e, int& blocks_out) {
+  int k = e->nslot == 1 ? 0 : e->nslot == 2 ? 1 : 2;
+  int blocks = e->wave_blocks[k];
+  if (blocks <= 0) {
+    int per = 0;
+    cudaError_t rc;
+    if (k == 0) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<1>, WAVE_THREADS, 0);
+    else if (k == 1) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<2>, WAVE_THREADS, 0);
+    else rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<4>, WAVE_THREADS, 0);
+    if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
+    blocks = std::max(1, per) * e->sm_count;
+    e->wave_blocks[k] = blocks;
+  }
+  blocks = std::min(blocks, (e->n_local + WAVE_THREADS / 32 - 1) / (WAVE_THREADS / 32));
+  blocks_out = std::max(blocks, 1);
+  return TS_OK;
+}
+
+void* wave_fn(ts_engine* e) {
+  if (e->nslot == 1) return (void*)k_wave<1>;
+  if (e->nslot == 2) return (void*)k_wave<2>;
+  return (void*)k_wave<4>;
+}
+
+void destroy_run_graph(ts_engine* e) {
+  if (e->run_exec) cudaGraphExecDestroy(e->run_exec);
+  if (e->run_graph) cudaGraphDestroy(e->run_graph);
+  e->run_exec = nullptr;
+  e->run_graph = nullptr;
+}
+
+// while (cond) { k_sched; k_wave }, cond cleared by k_sched when the batch is done
+int build_run_graph(ts_engine* e, const View& v) {
+  destroy_run_graph(e);
+  int blocks = 0, rc;
+  if ((rc = wave_grid(e, blocks))) return rc;
+  cudaGraph_t g = nullptr;
+  TS_CUDA_TRY(e, cudaGraphCreate(&g, 0));
+  e->run_graph = g;
+  cudaGraphConditionalHandle h;
+  TS_CUDA_TRY(e, cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cn;
+  TS_CUDA_TRY(e, cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  View vv = v;
+  ts_sched_record* rec = e->records;
+  int use_cond = 1, stepm1 = -1;
+  void* a1[] = {(void*)&vv, (void*)&rec, (void*)&h, (void*)&use_cond};
+  cudaKernelNodeParams k1;
+  memset(&k1, 0, sizeof(k1));
+  k1.func = (void*)k_sched;
+  k1.gridDim = dim3(1);
+  k1.blockDim = dim3(TT);
+  k1.sharedMemBytes = (unsigned)targets_smem();
+  k1.kernelParams = a1;
+  cudaGraphNode_t n1, n2;
+  TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1));
+  void* a2[] = {(void*)&vv, (void*)&stepm1};
+  cudaKernelNodeParams k2;
+  memset(&k2, 0, sizeof(k2));
+  k2.func = wave_fn(e);
+  k2.gridDim = dim3(blocks);
+  k2.blockDim = dim3(WAVE_THREADS);
+  k2.sharedMemBytes = 0;
+  k2.kernelParams = a2;
+  TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
+  TS_CUDA_TRY(e, cudaGraphInstantiate(&e->run_exec, g, 0));
+  e->run_view = v;
+  return TS_OK;
+}
+
 int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   int k = e->nslot == 1 ? 0 : e->nslot == 2 ? 1 : 2;
   int blocks = e->wave_blocks[k];
@@ -1424,6 +1581,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
   if (cr == cudaSuccess) cr = cudaMalloc((void**)&e->counts, sizeof(long long) * 3);
   if (cr == cudaSuccess)
     cr = cudaFuncSetAttribute(k_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
+  if (cr == cudaSuccess)
+    cr = cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   if (cr != cudaSuccess) {
     *out = e;
     return cuda_fail(e, cr, "engine allocation");
@@ -1440,6 +1599,7 @@ int ts_engine_destroy(ts_engine* e) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
+  destroy_run_graph(e);
   delete e;
   return TS_OK;
 }
@@ -1598,22 +1758,54 @@ int ts_step_wave(ts_engine* e, int32_t step, void* stream) {
 
 int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* stream) {
   if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (max_steps < 0) return fail(e, TS_INVALID_ARGUMENT, "max_steps must be >= 0");
   cudaStream_t s = (cudaStream_t)stream;
   int rc;
-  const int check_every = 8;
-  long long host_counts[3];
-  int step = 0;
-  for (; step < max_steps; ++step) {
-    if ((rc = ts_step_counts(e, step, (int64_t*)e->counts, stream))) return rc;
-    if (step % check_every == 0 && step >= e->max_arrival) {
-      TS_CUDA_TRY(e, cudaMemcpyAsync(host_counts, e->counts, sizeof(host_counts), cudaMemcpyDeviceToHost, s));
-      TS_CUDA_TRY(e, cudaStreamSynchronize(s));
-      if (host_counts[2] == 0) break;
+  if ((rc = ensure_log1p(e, 1 << 16, s))) return rc;
+  if ((rc = ensure_step_times(e, e->log1p_n + 1, s))) return rc;
+  for (;;) {
+    k_set_max_steps<<<1, 1, 0, s>>>(e->ctr, max_steps);
+    TS_LAUNCH_CHECK(e, "k_set_max_steps");
+    View v = make_view(e);
+    bool graphed = false;
+    if (!e->graph_failed) {
+      if (!e->run_exec || memcmp(&v, &e->run_view, sizeof(View)) != 0) {
+        if (build_run_graph(e, v) != TS_OK) {
+          destroy_run_graph(e);
+          e->graph_failed = true;
+          cudaGetLastError();
+        }
+      }
+      if (e->run_exec) {
+        TS_CUDA_TRY(e, cudaGraphLaunch(e->run_exec, s));
+        graphed = true;
+      }
     }
-    if ((rc = ts_step_admit(e, step, (const int64_t*)e->counts, 1, 0, stream))) return rc;
-    if ((rc = ts_step_records(e, step, e->records, stream))) return rc;
-    if ((rc = ts_step_targets(e, step, e->records, stream))) return rc;
-    if ((rc = ts_step_wave(e, step, stream))) return rc;
+    Counters c;
+    if (!graphed) {
+      // host-driven stepping (same kernels) when conditional graphs are unavailable
+      int blocks = 0;
+      if ((rc = wave_grid(e, blocks))) return rc;
+      for (int it = 0;; ++it) {
+        k_sched<<<1, TT, targets_smem(), s>>>(v, e->records, cudaGraphConditionalHandle(), 0);
+        TS_LAUNCH_CHECK(e, "k_sched");
+        if ((rc = launch_wave(e, v, -1, s))) return rc;
+        if (it % 8 == 7) {
+          TS_CUDA_TRY(e, cudaMemcpyAsync(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
+          TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+          if (c.finished >= e->n_local || c.step >= max_steps || c.step >= e->log1p_n) break;
+        }
+      }
+    } else {
+      e->launches += 2;  // per-step kernels counted from the device step count below
+    }
+    TS_CUDA_TRY(e, cudaMemcpyAsync(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+    if (graphed) e->launches += 2 * c.step;
+    if (c.finished >= e->n_local || c.step >= max_steps) break;
+    // the log1p table bounds the device loop: grow it and continue
+    if ((rc = ensure_log1p(e, e->log1p_n * 2, s))) return rc;
+    if ((rc = ensure_step_times(e, e->log1p_n + 1, s))) return rc;
   }
   if (stats_out) return ts_read_stats(e, stats_out, stream);
   return TS_OK;
