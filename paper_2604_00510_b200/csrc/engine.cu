@@ -704,26 +704,30 @@ struct WaveStats {
   unsigned long long rollouts, launched, nodes, scored, levels, path_nodes;
 };
 
+constexpr int WAVE_THREADS = 128;
+constexpr int WAVE_WARPS = WAVE_THREADS / 32;
+
 // One wave of one search, executed by one warp.
 //
 // Per rollout the warp walks root→leaf (select_leaf) and leaf→terminal
-// (simulate_to_terminal).  Only the descent's critical path runs per level:
-// in selection one round of child loads + WU-PUCT + argmax; in simulation the
-// children's rewards/terminal flags (needed by greedy_child) and the fold
-// absorb.  Everything else an expansion produces — priors (with CPython's
-// Neumaier sum), tokens, node records, parent links, negative-exit counts — is
-// generated after the descent in one lane-parallel batch: lane l owns the
-// expansion at depth l, using the fold states frozen at that depth.
+// (simulate_to_terminal).  Each selection level is one round of child loads,
+// WU-PUCT and an argmax.  Each simulation level computes, lane j = child j,
+// everything generate_steps draws for the child (reward, raw prior, tokens,
+// terminal flag) from the running fold states; greedy_child needs only the
+// rewards, the other draws fill the issue slots the dependent chain leaves
+// idle and are staged in shared memory.  After the descent one lane-parallel
+// batch (lane l = the expansion at depth l) normalises the priors with
+// CPython's Neumaier sum, writes the node records and parent links and counts
+// negative-exit leaves.
 //
 // Lane l also keeps path node l+1 in registers (id, meta, N|O word, W, reward,
 // prefix aggregate, golden flag, chosen child index), so registration and a
-// single-rollout backup are pure stores, and subtree-exhaustion propagates up
-// the path without loads.
-template <int NSLOT>
-__device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
-  constexpr int GS = 8 * NSLOT;
+// single-rollout backup are pure stores, and subtree exhaustion propagates up
+// the path without loads.  WT = compile-time width (0: runtime, <= 32).
+template <int NSLOT, int WT>
+__device__ void search_wave(const View& v, int s, int step, WaveStats& ws, double* s_raw, double* s_rew) {
+  constexpr int WS = WT ? WT : TS_MAX_WIDTH;  // shared-memory row stride
   const int lane = threadIdx.x & 31;
-  const int dl = lane % GS;  // depth index of this lane's fold states
   const ts_config& cf = v.cfg;
   SearchState* S = v.st + s;
   const ts_problem* pb = v.prob + s;
@@ -743,9 +747,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
   const bool has_shared = pb->has_shared != 0;
   const double off_lo = pb->off_lo, off_hi = pb->off_hi;
   const double sh_lo = pb->shared_lo, sh_hi = pb->shared_hi;
-  const int width = min(cf.expand_width, pb->branching);
-  int wp2 = 1;
-  while (wp2 < width) wp2 <<= 1;
+  const int width = WT ? WT : min(cf.expand_width, pb->branching);
   const int scheme = cf.scheme;
   const bool strict = cf.strict_negative_exit != 0;
   const bool prefix_bound = cf.futility_bound == TS_BOUND_PREFIX_AGGREGATE;
@@ -790,7 +792,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
   long long tok_acc = 0;  // per-lane token tally, reduced once per wave
   // last rollout's path registers (the P=1 backup uses them directly)
   int pnode = -1, plen = 0, pj = 0;
-  uint32_t pmeta = 0;
+  uint32_t pmeta = 0, lvl_term = 0;
   uint64_t pno = 0;
   double pW = 0.0, prew = 0.0, pagg = 1.0, pscore = 0.0;
   bool pgold = false;
@@ -848,7 +850,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
       if (!vb) { status = TS_EXHAUSTED; break; }
       scored += __popc(vb);
       ++levels;
-      const int j = warp_argmax(sc, valid, wp2);
+      const int j = warp_argmax(sc, valid, 0);
       node = fc + j;
       ++depth;
       nmeta = __shfl_sync(FULL, cm, j);
@@ -863,14 +865,14 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
         pnode = node; pmeta = nmeta; pno = nno; pW = nW; prew = nrew; pagg = agg.a; pgold = golden; pj = j;
       }
 #pragma unroll
-      for (int k = 0; k < NSLOT; ++k)
-        if (dl >= depth) h[k] = sm64(h[k] ^ (uint64_t)j);
+      for (int k = 0; k < NSLOT; ++k) h[k] = sm64(h[k] ^ (uint64_t)j);
     }
     if (status != TS_OK) break;
     const int d0 = depth;  // the selected non-terminal leaf
     const int fc0 = nnodes;
 
-    // --- simulate_to_terminal (tree.py:322-349): critical path only ---
+    // --- simulate_to_terminal (tree.py:322-349) with generate_steps replayed
+    //     (backend.py:230-269); lane j = child j ---
     bool forced = false;
     while (true) {
       if (depth >= cf.depth_cap) { forced = true; break; }  // tree.py:340-343
@@ -878,16 +880,19 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
       const int d = depth;
       const int len = d + 1;
       const uint64_t hr = state_at<NSLOT, 1>(h, d);
+      const uint64_t hp = state_at<NSLOT, 0>(h, d);
+      const uint64_t hk = state_at<NSLOT, 2>(h, d);
       const double graw = __shfl_sync(FULL, grew, d);
       const int gnext = __shfl_sync(FULL, gstep, d);
       const bool gchild = golden && len <= glen && lane == gnext;
+      const uint64_t jj = (uint64_t)lane;
       double rew;
       if (gchild) {
         rew = graw;
       } else {
         const bool shr = has_shared && len <= hidden;
         const double lo = shr ? sh_lo : off_lo, hi = shr ? sh_hi : off_hi;
-        rew = lo + (hi - lo) * u53(sm64(hr ^ (uint64_t)lane));
+        rew = lo + (hi - lo) * u53(sm64(hr ^ jj));
       }
       bool term;
       if (len < bdepth) {
@@ -896,10 +901,21 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
         term = true;
       } else {
         const uint64_t he = state_at<NSLOT, 3>(h, d);
-        term = gchild || (sm64(he ^ (uint64_t)lane) & 1ull) != 0;  // not _branch_extends
+        term = gchild || (sm64(he ^ jj) & 1ull) != 0;  // not _branch_extends
       }
-      const int j = warp_argmax(rew, lane < width, wp2);  // greedy_child (tree.py:307-319)
-      const bool jterm = __shfl_sync(FULL, term, j);
+      const bool vl = lane < width;
+      const int j = warp_argmax(rew, vl, 0);  // greedy_child (tree.py:307-319)
+      // off the critical path: raw prior and token count of child `lane`
+      const double raw = 0.5 + u53(sm64(hp ^ jj));
+      const long long tok = 40 + (long long)(sm64(hk ^ jj) % 81ull);
+      const unsigned tmask = __ballot_sync(FULL, vl && term);
+      if (vl) {
+        s_raw[d * WS + lane] = raw;
+        s_rew[d * WS + lane] = rew;
+        tok_acc += tok;
+      }
+      if (lane == d) lvl_term = tmask;
+      const bool jterm = (tmask >> j) & 1u;
       node = nnodes + j;
       nnodes += width;
       ++depth;
@@ -912,13 +928,13 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
         pnode = node; pmeta = nmeta; pno = O_ONE; pW = 0.0; prew = nrew; pagg = agg.a; pgold = golden; pj = j;
       }
 #pragma unroll
-      for (int k = 0; k < NSLOT; ++k)
-        if (dl >= depth) h[k] = sm64(h[k] ^ (uint64_t)j);
+      for (int k = 0; k < NSLOT; ++k) h[k] = sm64(h[k] ^ (uint64_t)j);
       if (jterm) break;
     }
     if (status != TS_OK) break;
-    const int dend = depth;        // terminal (or force-terminated) node depth
-    const int nlev = dend - d0;    // expansions happened at depths d0 .. dend-1
+    __syncwarp();
+    const int dend = depth;      // terminal (or force-terminated) node depth
+    const int nlev = dend - d0;  // expansions happened at depths d0 .. dend-1
     plen = dend;
     pscore = agg.value(scheme);
 
@@ -928,51 +944,45 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
     const uint32_t up_meta = __shfl_up_sync(FULL, pmeta, 1);
     const double up_rew = __shfl_up_sync(FULL, prew, 1);
     const double up_agg = __shfl_up_sync(FULL, pagg, 1);
-    const bool up_gold = __shfl_up_sync(FULL, pgold, 1);
+    const int upj = __shfl_up_sync(FULL, pj, 1);
     const int node_l = lane == 0 ? 0 : up_node;
     const uint32_t leaf_meta = lane == 0 ? root_meta : up_meta;
     const double rew_l = lane == 0 ? 1.0 : up_rew;
     const double agg_l = lane == 0 ? 1.0 : up_agg;
-    const bool gold_l = lane == 0 ? (glen >= 0) : up_gold;
-    // frozen fold states of depth `lane` for the four tags
-    const uint64_t st_prior = __shfl_sync(FULL, h[0], (0 / NSLOT) * GS + dl);
-    const uint64_t st_rew = __shfl_sync(FULL, h[1 % NSLOT], (1 / NSLOT) * GS + dl);
-    const uint64_t st_tok = __shfl_sync(FULL, h[2 % NSLOT], (2 / NSLOT) * GS + dl);
-    const uint64_t st_ext = __shfl_sync(FULL, h[3 % NSLOT], (3 / NSLOT) * GS + dl);
     const bool act = lane >= d0 && lane < d0 + nlev;
-    int live = 0;       // non-terminal children of this level
-    int ne_cnt = 0;     // NE: check-relevant viable new leaves
+    int live = 0;    // non-terminal children of this level
+    int ne_cnt = 0;  // NE: check-relevant viable new leaves
     uint32_t meta_l = 0;
     if (act) {
       const int l = lane;
       const int len = l + 1;
       const int fcl = fc0 + (l - d0) * width;
+      const double* rawl = s_raw + l * WS;
+      const double* rewl = s_rew + l * WS;
       // total = sum(raw_priors): CPython Neumaier sum in child order
-      double tot = 0.5 + u53(sm64(st_prior)), cc = 0.0;
-      for (int i = 1; i < width; ++i) {
-        const double x = 0.5 + u53(sm64(st_prior ^ (uint64_t)i));
+      double tot = rawl[0], cc = 0.0;
+#pragma unroll
+      for (int i = 1; i < WS; ++i) {
+        if (i >= width) break;
+        const double x = rawl[i];
         const double t = tot + x;
         if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
         else cc += (x - t) + tot;
         tot = t;
       }
       if (cc != 0.0 && isfinite(cc)) tot += cc;
-      const bool shr = has_shared && len <= hidden;
-      const double lo = shr ? sh_lo : off_lo, hi = shr ? sh_hi : off_hi;
       const bool last = l == dend - 1;
-      for (int j = 0; j < width; ++j) {
-        const bool gch = gold_l && len <= glen && j == gstep;
-        const double rew = gch ? grew : lo + (hi - lo) * u53(sm64(st_rew ^ (uint64_t)j));
-        bool term;
-        if (len < bdepth) term = false;
-        else if (len >= bdepth + 1) term = true;
-        else term = gch || (sm64(st_ext ^ (uint64_t)j) & 1ull) != 0;
-        tok_acc += 40 + (long long)(sm64(st_tok ^ (uint64_t)j) % 81ull);
+      const bool rel_d1 = strict || d1r >= theta1;
+#pragma unroll
+      for (int j = 0; j < WS; ++j) {
+        if (j >= width) break;
+        const double rew = rewl[j];
+        const bool term = (lvl_term >> j) & 1u;
         const int c = fcl + j;
         const bool onpath = j == pj;
         NO[c] = onpath ? O_ONE : 0ull;
         Wv[c] = 0.0;
-        PR[c] = (0.5 + u53(sm64(st_prior ^ (uint64_t)j))) / tot;
+        PR[c] = rawl[j] / tot;
         RW[c] = rew;
         PA[c] = node_l;
         // the on-path child expanded at the next level gets its fc/meta from lane l+1
@@ -985,30 +995,24 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
         if (!term) {
           ++live;
           // NE: a new non-terminal leaf, check-relevant and viable (scoring.py:119-175)
-          const bool rel = strict || (len == 1 ? rew : d1r) >= theta1;
-          const double bound = prefix_bound ? fmin(rew, l == 0 ? rew : (scheme == TS_SCHEME_PRODUCT ? agg_l * rew
-                                                                         : (rew < agg_l ? rew : agg_l)))
-                                            : rew;
+          const bool rel = len == 1 ? (strict || rew >= theta1) : rel_d1;
+          double bound = rew;
+          if (prefix_bound && l > 0) {
+            const double pre = scheme == TS_SCHEME_PRODUCT ? agg_l * rew : (rew < agg_l ? rew : agg_l);
+            bound = fmin(rew, pre);
+          }
           if (rel && !(bound < tau)) ++ne_cnt;
         }
       }
       // the expanded node (path node l) stops being a leaf
       if (l >= 1) {
-        const bool rel = strict || d1r >= theta1;
         const double bound = prefix_bound ? fmin(rew_l, agg_l) : rew_l;
-        if (rel && !(bound < tau)) --ne_cnt;
+        if (rel_d1 && !(bound < tau)) --ne_cnt;
       }
-    }
-    // meta of path node l: leaf meta (l == d0) or the fresh node's own fields
-    {
-      const int upj = __shfl_up_sync(FULL, pj, 1);
-      if (act) {
-        const int l = lane;
-        uint32_t m = l == d0 ? leaf_meta : ((uint32_t)l | ((uint32_t)upj << SH_REF));
-        meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
-        FC[node_l] = fc0 + (l - d0) * width;
-        ME[node_l] = meta_l;
-      }
+      const uint32_t m = l == d0 ? leaf_meta : ((uint32_t)l | ((uint32_t)upj << SH_REF));
+      meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
+      FC[node_l] = fcl;
+      ME[node_l] = meta_l;
     }
     // refresh the path meta registers (lane l-1 holds path node l)
     {
@@ -1024,7 +1028,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
       const int lid = __shfl_sync(FULL, pnode, dend - 1);
       if (lane == 0) ME[lid] = m;
     }
-    viable += __reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
+    viable += (int)__reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
     if (forced) {
       // NE: the force-terminated leaf leaves the leaf set
       const bool rel = strict || d1r >= theta1;
@@ -1170,11 +1174,14 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws) {
 }
 
 
-constexpr int WAVE_THREADS = 128;
 
-template <int NSLOT>
+template <int NSLOT, int WT>
 __global__ void __launch_bounds__(WAVE_THREADS) k_wave(View v, int step) {
-  const int lane = threadIdx.x & 31;
+  constexpr int WS = WT ? WT : TS_MAX_WIDTH;
+  extern __shared__ double wsm[];  // per warp: raw priors and rewards, [32 depths][WS]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* s_raw = wsm + (size_t)warp * 2 * 32 * WS;
+  double* s_rew = s_raw + 32 * WS;
   WaveStats ws = {0, 0, 0, 0, 0, 0};
   const int count = v.ctr->work_count;
   if (step < 0) step = v.ctr->cur_step;
@@ -1183,7 +1190,7 @@ __global__ void __launch_bounds__(WAVE_THREADS) k_wave(View v, int step) {
     if (lane == 0) item = atomicAdd(&v.ctr->work_next, 1);
     item = __shfl_sync(FULL, item, 0);
     if (item >= count) break;
-    search_wave<NSLOT>(v, v.work[item], step, ws);
+    search_wave<NSLOT, WT>(v, v.work[item], step, ws, s_raw, s_rew);
   }
   if (lane == 0 && ws.launched) {
     atomicAdd(&v.ctr->rollouts, ws.rollouts);
@@ -1194,6 +1201,15 @@ __global__ void __launch_bounds__(WAVE_THREADS) k_wave(View v, int step) {
     atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
   }
 }
+
+// kernel table: [nslot 1/2/4][width 2/4/8/runtime]
+typedef void (*wave_kernel_t)(View, int);
+__device__ __host__ inline int wkind_of_width(int w) { return w == 2 ? 0 : w == 4 ? 1 : w == 8 ? 2 : 3; }
+static const wave_kernel_t kWave[3][4] = {
+    {k_wave<1, 2>, k_wave<1, 4>, k_wave<1, 8>, k_wave<1, 0>},
+    {k_wave<2, 2>, k_wave<2, 4>, k_wave<2, 8>, k_wave<2, 0>},
+    {k_wave<4, 2>, k_wave<4, 4>, k_wave<4, 8>, k_wave<4, 0>},
+};
 
 __global__ void k_latency(View v, unsigned long long* out, int n) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1251,7 +1267,8 @@ struct ts_engine {
   ts_config cfg{};
   std::string err;
   int sm_count = 148;
-  int wave_blocks[3] = {0, 0, 0};
+  int wave_blocks[12] = {0};
+  int wkind = 3;
   // sizes
   int n_local = 0, goff = 0, n_global = 0, cap_searches = 0, cap_global = 0;
   long long cap = 0, pool_nodes = 0;
@@ -1429,28 +1446,31 @@ int validate_config(ts_engine* e, const ts_config& c) {
   return TS_OK;
 }
 
+int wave_index(ts_engine* e) { return (e->nslot == 1 ? 0 : e->nslot == 2 ? 1 : 2) * 4 + e->wkind; }
+size_t wave_smem_of(int wkind) {
+  const int ws = wkind == 0 ? 2 : wkind == 1 ? 4 : wkind == 2 ? 8 : TS_MAX_WIDTH;
+  return (size_t)WAVE_WARPS * 2 * 32 * ws * sizeof(double);
+}
+
 int wave_grid(ts_engine* e, int& blocks_out) {
-  int k = e->nslot == 1 ? 0 : e->nslot == 2 ? 1 : 2;
+  const int k = wave_index(e);
   int blocks = e->wave_blocks[k];
   if (blocks <= 0) {
     int per = 0;
-    cudaError_t rc;
-    if (k == 0) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<1>, WAVE_THREADS, 0);
-    else if (k == 1) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<2>, WAVE_THREADS, 0);
-    else rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<4>, WAVE_THREADS, 0);
+    cudaError_t rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)kWave[k / 4][k % 4],
+                                                                   WAVE_THREADS, wave_smem_of(k % 4));
     if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
     blocks = std::max(1, per) * e->sm_count;
     e->wave_blocks[k] = blocks;
   }
-  blocks = std::min(blocks, (e->n_local + WAVE_THREADS / 32 - 1) / (WAVE_THREADS / 32));
+  blocks = std::min(blocks, (e->n_local + WAVE_WARPS - 1) / WAVE_WARPS);
   blocks_out = std::max(blocks, 1);
   return TS_OK;
 }
 
 void* wave_fn(ts_engine* e) {
-  if (e->nslot == 1) return (void*)k_wave<1>;
-  if (e->nslot == 2) return (void*)k_wave<2>;
-  return (void*)k_wave<4>;
+  const int k = wave_index(e);
+  return (void*)kWave[k / 4][k % 4];
 }
 
 void destroy_run_graph(ts_engine* e) {
@@ -1497,7 +1517,7 @@ int build_run_graph(ts_engine* e, const View& v) {
   k2.func = wave_fn(e);
   k2.gridDim = dim3(blocks);
   k2.blockDim = dim3(WAVE_THREADS);
-  k2.sharedMemBytes = 0;
+  k2.sharedMemBytes = (unsigned)wave_smem_of(e->wkind);
   k2.kernelParams = a2;
   TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
   TS_CUDA_TRY(e, cudaGraphInstantiate(&e->run_exec, g, 0));
@@ -1506,21 +1526,8 @@ int build_run_graph(ts_engine* e, const View& v) {
 }
 
 int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
-  int k = e->nslot == 1 ? 0 : e->nslot == 2 ? 1 : 2;
-  int blocks = e->wave_blocks[k];
-  if (blocks <= 0) {
-    int per = 0;
-    cudaError_t rc;
-    if (k == 0) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<1>, WAVE_THREADS, 0);
-    else if (k == 1) rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<2>, WAVE_THREADS, 0);
-    else rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_wave<4>, WAVE_THREADS, 0);
-    if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
-    blocks = std::max(1, per) * e->sm_count;
-    e->wave_blocks[k] = blocks;
-  }
-  // never more warps than searches
-  blocks = std::min(blocks, (e->n_local + WAVE_THREADS / 32 - 1) / (WAVE_THREADS / 32));
-  blocks = std::max(blocks, 1);
+  int blocks = 0, rc;
+  if ((rc = wave_grid(e, blocks))) return rc;
   if (e->wave_ev_used + 2 > e->wave_ev.size()) {
     for (int i = 0; i < 64; ++i) {
       cudaEvent_t ev;
@@ -1529,9 +1536,8 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
     }
   }
   cudaEventRecord(e->wave_ev[e->wave_ev_used], s);
-  if (k == 0) k_wave<1><<<blocks, WAVE_THREADS, 0, s>>>(v, step);
-  else if (k == 1) k_wave<2><<<blocks, WAVE_THREADS, 0, s>>>(v, step);
-  else k_wave<4><<<blocks, WAVE_THREADS, 0, s>>>(v, step);
+  const int k = wave_index(e);
+  kWave[k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
   TS_LAUNCH_CHECK(e, "k_wave");
   cudaEventRecord(e->wave_ev[e->wave_ev_used + 1], s);
   e->wave_ev_used += 2;
@@ -1583,6 +1589,10 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     cr = cudaFuncSetAttribute(k_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   if (cr == cudaSuccess)
     cr = cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
+  for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
+    for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
+      cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)wave_smem_of(b));
   if (cr != cudaSuccess) {
     *out = e;
     return cuda_fail(e, cr, "engine allocation");
@@ -1631,6 +1641,12 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   }
   e->max_arrival = prev_arr;
   e->nslot = max_len <= 8 ? 1 : max_len <= 16 ? 2 : 4;
+  {
+    int w0 = std::min(c.expand_width, hp[0].branching);
+    bool same = true;
+    for (int i = 1; i < n_local && same; ++i) same = std::min(c.expand_width, hp[i].branching) == w0;
+    e->wkind = same ? wkind_of_width(w0) : 3;
+  }
   // nodes a search can create: every launched rollout (<= budget) expands at
   // most min(depth_cap, base_depth+1) levels of `width` children
   const long long cap = 1 + (long long)c.rollout_budget * max_width * max_len;
