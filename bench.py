@@ -156,24 +156,6 @@ class Dist:
         return float(t.item())
 
 
-def run_sharded(eng, d: Dist, n_local: int, counts, allc, recs, allr, max_steps=1 << 30):
-    """The wave loop of one rank: counts → all-gather → admit → records →
-    all-gather (NCCL over NVLink) → targets → wave."""
-    import torch
-
-    for step in range(max_steps):
-        eng.step_counts(step, counts.data_ptr())
-        d.pg.all_gather_into_tensor(allc, counts)
-        if step % 8 == 0 and int(allc.view(-1, 3)[:, 2].sum().item()) == 0:
-            return step
-        eng.step_admit(step, allc.data_ptr(), d.world, d.rank)
-        eng.step_records(step, recs.data_ptr())
-        d.pg.all_gather_into_tensor(allr, recs)
-        eng.step_targets(step, allr.data_ptr())
-        eng.step_wave(step)
-    return max_steps
-
-
 def algorithmic_bytes(st) -> int:
     return (B_SCORED * st.children_scored + B_LEVEL * st.select_levels + B_NODE * st.nodes
             + B_PATH * st.path_nodes)
@@ -226,16 +208,18 @@ def bench_ours(args, d: Dist):
     cfg = search_config(n_total)
     eng = Engine(cfg, d.local)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
-    allc = torch.zeros(3 * N, dtype=torch.int64, device="cuda")
-    recs = torch.zeros(PER_GPU * 16, dtype=torch.uint8, device="cuda")
-    allr = torch.zeros(n_total * 16, dtype=torch.uint8, device="cuda")
+
+    sharded = None
+    if N > 1:
+        from paper_2604_00510_b200.distributed import ShardedRun
+
+        sharded = ShardedRun(eng, d.pg, PER_GPU, n_total, torch.device("cuda", d.local))
 
     def one_step():
         if N == 1:
             eng.run()
         else:
-            run_sharded(eng, d, PER_GPU, counts, allc, recs, allr)
+            sharded.run()
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):

@@ -1,0 +1,100 @@
+"""Multi-GPU driver: one process per GPU, searches block-sharded over ranks.
+
+Searches are independent trees and the synthetic backend is stateless keyed
+RNG, so each rank owns a contiguous block of the global run queue
+(``Engine.load(table, global_offset, n_global)``).  The only data crossing
+GPUs per wave are the boosting scheduler's global terms:
+
+* 3 int64 counts per rank {running, arrived-but-pending, unfinished} — the
+  global FIFO admission (admit_jobs, scheduler.py:131-140) and the loop test;
+* one 16-byte ``ts_sched_record`` per search {S(i,t), flags} — the ordered
+  score sum and the merge ranks of compute_targets (scheduler.py:143-187).
+
+Both are all-gathered (NCCL over NVLink on GPUs; any torch.distributed
+backend works) in rank order, which is global run-queue order, and every rank
+then runs the scheduler kernel on the same global records and keeps its slice.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+RECORD_BYTES = 16
+COUNT_WORDS = 3
+
+
+def shard_bounds(n_total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of the global run queue owned by ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(n_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class ShardedRun:
+    """The per-wave exchange loop of one rank.
+
+    ``engine`` exposes the step API of :class:`paper_2604_00510_b200.engine.Engine`
+    (step_counts/step_admit/step_records/step_targets/step_wave taking device
+    pointers); ``dist`` is ``torch.distributed`` with an initialised group.
+    """
+
+    def __init__(self, engine, dist, n_local: int, n_total: int, device, group=None, check_every: int = 8):
+        import torch
+
+        self.engine = engine
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > 1 and any(s != n_local for s in self._all_sizes(n_local, device)):
+            raise ValueError("all-gather needs equal shard sizes; pad the run queue")
+        self.n_local = n_local
+        self.n_total = n_total
+        self.check_every = max(1, check_every)
+        self.counts = torch.zeros(COUNT_WORDS, dtype=torch.int64, device=device)
+        self.all_counts = torch.zeros(COUNT_WORDS * self.world, dtype=torch.int64, device=device)
+        self.records = torch.zeros(n_local * RECORD_BYTES, dtype=torch.uint8, device=device)
+        self.all_records = torch.zeros(n_total * RECORD_BYTES, dtype=torch.uint8, device=device)
+
+    def _all_sizes(self, n_local, device):
+        import torch
+
+        t = torch.tensor([n_local], dtype=torch.int64, device=device)
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [int(x.item()) for x in out]
+
+    def _gather(self, out, inp):
+        if self.dist.get_backend(self.group) == "nccl":
+            self.dist.all_gather_into_tensor(out, inp, group=self.group)
+            return
+        parts = list(out.chunk(self.world))
+        self.dist.all_gather(parts, inp, group=self.group)
+        if parts[0].data_ptr() != out.data_ptr():  # backend returned fresh tensors
+            out.copy_(__import__("torch").cat(parts))
+
+    def run(self, max_steps: int = 1 << 30) -> int:
+        """Advance waves until every search of every rank has exited; returns
+        the number of loop iterations (the reference loop's ``steps`` when it
+        breaks exactly at the first all-finished check)."""
+        eng = self.engine
+        for step in range(max_steps):
+            eng.step_counts(step, self.counts.data_ptr())
+            self._gather(self.all_counts, self.counts)
+            if step % self.check_every == 0:
+                unfinished = int(self.all_counts.view(-1, COUNT_WORDS)[:, 2].sum().item())
+                if unfinished == 0:
+                    return step
+            eng.step_admit(step, self.all_counts.data_ptr(), self.world, self.rank)
+            eng.step_records(step, self.records.data_ptr())
+            self._gather(self.all_records, self.records)
+            eng.step_targets(step, self.all_records.data_ptr())
+            eng.step_wave(step)
+        return max_steps
+
+
+def run_sharded(engine, dist, n_local: int, n_total: int, device, group=None,
+                max_steps: int = 1 << 30, check_every: int = 8) -> int:
+    return ShardedRun(engine, dist, n_local, n_total, device, group, check_every).run(max_steps)

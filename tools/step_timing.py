@@ -34,6 +34,11 @@ def main(mode):
             eng.step_targets(step, recs.data_ptr()); es[4].record()
             eng.step_wave(step); es[5].record()
             ev.append(es)
+            if rep == 1 and mode == "full" and step < 6:
+                torch.cuda.synchronize()
+                st = eng.stats()
+                print(f"  after wave {step}: launched={st.launched} rollouts={st.rollouts} nodes={st.nodes} "
+                      f"levels={st.select_levels} scored={st.children_scored} path={st.path_nodes}")
             step += 1
             if step % 8 == 0:
                 torch.cuda.synchronize()
