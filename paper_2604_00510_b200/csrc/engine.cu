@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -59,6 +60,7 @@ struct Counters {
   int cur_step, _pad;
   long long admit_lo, admit_hi;
   int work_count, work_next;
+  int heavy_count, heavy_next;  // searches with >= HEAVY_P rollouts this wave (pipelined CTA mode)
   int sum_fallbacks, sched_error;
   unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
 };
@@ -78,7 +80,9 @@ struct View {
   const ts_problem* prob;
   const int32_t* arrival;  // local arrival steps (non-decreasing)
   Counters* ctr;
-  int32_t* work;           // this wave's running local searches
+  int32_t* work;           // this wave's running local searches (single-warp mode)
+  int32_t* work_heavy;     // this wave's searches for the pipelined CTA mode
+  int32_t heavy_on;        // pipelined mode available (uniform width 2/4/8)
   int32_t* sp;             // scratch paths of a multi-rollout wave [n_local][budget][32]
   double* ss;              // scratch scores
   int32_t* sl;             // scratch lengths
@@ -286,6 +290,7 @@ __global__ void k_records(View v, int step, ts_sched_record* rec) {
 
 // ---- compute_targets (scheduler.py:143-187) in one CTA ------------------------
 constexpr int TT = 1024;
+constexpr int HEAVY_P = 8;  // rollouts in one wave from which a search runs in pipelined CTA mode
 constexpr int RUNCAP = 1536;  // runs per list kept in shared memory
 
 typedef unsigned __int128 u128;
@@ -572,7 +577,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   long long Rp = R - (tw0 + tw1);
   if (Rp < 0) Rp = 0;
   {
-    long long q0 = pos0, q1 = pos1, k0 = rid0 - 1, k1 = rid1 - 1, w = wpos;
+    long long q0 = pos0, q1 = pos1, k0 = rid0 - 1, k1 = rid1 - 1;
     double p0 = prev0, p1 = prev1;
     for (int i = lo; i < hi; ++i) {
       ts_sched_record r = rec[i];
@@ -620,15 +625,34 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
       } else if ((r.flags & 2u) == 0 && boost_on) {
         // gated: stays serial; advance nothing
       }
-      if (i >= glo && i < ghi) {
-        v.st[i - glo].target = (int)tgt;
-        v.work[w++] = i - glo;
-      }
+      if (i >= glo && i < ghi) v.st[i - glo].target = (int)tgt;
     }
   }
+  (void)wpos;
+  // phase 5: split the local running searches into the single-warp and the
+  // pipelined (many rollouts this wave) work lists, in run-queue order
+  long long nh = 0, nlt = 0;
+  const int loc_lo = max(lo, glo) - glo, loc_hi = min(hi, ghi) - glo;
+  for (int i = loc_lo; i < loc_hi; ++i) {
+    const SearchState& st = v.st[i];
+    if (st.state != ST_RUNNING) continue;
+    if (v.heavy_on && min(st.target, cf.rollout_budget - st.completed) >= HEAVY_P) ++nh;
+    else ++nlt;
+  }
+  long long tot_h, tot_l;
+  long long ph = block_scan_add(nh, &tot_h, shl);
+  long long pl = block_scan_add(nlt, &tot_l, shl);
+  for (int i = loc_lo; i < loc_hi; ++i) {
+    const SearchState& st = v.st[i];
+    if (st.state != ST_RUNNING) continue;
+    if (v.heavy_on && min(st.target, cf.rollout_budget - st.completed) >= HEAVY_P) v.work_heavy[ph++] = i;
+    else v.work[pl++] = i;
+  }
   if (tid == 0) {
-    v.ctr->work_count = (int)tot_loc;
+    v.ctr->work_count = (int)tot_l;
     v.ctr->work_next = 0;
+    v.ctr->heavy_count = (int)tot_h;
+    v.ctr->heavy_next = 0;
     v.ctr->cur_step = step;
   }
 }
@@ -666,6 +690,8 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
     } else {
       c->work_count = 0;
       c->work_next = 0;
+      c->heavy_count = 0;
+      c->heavy_next = 0;
       if (use_cond) cudaGraphSetConditional(cond, 0);
     }
     s_go = go;
@@ -1211,6 +1237,619 @@ static const wave_kernel_t kWave[3][4] = {
     {k_wave<4, 2>, k_wave<4, 4>, k_wave<4, 8>, k_wave<4, 0>},
 };
 
+// ---- pipelined CTA mode for searches with many rollouts in one wave ----------
+//
+// A wave's rollouts are sequential by definition: rollout k+1 selects against
+// the in-flight registrations (and expansions) of rollouts <= k.  But a
+// simulation only depends on its own selected leaf and path, and a later
+// selection only needs it once it reaches that leaf.  So one warp selects and
+// registers rollout after rollout while HEAVY_SIM warps simulate them, and the
+// simulators commit in rollout order (node ids in creation order, records,
+// subtree exhaustion, negative-exit counts).  Two waits keep this exactly the
+// sequential semantics:
+//  * the selector that arrives at a leaf whose expansion is not committed yet
+//    waits for that commit and then keeps descending;
+//  * a job whose exhaustion can propagate into pre-existing nodes ("risky":
+//    leaf depth >= min(base_depth, depth_cap) - 1, or width 1 — below that a
+//    fresh expansion always leaves a live child) is committed before the next
+//    selection starts.
+constexpr int HEAVY_SIM = 7;
+constexpr int HEAVY_THREADS = 32 * (HEAVY_SIM + 1);
+constexpr int HEAVY_RING = 16;
+
+struct HeavyJob {
+  int leaf, d0, risky, golden;
+  uint32_t leaf_meta, _pad;
+  double nrew, agg_a, agg_c, d1r;
+  int agg_n, _pad2;
+  int pnode[32];   // path node l+1 for l < d0 (the leaf is pnode[d0-1])
+  int pj[32];      // child index chosen at depth l
+};
+
+struct HeavyCtl {
+  volatile int issued, committed, done, status;
+  volatile int nnodes, viable;
+  unsigned long long created, tokens;
+};
+
+__device__ __forceinline__ void spin_until_ge(volatile int* p, int v) {
+  while (*p < v) __nanosleep(32);
+  __threadfence_block();
+}
+
+template <int NSLOT, int WT>
+__device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, int count, WaveStats& ws,
+                             uint64_t& rno_out, double& rW_out, int& decision_out) {
+  const int lane = threadIdx.x & 31;
+  const ts_config& cf = v.cfg;
+  const ts_problem* pb = v.prob + s;
+  const size_t base = (size_t)s * (size_t)v.cap;
+  uint64_t* NO = v.no + base;
+  double* Wv = v.W + base;
+  double* PR = v.prior + base;
+  double* RW = v.reward + base;
+  int32_t* FC = v.fc + base;
+  uint32_t* ME = v.meta + base;
+  const int bdepth = pb->base_depth;
+  const int glen = pb->golden_len;
+  const int width = WT;
+  const int scheme = cf.scheme;
+  const double c_puct = cf.c_puct;
+  const int gstep = lane < glen ? (int)pb->golden_path[lane] : -1;
+  const int risky_depth = min(bdepth, cf.depth_cap) - 1;
+  uint64_t rno = NO[0];
+  const double rW = Wv[0];
+  int decision = TS_EXIT_NONE;
+  int last_risky = -1;
+  int k = 0;
+  unsigned long long scored = 0, levels = 0;
+  for (; k < count; ++k) {
+    if (last_risky >= 0) spin_until_ge(&ctl->committed, last_risky + 1);
+    if (ctl->status != TS_OK) break;
+    uint32_t nmeta = ME[0];
+    if (!meta_expandable(nmeta)) {  // NoExpandableLeafError (tree.py:273-274)
+      if (k == 0) decision = -1;
+      break;
+    }
+    int node = 0, depth = 0, nfc = FC[0];
+    uint64_t nno = rno;
+    double nW = rW, nrew = 1.0;
+    int pnode = -1, pj = 0;
+    uint64_t pno = 0;
+    Agg agg;
+    agg.init();
+    bool golden = glen >= 0;
+    double d1r = 1.0;
+    int status = TS_OK;
+    for (;;) {
+      while (nmeta & M_KIDS) {
+        const long long pN = (long long)(uint32_t)nno, pO = (long long)(nno >> 32);
+        const double psq = sqrt((double)(pN + pO));
+        const double pq = pN == 0 ? 0.5 : nW / (double)pN;
+        const int fc = nfc;
+        bool valid = lane < width;
+        double sc = -INFINITY, cr = 0.0, cw = 0.0;
+        uint32_t cm = 0;
+        uint64_t cno = 0;
+        int cfc = -1;
+        if (valid) {
+          const int c = fc + lane;
+          cno = NO[c];
+          cw = Wv[c];
+          const double cp = PR[c];
+          cm = ME[c];
+          cr = RW[c];
+          cfc = FC[c];
+          valid = meta_expandable(cm);
+          if (valid) {
+            const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
+            const double q = cN == 0 ? pq : cw / (double)cN;
+            if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
+            sc = q + c_puct * cp * psq / (double)(1 + cN + cO);
+          }
+        }
+        const unsigned vb = __ballot_sync(FULL, valid);
+        if (__any_sync(FULL, status != TS_OK)) { status = TS_INVALID_ARGUMENT; break; }
+        if (!vb) { status = TS_EXHAUSTED; break; }
+        scored += __popc(vb);
+        ++levels;
+        const int j = warp_argmax(sc, valid, 0);
+        node = fc + j;
+        ++depth;
+        nmeta = __shfl_sync(FULL, cm, j);
+        nrew = __shfl_sync(FULL, cr, j);
+        nno = __shfl_sync(FULL, cno, j);
+        nW = __shfl_sync(FULL, cw, j);
+        nfc = __shfl_sync(FULL, cfc, j);
+        agg.add(nrew, scheme);
+        if (depth == 1) d1r = nrew;
+        golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
+        if (lane == depth - 1) { pnode = node; pno = nno; pj = j; }
+      }
+      if (status != TS_OK) break;
+      // a leaf whose expansion is still in flight: wait for its commit, descend on
+      const int c0 = ctl->committed, i0 = k;  // jobs [c0, k) are uncommitted
+      bool hit = false;
+      int jw = -1;
+      if (c0 + lane < i0) hit = ring[(c0 + lane) % HEAVY_RING].leaf == node;
+      const unsigned hm = __ballot_sync(FULL, hit);
+      if (!hm) break;
+      jw = c0 + __ffs(hm) - 1;
+      spin_until_ge(&ctl->committed, jw + 1);
+      if (ctl->status != TS_OK) { status = ctl->status; break; }
+      nmeta = ME[node];
+      nfc = FC[node];
+    }
+    if (status != TS_OK) {
+      if (lane == 0) atomicCAS((int*)&ctl->status, TS_OK, status);
+      break;
+    }
+    // in-flight registration of root..leaf (tree.py:282-283)
+    rno += O_ONE;
+    if (lane < depth) NO[pnode] = pno + O_ONE;
+    if (lane == 0) NO[0] = rno;
+    // hand the rollout to its simulator
+    if (k - ctl->committed >= HEAVY_RING) spin_until_ge(&ctl->committed, k - HEAVY_RING + 1);
+    HeavyJob& jb = ring[k % HEAVY_RING];
+    jb.pnode[lane] = pnode;
+    jb.pj[lane] = pj;
+    if (lane == 0) {
+      jb.leaf = node;
+      jb.d0 = depth;
+      jb.risky = (width == 1 || depth >= risky_depth) ? 1 : 0;
+      jb.golden = golden ? 1 : 0;
+      jb.leaf_meta = nmeta;
+      jb.nrew = nrew;
+      jb.agg_a = agg.a;
+      jb.agg_c = agg.c;
+      jb.agg_n = agg.n;
+      jb.d1r = d1r;
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) ctl->issued = k + 1;
+    if (width == 1 || depth >= risky_depth) last_risky = k;
+  }
+  if (lane == 0) ctl->done = 1;
+  spin_until_ge(&ctl->committed, k);
+  rno_out = rno;
+  rW_out = rW;
+  decision_out = decision;
+  ws.scored += scored;
+  ws.levels += levels;
+}
+
+template <int NSLOT, int WT>
+__device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, double* s_raw, double* s_rew,
+                               int si) {
+  constexpr int WS = WT;
+  const int lane = threadIdx.x & 31;
+  const ts_config& cf = v.cfg;
+  const ts_problem* pb = v.prob + s;
+  const size_t base = (size_t)s * (size_t)v.cap;
+  uint64_t* NO = v.no + base;
+  double* Wv = v.W + base;
+  double* PR = v.prior + base;
+  double* RW = v.reward + base;
+  int32_t* FC = v.fc + base;
+  int32_t* PA = v.parent + base;
+  uint32_t* ME = v.meta + base;
+  const uint64_t seed = pb->seed;
+  const int bdepth = pb->base_depth;
+  const int glen = pb->golden_len;
+  const int hidden = pb->hidden_until_depth;
+  const bool has_shared = pb->has_shared != 0;
+  const double off_lo = pb->off_lo, off_hi = pb->off_hi;
+  const double sh_lo = pb->shared_lo, sh_hi = pb->shared_hi;
+  const int width = WT;
+  const int scheme = cf.scheme;
+  const bool strict = cf.strict_negative_exit != 0;
+  const bool prefix_bound = cf.futility_bound == TS_BOUND_PREFIX_AGGREGATE;
+  const double tau = cf.accept_threshold, theta1 = cf.first_step_threshold;
+  const int gstep = lane < glen ? (int)pb->golden_path[lane] : -1;
+  const double grew = lane < glen ? pb->golden_rewards[lane] : 0.0;
+  const int budget = cf.rollout_budget;
+  int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
+  double* SSs = v.ss + (size_t)s * budget;
+  int32_t* SLs = v.sl + (size_t)s * budget;
+  uint64_t root_h[NSLOT];
+  {
+    const uint64_t h0 = sm64(MIX_INIT ^ seed);
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) {
+      uint64_t tag, len;
+      slot_header<NSLOT>(lane, k, tag, len);
+      root_h[k] = sm64(sm64(h0 ^ tag) ^ len);
+    }
+  }
+  long long tok_acc = 0;
+  unsigned long long created = 0;
+  for (int k = si;; k += HEAVY_SIM) {
+    while (ctl->issued <= k && !ctl->done) __nanosleep(32);
+    __threadfence_block();
+    if (ctl->issued <= k) break;
+    const HeavyJob& jb = ring[k % HEAVY_RING];
+    const int d0 = jb.d0;
+    int pnode = jb.pnode[lane], pj = jb.pj[lane];
+    uint64_t h[NSLOT];
+#pragma unroll
+    for (int q = 0; q < NSLOT; ++q) h[q] = root_h[q];
+    for (int i = 0; i < d0; ++i) {
+      const uint64_t j = (uint64_t)jb.pj[i];
+#pragma unroll
+      for (int q = 0; q < NSLOT; ++q) h[q] = sm64(h[q] ^ j);
+    }
+    Agg agg;
+    agg.a = jb.agg_a;
+    agg.c = jb.agg_c;
+    agg.n = jb.agg_n;
+    bool golden = jb.golden != 0;
+    double d1r = jb.d1r, nrew = jb.nrew;
+    uint32_t pmeta = 0, lvl_term = 0;
+    double prew = 0.0, pagg = 1.0;
+    if (lane == d0 - 1) { pmeta = jb.leaf_meta; prew = jb.nrew; pagg = jb.agg_a; }
+    const uint32_t leaf_meta0 = jb.leaf_meta;
+    const int leaf = jb.leaf;
+    const bool risky = jb.risky != 0;
+    int depth = d0, nrel = 0, node = leaf;
+    bool forced = false;
+    // --- simulate_to_terminal, critical path (node ids relative to the commit base) ---
+    while (true) {
+      if (depth >= cf.depth_cap) { forced = true; break; }
+      const int d = depth;
+      const int len = d + 1;
+      const uint64_t hr = state_at<NSLOT, 1>(h, d);
+      const uint64_t hp = state_at<NSLOT, 0>(h, d);
+      const uint64_t hk = state_at<NSLOT, 2>(h, d);
+      const double graw = __shfl_sync(FULL, grew, d);
+      const int gnext = __shfl_sync(FULL, gstep, d);
+      const bool gchild = golden && len <= glen && lane == gnext;
+      const uint64_t jj = (uint64_t)lane;
+      double rew;
+      if (gchild) {
+        rew = graw;
+      } else {
+        const bool shr = has_shared && len <= hidden;
+        const double lo = shr ? sh_lo : off_lo, hi = shr ? sh_hi : off_hi;
+        rew = lo + (hi - lo) * u53(sm64(hr ^ jj));
+      }
+      bool term;
+      if (len < bdepth) {
+        term = false;
+      } else if (len >= bdepth + 1) {
+        term = true;
+      } else {
+        const uint64_t he = state_at<NSLOT, 3>(h, d);
+        term = gchild || (sm64(he ^ jj) & 1ull) != 0;
+      }
+      const bool vl = lane < width;
+      const int j = warp_argmax(rew, vl, 0);
+      const double raw = 0.5 + u53(sm64(hp ^ jj));
+      const long long tok = 40 + (long long)(sm64(hk ^ jj) % 81ull);
+      const unsigned tmask = __ballot_sync(FULL, vl && term);
+      if (vl) {
+        s_raw[d * WS + lane] = raw;
+        s_rew[d * WS + lane] = rew;
+        tok_acc += tok;
+      }
+      if (lane == d) lvl_term = tmask;
+      const bool jterm = (tmask >> j) & 1u;
+      node = nrel + j;  // relative id
+      nrel += width;
+      ++depth;
+      nrew = __shfl_sync(FULL, rew, j);
+      const uint32_t nm = (uint32_t)depth | ((uint32_t)j << SH_REF) | (jterm ? M_TERM : 0u);
+      agg.add(nrew, scheme);
+      if (depth == 1) d1r = nrew;
+      golden = golden && depth <= glen && gnext == j;
+      if (lane == depth - 1) { pnode = node; pmeta = nm; prew = nrew; pagg = agg.a; pj = j; }
+#pragma unroll
+      for (int q = 0; q < NSLOT; ++q) h[q] = sm64(h[q] ^ (uint64_t)j);
+      if (jterm) break;
+    }
+    __syncwarp();
+    const int dend = depth;
+    const int nlev = dend - d0;
+    const double pscore = agg.value(scheme);
+    // --- commit in rollout order ---
+    spin_until_ge(&ctl->committed, k);
+    int cbase = ctl->nnodes;
+    bool ok = ctl->status == TS_OK;
+    if (ok && cbase + nlev * width > v.cap) {
+      ok = false;
+      if (lane == 0) ctl->status = TS_POOL_OVERFLOW;
+    }
+    if (ok) {
+      if (lane >= d0 && lane < dend) pnode += cbase;  // final ids of the new path nodes
+      const int fc0 = cbase;
+      uint32_t root_meta = ME[0];
+      if (risky && lane < d0 - 1) pmeta = ME[pnode];  // current metas for the propagation
+      const int up_node = __shfl_up_sync(FULL, pnode, 1);
+      const uint32_t up_meta = __shfl_up_sync(FULL, pmeta, 1);
+      const double up_rew = __shfl_up_sync(FULL, prew, 1);
+      const double up_agg = __shfl_up_sync(FULL, pagg, 1);
+      const int upj = __shfl_up_sync(FULL, pj, 1);
+      const int node_l = lane == 0 ? 0 : up_node;
+      const uint32_t leaf_meta = lane == 0 ? (d0 == 0 ? root_meta : leaf_meta0) : up_meta;
+      const double rew_l = lane == 0 ? 1.0 : up_rew;
+      const double agg_l = lane == 0 ? 1.0 : up_agg;
+      const bool act = lane >= d0 && lane < d0 + nlev;
+      int live = 0, ne_cnt = 0;
+      uint32_t meta_l = 0;
+      if (act) {
+        const int l = lane;
+        const int len = l + 1;
+        const int fcl = fc0 + (l - d0) * width;
+        const double* rawl = s_raw + l * WS;
+        const double* rewl = s_rew + l * WS;
+        double tot = rawl[0], cc = 0.0;
+#pragma unroll
+        for (int i = 1; i < WS; ++i) {
+          const double x = rawl[i];
+          const double t = tot + x;
+          if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
+          else cc += (x - t) + tot;
+          tot = t;
+        }
+        if (cc != 0.0 && isfinite(cc)) tot += cc;
+        const bool last = l == dend - 1;
+        const bool rel_d1 = strict || d1r >= theta1;
+#pragma unroll
+        for (int j = 0; j < WS; ++j) {
+          const double rew = rewl[j];
+          const bool term = (lvl_term >> j) & 1u;
+          const int c = fcl + j;
+          const bool onpath = j == pj;
+          NO[c] = onpath ? O_ONE : 0ull;
+          Wv[c] = 0.0;
+          PR[c] = rawl[j] / tot;
+          RW[c] = rew;
+          PA[c] = l == d0 ? leaf : node_l;
+          if (!onpath || last) {
+            FC[c] = -1;
+            uint32_t m = (uint32_t)len | ((uint32_t)j << SH_REF) | (term ? M_TERM : 0u);
+            if (onpath && forced) m |= M_TERM | M_FORCED;
+            ME[c] = m;
+          }
+          if (!term) {
+            ++live;
+            const bool rel = len == 1 ? (strict || rew >= theta1) : rel_d1;
+            double bound = rew;
+            if (prefix_bound && l > 0) {
+              const double pre = scheme == TS_SCHEME_PRODUCT ? agg_l * rew : (rew < agg_l ? rew : agg_l);
+              bound = fmin(rew, pre);
+            }
+            if (rel && !(bound < tau)) ++ne_cnt;
+          }
+        }
+        if (l >= 1) {
+          const double bound = prefix_bound ? fmin(rew_l, agg_l) : rew_l;
+          if (rel_d1 && !(bound < tau)) --ne_cnt;
+        }
+        const int nl_id = l == d0 ? leaf : node_l;
+        const uint32_t m = l == d0 ? leaf_meta : ((uint32_t)l | ((uint32_t)upj << SH_REF));
+        meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
+        FC[nl_id] = fcl;
+        ME[nl_id] = meta_l;
+      }
+      {
+        const uint32_t dn = __shfl_down_sync(FULL, meta_l, 1);
+        const bool dn_act = (lane + 1) >= d0 && (lane + 1) < d0 + nlev;
+        if (dn_act) pmeta = dn;
+        if (d0 == 0 && nlev > 0) root_meta = __shfl_sync(FULL, meta_l, 0);
+        if (forced && lane == dend - 1) pmeta |= M_TERM | M_FORCED;
+      }
+      if (forced && nlev == 0) {
+        const uint32_t m = __shfl_sync(FULL, pmeta, dend - 1);
+        const int lid = __shfl_sync(FULL, pnode, dend - 1);
+        if (lane == 0) ME[lid] = m;
+      }
+      int dv = (int)__reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
+      if (forced) {
+        const bool rel = strict || d1r >= theta1;
+        const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
+        if (rel && !(bound < tau)) --dv;
+      }
+      __syncwarp();
+      int dead_from = -1;
+      if (forced) dead_from = dend;
+      else if (nlev > 0 && __shfl_sync(FULL, live, dend - 1) == 0) dead_from = dend - 1;
+      if (dead_from >= 0) {
+        for (int i = dead_from - 1; i >= 0; --i) {
+          uint32_t m = i == 0 ? root_meta : __shfl_sync(FULL, pmeta, i - 1);
+          const int pid = i == 0 ? 0 : __shfl_sync(FULL, pnode, i - 1);
+          m -= NEXP_ONE;
+          if (lane == 0) ME[pid] = m;
+          if (i == 0) root_meta = m;
+          else if (lane == i - 1) pmeta = m;
+          if (meta_nexp(m) > 0) break;
+        }
+      }
+      SPs[(size_t)k * 32 + lane] = pnode;
+      if (lane == 0) {
+        SSs[k] = pscore;
+        SLs[k] = dend;
+        ctl->nnodes = cbase + nlev * width;
+        ctl->viable = ctl->viable + dv;
+      }
+      created += (unsigned long long)nlev * width;
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) ctl->committed = k + 1;
+  }
+  long long t = tok_acc;
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+  if (lane == 0) {
+    atomicAdd((unsigned long long*)&ctl->tokens, (unsigned long long)t);
+    atomicAdd((unsigned long long*)&ctl->created, created);
+  }
+}
+
+// warp 0 after all commits: backups, exit decisions, cancellations (as the
+// single-warp mode's multi-rollout path) and the search-state write-back
+__device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int nl, uint64_t rno, double rW,
+                             int decision, WaveStats& ws) {
+  const int lane = threadIdx.x & 31;
+  const ts_config& cf = v.cfg;
+  SearchState* S = v.st + s;
+  const size_t base = (size_t)s * (size_t)v.cap;
+  uint64_t* NO = v.no + base;
+  double* Wv = v.W + base;
+  uint32_t* ME = v.meta + base;
+  const int budget = cf.rollout_budget;
+  int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
+  double* SSs = v.ss + (size_t)s * budget;
+  int32_t* SLs = v.sl + (size_t)s * budget;
+  int completed = S->completed;
+  int best_term = S->best_term;
+  double best = S->best;
+  int launched = S->launched + nl, cancelled = S->cancelled;
+  int status = ctl->status;
+  const int viable = ctl->viable;
+  const uint32_t root_meta = ME[0];
+  unsigned long long done = 0, pathn = 0;
+  const bool exhausted = decision == -1;
+  if (exhausted) decision = TS_EXIT_NONE;
+  auto decide = [&](bool exh) -> int {
+    if (cf.positive_exit && best_term >= 0 && best >= cf.positive_exit_threshold) return TS_EXIT_POSITIVE;
+    if (cf.negative_exit && (root_meta & M_KIDS) && viable == 0) return TS_EXIT_NEGATIVE;
+    if (exh || completed >= budget) return TS_EXIT_BUDGET;
+    return TS_EXIT_NONE;
+  };
+  if (status == TS_OK && exhausted) decision = decide(true);
+  for (int r = 0; r < nl && status == TS_OK; ++r) {
+    if (completed >= budget) { status = TS_ACCOUNTING; break; }
+    const int len = SLs[r];
+    const double sc = SSs[r];
+    const int pn = lane < len ? SPs[(size_t)r * 32 + lane] : -1;
+    bool bad = false;
+    if (lane < len) {
+      const uint64_t x = NO[pn];
+      if ((x >> 32) < 1) bad = true;
+      NO[pn] = x + 1 - O_ONE;
+      Wv[pn] += sc;
+    }
+    if ((rno >> 32) < 1) bad = true;
+    rno = rno + 1 - O_ONE;
+    rW += sc;
+    if (lane == 0) { NO[0] = rno; Wv[0] = rW; }
+    if (__any_sync(FULL, bad)) { status = TS_ACCOUNTING; break; }
+    __syncwarp();
+    ++completed;
+    ++done;
+    pathn += len + 1;
+    if (best_term < 0 || sc > best) {
+      best = sc;
+      best_term = __shfl_sync(FULL, pn, len - 1);
+    }
+    decision = decide(false);
+    if (decision != TS_EXIT_NONE) {
+      for (int r2 = r + 1; r2 < nl; ++r2) {
+        const int len2 = SLs[r2];
+        const int pn2 = lane < len2 ? SPs[(size_t)r2 * 32 + lane] : -1;
+        bool bad2 = lane < len2 && (NO[pn2] >> 32) < 1;
+        if ((rno >> 32) < 1) bad2 = true;
+        if (__any_sync(FULL, bad2)) { status = TS_ACCOUNTING; break; }
+        if (lane < len2) NO[pn2] -= O_ONE;
+        rno -= O_ONE;
+        if (lane == 0) NO[0] = rno;
+        __syncwarp();
+        ++cancelled;
+        pathn += len2 + 1;
+      }
+      break;
+    }
+  }
+  if (lane == 0) {
+    S->completed = completed;
+    S->nodes = ctl->nnodes;
+    S->viable = viable;
+    S->best_term = best_term;
+    S->best = best;
+    S->tokens += (long long)ctl->tokens;
+    S->launched = launched;
+    S->cancelled = cancelled;
+    if (best_term >= 0 && best > S->job_best) S->job_best = best;
+    if (status != TS_OK || decision != TS_EXIT_NONE) {
+      S->state = ST_FINISHED;
+      S->exit_kind = status == TS_OK ? decision : TS_EXIT_NONE;
+      S->status = status;
+      S->exit_step = step;
+      S->t_exit = globaltimer();
+      atomicAdd((unsigned long long*)&v.ctr->running, (unsigned long long)-1ll);
+      atomicAdd((unsigned long long*)&v.ctr->finished, 1ull);
+      atomicMax(&v.ctr->last_exit_step, (long long)step);
+    }
+  }
+  ws.rollouts += done;
+  ws.launched += nl;
+  ws.nodes += ctl->created;
+  ws.path_nodes += pathn;
+}
+
+template <int NSLOT, int WT>
+__global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
+  extern __shared__ double hsm[];
+  __shared__ HeavyCtl ctl;
+  __shared__ HeavyJob ring[HEAVY_RING];
+  __shared__ int s_item;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WaveStats ws = {0, 0, 0, 0, 0, 0};
+  const int count_items = v.ctr->heavy_count;
+  if (step < 0) step = v.ctr->cur_step;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= count_items) break;
+    const int s = v.work_heavy[item];
+    const SearchState* S = v.st + s;
+    const int count = min(S->target, v.cfg.rollout_budget - S->completed);
+    if (threadIdx.x == 0) {
+      ctl.issued = 0;
+      ctl.committed = 0;
+      ctl.done = 0;
+      ctl.status = TS_OK;
+      ctl.nnodes = S->nodes;
+      ctl.viable = S->viable;
+      ctl.created = 0;
+      ctl.tokens = 0;
+    }
+    __syncthreads();
+    uint64_t rno = 0;
+    double rW = 0.0;
+    int decision = TS_EXIT_NONE;
+    if (warp == 0) {
+      heavy_select<NSLOT, WT>(v, s, &ctl, ring, count, ws, rno, rW, decision);
+    } else {
+      double* s_raw = hsm + (size_t)(warp - 1) * 2 * 32 * WT;
+      heavy_simulate<NSLOT, WT>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, warp - 1);
+    }
+    __syncthreads();
+    if (warp == 0) heavy_finish(v, s, step, &ctl, ctl.issued, rno, rW, decision, ws);
+    __syncthreads();
+  }
+  if (lane == 0 && warp == 0 && ws.launched) {
+    atomicAdd(&v.ctr->rollouts, ws.rollouts);
+    atomicAdd(&v.ctr->launched, ws.launched);
+    atomicAdd(&v.ctr->nodes, ws.nodes);
+    atomicAdd(&v.ctr->scored, ws.scored);
+    atomicAdd(&v.ctr->levels, ws.levels);
+    atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
+  }
+}
+
+static const wave_kernel_t kHeavy[3][3] = {
+    {k_heavy<1, 2>, k_heavy<1, 4>, k_heavy<1, 8>},
+    {k_heavy<2, 2>, k_heavy<2, 4>, k_heavy<2, 8>},
+    {k_heavy<4, 2>, k_heavy<4, 4>, k_heavy<4, 8>},
+};
+size_t heavy_smem_of(int wkind) {
+  const int ws = wkind == 0 ? 2 : wkind == 1 ? 4 : 8;
+  return (size_t)HEAVY_SIM * 2 * 32 * ws * sizeof(double);
+}
+
 __global__ void k_latency(View v, unsigned long long* out, int n) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
@@ -1269,6 +1908,7 @@ struct ts_engine {
   int sm_count = 148;
   int wave_blocks[12] = {0};
   int wkind = 3;
+  bool heavy_off = false;  // TS_NO_PIPELINE=1 disables the pipelined CTA mode (diagnostics)
   // sizes
   int n_local = 0, goff = 0, n_global = 0, cap_searches = 0, cap_global = 0;
   long long cap = 0, pool_nodes = 0;
@@ -1287,6 +1927,8 @@ struct ts_engine {
   int32_t* arrival = nullptr;
   Counters* ctr = nullptr;
   int32_t* work = nullptr;
+  int32_t* work_heavy = nullptr;
+  int heavy_blocks = 0;
   int32_t* sp = nullptr;
   double* ss = nullptr;
   int32_t* sl = nullptr;
@@ -1366,6 +2008,8 @@ View make_view(ts_engine* e) {
   v.arrival = e->arrival;
   v.ctr = e->ctr;
   v.work = e->work;
+  v.work_heavy = e->work_heavy;
+  v.heavy_on = (e->wkind != 3 && !e->heavy_off) ? 1 : 0;
   v.sp = e->sp;
   v.ss = e->ss;
   v.sl = e->sl;
@@ -1473,6 +2117,34 @@ void* wave_fn(ts_engine* e) {
   return (void*)kWave[k / 4][k % 4];
 }
 
+int heavy_grid(ts_engine* e, int& blocks_out) {
+  if (e->heavy_blocks <= 0) {
+    int per = 0;
+    const int k = wave_index(e);
+    cudaError_t rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per, (const void*)kHeavy[k / 4][std::min(k % 4, 2)], HEAVY_THREADS, heavy_smem_of(std::min(e->wkind, 2)));
+    if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
+    e->heavy_blocks = std::max(1, per) * e->sm_count;
+  }
+  blocks_out = std::max(1, std::min(e->heavy_blocks, e->n_local));
+  return TS_OK;
+}
+
+void* heavy_fn(ts_engine* e) {
+  const int k = wave_index(e);
+  return (void*)kHeavy[k / 4][std::min(k % 4, 2)];
+}
+
+int launch_heavy(ts_engine* e, const View& v, int step, cudaStream_t s) {
+  if (!v.heavy_on) return TS_OK;
+  int blocks = 0, rc;
+  if ((rc = heavy_grid(e, blocks))) return rc;
+  const int k = wave_index(e);
+  kHeavy[k / 4][std::min(k % 4, 2)]<<<blocks, HEAVY_THREADS, heavy_smem_of(std::min(e->wkind, 2)), s>>>(v, step);
+  TS_LAUNCH_CHECK(e, "k_heavy");
+  return TS_OK;
+}
+
 void destroy_run_graph(ts_engine* e) {
   if (e->run_exec) cudaGraphExecDestroy(e->run_exec);
   if (e->run_graph) cudaGraphDestroy(e->run_graph);
@@ -1520,6 +2192,17 @@ int build_run_graph(ts_engine* e, const View& v) {
   k2.sharedMemBytes = (unsigned)wave_smem_of(e->wkind);
   k2.kernelParams = a2;
   TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
+  if (v.heavy_on) {
+    int hb = 0;
+    if ((rc = heavy_grid(e, hb))) return rc;
+    cudaKernelNodeParams k3 = k2;
+    k3.func = heavy_fn(e);
+    k3.gridDim = dim3(hb);
+    k3.blockDim = dim3(HEAVY_THREADS);
+    k3.sharedMemBytes = (unsigned)heavy_smem_of(e->wkind);
+    cudaGraphNode_t n3;
+    TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n3, body, &n1, 1, &k3));
+  }
   TS_CUDA_TRY(e, cudaGraphInstantiate(&e->run_exec, g, 0));
   e->run_view = v;
   return TS_OK;
@@ -1539,6 +2222,7 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   const int k = wave_index(e);
   kWave[k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
   TS_LAUNCH_CHECK(e, "k_wave");
+  if ((rc = launch_heavy(e, v, step, s))) return rc;
   cudaEventRecord(e->wave_ev[e->wave_ev_used + 1], s);
   e->wave_ev_used += 2;
   return TS_OK;
@@ -1593,6 +2277,14 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
       cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)wave_smem_of(b));
+  for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
+    for (int b = 0; b < 3 && cr == cudaSuccess; ++b)
+      cr = cudaFuncSetAttribute((const void*)kHeavy[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)heavy_smem_of(b));
+  {
+    const char* env = getenv("TS_NO_PIPELINE");
+    e->heavy_off = env && env[0] == '1';
+  }
   if (cr != cudaSuccess) {
     *out = e;
     return cuda_fail(e, cr, "engine allocation");
@@ -1605,7 +2297,8 @@ int ts_engine_destroy(ts_engine* e) {
   if (!e) return TS_OK;
   void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->fc, e->parent, e->meta, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
-                  e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes};
+                  e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
+                  e->work_heavy};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
@@ -1671,11 +2364,12 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   }
   e->cap = cap;
   if (n_local > e->cap_searches || !e->st) {
-    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0;
+    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0, h6 = 0;
     if ((rc = grow(e, e->st, n_local, h0, "search state")) ||
         (rc = grow(e, e->prob, n_local, h1, "problem table")) ||
         (rc = grow(e, e->arrival, n_local, h2, "arrivals")) ||
         (rc = grow(e, e->work, n_local, h3, "work list")) ||
+        (rc = grow(e, e->work_heavy, n_local, h6, "work list")) ||
         (rc = grow(e, e->records, n_local, h4, "records")) ||
         (rc = grow(e, e->outcomes, n_local, h5, "outcomes")))
       return rc;
