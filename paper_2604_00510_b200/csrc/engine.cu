@@ -33,6 +33,9 @@ constexpr int SH_NEXP = 16;               // bits 16-21: # expandable children
 constexpr uint32_t NEXP_ONE = 1u << SH_NEXP;
 constexpr uint64_t O_ONE = 1ull << 32;    // no word: N in low 32, O (in-flight) in high 32
 
+__host__ __device__ inline uint64_t mk_mf(int fc, uint32_t meta) {
+  return ((uint64_t)(uint32_t)fc << 32) | (uint64_t)meta;
+}
 __host__ __device__ inline int meta_nexp(uint32_t m) { return (int)((m >> SH_NEXP) & 0x3Fu); }
 // _expandable (tree.py:175-181), maintained incrementally: a non-terminal
 // node is expandable iff it is a leaf or one of its children is.
@@ -72,9 +75,9 @@ struct View {
   double* W;         // value_sum
   double* prior;
   double* reward;    // prm_reward
-  int32_t* fc;       // first child (children are contiguous), -1 for leaves
+  uint64_t* mf;      // meta (low 32) | first child (high 32, -1 for leaves; children are
+                     // contiguous): one 8-byte word, so a reader sees both old or both new
   int32_t* parent;
-  uint32_t* meta;
   long long cap;
   SearchState* st;
   const ts_problem* prob;
@@ -83,6 +86,7 @@ struct View {
   int32_t* work;           // this wave's running local searches (single-warp mode)
   int32_t* work_heavy;     // this wave's searches for the pipelined CTA mode
   int32_t heavy_on;        // pipelined mode available (uniform width 2/4/8)
+  int32_t heavy_sync;      // diagnostics: commit every job before the next selection
   int32_t* sp;             // scratch paths of a multi-rollout wave [n_local][budget][32]
   double* ss;              // scratch scores
   int32_t* sl;             // scratch lengths
@@ -196,9 +200,8 @@ __global__ void k_init(View v) {
   v.W[r] = 0.0;
   v.prior[r] = 1.0;
   v.reward[r] = 1.0;
-  v.fc[r] = -1;
+  v.mf[r] = mk_mf(-1, 0);
   v.parent[r] = -1;
-  v.meta[r] = 0;
   SearchState z;
   z.state = ST_PENDING;
   z.completed = z.launched = z.cancelled = 0;
@@ -762,9 +765,9 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
   double* Wv = v.W + base;
   double* PR = v.prior + base;
   double* RW = v.reward + base;
-  int32_t* FC = v.fc + base;
+  uint64_t* MF = v.mf + base;
+  uint32_t* ME = (uint32_t*)MF;  // ME[2*i]: meta word of node i
   int32_t* PA = v.parent + base;
-  uint32_t* ME = v.meta + base;
 
   const uint64_t seed = pb->seed;
   const int bdepth = pb->base_depth;
@@ -809,10 +812,11 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     }
   }
   // the root's record lives in registers for the whole wave (sole writer)
-  uint32_t root_meta = ME[0];
+  const uint64_t rmf = MF[0];
+  uint32_t root_meta = (uint32_t)rmf;
   uint64_t rno = NO[0];
   double rW = Wv[0];
-  int rfc = FC[0];
+  int rfc = (int)(rmf >> 32);
   int decision = TS_EXIT_NONE;
   int nl = 0;
   long long tok_acc = 0;  // per-lane token tally, reduced once per wave
@@ -858,9 +862,10 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
         cno = NO[c];
         cw = Wv[c];
         const double cp = PR[c];
-        cm = ME[c];
+        const uint64_t cmf = MF[c];
+        cm = (uint32_t)cmf;
         cr = RW[c];
-        cfc = FC[c];
+        cfc = (int)(cmf >> 32);
         valid = meta_expandable(cm);
         if (valid) {
           const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
@@ -1013,10 +1018,9 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
         PA[c] = node_l;
         // the on-path child expanded at the next level gets its fc/meta from lane l+1
         if (!onpath || last) {
-          FC[c] = -1;
           uint32_t m = (uint32_t)len | ((uint32_t)j << SH_REF) | (term ? M_TERM : 0u);
           if (onpath && forced) m |= M_TERM | M_FORCED;
-          ME[c] = m;
+          MF[c] = mk_mf(-1, m);
         }
         if (!term) {
           ++live;
@@ -1037,8 +1041,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       }
       const uint32_t m = l == d0 ? leaf_meta : ((uint32_t)l | ((uint32_t)upj << SH_REF));
       meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
-      FC[node_l] = fcl;
-      ME[node_l] = meta_l;
+      MF[node_l] = mk_mf(fcl, meta_l);
     }
     // refresh the path meta registers (lane l-1 holds path node l)
     {
@@ -1052,7 +1055,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       // the selected leaf itself hit the depth cap (d0 >= 1 since depth_cap >= 1)
       const uint32_t m = __shfl_sync(FULL, pmeta, dend - 1);
       const int lid = __shfl_sync(FULL, pnode, dend - 1);
-      if (lane == 0) ME[lid] = m;
+      if (lane == 0) ME[2 * lid] = m;
     }
     viable += (int)__reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
     if (forced) {
@@ -1073,7 +1076,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
         uint32_t m = i == 0 ? root_meta : __shfl_sync(FULL, pmeta, i - 1);
         const int pid = i == 0 ? 0 : __shfl_sync(FULL, pnode, i - 1);
         m -= NEXP_ONE;
-        if (lane == 0) ME[pid] = m;
+        if (lane == 0) ME[2 * pid] = m;
         if (i == 0) root_meta = m;
         else if (lane == i - 1) pmeta = m;
         if (meta_nexp(m) > 0) break;
@@ -1277,6 +1280,19 @@ __device__ __forceinline__ void spin_until_ge(volatile int* p, int v) {
   __threadfence_block();
 }
 
+// If `node` is the selected leaf of a job that is issued but not committed,
+// wait for that commit (acquire) and return true: the caller must reload the
+// node's meta and first child.  Jobs [committed, issued) are checked lane-parallel.
+__device__ __forceinline__ bool heavy_wait_inflight(HeavyCtl* ctl, const HeavyJob* ring, int c0, int issued,
+                                                    int node) {
+  const int lane = threadIdx.x & 31;
+  const bool hit = c0 + lane < issued && ring[(c0 + lane) % HEAVY_RING].leaf == node;
+  const unsigned hm = __ballot_sync(FULL, hit);
+  if (!hm) return false;
+  spin_until_ge(&ctl->committed, c0 + __ffs(hm));
+  return true;
+}
+
 template <int NSLOT, int WT>
 __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, int count, WaveStats& ws,
                              uint64_t& rno_out, double& rW_out, int& decision_out) {
@@ -1288,8 +1304,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   double* Wv = v.W + base;
   double* PR = v.prior + base;
   double* RW = v.reward + base;
-  int32_t* FC = v.fc + base;
-  uint32_t* ME = v.meta + base;
+  uint64_t* MF = v.mf + base;
   const int bdepth = pb->base_depth;
   const int glen = pb->golden_len;
   const int width = WT;
@@ -1306,12 +1321,18 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   for (; k < count; ++k) {
     if (last_risky >= 0) spin_until_ge(&ctl->committed, last_risky + 1);
     if (ctl->status != TS_OK) break;
-    uint32_t nmeta = ME[0];
+    // jobs < cs are committed and visible from here on; jobs [cs, k) may commit
+    // while this selection reads the tree
+    const int cs = ctl->committed;
+    __threadfence_block();
+    heavy_wait_inflight(ctl, ring, cs, k, 0);  // the root itself may be an in-flight leaf
+    const uint64_t rmf = MF[0];
+    uint32_t nmeta = (uint32_t)rmf;
     if (!meta_expandable(nmeta)) {  // NoExpandableLeafError (tree.py:273-274)
       if (k == 0) decision = -1;
       break;
     }
-    int node = 0, depth = 0, nfc = FC[0];
+    int node = 0, depth = 0, nfc = (int)(rmf >> 32);
     uint64_t nno = rno;
     double nW = rW, nrew = 1.0;
     int pnode = -1, pj = 0;
@@ -1337,9 +1358,10 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
           cno = NO[c];
           cw = Wv[c];
           const double cp = PR[c];
-          cm = ME[c];
+          const uint64_t cmf = MF[c];
+          cm = (uint32_t)cmf;
           cr = RW[c];
-          cfc = FC[c];
+          cfc = (int)(cmf >> 32);
           valid = meta_expandable(cm);
           if (valid) {
             const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
@@ -1365,20 +1387,17 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         if (depth == 1) d1r = nrew;
         golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
         if (lane == depth - 1) { pnode = node; pno = nno; pj = j; }
+        // entering a leaf whose expansion may be in flight: its meta/fc/children
+        // are only valid after that job's commit
+        if (heavy_wait_inflight(ctl, ring, cs, k, node)) {
+          const uint64_t x = MF[node];
+          nmeta = (uint32_t)x;
+          nfc = (int)(x >> 32);
+        } else if (nmeta & M_KIDS) {
+          __threadfence_block();  // acquire: a commit published this node's children before its word
+        }
       }
-      if (status != TS_OK) break;
-      // a leaf whose expansion is still in flight: wait for its commit, descend on
-      const int c0 = ctl->committed, i0 = k;  // jobs [c0, k) are uncommitted
-      bool hit = false;
-      int jw = -1;
-      if (c0 + lane < i0) hit = ring[(c0 + lane) % HEAVY_RING].leaf == node;
-      const unsigned hm = __ballot_sync(FULL, hit);
-      if (!hm) break;
-      jw = c0 + __ffs(hm) - 1;
-      spin_until_ge(&ctl->committed, jw + 1);
-      if (ctl->status != TS_OK) { status = ctl->status; break; }
-      nmeta = ME[node];
-      nfc = FC[node];
+      break;
     }
     if (status != TS_OK) {
       if (lane == 0) atomicCAS((int*)&ctl->status, TS_OK, status);
@@ -1396,7 +1415,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     if (lane == 0) {
       jb.leaf = node;
       jb.d0 = depth;
-      jb.risky = (width == 1 || depth >= risky_depth) ? 1 : 0;
+      jb.risky = (width == 1 || depth >= risky_depth || v.heavy_sync) ? 1 : 0;
       jb.golden = golden ? 1 : 0;
       jb.leaf_meta = nmeta;
       jb.nrew = nrew;
@@ -1408,7 +1427,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     __threadfence_block();
     __syncwarp();
     if (lane == 0) ctl->issued = k + 1;
-    if (width == 1 || depth >= risky_depth) last_risky = k;
+    if (width == 1 || depth >= risky_depth || v.heavy_sync) last_risky = k;
   }
   if (lane == 0) ctl->done = 1;
   spin_until_ge(&ctl->committed, k);
@@ -1431,9 +1450,9 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
   double* Wv = v.W + base;
   double* PR = v.prior + base;
   double* RW = v.reward + base;
-  int32_t* FC = v.fc + base;
+  uint64_t* MF = v.mf + base;
+  uint32_t* ME = (uint32_t*)MF;
   int32_t* PA = v.parent + base;
-  uint32_t* ME = v.meta + base;
   const uint64_t seed = pb->seed;
   const int bdepth = pb->base_depth;
   const int glen = pb->golden_len;
@@ -1563,7 +1582,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
       if (lane >= d0 && lane < dend) pnode += cbase;  // final ids of the new path nodes
       const int fc0 = cbase;
       uint32_t root_meta = ME[0];
-      if (risky && lane < d0 - 1) pmeta = ME[pnode];  // current metas for the propagation
+      if (risky && lane < d0 - 1) pmeta = ME[2 * pnode];  // current metas for the propagation
       const int up_node = __shfl_up_sync(FULL, pnode, 1);
       const uint32_t up_meta = __shfl_up_sync(FULL, pmeta, 1);
       const double up_rew = __shfl_up_sync(FULL, prew, 1);
@@ -1606,10 +1625,9 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
           RW[c] = rew;
           PA[c] = l == d0 ? leaf : node_l;
           if (!onpath || last) {
-            FC[c] = -1;
             uint32_t m = (uint32_t)len | ((uint32_t)j << SH_REF) | (term ? M_TERM : 0u);
             if (onpath && forced) m |= M_TERM | M_FORCED;
-            ME[c] = m;
+            MF[c] = mk_mf(-1, m);
           }
           if (!term) {
             ++live;
@@ -1626,11 +1644,15 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
           const double bound = prefix_bound ? fmin(rew_l, agg_l) : rew_l;
           if (rel_d1 && !(bound < tau)) --ne_cnt;
         }
-        const int nl_id = l == d0 ? leaf : node_l;
         const uint32_t m = l == d0 ? leaf_meta : ((uint32_t)l | ((uint32_t)upj << SH_REF));
         meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
-        FC[nl_id] = fcl;
-        ME[nl_id] = meta_l;
+      }
+      // publish the expanded nodes only after their children are written
+      __threadfence_block();
+      __syncwarp();
+      if (act) {
+        const int nl_id = lane == d0 ? leaf : node_l;
+        MF[nl_id] = mk_mf(fc0 + (lane - d0) * width, meta_l);
       }
       {
         const uint32_t dn = __shfl_down_sync(FULL, meta_l, 1);
@@ -1642,7 +1664,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
       if (forced && nlev == 0) {
         const uint32_t m = __shfl_sync(FULL, pmeta, dend - 1);
         const int lid = __shfl_sync(FULL, pnode, dend - 1);
-        if (lane == 0) ME[lid] = m;
+        if (lane == 0) ME[2 * lid] = m;
       }
       int dv = (int)__reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
       if (forced) {
@@ -1659,7 +1681,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
           uint32_t m = i == 0 ? root_meta : __shfl_sync(FULL, pmeta, i - 1);
           const int pid = i == 0 ? 0 : __shfl_sync(FULL, pnode, i - 1);
           m -= NEXP_ONE;
-          if (lane == 0) ME[pid] = m;
+          if (lane == 0) ME[2 * pid] = m;
           if (i == 0) root_meta = m;
           else if (lane == i - 1) pmeta = m;
           if (meta_nexp(m) > 0) break;
@@ -1696,7 +1718,7 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
   const size_t base = (size_t)s * (size_t)v.cap;
   uint64_t* NO = v.no + base;
   double* Wv = v.W + base;
-  uint32_t* ME = v.meta + base;
+  const uint32_t* ME = (const uint32_t*)(v.mf + base);
   const int budget = cf.rollout_budget;
   int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
   double* SSs = v.ss + (size_t)s * budget;
@@ -1886,7 +1908,8 @@ __global__ void k_outcomes(View v, ts_outcome* out, int n) {
     int n2 = 0;
     for (int c = st.best_term; c > 0 && n2 <= TS_MAX_DEPTH; c = v.parent[base + c]) ids[n2++] = c;
     o.best_len = n2;
-    for (int i = 0; i < n2; ++i) o.best_path[i] = (uint8_t)((v.meta[base + ids[n2 - 1 - i]] >> SH_REF) & 31u);
+    for (int i = 0; i < n2; ++i)
+      o.best_path[i] = (uint8_t)(((uint32_t)v.mf[base + ids[n2 - 1 - i]] >> SH_REF) & 31u);
     if (pb->golden_len >= 0 && o.best_len == pb->golden_len) {
       o.solved = 1;
       for (int i = 0; i < n2; ++i)
@@ -1909,6 +1932,7 @@ struct ts_engine {
   int wave_blocks[12] = {0};
   int wkind = 3;
   bool heavy_off = false;  // TS_NO_PIPELINE=1 disables the pipelined CTA mode (diagnostics)
+  bool heavy_sync = false; // TS_PIPELINE_SYNC=1 serialises it (diagnostics)
   // sizes
   int n_local = 0, goff = 0, n_global = 0, cap_searches = 0, cap_global = 0;
   long long cap = 0, pool_nodes = 0;
@@ -1919,9 +1943,8 @@ struct ts_engine {
   double* W = nullptr;
   double* prior = nullptr;
   double* reward = nullptr;
-  int32_t* fc = nullptr;
+  uint64_t* mf = nullptr;
   int32_t* parent = nullptr;
-  uint32_t* meta = nullptr;
   SearchState* st = nullptr;
   ts_problem* prob = nullptr;
   int32_t* arrival = nullptr;
@@ -1999,9 +2022,8 @@ View make_view(ts_engine* e) {
   v.W = e->W;
   v.prior = e->prior;
   v.reward = e->reward;
-  v.fc = e->fc;
+  v.mf = e->mf;
   v.parent = e->parent;
-  v.meta = e->meta;
   v.cap = e->cap;
   v.st = e->st;
   v.prob = e->prob;
@@ -2010,6 +2032,7 @@ View make_view(ts_engine* e) {
   v.work = e->work;
   v.work_heavy = e->work_heavy;
   v.heavy_on = (e->wkind != 3 && !e->heavy_off) ? 1 : 0;
+  v.heavy_sync = e->heavy_sync ? 1 : 0;
   v.sp = e->sp;
   v.ss = e->ss;
   v.sl = e->sl;
@@ -2284,6 +2307,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
   {
     const char* env = getenv("TS_NO_PIPELINE");
     e->heavy_off = env && env[0] == '1';
+    const char* env2 = getenv("TS_PIPELINE_SYNC");
+    e->heavy_sync = env2 && env2[0] == '1';
   }
   if (cr != cudaSuccess) {
     *out = e;
@@ -2295,7 +2320,7 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
 
 int ts_engine_destroy(ts_engine* e) {
   if (!e) return TS_OK;
-  void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->fc, e->parent, e->meta, e->st, e->prob,
+  void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
                   e->work_heavy};
@@ -2347,19 +2372,18 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   int rc;
   const size_t pool = (size_t)cap * (size_t)n_local;
   if (pool > (size_t)e->pool_nodes || !e->no) {
-    void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->fc, e->parent, e->meta};
+    void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->mf, e->parent};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     e->no = nullptr; e->W = nullptr; e->prior = nullptr; e->reward = nullptr;
-    e->fc = nullptr; e->parent = nullptr; e->meta = nullptr;
+    e->mf = nullptr; e->parent = nullptr;
     e->pool_nodes = 0;
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->no, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->W, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->prior, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->reward, pool * 8));
-    TS_CUDA_TRY(e, cudaMalloc((void**)&e->fc, pool * 4));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->mf, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->parent, pool * 4));
-    TS_CUDA_TRY(e, cudaMalloc((void**)&e->meta, pool * 4));
     e->pool_nodes = (long long)pool;
   }
   e->cap = cap;
@@ -2619,9 +2643,9 @@ int ts_dump_tree(ts_engine* e, int32_t search, int32_t* parent, double* reward, 
   if (rc) return rc;
   const size_t b = (size_t)search * (size_t)e->cap;
   std::vector<uint64_t> no(n);
-  std::vector<uint32_t> me(n);
+  std::vector<uint64_t> me(n);
   TS_CUDA_TRY(e, cudaMemcpy(no.data(), e->no + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
-  TS_CUDA_TRY(e, cudaMemcpy(me.data(), e->meta + b, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  TS_CUDA_TRY(e, cudaMemcpy(me.data(), e->mf + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
   if (parent) TS_CUDA_TRY(e, cudaMemcpy(parent, e->parent + b, 4 * (size_t)n, cudaMemcpyDeviceToHost));
   if (reward) TS_CUDA_TRY(e, cudaMemcpy(reward, e->reward + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
   if (prior) TS_CUDA_TRY(e, cudaMemcpy(prior, e->prior + b, 8 * (size_t)n, cudaMemcpyDeviceToHost));
@@ -2629,9 +2653,10 @@ int ts_dump_tree(ts_engine* e, int32_t search, int32_t* parent, double* reward, 
   for (int i = 0; i < n; ++i) {
     if (visits) visits[i] = (int32_t)(uint32_t)no[i];
     if (inflight) inflight[i] = (int32_t)(no[i] >> 32);
-    if (terminal) terminal[i] = (me[i] & M_TERM) ? 1 : 0;
-    if (depth) depth[i] = (int32_t)(me[i] & M_DEPTH);
-    if (step_ref) step_ref[i] = i == 0 ? -1 : (int32_t)((me[i] >> SH_REF) & 31u);
+    const uint32_t m = (uint32_t)me[i];
+    if (terminal) terminal[i] = (m & M_TERM) ? 1 : 0;
+    if (depth) depth[i] = (int32_t)(m & M_DEPTH);
+    if (step_ref) step_ref[i] = i == 0 ? -1 : (int32_t)((m >> SH_REF) & 31u);
   }
   return TS_OK;
 }

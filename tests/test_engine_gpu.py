@@ -293,3 +293,35 @@ def test_invalid_config_raises():
     c = TsConfig()
     with pytest.raises(ValueError):
         Engine(c, 0)
+
+
+@pytest.mark.parametrize("seed,M,budget,cap,b,base", [(0, 256, 32, 8, 4, 7), (5, 4096, 128, 16, 4, 15),
+                                                      (9, 512, 64, 12, 8, 11), (3, 1024, 48, 6, 2, 7)])
+def test_pipelined_mode_matches_single_warp_mode(seed, M, budget, cap, b, base, monkeypatch):
+    """Searches with many rollouts per wave run in the pipelined CTA mode
+    (selector warp + simulator warps, in-order commits); the result must equal
+    the single-warp mode bit for bit — outcomes and whole trees."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    n = M // 4
+    specs = B.make_workload(n, (0.5, 0.3, 0.2), seed, branching=b,
+                            depth_ranges={d: (base, base) for d in B.Difficulty})
+    t = B.problem_table(specs)
+    cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=M), rollout_budget=budget, depth_cap=cap,
+                       expand_width=b)
+    res = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("TS_NO_PIPELINE", mode)
+        with _engine(cfg) as eng:
+            eng.load(t)
+            st = eng.run()
+            outs = eng.outcomes()
+            trees = [eng.tree(i) for i in range(0, n, max(1, n // 16))]
+            res[mode] = (st.steps, st.rollouts, st.launched, st.nodes, outs, trees)
+    a, c = res["0"], res["1"]
+    assert a[:4] == c[:4]
+    _cmp_outcomes(a[4], c[4], f"pipelined[{seed}]")
+    for x, y in zip(a[5], c[5]):
+        assert_tree_equal(x, {k: v.tolist() for k, v in y.items()}, "pipelined tree")
