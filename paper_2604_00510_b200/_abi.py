@@ -127,7 +127,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("TS_LIB_PATH") or LIB_PATH
     if not os.path.exists(p):
         raise ImportError(
             f"{p} is missing: build the CUDA extension first (python -c 'import __graft_entry__ as g; g.build()')"

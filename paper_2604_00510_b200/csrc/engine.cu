@@ -66,6 +66,7 @@ struct Counters {
   int heavy_count, heavy_next;  // searches with >= HEAVY_P rollouts this wave (pipelined CTA mode)
   int sum_fallbacks, sched_error;
   unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
+  unsigned long long prof[16];  // TS_HEAVY_PROF diagnostics (cycles), zero otherwise
 };
 
 // Kernel-side view of one engine.
@@ -73,6 +74,7 @@ struct View {
   // SoA node pool; search s owns nodes [s*cap, (s+1)*cap), ids in creation order
   uint64_t* no;      // N | O << 32
   double* W;         // value_sum
+  double* Q;         // mean value W/N, valid when N > 0 (rewritten at every backup)
   double* prior;
   double* reward;    // prm_reward
   uint64_t* mf;      // meta (low 32) | first child (high 32, -1 for leaves; children are
@@ -198,6 +200,7 @@ __global__ void k_init(View v) {
   size_t r = (size_t)s * (size_t)v.cap;
   v.no[r] = 0;
   v.W[r] = 0.0;
+  v.Q[r] = 0.0;
   v.prior[r] = 1.0;
   v.reward[r] = 1.0;
   v.mf[r] = mk_mf(-1, 0);
@@ -287,6 +290,7 @@ __global__ void k_records(View v, int step, ts_sched_record* rec) {
     double boost = ratio > cf.proximity ? cf.beta : 0.0;
     r.score = v.log1p_tab[waited] + boost;
     r.flags = 1u | (s->completed >= cf.obs_threshold ? 2u : 0u) | (ratio > cf.proximity ? 4u : 0u);
+    r._pad = (uint32_t)s->completed;
   }
   rec[i] = r;
 }
@@ -294,6 +298,8 @@ __global__ void k_records(View v, int step, ts_sched_record* rec) {
 // ---- compute_targets (scheduler.py:143-187) in one CTA ------------------------
 constexpr int TT = 1024;
 constexpr int HEAVY_P = 8;  // rollouts in one wave from which a search runs in pipelined CTA mode
+constexpr int HBITS_WORDS = 2048;  // run-queue slots with a pipelined-mode flag bit (65536)
+constexpr int SREC_MAX = 4096;     // k_sched keeps the records of up to this many searches in shared memory
 constexpr int RUNCAP = 1536;  // runs per list kept in shared memory
 
 typedef unsigned __int128 u128;
@@ -358,6 +364,43 @@ __device__ long long block_scan_add(long long x, long long* total, long long* sh
   __syncthreads();
   return res;
 }
+// Four exclusive (+) scans in one pass; totals in tot[4].  All threads must call.
+__device__ void block_scan_add4(long long (&x)[4], long long (&tot)[4], long long* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long incl[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    incl[q] = x[q];
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(FULL, incl[q], o);
+      if (lane >= o) incl[q] += y;
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) sh[q * 32 + wid] = incl[q];
+  }
+  __syncthreads();
+  if (wid < 4) {
+    long long w = sh[wid * 32 + lane];
+    long long wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(FULL, wi, o);
+      if (lane >= o) wi += y;
+    }
+    sh[128 + wid * 32 + lane] = wi - w;
+    if (lane == 31) sh[256 + wid] = wi;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const long long base = sh[128 + q * 32 + wid];
+    tot[q] = sh[256 + q];
+    x[q] = base + incl[q] - x[q];
+  }
+  __syncthreads();
+}
+
 // Exclusive min-scan of doubles (identity +inf).
 __device__ double block_scan_min(double x, double* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -413,10 +456,11 @@ __device__ __forceinline__ int runs_lower(const double* runS, int nr, double s) 
 // below); it is computed exactly in 128-bit fixed point.
 __device__ void targets_block(const View& v, int step, const ts_sched_record* rec) {
   extern __shared__ __align__(16) unsigned char smem[];
-  long long* shl = (long long*)smem;                 // 80 long longs of scan scratch
-  double* shd = (double*)(smem + 80 * 8);            // 80 doubles
-  u128* shq = (u128*)(smem + 160 * 8);               // 32 u128
-  double* s_runS = (double*)(smem + 160 * 8 + 32 * 16);
+  long long* shl = (long long*)smem;                 // 264 long longs of scan scratch
+  double* shd = (double*)(smem + 264 * 8);           // 80 doubles
+  u128* shq = (u128*)(smem + 344 * 8);               // 32 u128
+  uint32_t* hbits = (uint32_t*)(smem + 344 * 8 + 32 * 16);  // pipelined-mode flag per run-queue slot
+  double* s_runS = (double*)(smem + 344 * 8 + 32 * 16 + HBITS_WORDS * 4);
   int32_t* s_runStart = (int32_t*)(s_runS + 2 * RUNCAP);
   long long* s_runWant = (long long*)(s_runStart + 2 * RUNCAP);
   long long* s_runPW = s_runWant + 2 * RUNCAP;
@@ -430,6 +474,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   const int per = (n + TT - 1) / TT;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   const int glo = v.goff, ghi = v.goff + v.n_local;
+  for (int w = tid; w < (v.n_local + 31) / 32 && w < HBITS_WORDS; w += TT) hbits[w] = 0u;
 
   // phase 1: counts, exact score sum, list positions
   u128 fx = 0;
@@ -449,11 +494,11 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
       else { ++cnt0; min0 = fmin(min0, r.score); }
     }
   }
-  long long tot_run, len0, len1, tot_loc;
-  block_scan_add(nrun, &tot_run, shl);
-  long long pos0 = block_scan_add(cnt0, &len0, shl);
-  long long pos1 = block_scan_add(cnt1, &len1, shl);
-  long long wpos = block_scan_add(nloc, &tot_loc, shl);
+  long long sc4[4] = {nrun, cnt0, cnt1, nloc}, tt4[4];
+  block_scan_add4(sc4, tt4, shl);
+  const long long tot_run = tt4[0], len0 = tt4[1], len1 = tt4[2], tot_loc = tt4[3];
+  const long long pos0 = sc4[1], pos1 = sc4[2], wpos = sc4[3];
+  (void)tot_loc;
   // u128 reduction
   {
     const int lane = tid & 31, wid = tid >> 5;
@@ -501,9 +546,10 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     __syncthreads();
   }
   const double T = sT;
-  const bool boost_on = cf.boosting_enabled != 0 && tot_run > 0;
   const long long M = cf.max_concurrency;
   const long long R = M - tot_run;
+  // no free slot or nobody past the observation gate: every running job gets 1
+  const bool boost_on = cf.boosting_enabled != 0 && tot_run > 0 && R > 0 && len0 + len1 > 0;
 
   // phase 2: runs of equal score in each list (lists are non-increasing)
   double prev0 = block_scan_min(min0, shd);
@@ -628,36 +674,44 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
       } else if ((r.flags & 2u) == 0 && boost_on) {
         // gated: stays serial; advance nothing
       }
-      if (i >= glo && i < ghi) v.st[i - glo].target = (int)tgt;
+      if (i >= glo && i < ghi) {
+        v.st[i - glo].target = (int)tgt;
+        // rollouts this wave = min(P_i, budget - completed); `_pad` carries completed
+        if (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P)
+          atomicOr(&hbits[(i - glo) >> 5], 1u << ((i - glo) & 31));
+      }
     }
   }
   (void)wpos;
+  __syncthreads();
   // phase 5: split the local running searches into the single-warp and the
   // pipelined (many rollouts this wave) work lists, in run-queue order
   long long nh = 0, nlt = 0;
-  const int loc_lo = max(lo, glo) - glo, loc_hi = min(hi, ghi) - glo;
+  const int loc_lo = max(lo, glo) - glo, loc_hi = max(loc_lo, min(hi, ghi) - glo);
   for (int i = loc_lo; i < loc_hi; ++i) {
-    const SearchState& st = v.st[i];
-    if (st.state != ST_RUNNING) continue;
-    if (v.heavy_on && min(st.target, cf.rollout_budget - st.completed) >= HEAVY_P) ++nh;
+    if (!(rec[i + glo].flags & 1u)) continue;
+    if ((hbits[i >> 5] >> (i & 31)) & 1u) ++nh;
     else ++nlt;
   }
-  long long tot_h, tot_l;
-  long long ph = block_scan_add(nh, &tot_h, shl);
-  long long pl = block_scan_add(nlt, &tot_l, shl);
+  long long sc2[4] = {nh, nlt, 0, 0}, tt2[4];
+  block_scan_add4(sc2, tt2, shl);
+  long long ph = sc2[0], pl = sc2[1];
   for (int i = loc_lo; i < loc_hi; ++i) {
-    const SearchState& st = v.st[i];
-    if (st.state != ST_RUNNING) continue;
-    if (v.heavy_on && min(st.target, cf.rollout_budget - st.completed) >= HEAVY_P) v.work_heavy[ph++] = i;
+    if (!(rec[i + glo].flags & 1u)) continue;
+    if ((hbits[i >> 5] >> (i & 31)) & 1u) v.work_heavy[ph++] = i;
     else v.work[pl++] = i;
   }
   if (tid == 0) {
-    v.ctr->work_count = (int)tot_l;
+    v.ctr->work_count = (int)tt2[1];
     v.ctr->work_next = 0;
-    v.ctr->heavy_count = (int)tot_h;
+    v.ctr->heavy_count = (int)tt2[0];
     v.ctr->heavy_next = 0;
     v.ctr->cur_step = step;
   }
+}
+
+__device__ __forceinline__ size_t targets_smem_dev() {
+  return 344 * 8 + 32 * 16 + HBITS_WORDS * 4 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8);
 }
 
 __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
@@ -703,6 +757,12 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
   if (!s_go) return;
   const long long alo = c->admit_lo, ahi = c->admit_hi;
   const ts_config& cf = v.cfg;
+  // one GPU: the run queue's records stay in shared memory when they fit
+  extern __shared__ __align__(16) unsigned char smem[];
+  ts_sched_record* srec = v.n_local <= SREC_MAX && v.n_global == v.n_local
+                              ? (ts_sched_record*)(smem + targets_smem_dev())
+                              : rec;
+#pragma unroll 4
   for (int i = threadIdx.x; i < v.n_local; i += TT) {
     SearchState* st = v.st + i;
     int state = st->state;
@@ -719,12 +779,14 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
       const double ratio = st->job_best / cf.positive_exit_threshold;
       const bool boosted = ratio > cf.proximity;
       r.score = v.log1p_tab[step - v.arrival[i]] + (boosted ? cf.beta : 0.0);
-      r.flags = 1u | (st->completed >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
+      const int done = st->completed;
+      r.flags = 1u | (done >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
+      r._pad = (uint32_t)done;
     }
-    rec[i] = r;
+    srec[i] = r;
   }
   __syncthreads();
-  targets_block(v, step, rec);
+  targets_block(v, step, srec);
   if (threadIdx.x == 0) c->step = step + 1;
 }
 
@@ -765,6 +827,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
   double* Wv = v.W + base;
   double* PR = v.prior + base;
   double* RW = v.reward + base;
+  double* QQ = v.Q + base;
   uint64_t* MF = v.mf + base;
   uint32_t* ME = (uint32_t*)MF;  // ME[2*i]: meta word of node i
   int32_t* PA = v.parent + base;
@@ -816,6 +879,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
   uint32_t root_meta = (uint32_t)rmf;
   uint64_t rno = NO[0];
   double rW = Wv[0];
+  const double rQ = QQ[0];  // W/N of the root (N > 0), constant during a wave
   int rfc = (int)(rmf >> 32);
   int decision = TS_EXIT_NONE;
   int nl = 0;
@@ -839,7 +903,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     int node = 0, depth = 0, nfc = rfc;
     uint32_t nmeta = root_meta;
     uint64_t nno = rno;
-    double nW = rW, nrew = 1.0;
+    double nW = rW, nQ = rQ, nrew = 1.0;
     pnode = -1;
     Agg agg;
     agg.init();
@@ -850,10 +914,10 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     while (nmeta & M_KIDS) {
       const long long pN = (long long)(uint32_t)nno, pO = (long long)(nno >> 32);
       const double psq = sqrt((double)(pN + pO));
-      const double pq = pN == 0 ? 0.5 : nW / (double)pN;
+      const double pq = pN == 0 ? 0.5 : nQ;  // parent.mean_value(default=0.5)
       const int fc = nfc;
       bool valid = lane < width;
-      double sc = -INFINITY, cr = 0.0, cw = 0.0;
+      double sc = -INFINITY, cr = 0.0, cw = 0.0, cq = 0.0;
       uint32_t cm = 0;
       uint64_t cno = 0;
       int cfc = -1;
@@ -861,6 +925,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
         const int c = fc + lane;
         cno = NO[c];
         cw = Wv[c];
+        cq = QQ[c];
         const double cp = PR[c];
         const uint64_t cmf = MF[c];
         cm = (uint32_t)cmf;
@@ -869,8 +934,8 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
         valid = meta_expandable(cm);
         if (valid) {
           const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
-          // _child_q (tree.py:235-239)
-          const double q = cN == 0 ? pq : cw / (double)cN;
+          // _child_q (tree.py:235-239): W/N, kept as Q since the last backup
+          const double q = cN == 0 ? pq : cq;
           if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
           // wu_puct_score (tree.py:232): q + c*P*sqrt(N_s+O_s)/(1+N_sa+O_sa)
           sc = q + c_puct * cp * psq / (double)(1 + cN + cO);
@@ -888,6 +953,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       nrew = __shfl_sync(FULL, cr, j);
       nno = __shfl_sync(FULL, cno, j);
       nW = __shfl_sync(FULL, cw, j);
+      nQ = __shfl_sync(FULL, cq, j);
       nfc = __shfl_sync(FULL, cfc, j);
       agg.add(nrew, scheme);
       if (depth == 1) d1r = nrew;
@@ -1126,8 +1192,11 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       if (lane < len) {
         const uint64_t x = NO[pn];
         if ((x >> 32) < 1) bad = true;
-        NO[pn] = x + 1 - O_ONE;
-        Wv[pn] += sc;
+        const uint64_t nx = x + 1 - O_ONE;
+        const double w2 = Wv[pn] + sc;
+        NO[pn] = nx;
+        Wv[pn] = w2;
+        QQ[pn] = w2 / (double)(uint32_t)nx;
       }
     } else {
       // single rollout: the path's N|O and W are still the registers' values
@@ -1136,14 +1205,17 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       pn = pnode;
       if (lane < len) {
         if ((pno >> 32) < 1) bad = true;
-        NO[pn] = pno + 1 - O_ONE;
-        Wv[pn] = pW + sc;
+        const uint64_t nx = pno + 1 - O_ONE;
+        const double w2 = pW + sc;
+        NO[pn] = nx;
+        Wv[pn] = w2;
+        QQ[pn] = w2 / (double)(uint32_t)nx;
       }
     }
     if ((rno >> 32) < 1) bad = true;
     rno = rno + 1 - O_ONE;
     rW += sc;
-    if (lane == 0) { NO[0] = rno; Wv[0] = rW; }
+    if (lane == 0) { NO[0] = rno; Wv[0] = rW; QQ[0] = rW / (double)(uint32_t)rno; }
     if (__any_sync(FULL, bad)) { status = TS_ACCOUNTING; break; }
     __syncwarp();
     ++completed;
@@ -1280,6 +1352,14 @@ __device__ __forceinline__ void spin_until_ge(volatile int* p, int v) {
   __threadfence_block();
 }
 
+#ifdef TS_HEAVY_PROF
+#define HPROF_T0(x) long long x = clock64()
+#define HPROF_ACC(acc, t0) acc += clock64() - (t0)
+#else
+#define HPROF_T0(x) (void)0
+#define HPROF_ACC(acc, t0) (void)0
+#endif
+
 // If `node` is the selected leaf of a job that is issued but not committed,
 // wait for that commit (acquire) and return true: the caller must reload the
 // node's meta and first child.  Jobs [committed, issued) are checked lane-parallel.
@@ -1293,9 +1373,14 @@ __device__ __forceinline__ bool heavy_wait_inflight(HeavyCtl* ctl, const HeavyJo
   return true;
 }
 
+constexpr int SQRT_TAB = 2048;  // sqrt(k) for k < SQRT_TAB in shared memory (IEEE sqrt is exact-rounded)
+__device__ __forceinline__ double isqrt_tab(const double* sqt, long long n) {
+  return n < SQRT_TAB ? sqt[n] : sqrt((double)n);
+}
+
 template <int NSLOT, int WT>
-__device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, int count, WaveStats& ws,
-                             uint64_t& rno_out, double& rW_out, int& decision_out) {
+__device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, const double* sqt, int count,
+                             WaveStats& ws, uint64_t& rno_out, double& rW_out, int& decision_out) {
   const int lane = threadIdx.x & 31;
   const ts_config& cf = v.cfg;
   const ts_problem* pb = v.prob + s;
@@ -1305,6 +1390,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   double* PR = v.prior + base;
   double* RW = v.reward + base;
   uint64_t* MF = v.mf + base;
+  const double* QQ = v.Q + base;
   const int bdepth = pb->base_depth;
   const int glen = pb->golden_len;
   const int width = WT;
@@ -1314,90 +1400,116 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   const int risky_depth = min(bdepth, cf.depth_cap) - 1;
   uint64_t rno = NO[0];
   const double rW = Wv[0];
+  const long long rN = (long long)(uint32_t)rno;
+  const double rq = rN == 0 ? 0.5 : QQ[0];  // the root's mean (constant during a wave)
+  uint64_t rmf = MF[0];
+  int root_seen = 0;  // commits of jobs below this index have been folded into rmf
   int decision = TS_EXIT_NONE;
   int last_risky = -1;
   int k = 0;
   unsigned long long scored = 0, levels = 0;
+#ifdef TS_HEAVY_PROF
+  long long p_total = 0, p_risky = 0, p_infl = 0, p_ring = 0, p_load = 0, p_math = 0, p_lvls = 0;
+  HPROF_T0(p_start);
+#endif
   for (; k < count; ++k) {
+    HPROF_T0(t_r);
     if (last_risky >= 0) spin_until_ge(&ctl->committed, last_risky + 1);
+    HPROF_ACC(p_risky, t_r);
     if (ctl->status != TS_OK) break;
     // jobs < cs are committed and visible from here on; jobs [cs, k) may commit
-    // while this selection reads the tree
+    // while this selection reads the tree (they are checked at every node entered)
     const int cs = ctl->committed;
     __threadfence_block();
-    heavy_wait_inflight(ctl, ring, cs, k, 0);  // the root itself may be an in-flight leaf
-    const uint64_t rmf = MF[0];
+    {
+      // the root's word changes only when a committed job had the root as its
+      // leaf or was risky
+      bool stale = false;
+      for (int j = root_seen; j < cs; ++j) {
+        const HeavyJob& jb = ring[j % HEAVY_RING];
+        stale |= jb.leaf == 0 || jb.risky != 0;
+      }
+      root_seen = cs;
+      if (heavy_wait_inflight(ctl, ring, cs, k, 0)) stale = true;
+      if (stale) rmf = MF[0];
+    }
     uint32_t nmeta = (uint32_t)rmf;
     if (!meta_expandable(nmeta)) {  // NoExpandableLeafError (tree.py:273-274)
       if (k == 0) decision = -1;
       break;
     }
     int node = 0, depth = 0, nfc = (int)(rmf >> 32);
-    uint64_t nno = rno;
-    double nW = rW, nrew = 1.0;
+    // the current node's mean W/N (0.5 unvisited) and sqrt(N+O), ready before its children are scored
+    double pq = rq, psq = isqrt_tab(sqt, rN + (long long)(rno >> 32));
     int pnode = -1, pj = 0;
     uint64_t pno = 0;
+    double nrew = 1.0;
     Agg agg;
     agg.init();
     bool golden = glen >= 0;
     double d1r = 1.0;
     int status = TS_OK;
-    for (;;) {
-      while (nmeta & M_KIDS) {
-        const long long pN = (long long)(uint32_t)nno, pO = (long long)(nno >> 32);
-        const double psq = sqrt((double)(pN + pO));
-        const double pq = pN == 0 ? 0.5 : nW / (double)pN;
-        const int fc = nfc;
-        bool valid = lane < width;
-        double sc = -INFINITY, cr = 0.0, cw = 0.0;
-        uint32_t cm = 0;
-        uint64_t cno = 0;
-        int cfc = -1;
+    while (nmeta & M_KIDS) {
+      const int fc = nfc;
+      bool valid = lane < width;
+      double sc = -INFINITY, cr = 0.0, nq = 0.5, nsq = 0.0;
+      uint64_t cno = 0, cmf = 0;
+#ifdef TS_HEAVY_PROF
+      long long t_l0 = clock64();
+#endif
+      if (valid) {
+        const int c = fc + lane;
+        cno = NO[c];
+        const double cq = QQ[c];
+        const double cp = PR[c];
+        cmf = MF[c];
+        cr = RW[c];
+        valid = meta_expandable((uint32_t)cmf);
+#ifdef TS_HEAVY_PROF
+        if (lane == 0) p_load += clock64() - t_l0 + (cq == -1.0 ? 1 : 0) + (cp == -1.0 ? 1 : 0) + (cr == -1.0 ? 1 : 0);
+#endif
+        const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
+        nq = cN == 0 ? 0.5 : cq;  // this child's mean, the next level's parent term
+        nsq = isqrt_tab(sqt, cN + cO);
         if (valid) {
-          const int c = fc + lane;
-          cno = NO[c];
-          cw = Wv[c];
-          const double cp = PR[c];
-          const uint64_t cmf = MF[c];
-          cm = (uint32_t)cmf;
-          cr = RW[c];
-          cfc = (int)(cmf >> 32);
-          valid = meta_expandable(cm);
-          if (valid) {
-            const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
-            const double q = cN == 0 ? pq : cw / (double)cN;
-            if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
-            sc = q + c_puct * cp * psq / (double)(1 + cN + cO);
-          }
-        }
-        const unsigned vb = __ballot_sync(FULL, valid);
-        if (__any_sync(FULL, status != TS_OK)) { status = TS_INVALID_ARGUMENT; break; }
-        if (!vb) { status = TS_EXHAUSTED; break; }
-        scored += __popc(vb);
-        ++levels;
-        const int j = warp_argmax(sc, valid, 0);
-        node = fc + j;
-        ++depth;
-        nmeta = __shfl_sync(FULL, cm, j);
-        nrew = __shfl_sync(FULL, cr, j);
-        nno = __shfl_sync(FULL, cno, j);
-        nW = __shfl_sync(FULL, cw, j);
-        nfc = __shfl_sync(FULL, cfc, j);
-        agg.add(nrew, scheme);
-        if (depth == 1) d1r = nrew;
-        golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
-        if (lane == depth - 1) { pnode = node; pno = nno; pj = j; }
-        // entering a leaf whose expansion may be in flight: its meta/fc/children
-        // are only valid after that job's commit
-        if (heavy_wait_inflight(ctl, ring, cs, k, node)) {
-          const uint64_t x = MF[node];
-          nmeta = (uint32_t)x;
-          nfc = (int)(x >> 32);
-        } else if (nmeta & M_KIDS) {
-          __threadfence_block();  // acquire: a commit published this node's children before its word
+          // _child_q (tree.py:235-239); wu_puct_score (tree.py:232)
+          const double q = cN == 0 ? pq : nq;
+          if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
+          sc = q + c_puct * cp * psq / (double)(1 + cN + cO);
         }
       }
-      break;
+      const unsigned vb = __ballot_sync(FULL, valid);
+      if (__any_sync(FULL, status != TS_OK)) { status = TS_INVALID_ARGUMENT; break; }
+      if (!vb) { status = TS_EXHAUSTED; break; }
+      scored += __popc(vb);
+      ++levels;
+      const int j = warp_argmax(sc, valid, 0);
+#ifdef TS_HEAVY_PROF
+      if (lane == 0) p_math += clock64() - t_l0;
+#endif
+      node = fc + j;
+      ++depth;
+      const uint64_t wmf = __shfl_sync(FULL, cmf, j);
+      nmeta = (uint32_t)wmf;
+      nfc = (int)(wmf >> 32);
+      nrew = __shfl_sync(FULL, cr, j);
+      const uint64_t nno = __shfl_sync(FULL, cno, j);
+      pq = __shfl_sync(FULL, nq, j);
+      psq = __shfl_sync(FULL, nsq, j);
+      agg.add(nrew, scheme);
+      if (depth == 1) d1r = nrew;
+      golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
+      if (lane == depth - 1) { pnode = node; pno = nno; pj = j; }
+      // entering a leaf whose expansion may be in flight: its word and children
+      // are only valid after that job's commit (acquired in the wait)
+      HPROF_T0(t_i);
+      const bool waited = heavy_wait_inflight(ctl, ring, cs, k, node);
+      HPROF_ACC(p_infl, t_i);
+      if (waited) {
+        const uint64_t x = MF[node];
+        nmeta = (uint32_t)x;
+        nfc = (int)(x >> 32);
+      }
     }
     if (status != TS_OK) {
       if (lane == 0) atomicCAS((int*)&ctl->status, TS_OK, status);
@@ -1408,7 +1520,18 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     if (lane < depth) NO[pnode] = pno + O_ONE;
     if (lane == 0) NO[0] = rno;
     // hand the rollout to its simulator
+    HPROF_T0(t_g);
     if (k - ctl->committed >= HEAVY_RING) spin_until_ge(&ctl->committed, k - HEAVY_RING + 1);
+    HPROF_ACC(p_ring, t_g);
+    if (root_seen <= k - HEAVY_RING) {  // fold commits whose ring slot is about to be reused
+      bool stale = false;
+      for (int j = root_seen; j <= k - HEAVY_RING; ++j) {
+        const HeavyJob& jb = ring[j % HEAVY_RING];
+        stale |= jb.leaf == 0 || jb.risky != 0;
+      }
+      root_seen = k - HEAVY_RING + 1;
+      if (stale) rmf = MF[0];
+    }
     HeavyJob& jb = ring[k % HEAVY_RING];
     jb.pnode[lane] = pnode;
     jb.pj[lane] = pj;
@@ -1430,7 +1553,26 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     if (width == 1 || depth >= risky_depth || v.heavy_sync) last_risky = k;
   }
   if (lane == 0) ctl->done = 1;
+#ifdef TS_HEAVY_PROF
+  HPROF_ACC(p_total, p_start);
+  HPROF_T0(t_end);
+#endif
   spin_until_ge(&ctl->committed, k);
+#ifdef TS_HEAVY_PROF
+  long long p_drain = 0;
+  HPROF_ACC(p_drain, t_end);
+  if (lane == 0) {
+    atomicAdd(&v.ctr->prof[0], (unsigned long long)p_total);
+    atomicAdd(&v.ctr->prof[1], (unsigned long long)p_risky);
+    atomicAdd(&v.ctr->prof[2], (unsigned long long)p_infl);
+    atomicAdd(&v.ctr->prof[3], (unsigned long long)p_ring);
+    atomicAdd(&v.ctr->prof[4], (unsigned long long)p_drain);
+    atomicAdd(&v.ctr->prof[5], (unsigned long long)k);
+    atomicAdd(&v.ctr->prof[6], (unsigned long long)p_load);
+    atomicAdd(&v.ctr->prof[7], (unsigned long long)p_math);
+    atomicAdd(&v.ctr->prof[12], (unsigned long long)levels);
+  }
+#endif
   rno_out = rno;
   rW_out = rW;
   decision_out = decision;
@@ -1483,8 +1625,14 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
   }
   long long tok_acc = 0;
   unsigned long long created = 0;
+#ifdef TS_HEAVY_PROF
+  long long q_issue = 0, q_comp = 0, q_cwait = 0, q_commit = 0;
+#endif
   for (int k = si;; k += HEAVY_SIM) {
+    HPROF_T0(t_a);
     while (ctl->issued <= k && !ctl->done) __nanosleep(32);
+    HPROF_ACC(q_issue, t_a);
+    HPROF_T0(t_b);
     __threadfence_block();
     if (ctl->issued <= k) break;
     const HeavyJob& jb = ring[k % HEAVY_RING];
@@ -1507,7 +1655,6 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     uint32_t pmeta = 0, lvl_term = 0;
     double prew = 0.0, pagg = 1.0;
     if (lane == d0 - 1) { pmeta = jb.leaf_meta; prew = jb.nrew; pagg = jb.agg_a; }
-    const uint32_t leaf_meta0 = jb.leaf_meta;
     const int leaf = jb.leaf;
     const bool risky = jb.risky != 0;
     int depth = d0, nrel = 0, node = leaf;
@@ -1570,8 +1717,68 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     const int dend = depth;
     const int nlev = dend - d0;
     const double pscore = agg.value(scheme);
-    // --- commit in rollout order ---
+    // --- everything that does not depend on the node ids, before the commit turn ---
+    const double up_rew = __shfl_up_sync(FULL, prew, 1);
+    const double up_agg = __shfl_up_sync(FULL, pagg, 1);
+    const int upj = __shfl_up_sync(FULL, pj, 1);
+    const uint32_t up_meta = __shfl_up_sync(FULL, pmeta, 1);
+    const double rew_l = lane == 0 ? 1.0 : up_rew;
+    const double agg_l = lane == 0 ? 1.0 : up_agg;
+    const bool act = lane >= d0 && lane < d0 + nlev;
+    int live = 0, ne_cnt = 0;
+    uint32_t meta_l = 0;  // word of path node l (expanded at depth l), minus the root's case
+    if (act) {
+      const int l = lane;
+      const int len = l + 1;
+      double* rawl = s_raw + l * WS;
+      const double* rewl = s_rew + l * WS;
+      double tot = rawl[0], cc = 0.0;
+#pragma unroll
+      for (int i = 1; i < WS; ++i) {
+        const double x = rawl[i];
+        const double t = tot + x;
+        if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
+        else cc += (x - t) + tot;
+        tot = t;
+      }
+      if (cc != 0.0 && isfinite(cc)) tot += cc;
+      const bool rel_d1 = strict || d1r >= theta1;
+#pragma unroll
+      for (int j = 0; j < WS; ++j) {
+        rawl[j] = rawl[j] / tot;  // the normalised prior, in place
+        if (!((lvl_term >> j) & 1u)) {
+          const double rew = rewl[j];
+          ++live;
+          // NE: a new non-terminal leaf, check-relevant and viable (scoring.py:119-175)
+          const bool rel = len == 1 ? (strict || rew >= theta1) : rel_d1;
+          double bound = rew;
+          if (prefix_bound && l > 0) {
+            const double pre = scheme == TS_SCHEME_PRODUCT ? agg_l * rew : (rew < agg_l ? rew : agg_l);
+            bound = fmin(rew, pre);
+          }
+          if (rel && !(bound < tau)) ++ne_cnt;
+        }
+      }
+      if (l >= 1) {  // the expanded node stops being a leaf
+        const double bound = prefix_bound ? fmin(rew_l, agg_l) : rew_l;
+        if (rel_d1 && !(bound < tau)) --ne_cnt;
+      }
+      const uint32_t m = l == d0 ? (d0 == 0 ? 0u : up_meta) : ((uint32_t)l | ((uint32_t)upj << SH_REF));
+      meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
+    }
+    int dv = (int)__reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
+    if (forced) {
+      const bool rel = strict || d1r >= theta1;
+      const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
+      if (rel && !(bound < tau)) --dv;
+    }
+    __syncwarp();
+    // --- commit in rollout order: node ids, records, parent links, exhaustion ---
+    HPROF_ACC(q_comp, t_b);
+    HPROF_T0(t_c);
     spin_until_ge(&ctl->committed, k);
+    HPROF_ACC(q_cwait, t_c);
+    HPROF_T0(t_d);
     int cbase = ctl->nnodes;
     bool ok = ctl->status == TS_OK;
     if (ok && cbase + nlev * width > v.cap) {
@@ -1582,78 +1789,39 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
       if (lane >= d0 && lane < dend) pnode += cbase;  // final ids of the new path nodes
       const int fc0 = cbase;
       uint32_t root_meta = ME[0];
+      if (d0 == 0 && lane == 0) meta_l |= root_meta;  // the root was the selected leaf
       if (risky && lane < d0 - 1) pmeta = ME[2 * pnode];  // current metas for the propagation
       const int up_node = __shfl_up_sync(FULL, pnode, 1);
-      const uint32_t up_meta = __shfl_up_sync(FULL, pmeta, 1);
-      const double up_rew = __shfl_up_sync(FULL, prew, 1);
-      const double up_agg = __shfl_up_sync(FULL, pagg, 1);
-      const int upj = __shfl_up_sync(FULL, pj, 1);
       const int node_l = lane == 0 ? 0 : up_node;
-      const uint32_t leaf_meta = lane == 0 ? (d0 == 0 ? root_meta : leaf_meta0) : up_meta;
-      const double rew_l = lane == 0 ? 1.0 : up_rew;
-      const double agg_l = lane == 0 ? 1.0 : up_agg;
-      const bool act = lane >= d0 && lane < d0 + nlev;
-      int live = 0, ne_cnt = 0;
-      uint32_t meta_l = 0;
       if (act) {
         const int l = lane;
         const int len = l + 1;
         const int fcl = fc0 + (l - d0) * width;
-        const double* rawl = s_raw + l * WS;
+        const double* prl = s_raw + l * WS;
         const double* rewl = s_rew + l * WS;
-        double tot = rawl[0], cc = 0.0;
-#pragma unroll
-        for (int i = 1; i < WS; ++i) {
-          const double x = rawl[i];
-          const double t = tot + x;
-          if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
-          else cc += (x - t) + tot;
-          tot = t;
-        }
-        if (cc != 0.0 && isfinite(cc)) tot += cc;
         const bool last = l == dend - 1;
-        const bool rel_d1 = strict || d1r >= theta1;
+        const int par = l == d0 ? leaf : node_l;
 #pragma unroll
         for (int j = 0; j < WS; ++j) {
-          const double rew = rewl[j];
-          const bool term = (lvl_term >> j) & 1u;
           const int c = fcl + j;
           const bool onpath = j == pj;
           NO[c] = onpath ? O_ONE : 0ull;
           Wv[c] = 0.0;
-          PR[c] = rawl[j] / tot;
-          RW[c] = rew;
-          PA[c] = l == d0 ? leaf : node_l;
+          PR[c] = prl[j];
+          RW[c] = rewl[j];
+          PA[c] = par;
+          // the on-path child expanded at the next level gets its word from lane l+1
           if (!onpath || last) {
-            uint32_t m = (uint32_t)len | ((uint32_t)j << SH_REF) | (term ? M_TERM : 0u);
+            uint32_t m = (uint32_t)len | ((uint32_t)j << SH_REF) | (((lvl_term >> j) & 1u) ? M_TERM : 0u);
             if (onpath && forced) m |= M_TERM | M_FORCED;
             MF[c] = mk_mf(-1, m);
           }
-          if (!term) {
-            ++live;
-            const bool rel = len == 1 ? (strict || rew >= theta1) : rel_d1;
-            double bound = rew;
-            if (prefix_bound && l > 0) {
-              const double pre = scheme == TS_SCHEME_PRODUCT ? agg_l * rew : (rew < agg_l ? rew : agg_l);
-              bound = fmin(rew, pre);
-            }
-            if (rel && !(bound < tau)) ++ne_cnt;
-          }
         }
-        if (l >= 1) {
-          const double bound = prefix_bound ? fmin(rew_l, agg_l) : rew_l;
-          if (rel_d1 && !(bound < tau)) --ne_cnt;
-        }
-        const uint32_t m = l == d0 ? leaf_meta : ((uint32_t)l | ((uint32_t)upj << SH_REF));
-        meta_l = m | M_KIDS | ((uint32_t)live << SH_NEXP);
       }
       // publish the expanded nodes only after their children are written
       __threadfence_block();
       __syncwarp();
-      if (act) {
-        const int nl_id = lane == d0 ? leaf : node_l;
-        MF[nl_id] = mk_mf(fc0 + (lane - d0) * width, meta_l);
-      }
+      if (act) MF[lane == d0 ? leaf : node_l] = mk_mf(fc0 + (lane - d0) * width, meta_l);
       {
         const uint32_t dn = __shfl_down_sync(FULL, meta_l, 1);
         const bool dn_act = (lane + 1) >= d0 && (lane + 1) < d0 + nlev;
@@ -1665,12 +1833,6 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
         const uint32_t m = __shfl_sync(FULL, pmeta, dend - 1);
         const int lid = __shfl_sync(FULL, pnode, dend - 1);
         if (lane == 0) ME[2 * lid] = m;
-      }
-      int dv = (int)__reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
-      if (forced) {
-        const bool rel = strict || d1r >= theta1;
-        const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
-        if (rel && !(bound < tau)) --dv;
       }
       __syncwarp();
       int dead_from = -1;
@@ -1699,7 +1861,16 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     __threadfence_block();
     __syncwarp();
     if (lane == 0) ctl->committed = k + 1;
+    HPROF_ACC(q_commit, t_d);
   }
+#ifdef TS_HEAVY_PROF
+  if (lane == 0) {
+    atomicAdd(&v.ctr->prof[8], (unsigned long long)q_issue);
+    atomicAdd(&v.ctr->prof[9], (unsigned long long)q_comp);
+    atomicAdd(&v.ctr->prof[10], (unsigned long long)q_cwait);
+    atomicAdd(&v.ctr->prof[11], (unsigned long long)q_commit);
+  }
+#endif
   long long t = tok_acc;
   for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
   if (lane == 0) {
@@ -1719,6 +1890,7 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
   uint64_t* NO = v.no + base;
   double* Wv = v.W + base;
   const uint32_t* ME = (const uint32_t*)(v.mf + base);
+  double* QQ = v.Q + base;
   const int budget = cf.rollout_budget;
   int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
   double* SSs = v.ss + (size_t)s * budget;
@@ -1749,13 +1921,16 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
     if (lane < len) {
       const uint64_t x = NO[pn];
       if ((x >> 32) < 1) bad = true;
-      NO[pn] = x + 1 - O_ONE;
-      Wv[pn] += sc;
+      const uint64_t nx = x + 1 - O_ONE;
+      const double w2 = Wv[pn] + sc;
+      NO[pn] = nx;
+      Wv[pn] = w2;
+      QQ[pn] = w2 / (double)(uint32_t)nx;
     }
     if ((rno >> 32) < 1) bad = true;
     rno = rno + 1 - O_ONE;
     rW += sc;
-    if (lane == 0) { NO[0] = rno; Wv[0] = rW; }
+    if (lane == 0) { NO[0] = rno; Wv[0] = rW; QQ[0] = rW / (double)(uint32_t)rno; }
     if (__any_sync(FULL, bad)) { status = TS_ACCOUNTING; break; }
     __syncwarp();
     ++completed;
@@ -1816,6 +1991,9 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
   __shared__ HeavyCtl ctl;
   __shared__ HeavyJob ring[HEAVY_RING];
   __shared__ int s_item;
+  __shared__ double sqt[SQRT_TAB];
+  for (int i = threadIdx.x; i < SQRT_TAB; i += HEAVY_THREADS) sqt[i] = sqrt((double)i);
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WaveStats ws = {0, 0, 0, 0, 0, 0};
   const int count_items = v.ctr->heavy_count;
@@ -1843,7 +2021,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
     double rW = 0.0;
     int decision = TS_EXIT_NONE;
     if (warp == 0) {
-      heavy_select<NSLOT, WT>(v, s, &ctl, ring, count, ws, rno, rW, decision);
+      heavy_select<NSLOT, WT>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
     } else {
       double* s_raw = hsm + (size_t)(warp - 1) * 2 * 32 * WT;
       heavy_simulate<NSLOT, WT>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, warp - 1);
@@ -1941,6 +2119,7 @@ struct ts_engine {
   // device buffers
   uint64_t* no = nullptr;
   double* W = nullptr;
+  double* Q = nullptr;
   double* prior = nullptr;
   double* reward = nullptr;
   uint64_t* mf = nullptr;
@@ -2020,6 +2199,7 @@ View make_view(ts_engine* e) {
   memset(&v, 0, sizeof(v));
   v.no = e->no;
   v.W = e->W;
+  v.Q = e->Q;
   v.prior = e->prior;
   v.reward = e->reward;
   v.mf = e->mf;
@@ -2031,7 +2211,7 @@ View make_view(ts_engine* e) {
   v.ctr = e->ctr;
   v.work = e->work;
   v.work_heavy = e->work_heavy;
-  v.heavy_on = (e->wkind != 3 && !e->heavy_off) ? 1 : 0;
+  v.heavy_on = (e->wkind != 3 && !e->heavy_off && e->n_local <= HBITS_WORDS * 32) ? 1 : 0;
   v.heavy_sync = e->heavy_sync ? 1 : 0;
   v.sp = e->sp;
   v.ss = e->ss;
@@ -2051,7 +2231,8 @@ View make_view(ts_engine* e) {
   return v;
 }
 
-size_t targets_smem() { return 160 * 8 + 32 * 16 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8); }
+size_t targets_smem() { return 344 * 8 + 32 * 16 + HBITS_WORDS * 4 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8); }
+size_t sched_smem() { return targets_smem() + (size_t)SREC_MAX * sizeof(ts_sched_record); }
 
 // log1p(k) for k < n from the host libm (the reference calls math.log1p,
 // scheduler.py:128, which is the same C library function).
@@ -2202,7 +2383,7 @@ int build_run_graph(ts_engine* e, const View& v) {
   k1.func = (void*)k_sched;
   k1.gridDim = dim3(1);
   k1.blockDim = dim3(TT);
-  k1.sharedMemBytes = (unsigned)targets_smem();
+  k1.sharedMemBytes = (unsigned)sched_smem();
   k1.kernelParams = a1;
   cudaGraphNode_t n1, n2;
   TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1));
@@ -2295,7 +2476,7 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
   if (cr == cudaSuccess)
     cr = cudaFuncSetAttribute(k_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   if (cr == cudaSuccess)
-    cr = cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
+    cr = cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sched_smem());
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
       cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2320,7 +2501,7 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
 
 int ts_engine_destroy(ts_engine* e) {
   if (!e) return TS_OK;
-  void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
+  void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
                   e->work_heavy};
@@ -2372,14 +2553,15 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   int rc;
   const size_t pool = (size_t)cap * (size_t)n_local;
   if (pool > (size_t)e->pool_nodes || !e->no) {
-    void* ptrs[] = {e->no, e->W, e->prior, e->reward, e->mf, e->parent};
+    void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent};
     for (void* p : ptrs)
       if (p) cudaFree(p);
-    e->no = nullptr; e->W = nullptr; e->prior = nullptr; e->reward = nullptr;
+    e->no = nullptr; e->W = nullptr; e->Q = nullptr; e->prior = nullptr; e->reward = nullptr;
     e->mf = nullptr; e->parent = nullptr;
     e->pool_nodes = 0;
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->no, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->W, pool * 8));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->Q, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->prior, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->reward, pool * 8));
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->mf, pool * 8));
@@ -2521,7 +2703,7 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
       int blocks = 0;
       if ((rc = wave_grid(e, blocks))) return rc;
       for (int it = 0;; ++it) {
-        k_sched<<<1, TT, targets_smem(), s>>>(v, e->records, cudaGraphConditionalHandle(), 0);
+        k_sched<<<1, TT, sched_smem(), s>>>(v, e->records, cudaGraphConditionalHandle(), 0);
         TS_LAUNCH_CHECK(e, "k_sched");
         if ((rc = launch_wave(e, v, -1, s))) return rc;
         if (it % 8 == 7) {
@@ -2594,6 +2776,16 @@ int ts_read_targets(ts_engine* e, int32_t* host_out, int32_t n, void* stream) {
   for (int i = 0; i < n; ++i) host_out[i] = st[i].target;
   return TS_OK;
 }
+
+#ifdef TS_HEAVY_PROF
+// diagnostics build only (not part of the C-ABI): the pipelined-mode phase counters
+int ts_debug_prof(ts_engine* e, uint64_t* host16) {
+  Counters c;
+  TS_CUDA_TRY(e, cudaMemcpy(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost));
+  memcpy(host16, c.prof, sizeof(c.prof));
+  return TS_OK;
+}
+#endif
 
 int ts_read_latencies(ts_engine* e, uint64_t* host_out, int32_t n, void* stream) {
   if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");

@@ -1,0 +1,32 @@
+"""Phase counters of the pipelined CTA mode (diagnostics build
+lib/libtreeserve_b200_prof.so, -DTS_HEAVY_PROF).   TS_LIB_PATH=... python tools/heavy_prof.py"""
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("TS_LIB_PATH", os.path.join(ROOT, "paper_2604_00510_b200", "lib", "libtreeserve_b200_prof.so"))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2604_00510_b200.backend import problem_table  # noqa: E402
+from paper_2604_00510_b200.engine import Engine  # noqa: E402
+
+table = problem_table(bench.workload(bench.PER_GPU))
+eng = Engine(bench.search_config(bench.PER_GPU), 0)
+for rep in range(2):
+    eng.load(table)
+    st = eng.run()
+torch.cuda.synchronize()
+buf = (ctypes.c_uint64 * 16)()
+eng.lib.ts_debug_prof.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+eng.lib.ts_debug_prof(eng._h, buf)
+p = list(buf)
+jobs = max(1, p[5])
+print("jobs", jobs, "rollouts", st.rollouts)
+print("selector cycles/job: total %.0f risky-wait %.0f inflight-wait %.0f ring-wait %.0f | drain total %.0f" %
+      (p[0] / jobs, p[1] / jobs, p[2] / jobs, p[3] / jobs, p[4]))
+print("selector per level: load %.0f load+math+argmax %.0f (levels %d)" % (p[6] / max(1, p[12]), p[7] / max(1, p[12]), p[12]))
+print("simulator cycles/job: wait-issue %.0f compute %.0f wait-commit %.0f commit %.0f" %
+      (p[8] / jobs, p[9] / jobs, p[10] / jobs, p[11] / jobs))
