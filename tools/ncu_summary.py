@@ -1,0 +1,62 @@
+"""Summarise ncu CSV outputs into profiles/ JSON (run here, after gpurun).
+
+    python tools/ncu_summary.py launches <launches.csv> <out.json> <note>
+    python tools/ncu_summary.py dram <dram.csv> <out.json> <note>
+"""
+import collections
+import csv
+import json
+import sys
+
+
+def rows(path):
+    hdr, out = None, []
+    for r in csv.reader(open(path)):
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            out.append(dict(zip(hdr, r)))
+    return out
+
+
+def val(d):
+    v = float(d["Metric Value"].replace(",", ""))
+    u = d["Metric Unit"]
+    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6,
+             "Gbyte": 1e9}
+    return v * scale.get(u, 1.0)
+
+
+def launches(path):
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for d in rows(path):
+        if d["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        k = d["Kernel Name"].split("(")[0]
+        agg[k][0] += 1
+        agg[k][1] += val(d)
+    tot = sum(x[1] for x in agg.values())
+    return {k: {"launches": n, "total_us": round(t / 1e3, 1), "avg_us": round(t / n / 1e3, 2),
+                "share": round(t / tot, 3)} for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1])}
+
+
+def dram(path):
+    per = collections.defaultdict(lambda: collections.defaultdict(float))
+    for d in rows(path):
+        k = d["Kernel Name"].split("(")[0]
+        per[(k, d["ID"])][d["Metric Name"]] += val(d)
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for (k, _), m in per.items():
+        agg[k][0] += 1
+        agg[k][1] += m.get("dram__bytes_read.sum", 0.0)
+        agg[k][2] += m.get("dram__bytes_write.sum", 0.0)
+    return {k: {"launches": n, "dram_read_bytes": r, "dram_write_bytes": w, "bytes_per_launch": (r + w) / n}
+            for k, (n, r, w) in agg.items()}
+
+
+if __name__ == "__main__":
+    mode, src, dst, note = sys.argv[1:5]
+    out = {"note": note, "kernels": launches(src) if mode == "launches" else dram(src)}
+    json.dump(out, open(dst, "w"), indent=1)
+    print(json.dumps(out, indent=1)[:1500])
