@@ -1277,7 +1277,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
 
 
 template <int NSLOT, int WT>
-__global__ void __launch_bounds__(WAVE_THREADS) k_wave(View v, int step) {
+__global__ void __launch_bounds__(WAVE_THREADS, 4) k_wave(View v, int step) {
   constexpr int WS = WT ? WT : TS_MAX_WIDTH;
   extern __shared__ double wsm[];  // per warp: raw priors and rewards, [32 depths][WS]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

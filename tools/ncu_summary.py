@@ -60,3 +60,50 @@ if __name__ == "__main__":
     out = {"note": note, "kernels": launches(src) if mode == "launches" else dram(src)}
     json.dump(out, open(dst, "w"), indent=1)
     print(json.dumps(out, indent=1)[:1500])
+
+
+def details(rep):
+    """Key metrics of one `ncu --set full` capture (ncu -i <rep> --page details)."""
+    import subprocess
+
+    out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(out.splitlines()))
+    hdr = r[0]
+    keep = {"Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput", "Memory Throughput",
+            "L1/TEX Hit Rate", "L2 Hit Rate", "Compute (SM) Throughput", "Executed Ipc Active",
+            "Issue Slots Busy", "Registers Per Thread", "Achieved Occupancy", "Theoretical Occupancy",
+            "Block Size", "Grid Size", "Dynamic Shared Memory Per Block", "Warp Cycles Per Issued Instruction",
+            "No Eligible", "Executed Instructions"}
+    res = {}
+    for row in r[1:]:
+        d = dict(zip(hdr, row))
+        if d.get("Metric Name") in keep:
+            res[d["Metric Name"]] = f'{d["Metric Value"]} {d["Metric Unit"]}'.strip()
+    return res
+
+
+def stalls(rep):
+    """Warp-stall reasons summed over the source page of one capture."""
+    import subprocess
+
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+                         capture_output=True, text=True).stdout
+    agg = collections.Counter()
+    hdr = None
+    for r in csv.reader(out.splitlines()):
+        if r and r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr) and r[2] == "-":
+            for i, h in enumerate(hdr):
+                if h.startswith("stall_") and "Not Issued" not in h and r[i]:
+                    try:
+                        agg[h] += int(r[i])
+                    except ValueError:
+                        pass
+    tot = sum(agg.values()) or 1
+    return {k: round(v / tot, 3) for k, v in agg.most_common(8)}
+
+
+if __name__ == "__main__" and sys.argv[1] == "capture":
+    pass
