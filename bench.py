@@ -167,12 +167,21 @@ def algorithmic_bytes(st) -> int:
             + B_PATH * st.path_nodes)
 
 
-def profile_waves(eng, table, lo, n_total, d: Dist):
-    """Σ k_wave time (CUDA events on the launch stream) and algorithmic bytes of one batch."""
+def profile_waves(eng, table, lo, n_total, d: Dist, sharded=None):
+    """Σ wave-kernel time (CUDA events on the launch stream) and algorithmic
+    bytes of one batch; for N ranks the bytes of all ranks over the slowest
+    rank's wave time."""
     import torch
 
     if d.world > 1:
-        return 0.0, 0
+        eng.load(table, lo, n_total)
+        evs = []
+        torch.cuda.synchronize()
+        d.barrier()
+        sharded.run(wave_events=evs)
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in evs)
+        return d.max(ms), int(d.sum(algorithmic_bytes(eng.stats())))
     n = len(table)
     eng.load(table, lo, n_total)
     counts = torch.zeros(3, dtype=torch.int64, device="cuda")
@@ -260,10 +269,27 @@ def bench_ours(args, d: Dist):
     # roofline: one extra batch through the step API with CUDA events around
     # every k_wave launch on the launch stream (the graph path above has no
     # per-kernel events); algorithmic bytes from the engine counters
-    wave_ms, byte_total = profile_waves(eng, table, lo, n_total, d)
+    wave_ms, byte_total = profile_waves(eng, table, lo, n_total, d, sharded)
 
-    # e2e: host problem table in → host outcomes out through one C-ABI call
+    # e2e: host problem table in → host outcomes out through the public API
     e2e = None
+    if N > 1:
+        from paper_2604_00510_b200._abi import TsOutcome, TsProblem
+
+        ts, ro = [], 0
+        for _ in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            d.barrier()
+            t0 = time.perf_counter()
+            eng.load(table, lo, n_total)  # H2D of this rank's problem table
+            sharded.run()
+            eng.outcomes()  # D2H of this rank's outcomes
+            ts.append(d.max(time.perf_counter() - t0))
+            ro = d.sum(eng.stats().rollouts)
+        e2e = {"value": ro / statistics.median(ts), "unit": UNIT,
+               "h2d_bytes_per_step": ctypes.sizeof(TsProblem) * n_total,
+               "d2h_bytes_per_step": ctypes.sizeof(TsOutcome) * n_total,
+               "ms_per_step": 1e3 * statistics.median(ts), "api": "Engine.load + ShardedRun.run + Engine.outcomes"}
     if N == 1:
         ts = []
         ro = 0
@@ -309,7 +335,7 @@ def bench_ours(args, d: Dist):
         eng.close()
         return None
     hbm, src = peaks()
-    achieved = byte_total / (wave_ms / 1e3) / 1e9
+    achieved = byte_total / (wave_ms / 1e3) / 1e9 if wave_ms > 0 else 0.0
     traffic = None
     try:  # DRAM bytes of the same wave kernels over one batch, from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "r01_ncu_dram_c2_full.json")) as f:
@@ -380,7 +406,7 @@ def bench_reference(args):
     oracle.build()
     threads = os.cpu_count() or 1
     specs = workload(PER_GPU)
-    sample = 512
+    sample = PER_GPU  # the whole config-2 batch: ~30 ms per step on 16 host threads
     t = problem_table(specs[:sample])
     cfg = search_config(sample).to_c()
     for _ in range(args.warmup):
@@ -398,10 +424,11 @@ def bench_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
-        "config": {"workload": f"c2 sample: first {sample} of {PER_GPU} searches, M={sample}"},
+        "config": {"workload": f"c2: {PER_GPU}/GPU searches, b={BRANCH}, depth {BASE + 1}, budget {BUDGET}, "
+                               f"PE+NE+boost, M={PER_GPU}", "searches": sample},
         "p99_search_latency_ms": percentile(lat, 99),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{sample} searches per step"},
+                         "sample": f"the full batch of {sample} searches per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -75,10 +75,11 @@ class ShardedRun:
         if parts[0].data_ptr() != out.data_ptr():  # backend returned fresh tensors
             out.copy_(__import__("torch").cat(parts))
 
-    def run(self, max_steps: int = 1 << 30) -> int:
+    def run(self, max_steps: int = 1 << 30, wave_events: Optional[list] = None) -> int:
         """Advance waves until every search of every rank has exited; returns
         the number of loop iterations (the reference loop's ``steps`` when it
-        breaks exactly at the first all-finished check)."""
+        breaks exactly at the first all-finished check).  ``wave_events``
+        collects (start, stop) CUDA events around every wave launch."""
         eng = self.engine
         for step in range(max_steps):
             eng.step_counts(step, self.counts.data_ptr())
@@ -91,7 +92,16 @@ class ShardedRun:
             eng.step_records(step, self.records.data_ptr())
             self._gather(self.all_records, self.records)
             eng.step_targets(step, self.all_records.data_ptr())
-            eng.step_wave(step)
+            if wave_events is None:
+                eng.step_wave(step)
+            else:
+                import torch
+
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                eng.step_wave(step)
+                e1.record()
+                wave_events.append((e0, e1))
         return max_steps
 
 

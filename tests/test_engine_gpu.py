@@ -325,3 +325,42 @@ def test_pipelined_mode_matches_single_warp_mode(seed, M, budget, cap, b, base, 
     _cmp_outcomes(a[4], c[4], f"pipelined[{seed}]")
     for x, y in zip(a[5], c[5]):
         assert_tree_equal(x, {k: v.tolist() for k, v in y.items()}, "pipelined tree")
+
+
+def test_sum_scheme_q_out_of_range_raises_like_reference():
+    """CUMULATIVE_SUM scores exceed 1, so W/N > 1 and wu_puct_score raises
+    ValueError("q_value out of range") (tree.py:227-229) once a visited child is
+    scored; the engine reports it per search and the drop-in raises it."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.scoring import AggregationScheme, ScoringConfig
+    from paper_2604_00510_b200.search import run_tree_search
+
+    p = B.make_workload(8, (1.0, 0.0, 0.0), 4, branching=2, depth_ranges={d: (4, 4) for d in B.Difficulty})[0]
+    with pytest.raises(ValueError):
+        run_tree_search(p, ScoringConfig(scheme=AggregationScheme.CUMULATIVE_SUM), rollout_budget=32,
+                        depth_cap=8, expand_width=2, positive_exit=False, negative_exit=False)
+
+
+def test_minimum_scheme_and_prefix_bound_trees_vs_oracle():
+    """MINIMUM aggregation with the PREFIX_AGGREGATE futility bound under boosting."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+    from paper_2604_00510_b200.scoring import AggregationScheme, FutilityBound, ScoringConfig
+
+    specs = B.make_workload(300, (0.4, 0.3, 0.3), 21, branching=3,
+                            depth_ranges={d: (5, 9) for d in B.Difficulty})
+    t = B.problem_table(specs)
+    cfg = SearchConfig(scoring=ScoringConfig(scheme=AggregationScheme.MINIMUM, futility_bound=FutilityBound.PREFIX_AGGREGATE,
+                                             strict_negative_exit=True, positive_exit_threshold=0.6),
+                       scheduler=SchedulerConfig(max_concurrency=900, obs_threshold=1), rollout_budget=40,
+                       depth_cap=7, expand_width=3)
+    ref = oracle.OracleRun(t, cfg.to_c(), threads=8)
+    with _engine(cfg) as eng:
+        eng.load(t)
+        st = eng.run()
+        _cmp_outcomes(eng.outcomes(), ref.outcomes, "min-prefix")
+        assert st.steps == ref.steps
+        for i in (0, 7, 150, 299):
+            assert_tree_equal(eng.tree(i), ref.tree(i), f"min-prefix[{i}]")
+    ref.close()
