@@ -912,7 +912,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
 
     // --- select_leaf (tree.py:264-284): one round of child loads per level ---
     while (nmeta & M_KIDS) {
-      const long long pN = (long long)(uint32_t)nno, pO = (long long)(nno >> 32);
+      const unsigned pN = (uint32_t)nno, pO = (uint32_t)(nno >> 32);
       const double psq = sqrt((double)(pN + pO));
       const double pq = pN == 0 ? 0.5 : nQ;  // parent.mean_value(default=0.5)
       const int fc = nfc;
@@ -932,14 +932,14 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
         cr = RW[c];
         cfc = (int)(cmf >> 32);
         valid = meta_expandable(cm);
-        if (valid) {
-          const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
-          // _child_q (tree.py:235-239): W/N, kept as Q since the last backup
-          const double q = cN == 0 ? pq : cq;
-          if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
-          // wu_puct_score (tree.py:232): q + c*P*sqrt(N_s+O_s)/(1+N_sa+O_sa)
-          sc = q + c_puct * cp * psq / (double)(1 + cN + cO);
-        }
+        // branch-free, so all loads issue together; masked by `valid`
+        const unsigned cN = (uint32_t)cno, cO = (uint32_t)(cno >> 32);
+        // _child_q (tree.py:235-239): W/N, kept as Q since the last backup
+        const double q = cN == 0 ? pq : cq;
+        // wu_puct_score (tree.py:232): q + c*P*sqrt(N_s+O_s)/(1+N_sa+O_sa)
+        const double u = c_puct * cp * psq / (double)(1u + cN + cO);
+        if (valid && (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0))) status = TS_INVALID_ARGUMENT;
+        sc = valid ? q + u : -INFINITY;
       }
       const unsigned vb = __ballot_sync(FULL, valid);
       if (__any_sync(FULL, status != TS_OK)) { status = TS_INVALID_ARGUMENT; break; }
@@ -1251,6 +1251,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     S->best_term = best_term;
     S->best = best;
     S->tokens += tok_acc;
+    atomicAdd(&v.ctr->tokens, (unsigned long long)tok_acc);
     S->launched = launched;
     S->cancelled = cancelled;
     // on_rollout_complete (scheduler.py:217-233): refresh Job.best_score
@@ -1347,9 +1348,17 @@ struct HeavyCtl {
   unsigned long long created, tokens;
 };
 
+// CTA-scope acquire load / release store on shared-memory counters
+__device__ __forceinline__ int ld_acquire_cta(const volatile int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared((const void*)p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(volatile int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" :: "r"((unsigned)__cvta_generic_to_shared((const void*)p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ void spin_until_ge(volatile int* p, int v) {
-  while (*p < v) __nanosleep(32);
-  __threadfence_block();
+  while (ld_acquire_cta(p) < v) __nanosleep(32);
 }
 
 #ifdef TS_HEAVY_PROF
@@ -1363,13 +1372,15 @@ __device__ __forceinline__ void spin_until_ge(volatile int* p, int v) {
 // If `node` is the selected leaf of a job that is issued but not committed,
 // wait for that commit (acquire) and return true: the caller must reload the
 // node's meta and first child.  Jobs [committed, issued) are checked lane-parallel.
-__device__ __forceinline__ bool heavy_wait_inflight(HeavyCtl* ctl, const HeavyJob* ring, int c0, int issued,
-                                                    int node) {
+// Lane l holds the leaf of job (issued - 1 - l) for the last 32 jobs (lleaf),
+// so the check is a compare and a ballot.
+__device__ __forceinline__ bool heavy_wait_inflight(HeavyCtl* ctl, int lleaf, int c0, int issued, int node) {
   const int lane = threadIdx.x & 31;
-  const bool hit = c0 + lane < issued && ring[(c0 + lane) % HEAVY_RING].leaf == node;
+  const int job = issued - 1 - lane;
+  const bool hit = job >= c0 && lleaf == node;
   const unsigned hm = __ballot_sync(FULL, hit);
   if (!hm) return false;
-  spin_until_ge(&ctl->committed, c0 + __ffs(hm));
+  spin_until_ge(&ctl->committed, issued - __ffs(hm) + 1);  // the most recent matching job
   return true;
 }
 
@@ -1406,6 +1417,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   int root_seen = 0;  // commits of jobs below this index have been folded into rmf
   int decision = TS_EXIT_NONE;
   int last_risky = -1;
+  int lleaf = -1;  // lane l: leaf of job k-1-l
   int k = 0;
   unsigned long long scored = 0, levels = 0;
 #ifdef TS_HEAVY_PROF
@@ -1419,8 +1431,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     if (ctl->status != TS_OK) break;
     // jobs < cs are committed and visible from here on; jobs [cs, k) may commit
     // while this selection reads the tree (they are checked at every node entered)
-    const int cs = ctl->committed;
-    __threadfence_block();
+    const int cs = ld_acquire_cta(&ctl->committed);
     {
       // the root's word changes only when a committed job had the root as its
       // leaf or was risky
@@ -1430,7 +1441,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         stale |= jb.leaf == 0 || jb.risky != 0;
       }
       root_seen = cs;
-      if (heavy_wait_inflight(ctl, ring, cs, k, 0)) stale = true;
+      if (heavy_wait_inflight(ctl, lleaf, cs, k, 0)) stale = true;
       if (stale) rmf = MF[0];
     }
     uint32_t nmeta = (uint32_t)rmf;
@@ -1468,15 +1479,15 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
 #ifdef TS_HEAVY_PROF
         if (lane == 0) p_load += clock64() - t_l0 + (cq == -1.0 ? 1 : 0) + (cp == -1.0 ? 1 : 0) + (cr == -1.0 ? 1 : 0);
 #endif
-        const long long cN = (long long)(uint32_t)cno, cO = (long long)(cno >> 32);
+        // branch-free, so all five loads issue together; masked by `valid`
+        const unsigned cN = (uint32_t)cno, cO = (uint32_t)(cno >> 32);
         nq = cN == 0 ? 0.5 : cq;  // this child's mean, the next level's parent term
-        nsq = isqrt_tab(sqt, cN + cO);
-        if (valid) {
-          // _child_q (tree.py:235-239); wu_puct_score (tree.py:232)
-          const double q = cN == 0 ? pq : nq;
-          if (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0)) status = TS_INVALID_ARGUMENT;
-          sc = q + c_puct * cp * psq / (double)(1 + cN + cO);
-        }
+        nsq = isqrt_tab(sqt, (long long)cN + cO);
+        // _child_q (tree.py:235-239); wu_puct_score (tree.py:232)
+        const double q = cN == 0 ? pq : cq;
+        const double u = c_puct * cp * psq / (double)(1u + cN + cO);
+        if (valid && (!(q >= 0.0 && q <= 1.0) || !(cp >= 0.0 && cp <= 1.0))) status = TS_INVALID_ARGUMENT;
+        sc = valid ? q + u : -INFINITY;
       }
       const unsigned vb = __ballot_sync(FULL, valid);
       if (__any_sync(FULL, status != TS_OK)) { status = TS_INVALID_ARGUMENT; break; }
@@ -1503,7 +1514,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       // entering a leaf whose expansion may be in flight: its word and children
       // are only valid after that job's commit (acquired in the wait)
       HPROF_T0(t_i);
-      const bool waited = heavy_wait_inflight(ctl, ring, cs, k, node);
+      const bool waited = heavy_wait_inflight(ctl, lleaf, cs, k, node);
       HPROF_ACC(p_infl, t_i);
       if (waited) {
         const uint64_t x = MF[node];
@@ -1515,10 +1526,6 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       if (lane == 0) atomicCAS((int*)&ctl->status, TS_OK, status);
       break;
     }
-    // in-flight registration of root..leaf (tree.py:282-283)
-    rno += O_ONE;
-    if (lane < depth) NO[pnode] = pno + O_ONE;
-    if (lane == 0) NO[0] = rno;
     // hand the rollout to its simulator
     HPROF_T0(t_g);
     if (k - ctl->committed >= HEAVY_RING) spin_until_ge(&ctl->committed, k - HEAVY_RING + 1);
@@ -1547,10 +1554,17 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       jb.agg_n = agg.n;
       jb.d1r = d1r;
     }
-    __threadfence_block();
     __syncwarp();
-    if (lane == 0) ctl->issued = k + 1;
+    if (lane == 0) st_release_cta(&ctl->issued, k + 1);
     if (width == 1 || depth >= risky_depth || v.heavy_sync) last_risky = k;
+    // in-flight registration of root..leaf (tree.py:282-283); only this warp
+    // reads N|O of pre-existing nodes during the wave
+    rno += O_ONE;
+    if (lane < depth) NO[pnode] = pno + O_ONE;
+    if (lane == 0) NO[0] = rno;
+    lleaf = __shfl_up_sync(FULL, lleaf, 1);
+    if (lane == 0) lleaf = node;
+    __syncwarp();
   }
   if (lane == 0) ctl->done = 1;
 #ifdef TS_HEAVY_PROF
@@ -1630,11 +1644,10 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
 #endif
   for (int k = si;; k += HEAVY_SIM) {
     HPROF_T0(t_a);
-    while (ctl->issued <= k && !ctl->done) __nanosleep(32);
+    while (ld_acquire_cta(&ctl->issued) <= k && !ctl->done) __nanosleep(32);
     HPROF_ACC(q_issue, t_a);
     HPROF_T0(t_b);
-    __threadfence_block();
-    if (ctl->issued <= k) break;
+    if (ld_acquire_cta(&ctl->issued) <= k) break;
     const HeavyJob& jb = ring[k % HEAVY_RING];
     const int d0 = jb.d0;
     int pnode = jb.pnode[lane], pj = jb.pj[lane];
@@ -1818,9 +1831,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
           }
         }
       }
-      // publish the expanded nodes only after their children are written
-      __threadfence_block();
-      __syncwarp();
+      // the selector reads this job's nodes only after acquiring its commit
       if (act) MF[lane == d0 ? leaf : node_l] = mk_mf(fc0 + (lane - d0) * width, meta_l);
       {
         const uint32_t dn = __shfl_down_sync(FULL, meta_l, 1);
@@ -1858,9 +1869,8 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
       }
       created += (unsigned long long)nlev * width;
     }
-    __threadfence_block();
     __syncwarp();
-    if (lane == 0) ctl->committed = k + 1;
+    if (lane == 0) st_release_cta(&ctl->committed, k + 1);
     HPROF_ACC(q_commit, t_d);
   }
 #ifdef TS_HEAVY_PROF
@@ -1965,6 +1975,7 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
     S->best_term = best_term;
     S->best = best;
     S->tokens += (long long)ctl->tokens;
+    atomicAdd(&v.ctr->tokens, ctl->tokens);
     S->launched = launched;
     S->cancelled = cancelled;
     if (best_term >= 0 && best > S->job_best) S->job_best = best;
@@ -2150,6 +2161,8 @@ struct ts_engine {
   std::vector<int32_t> h_arrival;
   int max_arrival = 0;
   long long launches = 0;
+  void* pin = nullptr;  // pinned staging for host tables (problems in, outcomes out)
+  size_t pin_bytes = 0;
   std::vector<cudaEvent_t> wave_ev;  // start/stop pairs of every wave since load
   size_t wave_ev_used = 0;
   // ts_run: CUDA graph with a device-driven while loop over {k_sched, k_wave}
@@ -2248,6 +2261,16 @@ int ensure_log1p(ts_engine* e, int need, cudaStream_t s) {
   if (e->log1p_tab) cudaFree(e->log1p_tab);
   e->log1p_tab = p;
   e->log1p_n = n;
+  return TS_OK;
+}
+
+int ensure_pinned(ts_engine* e, size_t bytes) {
+  if (bytes <= e->pin_bytes && e->pin) return TS_OK;
+  if (e->pin) cudaFreeHost(e->pin);
+  e->pin = nullptr;
+  e->pin_bytes = 0;
+  TS_CUDA_TRY(e, cudaMallocHost(&e->pin, bytes));
+  e->pin_bytes = bytes;
   return TS_OK;
 }
 
@@ -2438,11 +2461,11 @@ void host_stats(const Counters& c, ts_run_stats* o) {
   o->rollouts = (int64_t)c.rollouts;
   o->launched = (int64_t)c.launched;
   o->nodes = (int64_t)c.nodes;
-  o->tokens = 0;
   o->children_scored = (int64_t)c.scored;
   o->select_levels = (int64_t)c.levels;
   o->path_nodes = (int64_t)c.path_nodes;
   o->kernel_launches = 0;
+  o->tokens = (int64_t)c.tokens;
 }
 
 }  // namespace
@@ -2509,6 +2532,7 @@ int ts_engine_destroy(ts_engine* e) {
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
   destroy_run_graph(e);
+  if (e->pin) cudaFreeHost(e->pin);
   delete e;
   return TS_OK;
 }
@@ -2605,7 +2629,14 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   e->n_local = n_local;
   e->goff = global_offset;
   e->n_global = n_global;
-  TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, hp, sizeof(ts_problem) * n_local, cudaMemcpyHostToDevice, s));
+  {
+    // stage through pinned memory so the upload is one DMA at full PCIe rate
+    const size_t bytes = sizeof(ts_problem) * (size_t)n_local;
+    if ((rc = ensure_pinned(e, bytes))) return rc;
+    TS_CUDA_TRY(e, cudaStreamSynchronize(s));  // the staging buffer may still feed an earlier copy
+    memcpy(e->pin, hp, bytes);
+    TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, e->pin, bytes, cudaMemcpyHostToDevice, s));
+  }
   TS_CUDA_TRY(e, cudaMemcpyAsync(e->arrival, e->h_arrival.data(), sizeof(int32_t) * n_local,
                                  cudaMemcpyHostToDevice, s));
   if ((rc = ensure_log1p(e, 1024, s))) return rc;
@@ -2741,14 +2772,6 @@ int ts_read_stats(ts_engine* e, ts_run_stats* o, void* stream) {
     TS_CUDA_TRY(e, cudaEventElapsedTime(&ms, e->wave_ev[i], e->wave_ev[i + 1]));
     o->wave_ms += ms;
   }
-  // tokens are per search
-  if (e->loaded) {
-    std::vector<SearchState> st(e->n_local);
-    TS_CUDA_TRY(e, cudaMemcpy(st.data(), e->st, sizeof(SearchState) * e->n_local, cudaMemcpyDeviceToHost));
-    long long t = 0;
-    for (auto& x : st) t += x.tokens;
-    o->tokens = t;
-  }
   if (c.sched_error) return fail(e, TS_INVALID_ARGUMENT, "run queue scores not ordered by arrival");
   return TS_OK;
 }
@@ -2761,7 +2784,12 @@ int ts_read_outcomes(ts_engine* e, ts_outcome* host_out, int32_t n, void* stream
   View v = make_view(e);
   k_outcomes<<<(n + 127) / 128, 128, 0, s>>>(v, e->outcomes, n);
   TS_LAUNCH_CHECK(e, "k_outcomes");
-  TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, e->outcomes, sizeof(ts_outcome) * n, cudaMemcpyDeviceToHost, s));
+  const size_t bytes = sizeof(ts_outcome) * (size_t)n;
+  int rc;
+  if ((rc = ensure_pinned(e, bytes))) return rc;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(e->pin, e->outcomes, bytes, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  memcpy(host_out, e->pin, bytes);
   TS_CUDA_TRY(e, cudaStreamSynchronize(s));
   return TS_OK;
 }
