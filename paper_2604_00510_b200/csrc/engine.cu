@@ -2264,6 +2264,15 @@ int ensure_log1p(ts_engine* e, int need, cudaStream_t s) {
   return TS_OK;
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int ensure_pinned(ts_engine* e, size_t bytes) {
   if (bytes <= e->pin_bytes && e->pin) return TS_OK;
   if (e->pin) cudaFreeHost(e->pin);
@@ -2630,12 +2639,16 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   e->goff = global_offset;
   e->n_global = n_global;
   {
-    // stage through pinned memory so the upload is one DMA at full PCIe rate
+    // one DMA at full PCIe rate: directly from pinned caller memory, else via pinned staging
     const size_t bytes = sizeof(ts_problem) * (size_t)n_local;
-    if ((rc = ensure_pinned(e, bytes))) return rc;
-    TS_CUDA_TRY(e, cudaStreamSynchronize(s));  // the staging buffer may still feed an earlier copy
-    memcpy(e->pin, hp, bytes);
-    TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, e->pin, bytes, cudaMemcpyHostToDevice, s));
+    if (is_pinned(hp)) {
+      TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, hp, bytes, cudaMemcpyHostToDevice, s));
+    } else {
+      if ((rc = ensure_pinned(e, bytes))) return rc;
+      TS_CUDA_TRY(e, cudaStreamSynchronize(s));  // the staging buffer may still feed an earlier copy
+      memcpy(e->pin, hp, bytes);
+      TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, e->pin, bytes, cudaMemcpyHostToDevice, s));
+    }
   }
   TS_CUDA_TRY(e, cudaMemcpyAsync(e->arrival, e->h_arrival.data(), sizeof(int32_t) * n_local,
                                  cudaMemcpyHostToDevice, s));
@@ -2710,6 +2723,7 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
   int rc;
   if ((rc = ensure_log1p(e, 1 << 16, s))) return rc;
   if ((rc = ensure_step_times(e, e->log1p_n + 1, s))) return rc;
+  Counters c;
   for (;;) {
     k_set_max_steps<<<1, 1, 0, s>>>(e->ctr, max_steps);
     TS_LAUNCH_CHECK(e, "k_set_max_steps");
@@ -2728,7 +2742,6 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
         graphed = true;
       }
     }
-    Counters c;
     if (!graphed) {
       // host-driven stepping (same kernels) when conditional graphs are unavailable
       int blocks = 0;
@@ -2754,7 +2767,13 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
     if ((rc = ensure_log1p(e, e->log1p_n * 2, s))) return rc;
     if ((rc = ensure_step_times(e, e->log1p_n + 1, s))) return rc;
   }
-  if (stats_out) return ts_read_stats(e, stats_out, stream);
+  if (stats_out) {
+    // the counters were read after the last launch above: no second round trip
+    host_stats(c, stats_out);
+    stats_out->kernel_launches = e->launches;
+    stats_out->wave_ms = 0.0;
+    if (c.sched_error) return fail(e, TS_INVALID_ARGUMENT, "run queue scores not ordered by arrival");
+  }
   return TS_OK;
 }
 
@@ -2785,11 +2804,16 @@ int ts_read_outcomes(ts_engine* e, ts_outcome* host_out, int32_t n, void* stream
   k_outcomes<<<(n + 127) / 128, 128, 0, s>>>(v, e->outcomes, n);
   TS_LAUNCH_CHECK(e, "k_outcomes");
   const size_t bytes = sizeof(ts_outcome) * (size_t)n;
-  int rc;
-  if ((rc = ensure_pinned(e, bytes))) return rc;
-  TS_CUDA_TRY(e, cudaMemcpyAsync(e->pin, e->outcomes, bytes, cudaMemcpyDeviceToHost, s));
-  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
-  memcpy(host_out, e->pin, bytes);
+  if (is_pinned(host_out)) {
+    TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, e->outcomes, bytes, cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  } else {
+    int rc;
+    if ((rc = ensure_pinned(e, bytes))) return rc;
+    TS_CUDA_TRY(e, cudaMemcpyAsync(e->pin, e->outcomes, bytes, cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+    memcpy(host_out, e->pin, bytes);
+  }
   TS_CUDA_TRY(e, cudaStreamSynchronize(s));
   return TS_OK;
 }

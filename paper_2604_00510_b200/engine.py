@@ -168,10 +168,11 @@ class Engine:
                                                 self.stream), "ts_read_step_times")
         return buf[:n]
 
-    def run_batch_host(self, table, max_steps: int = (1 << 31) - 1):
-        """End to end through one C-ABI call: host table in, host outcomes out."""
+    def run_batch_host(self, table, max_steps: int = (1 << 31) - 1, out=None):
+        """End to end through one C-ABI call: host table in, host outcomes out
+        (pinned buffers from :func:`pinned_array` are copied by DMA directly)."""
         n = len(table)
-        out = (TsOutcome * n)()
+        out = (TsOutcome * n)() if out is None else out
         st = TsRunStats()
         self._check(self.lib.ts_run_batch_host(self._h, table, n, max_steps, out, ctypes.byref(st), self.stream),
                     "ts_run_batch_host")
@@ -190,3 +191,16 @@ def fill_problem(seed: int, solvable: bool, depth_range, branching: int, profile
                              sh[0] if sh else 0.0, sh[1] if sh else 0.0, profile.target_aggregate, ctypes.byref(p))
     raise_for_status(rc, "ts_fill_problem")
     return p
+
+
+def pinned_array(ctype, n: int, init=None):
+    """A ctypes array of ``n`` ``ctype`` in page-locked host memory (kept alive
+    by the returned array's ``_owner``), optionally filled from ``init``."""
+    import torch
+
+    buf = torch.empty(ctypes.sizeof(ctype) * max(1, n), dtype=torch.uint8, pin_memory=True)
+    arr = (ctype * n).from_address(buf.data_ptr())
+    arr._owner = buf
+    if init is not None:
+        ctypes.memmove(arr, init, ctypes.sizeof(ctype) * n)
+    return arr
