@@ -1431,6 +1431,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     if (ctl->status != TS_OK) break;
     // jobs < cs are committed and visible from here on; jobs [cs, k) may commit
     // while this selection reads the tree (they are checked at every node entered)
+    HPROF_T0(t_pro);
     const int cs = ld_acquire_cta(&ctl->committed);
     {
       // the root's word changes only when a committed job had the root as its
@@ -1449,6 +1450,8 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       if (k == 0) decision = -1;
       break;
     }
+    HPROF_ACC(p_load, t_pro);
+    HPROF_T0(t_desc);
     int node = 0, depth = 0, nfc = (int)(rmf >> 32);
     // the current node's mean W/N (0.5 unvisited) and sqrt(N+O), ready before its children are scored
     double pq = rq, psq = isqrt_tab(sqt, rN + (long long)(rno >> 32));
@@ -1460,6 +1463,97 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     bool golden = glen >= 0;
     double d1r = 1.0;
     int status = TS_OK;
+    // per-lane record of a scored node; `take` moves the descent into the node scored by lane `src`
+    auto take = [&](int src, int child_index, int fc_parent, uint64_t xno, uint64_t xmf, double xr, double xnq,
+                    double xnsq) {
+      node = fc_parent + child_index;
+      ++depth;
+      const uint64_t wmf = __shfl_sync(FULL, xmf, src);
+      nmeta = (uint32_t)wmf;
+      nfc = (int)(wmf >> 32);
+      nrew = __shfl_sync(FULL, xr, src);
+      const uint64_t nno = __shfl_sync(FULL, xno, src);
+      pq = __shfl_sync(FULL, xnq, src);
+      psq = __shfl_sync(FULL, xnsq, src);
+      agg.add(nrew, scheme);
+      if (depth == 1) d1r = nrew;
+      golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == child_index;
+      if (lane == depth - 1) { pnode = node; pno = nno; pj = child_index; }
+      // entering a leaf whose expansion may be in flight: its word and children
+      // are only valid after that job's commit (acquired in the wait)
+      const bool waited = heavy_wait_inflight(ctl, lleaf, cs, k, node);
+      if (waited) {
+        const uint64_t x = MF[node];
+        nmeta = (uint32_t)x;
+        nfc = (int)(x >> 32);
+      }
+      return waited;
+    };
+    if constexpr (WT * (WT + 1) <= 32) {
+      // two levels per round: lanes [0, W) score the children, lanes
+      // [W, W + W*W) the children of every child; the second argmax runs in the
+      // group of the child the first one picked
+      const bool l1 = lane < WT;
+      const bool l2lane = lane >= WT && lane < WT + WT * WT;
+      const int gj = l2lane ? (lane - WT) / WT : 0, gi = l2lane ? (lane - WT) % WT : 0;
+      while (nmeta & M_KIDS) {
+        const int fc = nfc;
+        uint64_t xno = 0, xmf = 0;
+        double xq = 0.0, xp = 0.0, xr = 0.0;
+        if (l1) {
+          const int c = fc + lane;
+          xno = NO[c];
+          xq = QQ[c];
+          xp = PR[c];
+          xmf = MF[c];
+          xr = RW[c];
+        }
+        // the grandchild lanes read their parent child's record
+        const int src = l1 ? lane : gj;
+        const uint64_t gpmf = __shfl_sync(FULL, xmf, src);
+        const uint64_t gpno = __shfl_sync(FULL, xno, src);
+        const double gpq = __shfl_sync(FULL, xq, src);
+        const bool l2 = l2lane && ((uint32_t)gpmf & M_KIDS);
+        if (l2) {
+          const int c = (int)(gpmf >> 32) + gi;
+          xno = NO[c];
+          xq = QQ[c];
+          xp = PR[c];
+          xmf = MF[c];
+          xr = RW[c];
+        }
+        // the scored node's parent terms: the current node for l1, the child for l2
+        const unsigned gN = (uint32_t)gpno, gO = (uint32_t)(gpno >> 32);
+        const double ppq = l1 ? pq : (gN == 0 ? 0.5 : gpq);
+        const double ppsq = l1 ? psq : isqrt_tab(sqt, (long long)gN + gO);
+        const bool valid = (l1 || l2) && meta_expandable((uint32_t)xmf);
+        const unsigned xN = (uint32_t)xno, xO = (uint32_t)(xno >> 32);
+        const double xnq = xN == 0 ? 0.5 : xq;
+        const double xnsq = isqrt_tab(sqt, (long long)xN + xO);
+        // _child_q (tree.py:235-239); wu_puct_score (tree.py:232)
+        const double q = xN == 0 ? ppq : xq;
+        const double sc = valid ? q + c_puct * xp * ppsq / (double)(1u + xN + xO) : -INFINITY;
+        const bool bad = valid && (!(q >= 0.0 && q <= 1.0) || !(xp >= 0.0 && xp <= 1.0));
+        // level 1
+        const unsigned vb1 = __ballot_sync(FULL, valid && l1);
+        if (__ballot_sync(FULL, bad && l1)) { status = TS_INVALID_ARGUMENT; break; }
+        if (!vb1) { status = TS_EXHAUSTED; break; }
+        scored += __popc(vb1);
+        ++levels;
+        const int j1 = warp_argmax(sc, valid && l1, 0);
+        if (take(j1, j1, fc, xno, xmf, xr, xnq, xnsq)) continue;  // the group is stale after a commit
+        if (!(nmeta & M_KIDS)) break;
+        // level 2, within the group of child j1
+        const bool ing = l2lane && gj == j1;
+        const unsigned vb2 = __ballot_sync(FULL, valid && ing);
+        if (__ballot_sync(FULL, bad && ing)) { status = TS_INVALID_ARGUMENT; break; }
+        if (!vb2) { status = TS_EXHAUSTED; break; }
+        scored += __popc(vb2);
+        ++levels;
+        const int s2 = warp_argmax(sc, valid && ing, 0);
+        take(s2, (s2 - WT) % WT, nfc, xno, xmf, xr, xnq, xnsq);
+      }
+    } else {
     while (nmeta & M_KIDS) {
       const int fc = nfc;
       bool valid = lane < width;
@@ -1522,6 +1616,9 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         nfc = (int)(x >> 32);
       }
     }
+    }
+    HPROF_ACC(p_math, t_desc);
+    HPROF_T0(t_epi);
     if (status != TS_OK) {
       if (lane == 0) atomicCAS((int*)&ctl->status, TS_OK, status);
       break;
@@ -1565,6 +1662,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     lleaf = __shfl_up_sync(FULL, lleaf, 1);
     if (lane == 0) lleaf = node;
     __syncwarp();
+    HPROF_ACC(p_infl, t_epi);
   }
   if (lane == 0) ctl->done = 1;
 #ifdef TS_HEAVY_PROF
@@ -1581,6 +1679,8 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     atomicAdd(&v.ctr->prof[2], (unsigned long long)p_infl);
     atomicAdd(&v.ctr->prof[3], (unsigned long long)p_ring);
     atomicAdd(&v.ctr->prof[4], (unsigned long long)p_drain);
+    atomicMax(&v.ctr->prof[13], (unsigned long long)p_total);
+    atomicMax(&v.ctr->prof[14], (unsigned long long)p_drain);
     atomicAdd(&v.ctr->prof[5], (unsigned long long)k);
     atomicAdd(&v.ctr->prof[6], (unsigned long long)p_load);
     atomicAdd(&v.ctr->prof[7], (unsigned long long)p_math);
@@ -1952,19 +2052,35 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
     }
     decision = decide(false);
     if (decision != TS_EXIT_NONE) {
-      for (int r2 = r + 1; r2 < nl; ++r2) {
+      // cancel_inflight (tree.py:374-380) for the wave's remaining rollouts.
+      // Their order does not matter (O -= 1 on each path node), so lanes take
+      // whole rollouts and decrement with atomics; a node's in-flight count
+      // must not underflow (AccountingError), checked after all decrements.
+      const int first = r + 1, ncan = nl - first;
+      long long pl = 0;
+      for (int r2 = first + lane; r2 < nl; r2 += 32) {
         const int len2 = SLs[r2];
-        const int pn2 = lane < len2 ? SPs[(size_t)r2 * 32 + lane] : -1;
-        bool bad2 = lane < len2 && (NO[pn2] >> 32) < 1;
-        if ((rno >> 32) < 1) bad2 = true;
-        if (__any_sync(FULL, bad2)) { status = TS_ACCOUNTING; break; }
-        if (lane < len2) NO[pn2] -= O_ONE;
-        rno -= O_ONE;
-        if (lane == 0) NO[0] = rno;
-        __syncwarp();
-        ++cancelled;
-        pathn += len2 + 1;
+        const int32_t* row = SPs + (size_t)r2 * 32;
+        for (int i = 0; i < len2; ++i)
+          atomicAdd((unsigned long long*)&NO[row[i]], (unsigned long long)(0ull - O_ONE));
+        pl += len2 + 1;
       }
+      for (int o = 16; o > 0; o >>= 1) pl += __shfl_xor_sync(FULL, pl, o);
+      __threadfence_block();
+      __syncwarp();
+      bool bad2 = (long long)(rno >> 32) < ncan;
+      for (int r2 = first + lane; r2 < nl; r2 += 32) {
+        const int len2 = SLs[r2];
+        const int32_t* row = SPs + (size_t)r2 * 32;
+        for (int i = 0; i < len2; ++i)
+          if ((NO[row[i]] >> 32) > (uint64_t)budget) bad2 = true;  // wrapped below zero
+      }
+      if (__any_sync(FULL, bad2)) { status = TS_ACCOUNTING; break; }
+      rno -= (uint64_t)ncan * O_ONE;
+      if (lane == 0) NO[0] = rno;
+      __syncwarp();
+      cancelled += ncan;
+      pathn += (unsigned long long)pl;
       break;
     }
   }
@@ -2038,7 +2154,13 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
       heavy_simulate<NSLOT, WT>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, warp - 1);
     }
     __syncthreads();
+#ifdef TS_HEAVY_PROF
+    long long t_fin = clock64();
+#endif
     if (warp == 0) heavy_finish(v, s, step, &ctl, ctl.issued, rno, rW, decision, ws);
+#ifdef TS_HEAVY_PROF
+    if (threadIdx.x == 0) atomicMax(&v.ctr->prof[15], (unsigned long long)(clock64() - t_fin));
+#endif
     __syncthreads();
   }
   if (lane == 0 && warp == 0 && ws.launched) {

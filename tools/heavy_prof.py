@@ -27,6 +27,7 @@ jobs = max(1, p[5])
 print("jobs", jobs, "rollouts", st.rollouts)
 print("selector cycles/job: total %.0f risky-wait %.0f inflight-wait %.0f ring-wait %.0f | drain total %.0f" %
       (p[0] / jobs, p[1] / jobs, p[2] / jobs, p[3] / jobs, p[4]))
-print("selector per level: load %.0f load+math+argmax %.0f (levels %d)" % (p[6] / max(1, p[12]), p[7] / max(1, p[12]), p[12]))
+print("selector per job: prologue %.0f descent %.0f epilogue %.0f (levels/job %.2f)" % (p[6] / jobs, p[7] / jobs, p[2] / jobs, p[12] / jobs))
+print("max over searches: selector loop %d drain %d finish %d cycles" % (p[13], p[14], p[15]))
 print("simulator cycles/job: wait-issue %.0f compute %.0f wait-commit %.0f commit %.0f" %
       (p[8] / jobs, p[9] / jobs, p[10] / jobs, p[11] / jobs))
