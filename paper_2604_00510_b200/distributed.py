@@ -40,7 +40,8 @@ class ShardedRun:
     pointers); ``dist`` is ``torch.distributed`` with an initialised group.
     """
 
-    def __init__(self, engine, dist, n_local: int, n_total: int, device, group=None, check_every: int = 8):
+    def __init__(self, engine, dist, n_local: int, n_total: int, device, group=None, check_every: int = 8,
+                 host_staging: bool = False):
         import torch
 
         self.engine = engine
@@ -48,7 +49,11 @@ class ShardedRun:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        if self.world > 1 and any(s != n_local for s in self._all_sizes(n_local, device)):
+        # host_staging: exchange through host memory (a backend without device
+        # tensors, e.g. gloo with several ranks on one GPU in tests)
+        self.host = host_staging
+        xdev = "cpu" if host_staging else device
+        if self.world > 1 and any(s != n_local for s in self._all_sizes(n_local, xdev)):
             raise ValueError("all-gather needs equal shard sizes; pad the run queue")
         self.n_local = n_local
         self.n_total = n_total
@@ -67,6 +72,12 @@ class ShardedRun:
         return [int(x.item()) for x in out]
 
     def _gather(self, out, inp):
+        if self.host:
+            o = out.new_empty(out.shape, device="cpu")
+            parts = list(o.chunk(self.world))
+            self.dist.all_gather(parts, inp.cpu(), group=self.group)
+            out.copy_(o if parts[0].data_ptr() == o.data_ptr() else __import__("torch").cat(parts))
+            return
         if self.dist.get_backend(self.group) == "nccl":
             self.dist.all_gather_into_tensor(out, inp, group=self.group)
             return
@@ -106,5 +117,5 @@ class ShardedRun:
 
 
 def run_sharded(engine, dist, n_local: int, n_total: int, device, group=None,
-                max_steps: int = 1 << 30, check_every: int = 8) -> int:
-    return ShardedRun(engine, dist, n_local, n_total, device, group, check_every).run(max_steps)
+                max_steps: int = 1 << 30, check_every: int = 8, host_staging: bool = False) -> int:
+    return ShardedRun(engine, dist, n_local, n_total, device, group, check_every, host_staging).run(max_steps)
