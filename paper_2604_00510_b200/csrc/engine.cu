@@ -2022,50 +2022,99 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
     return TS_EXIT_NONE;
   };
   if (status == TS_OK && exhausted) decision = decide(true);
-  for (int r = 0; r < nl && status == TS_OK; ++r) {
-    if (completed >= budget) { status = TS_ACCOUNTING; break; }
-    const int len = SLs[r];
-    const double sc = SSs[r];
-    const int pn = lane < len ? SPs[(size_t)r * 32 + lane] : -1;
+  if (status == TS_OK && !exhausted && nl > 0) {
+    // All expansions of the wave are done, so the viable-leaf count and the
+    // root are final: the first backup after which decide_exit fires
+    // (scoring.py:184-207) depends only on the scores.  PE fires at the first
+    // score >= theta, NE at the first backup, the budget at the last allowed one.
+    int rstar = budget - completed - 1;  // nl <= budget - completed
+    if (cf.negative_exit && (root_meta & M_KIDS) && viable == 0) rstar = 0;
+    if (cf.positive_exit) {
+      for (int r0 = 0; r0 < nl && r0 <= rstar; r0 += 32) {
+        const int r = r0 + lane;
+        const unsigned m = __ballot_sync(FULL, r < nl && SSs[r] >= cf.positive_exit_threshold);
+        if (m) {
+          rstar = min(rstar, r0 + __ffs(m) - 1);
+          break;
+        }
+      }
+    }
+    const int nb = min(rstar, nl - 1) + 1;  // rollouts backed up, in launch order
+    // best trajectory: the first of the maximal scores, if it beats the old best (tree.py:370)
+    {
+      double mx = -INFINITY;
+      for (int r = lane; r < nb; r += 32) mx = fmax(mx, SSs[r]);
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+      int rb = nb;
+      for (int r0 = 0; r0 < nb; r0 += 32) {
+        const unsigned m = __ballot_sync(FULL, r0 + lane < nb && SSs[r0 + lane] == mx);
+        if (m) { rb = r0 + __ffs(m) - 1; break; }
+      }
+      if (best_term < 0 || mx > best) {
+        best = mx;
+        best_term = SPs[(size_t)rb * 32 + SLs[rb] - 1];
+      }
+    }
+    // backpropagate (tree.py:352-371) of rollouts [0, nb): lane i owns depth
+    // i+1 (a node has one depth, so lanes never share a node) and adds the
+    // scores in launch order, keeping runs of the same node in registers
     bool bad = false;
-    if (lane < len) {
-      const uint64_t x = NO[pn];
-      if ((x >> 32) < 1) bad = true;
-      const uint64_t nx = x + 1 - O_ONE;
-      const double w2 = Wv[pn] + sc;
-      NO[pn] = nx;
-      Wv[pn] = w2;
-      QQ[pn] = w2 / (double)(uint32_t)nx;
+    int cur = -1;
+    uint64_t cno = 0;
+    double cw = 0.0;
+    unsigned long long pl = 0;
+#pragma unroll 4
+    for (int r = 0; r < nb; ++r) {
+      const int len = SLs[r];
+      const double sc = SSs[r];
+      pl += len + 1;
+      if ((rno >> 32) < 1) bad = true;
+      rno = rno + 1 - O_ONE;
+      rW += sc;
+      if (lane < len) {
+        const int nd = SPs[(size_t)r * 32 + lane];
+        if (nd != cur) {
+          if (cur >= 0) {
+            NO[cur] = cno;
+            Wv[cur] = cw;
+            QQ[cur] = cw / (double)(uint32_t)cno;
+          }
+          cur = nd;
+          cno = NO[nd];
+          cw = Wv[nd];
+        }
+        if ((cno >> 32) < 1) bad = true;
+        cno = cno + 1 - O_ONE;
+        cw += sc;
+      }
     }
-    if ((rno >> 32) < 1) bad = true;
-    rno = rno + 1 - O_ONE;
-    rW += sc;
+    if (cur >= 0) {
+      NO[cur] = cno;
+      Wv[cur] = cw;
+      QQ[cur] = cw / (double)(uint32_t)cno;
+    }
     if (lane == 0) { NO[0] = rno; Wv[0] = rW; QQ[0] = rW / (double)(uint32_t)rno; }
-    if (__any_sync(FULL, bad)) { status = TS_ACCOUNTING; break; }
+    if (__any_sync(FULL, bad)) status = TS_ACCOUNTING;
+    completed += nb;
+    done += nb;
+    pathn += pl;
+    if (status == TS_OK) decision = decide(false);
     __syncwarp();
-    ++completed;
-    ++done;
-    pathn += len + 1;
-    if (best_term < 0 || sc > best) {
-      best = sc;
-      best_term = __shfl_sync(FULL, pn, len - 1);
-    }
-    decision = decide(false);
-    if (decision != TS_EXIT_NONE) {
+    if (status == TS_OK && nb < nl) {
       // cancel_inflight (tree.py:374-380) for the wave's remaining rollouts.
       // Their order does not matter (O -= 1 on each path node), so lanes take
       // whole rollouts and decrement with atomics; a node's in-flight count
       // must not underflow (AccountingError), checked after all decrements.
-      const int first = r + 1, ncan = nl - first;
-      long long pl = 0;
+      const int first = nb, ncan = nl - first;
+      long long pc = 0;
       for (int r2 = first + lane; r2 < nl; r2 += 32) {
         const int len2 = SLs[r2];
         const int32_t* row = SPs + (size_t)r2 * 32;
         for (int i = 0; i < len2; ++i)
           atomicAdd((unsigned long long*)&NO[row[i]], (unsigned long long)(0ull - O_ONE));
-        pl += len2 + 1;
+        pc += len2 + 1;
       }
-      for (int o = 16; o > 0; o >>= 1) pl += __shfl_xor_sync(FULL, pl, o);
+      for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
       __threadfence_block();
       __syncwarp();
       bool bad2 = (long long)(rno >> 32) < ncan;
@@ -2075,13 +2124,12 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
         for (int i = 0; i < len2; ++i)
           if ((NO[row[i]] >> 32) > (uint64_t)budget) bad2 = true;  // wrapped below zero
       }
-      if (__any_sync(FULL, bad2)) { status = TS_ACCOUNTING; break; }
+      if (__any_sync(FULL, bad2)) status = TS_ACCOUNTING;
       rno -= (uint64_t)ncan * O_ONE;
       if (lane == 0) NO[0] = rno;
       __syncwarp();
       cancelled += ncan;
-      pathn += (unsigned long long)pl;
-      break;
+      pathn += (unsigned long long)pc;
     }
   }
   if (lane == 0) {
