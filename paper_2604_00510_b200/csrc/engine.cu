@@ -60,6 +60,7 @@ struct SearchState {
 struct Counters {
   long long running, head, finished, last_exit_step;
   long long step, max_steps;  // device-side step counter of ts_run's graph loop
+  long long win_lo;           // lowest admitted search that may still be running (k_sched window)
   int cur_step, _pad;
   long long admit_lo, admit_hi;
   int work_count, work_next;
@@ -454,7 +455,10 @@ __device__ __forceinline__ int runs_lower(const double* runS, int nr, double s) 
 // The score sum Σ S (scheduler.py:165, CPython's Neumaier sum) equals the
 // correctly rounded exact sum when all compensation terms are exact (checked
 // below); it is computed exactly in 128-bit fixed point.
-__device__ void targets_block(const View& v, int step, const ts_sched_record* rec) {
+// rec holds n records in global run-queue order; records [glo, ghi) are this
+// engine's searches base + (i - glo).
+__device__ void targets_block(const View& v, int step, const ts_sched_record* rec, int n, int glo, int ghi,
+                              int base) {
   extern __shared__ __align__(16) unsigned char smem[];
   long long* shl = (long long*)smem;                 // 264 long longs of scan scratch
   double* shd = (double*)(smem + 264 * 8);           // 80 doubles
@@ -470,11 +474,9 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   const int tid = threadIdx.x;
   const ts_config& cf = v.cfg;
   if (tid == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
-  const int n = v.n_global;
   const int per = (n + TT - 1) / TT;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
-  const int glo = v.goff, ghi = v.goff + v.n_local;
-  for (int w = tid; w < (v.n_local + 31) / 32 && w < HBITS_WORDS; w += TT) hbits[w] = 0u;
+  for (int w = tid; w < (ghi - glo + 31) / 32 && w < HBITS_WORDS; w += TT) hbits[w] = 0u;
 
   // phase 1: counts, exact score sum, list positions
   u128 fx = 0;
@@ -631,7 +633,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     for (int i = lo; i < hi; ++i) {
       ts_sched_record r = rec[i];
       if (!(r.flags & 1u)) {
-        if (i >= glo && i < ghi) v.st[i - glo].target = 0;
+        if (i >= glo && i < ghi) v.st[base + i - glo].target = 0;
         continue;
       }
       long long tgt = 1;
@@ -675,7 +677,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
         // gated: stays serial; advance nothing
       }
       if (i >= glo && i < ghi) {
-        v.st[i - glo].target = (int)tgt;
+        v.st[base + i - glo].target = (int)tgt;
         // rollouts this wave = min(P_i, budget - completed); `_pad` carries completed
         if (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P)
           atomicOr(&hbits[(i - glo) >> 5], 1u << ((i - glo) & 31));
@@ -698,8 +700,8 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   long long ph = sc2[0], pl = sc2[1];
   for (int i = loc_lo; i < loc_hi; ++i) {
     if (!(rec[i + glo].flags & 1u)) continue;
-    if ((hbits[i >> 5] >> (i & 31)) & 1u) v.work_heavy[ph++] = i;
-    else v.work[pl++] = i;
+    if ((hbits[i >> 5] >> (i & 31)) & 1u) v.work_heavy[ph++] = base + i;
+    else v.work[pl++] = base + i;
   }
   if (tid == 0) {
     v.ctr->work_count = (int)tt2[1];
@@ -715,7 +717,7 @@ __device__ __forceinline__ size_t targets_smem_dev() {
 }
 
 __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
-  targets_block(v, step, rec);
+  targets_block(v, step, rec, v.n_global, v.goff, v.goff + v.n_local, 0);
 }
 
 // One scheduler pass of a single-GPU run, fused: the loop test of the wave
@@ -757,13 +759,19 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
   if (!s_go) return;
   const long long alo = c->admit_lo, ahi = c->admit_hi;
   const ts_config& cf = v.cfg;
-  // one GPU: the run queue's records stay in shared memory when they fit
+  // the run queue is the window [win_lo, head): searches below win_lo have
+  // exited, searches from head on are not admitted yet
+  const int wlo = (int)c->win_lo, whi = (int)c->head;
+  const int nw = whi - wlo;
+  // one GPU: the window's records stay in shared memory when they fit
   extern __shared__ __align__(16) unsigned char smem[];
-  ts_sched_record* srec = v.n_local <= SREC_MAX && v.n_global == v.n_local
-                              ? (ts_sched_record*)(smem + targets_smem_dev())
-                              : rec;
+  ts_sched_record* srec = nw <= SREC_MAX ? (ts_sched_record*)(smem + targets_smem_dev()) : rec;
+  __shared__ int s_min;
+  if (threadIdx.x == 0) s_min = whi;
+  __syncthreads();
+  int my_min = whi;
 #pragma unroll 4
-  for (int i = threadIdx.x; i < v.n_local; i += TT) {
+  for (int i = wlo + threadIdx.x; i < whi; i += TT) {
     SearchState* st = v.st + i;
     int state = st->state;
     if (i >= alo && i < ahi) {
@@ -776,6 +784,7 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
     r.flags = 0;
     r._pad = 0;
     if (state == ST_RUNNING) {
+      my_min = min(my_min, i);
       const double ratio = st->job_best / cf.positive_exit_threshold;
       const bool boosted = ratio > cf.proximity;
       r.score = v.log1p_tab[step - v.arrival[i]] + (boosted ? cf.beta : 0.0);
@@ -783,11 +792,16 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
       r.flags = 1u | (done >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
       r._pad = (uint32_t)done;
     }
-    srec[i] = r;
+    srec[i - wlo] = r;
   }
+  for (int o = 16; o > 0; o >>= 1) my_min = min(my_min, __shfl_xor_sync(FULL, my_min, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(&s_min, my_min);
   __syncthreads();
-  targets_block(v, step, srec);
-  if (threadIdx.x == 0) c->step = step + 1;
+  targets_block(v, step, srec, nw, 0, nw, wlo);
+  if (threadIdx.x == 0) {
+    c->win_lo = s_min;  // no running search below this index
+    c->step = step + 1;
+  }
 }
 
 // ---- the wave: one warp per running search ----------------------------------

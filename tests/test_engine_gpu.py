@@ -364,3 +364,28 @@ def test_minimum_scheme_and_prefix_bound_trees_vs_oracle():
         for i in (0, 7, 150, 299):
             assert_tree_equal(eng.tree(i), ref.tree(i), f"min-prefix[{i}]")
     ref.close()
+
+
+@pytest.mark.parametrize("boost", [True, False])
+def test_serving_arrivals_vs_oracle(boost):
+    """Config-5 shape: Poisson arrivals (reference generator, step-quantised),
+    FIFO admission under M, PE(+NE+boost); the windowed scheduler vs the oracle."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    n = 6000
+    specs = B.make_workload(n, (0.6, 0.25, 0.15), 20260810)
+    arrivals = B.serving_arrival_steps(n, 1.0, 20260810, 1.0 / 700.0)
+    t = B.problem_table(specs, arrivals)
+    cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=1024, boosting_enabled=boost), rollout_budget=32,
+                       depth_cap=16, expand_width=4, negative_exit=boost)
+    ref = oracle.OracleRun(t, cfg.to_c(), threads=8)
+    with _engine(cfg) as eng:
+        eng.load(t)
+        st = eng.run()
+        _cmp_outcomes(eng.outcomes(), ref.outcomes, f"serving[{boost}]")
+        assert st.steps == ref.steps
+        for i in (0, 1234, n - 1):
+            assert_tree_equal(eng.tree(i), ref.tree(i), f"serving[{i}]")
+    ref.close()
