@@ -90,6 +90,7 @@ struct View {
   int32_t* work_heavy;     // this wave's searches for the pipelined CTA mode
   int32_t heavy_on;        // pipelined mode available (uniform width 2/4/8)
   int32_t heavy_sync;      // diagnostics: commit every job before the next selection
+  int32_t max_arrival;     // last arrival step of the loaded requests
   int32_t* sp;             // scratch paths of a multi-rollout wave [n_local][budget][32]
   double* ss;              // scratch scores
   int32_t* sl;             // scratch lengths
@@ -720,6 +721,25 @@ __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched
   targets_block(v, step, rec, v.n_global, v.goff, v.goff + v.n_local, 0);
 }
 
+// Number of requests with arrival_step <= step (arrivals are non-decreasing),
+// by one warp: a 32-way split per round instead of a binary search.
+__device__ int arrived_count(const View& v, int step) {
+  if (step >= v.max_arrival) return v.n_local;
+  const int lane = threadIdx.x & 31;
+  // invariant: arrival[i] <= step for i < lo, arrival[i] > step for i >= hi
+  int lo = 0, hi = v.n_local;
+  while (hi - lo > 32) {
+    const int span = (hi - lo + 31) / 32;
+    const int p = lo + lane * span;
+    const int t = __popc(__ballot_sync(FULL, p < hi && v.arrival[p] <= step));  // a prefix of the samples
+    if (t == 0) { hi = lo; break; }
+    const int nhi = min(hi, lo + t * span);  // sample t (if any) is past step
+    lo = lo + (t - 1) * span + 1;            // sample t-1 is not
+    hi = nhi;
+  }
+  return lo + __popc(__ballot_sync(FULL, lo + lane < hi && v.arrival[lo + lane] <= step));
+}
+
 // One scheduler pass of a single-GPU run, fused: the loop test of the wave
 // driver, admit_jobs, parallelism_score records and compute_targets.  The
 // step counter lives on the device, so a CUDA-graph while-loop of
@@ -729,13 +749,10 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
   __shared__ int s_go;
   Counters* c = v.ctr;
   const int step = (int)c->step;
+  int arrived = 0;
+  if (threadIdx.x < 32) arrived = arrived_count(v, step);
   if (threadIdx.x == 0) {
-    int lo = 0, hi = v.n_local;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (v.arrival[mid] <= step) lo = mid + 1;
-      else hi = mid;
-    }
+    const int lo = arrived;
     const long long unfinished = (long long)v.n_local - c->finished;
     const bool go = unfinished > 0 && step < c->max_steps && step < v.log1p_n;
     if (go) {
@@ -2410,6 +2427,7 @@ View make_view(ts_engine* e) {
   v.work_heavy = e->work_heavy;
   v.heavy_on = (e->wkind != 3 && !e->heavy_off && e->n_local <= HBITS_WORDS * 32) ? 1 : 0;
   v.heavy_sync = e->heavy_sync ? 1 : 0;
+  v.max_arrival = e->max_arrival;
   v.sp = e->sp;
   v.ss = e->ss;
   v.sl = e->sl;
