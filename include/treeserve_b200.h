@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 2
+#define TS_ABI_VERSION 3
 #define TS_MAX_DEPTH 32 /* golden path / reward table length; base_depth <= 31 */
 #define TS_MAX_WIDTH 32 /* branching <= one warp                                */
 
@@ -205,6 +205,83 @@ int ts_fill_problem(uint64_t seed, int32_t solvable, int32_t depth_lo, int32_t d
                     double off_hi, int32_t hidden_until_depth, int32_t has_shared,
                     double shared_lo, double shared_hi, double target_aggregate,
                     ts_problem* out);
+
+/* ---- standalone batched policy operators (csrc/policy.cu) ------------------
+ * The reference's scheduler and exit-policy entry points applied to state the
+ * caller owns (its own run queue or trees), for callers that do not run whole
+ * searches in an engine.  No engine handle: errors are reported by the return
+ * code and ts_policy_last_error().  Every device pointer is read on `stream`;
+ * the calls that return a ValueError condition synchronise the stream. */
+const char* ts_policy_last_error(void);
+
+/* SchedulerConfig (scheduler.py:77-93) + positive_exit_threshold. */
+typedef struct ts_sched_params {
+  int64_t max_concurrency;
+  double beta;
+  double proximity;
+  int32_t obs_threshold;
+  int32_t boosting_enabled;
+  double positive_exit_threshold;
+} ts_sched_params;
+
+/* Diagnostics of one ts_compute_targets call. */
+typedef struct ts_targets_info {
+  double total_score;      /* Σ S over the run queue (CPython sum semantics) */
+  int64_t ungated;         /* jobs past the observation gate */
+  int32_t first_bad;       /* lowest index with now < arrival (n if none) */
+  int32_t sum_fallback;    /* 1 if Σ S needed the sequential loop */
+  int32_t kernel_launches;
+  int32_t _pad;
+} ts_targets_info;
+
+/* parallelism_score (scheduler.py:118-128) for n jobs: scores[i] =
+ * log1p(now - arrival[i]) + (beta if best[i]/θ_pos > proximity else 0), log1p
+ * bit-identical to the host libm.  TS_INVALID_ARGUMENT (ValueError) when some
+ * now < arrival[i]; *host_first_bad = the lowest such i (n if none). */
+int ts_parallelism_scores(double now, double positive_exit_threshold, double beta, double proximity,
+                          const double* dev_arrival, const double* dev_best, int32_t n, double* dev_scores,
+                          int32_t* host_first_bad, void* stream);
+
+/* compute_targets (scheduler.py:143-187) for a run queue of n RUNNING jobs in
+ * run-queue order (device arrays; job ids unique): dev_targets[i] = the
+ * target parallelism of job i.  Any arrival order is accepted (the ungated
+ * jobs are sorted on the device by (-S, arrival, id)).  Errors as the
+ * reference: n == 0 → "run queue holds no running jobs", now < arrival →
+ * ValueError (only when boosting is enabled, like the reference). */
+int ts_compute_targets(const ts_sched_params* params, double now, const double* dev_arrival,
+                       const double* dev_best, const int32_t* dev_completed, const int64_t* dev_job_id,
+                       int32_t n, int32_t* dev_targets, ts_targets_info* host_info, void* stream);
+
+/* A forest of SearchTrees (tree.py:117-181) in flat device arrays: tree t owns
+ * nodes [offsets[t], offsets[t+1]), its root first; parent[] holds forest
+ * indices (-1 for a root); per-tree fields feed decide_exit and may be NULL
+ * (no best trajectory / not exhausted / no budget check). */
+enum { TS_NODE_TERMINAL = 1, TS_NODE_HAS_CHILDREN = 2 };
+typedef struct ts_forest {
+  int32_t n_trees, n_nodes;
+  const int32_t* offsets;    /* n_trees + 1 */
+  const int32_t* tree_of;    /* n_nodes: owning tree */
+  const int32_t* parent;     /* n_nodes */
+  const double* reward;      /* n_nodes: prm_reward */
+  const int32_t* depth;      /* n_nodes: StepNode.depth */
+  const uint8_t* flags;      /* n_nodes: TS_NODE_* */
+  const double* best_score;  /* n_trees: best_trajectory.aggregate_score */
+  const uint8_t* has_best;   /* n_trees: best_trajectory is not None */
+  const int32_t* completed;  /* n_trees: completed_rollouts */
+  const int32_t* budget;     /* n_trees: rollout_budget */
+  const uint8_t* exhausted;  /* n_trees: decide_exit(tree_exhausted=...) */
+} ts_forest;
+
+/* check_negative_exit (scoring.py:153-175) and decide_exit (184-207) for every
+ * tree of the forest under one ScoringConfig + enable flags (cfg->scheme,
+ * futility_bound, strict_negative_exit, accept_threshold, first_step_threshold,
+ * positive_exit_threshold, positive_exit, negative_exit; other fields unused).
+ * dev_ne[t] (may be NULL) = 1 if check_negative_exit fires, 0 if not, 2 if it
+ * would raise UnsupportedSchemeError (a check-relevant leaf under SUM/AVERAGE).
+ * dev_kind[t] (may be NULL) = the ExitKind (TS_EXIT_*; NONE = CONTINUE), or
+ * -TS_UNSUPPORTED_SCHEME where decide_exit raises. */
+int ts_exit_policy(const ts_config* cfg, const ts_forest* forest, int32_t* dev_kind, uint8_t* dev_ne,
+                   void* stream);
 
 #ifdef __cplusplus
 }

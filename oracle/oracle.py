@@ -63,6 +63,10 @@ def lib() -> ctypes.CDLL:
         L.or_generate_steps.argtypes = [P(TsProblem), P(i32), i32, i32, P(OrCandidate)]
         L.or_compute_targets.restype = i32
         L.or_compute_targets.argtypes = [P(TsConfig), i32, i32, P(i32), P(i32), P(ctypes.c_double), P(i32)]
+        L.or_compute_targets_general.restype = i32
+        L.or_compute_targets_general.argtypes = [P(TsConfig), ctypes.c_double, i32] + [ctypes.c_void_p] * 5
+        L.or_forest_policy.restype = None
+        L.or_forest_policy.argtypes = [P(TsConfig), i32] + [ctypes.c_void_p] * 12
         L.or_run_waves.restype = ctypes.c_void_p
         L.or_run_waves.argtypes = [P(TsProblem), i32, P(TsConfig), i32, i32, P(i32), ctypes.c_int64,
                                    P(ctypes.c_int64)]
@@ -153,6 +157,40 @@ def compute_targets(cfg: TsConfig, now_step, arrival, completed, best):
     if rc:
         raise ValueError("run queue holds no running jobs")
     return list(T)
+
+
+def compute_targets_general(cfg: TsConfig, now, arrival, completed, best, ids):
+    """compute_targets on a general run queue; raises ValueError like the reference."""
+    import numpy as np
+
+    n = len(arrival)
+    A = np.ascontiguousarray(arrival, np.float64)
+    C = np.ascontiguousarray(completed, np.int32)
+    B = np.ascontiguousarray(best, np.float64)
+    I = np.ascontiguousarray(ids, np.int64)  # noqa: E741
+    T = np.zeros(max(1, n), np.int32)
+    rc = lib().or_compute_targets_general(ctypes.byref(cfg), float(now), n, A.ctypes.data, C.ctypes.data,
+                                          B.ctypes.data, I.ctypes.data, T.ctypes.data)
+    if rc < 0:
+        raise ValueError(f"now={now} precedes arrival={A[-rc - 1]}")
+    if rc:
+        raise ValueError("run queue holds no running jobs")
+    return T[:n].tolist()
+
+
+def forest_policy(cfg: TsConfig, off, parent, reward, depth, flags, best, has_best, completed, budget, exhausted):
+    """(kinds, ne) of every tree of a flat forest (see or_forest_policy)."""
+    import numpy as np
+
+    arrs = [np.ascontiguousarray(a, dt) for a, dt in
+            ((off, np.int32), (parent, np.int32), (reward, np.float64), (depth, np.int32), (flags, np.uint8),
+             (best, np.float64), (has_best, np.uint8), (completed, np.int32), (budget, np.int32),
+             (exhausted, np.uint8))]
+    nt = len(off) - 1
+    kind = np.zeros(max(1, nt), np.int32)
+    ne = np.zeros(max(1, nt), np.uint8)
+    lib().or_forest_policy(ctypes.byref(cfg), nt, *[a.ctypes.data for a in arrs], kind.ctypes.data, ne.ctypes.data)
+    return kind[:nt], ne[:nt]
 
 
 class OracleRun:

@@ -12,7 +12,7 @@ import os
 
 TS_MAX_DEPTH = 32
 TS_MAX_WIDTH = 32
-TS_ABI_VERSION = 2
+TS_ABI_VERSION = 3
 
 TS_OK = 0
 TS_INVALID_ARGUMENT = 1
@@ -117,7 +117,43 @@ EXPORTED = (
     "ts_load_problems", "ts_step_counts", "ts_step_admit", "ts_step_records", "ts_step_targets",
     "ts_step_wave", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_read_targets",
     "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
+    "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
 )
+
+
+class TsSchedParams(ctypes.Structure):
+    _fields_ = [
+        ("max_concurrency", ctypes.c_int64),
+        ("beta", ctypes.c_double),
+        ("proximity", ctypes.c_double),
+        ("obs_threshold", ctypes.c_int32),
+        ("boosting_enabled", ctypes.c_int32),
+        ("positive_exit_threshold", ctypes.c_double),
+    ]
+
+
+class TsTargetsInfo(ctypes.Structure):
+    _fields_ = [
+        ("total_score", ctypes.c_double),
+        ("ungated", ctypes.c_int64),
+        ("first_bad", ctypes.c_int32),
+        ("sum_fallback", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+    ]
+
+
+TS_NODE_TERMINAL = 1
+TS_NODE_HAS_CHILDREN = 2
+
+
+class TsForest(ctypes.Structure):
+    _fields_ = [("n_trees", ctypes.c_int32), ("n_nodes", ctypes.c_int32)] + [
+        (name, ctypes.c_void_p)
+        for name in ("offsets", "tree_of", "parent", "reward", "depth", "flags", "best_score", "has_best",
+                     "completed", "budget", "exhausted")
+    ]
+
 
 _lib = None
 
@@ -156,6 +192,11 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_run_batch_host": (ctypes.c_int, [vp, P(TsProblem), i32, i32, P(TsOutcome), P(TsRunStats), vp]),
         "ts_tree_size": (ctypes.c_int, [vp, i32, P(i32)]),
         "ts_dump_tree": (ctypes.c_int, [vp, i32] + [vp] * 9),
+        "ts_policy_last_error": (ctypes.c_char_p, []),
+        "ts_parallelism_scores": (ctypes.c_int, [ctypes.c_double] * 4 + [vp, vp, i32, vp, P(i32), vp]),
+        "ts_compute_targets": (ctypes.c_int, [P(TsSchedParams), ctypes.c_double, vp, vp, vp, vp, i32, vp,
+                                              P(TsTargetsInfo), vp]),
+        "ts_exit_policy": (ctypes.c_int, [P(TsConfig), P(TsForest), vp, vp, vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

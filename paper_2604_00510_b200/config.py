@@ -81,3 +81,17 @@ def serial_config(
 
 
 MAX_NODE_DEPTH = TS_MAX_DEPTH
+
+
+def scoring_to_c(scoring: ScoringConfig, positive_exit: bool = True, negative_exit: bool = True) -> TsConfig:
+    """The ScoringConfig part of ts_config (for the standalone exit policy)."""
+    c = TsConfig()
+    c.scheme = SCHEME_CODE[scoring.scheme]
+    c.futility_bound = 0 if scoring.futility_bound is FutilityBound.LEAF_REWARD else 1
+    c.strict_negative_exit = int(scoring.strict_negative_exit)
+    c.positive_exit = int(positive_exit)
+    c.negative_exit = int(negative_exit)
+    c.accept_threshold = scoring.accept_threshold
+    c.positive_exit_threshold = scoring.positive_exit_threshold
+    c.first_step_threshold = scoring.first_step_threshold
+    return c

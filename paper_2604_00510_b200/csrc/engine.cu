@@ -18,8 +18,12 @@
 #include <vector>
 
 #include "../../include/treeserve_b200.h"
+#include "exact.cuh"
 
 namespace {
+using tsx::u128;
+using tsx::to_fixed;
+using tsx::fixed_to_double;
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -303,41 +307,6 @@ constexpr int HEAVY_P = 8;  // rollouts in one wave from which a search runs in 
 constexpr int HBITS_WORDS = 2048;  // run-queue slots with a pipelined-mode flag bit (65536)
 constexpr int SREC_MAX = 4096;     // k_sched keeps the records of up to this many searches in shared memory
 constexpr int RUNCAP = 1536;  // runs per list kept in shared memory
-
-typedef unsigned __int128 u128;
-
-// Exact fixed-point image of a score (LSB 2^-64).  Returns false when the
-// score has bits below 2^-64 (then the sum falls back to the sequential loop).
-__device__ __forceinline__ bool to_fixed(double x, u128& out) {
-  uint64_t b = (uint64_t)__double_as_longlong(x);
-  int ex = (int)((b >> 52) & 0x7FF);
-  uint64_t m = b & ((1ull << 52) - 1);
-  if (ex == 0) {
-    out = 0;
-    return m == 0;
-  }
-  m |= 1ull << 52;
-  int sh = ex - 1075 + 64;  // value = m * 2^(ex-1075) = (m << sh) * 2^-64
-  if (sh < 0 || sh > 74) return false;
-  out = (u128)m << sh;
-  return true;
-}
-// Round-to-nearest-even of fixed-point value × 2^-64.
-__device__ double fixed_to_double(u128 v) {
-  if (v == 0) return 0.0;
-  uint64_t hi = (uint64_t)(v >> 64), lo = (uint64_t)v;
-  int p = hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
-  if (p <= 52) return (double)lo * 0x1p-64;
-  int sh = p - 52;
-  uint64_t mant = (uint64_t)(v >> sh);
-  u128 rem = v & (((u128)1 << sh) - 1);
-  u128 half = (u128)1 << (sh - 1);
-  if (rem > half || (rem == half && (mant & 1))) {
-    ++mant;
-    if (mant == (1ull << 53)) { mant >>= 1; ++sh; }
-  }
-  return ldexp((double)mant, sh - 64);
-}
 
 // Block-wide exclusive scan (+) of one value per thread; returns the prefix,
 // writes the block total.  All threads must call.

@@ -1,14 +1,20 @@
-"""Scoring/exit-policy configuration (reference scoring.py:38-103).
+"""Scoring and exit policy (reference scoring.py), drop-in names.
 
-The exit tests themselves run on the device after every backup (csrc/engine.cu:
-``decide_exit`` with an incremental viable-leaf counter in place of the
-reference's full-tree scan, scoring.py:153-175).
+Inside the engine the exit tests run on the device after every backup
+(csrc/engine.cu: ``decide_exit`` with an incremental viable-leaf counter in
+place of the reference's full-tree scan, scoring.py:153-175).  For callers
+that hold their own trees, ``check_negative_exit``, ``check_positive_exit``
+and ``decide_exit`` (and the batched ``decide_exits``) take reference-style
+``SearchTree`` objects (or their ``to_dict()`` dumps) and run the standalone
+forest kernels of csrc/policy.cu: one thread per node classifies the
+expandable leaves, one per tree decides.
 """
 
 from __future__ import annotations
 
 import enum
 from dataclasses import dataclass
+from typing import Optional, Sequence
 
 
 class UnsupportedSchemeError(Exception):
@@ -84,3 +90,60 @@ def check_scheme_for_pruning(config: ScoringConfig) -> None:
         raise UnsupportedSchemeError(
             f"negative exit is unsound under {config.scheme.value} aggregation"
         )
+
+
+_KIND_OF_CODE = EXIT_FROM_CODE
+
+
+def _decisions(trees: Sequence, config: ScoringConfig, positive_enabled: bool, negative_enabled: bool,
+               tree_exhausted: Optional[Sequence[bool]], device: int):
+    from .policy import Forest, exit_policy
+
+    forest = Forest(trees, tree_exhausted, device)
+    kinds, ne = exit_policy(forest, config, positive_enabled, negative_enabled)
+    return forest, kinds, ne
+
+
+def _unsupported(config: ScoringConfig) -> UnsupportedSchemeError:
+    return UnsupportedSchemeError(f"negative exit is unsound under {config.scheme.value} aggregation")
+
+
+def decide_exits(trees: Sequence, config: ScoringConfig, positive_enabled: bool = True,
+                 negative_enabled: bool = True, tree_exhausted: Optional[Sequence[bool]] = None,
+                 device: int = 0) -> list:
+    """decide_exit (scoring.py:184-207) for many trees in one pass on the device."""
+    forest, kinds, _ = _decisions(trees, config, positive_enabled, negative_enabled, tree_exhausted, device)
+    out = []
+    for t, k in enumerate(kinds.tolist()):
+        if k < 0:
+            raise _unsupported(config)
+        out.append(ExitDecision(_KIND_OF_CODE[k], float(forest.best[t]) if forest.has_best[t] else 0.0))
+    return out
+
+
+def decide_exit(tree, config: ScoringConfig, positive_enabled: bool = True, negative_enabled: bool = True,
+                tree_exhausted: bool = False) -> ExitDecision:
+    """Combine the exit checks after a completed rollout (scoring.py:184-207)."""
+    return decide_exits([tree], config, positive_enabled, negative_enabled, [tree_exhausted])[0]
+
+
+def check_negative_exit_many(trees: Sequence, config: ScoringConfig, device: int = 0) -> list:
+    """check_negative_exit (scoring.py:153-175) for many trees on the device."""
+    _, _, ne = _decisions(trees, config, False, True, None, device)
+    res = []
+    for v in ne.tolist():
+        if v == 2:
+            raise _unsupported(config)
+        res.append(v == 1)
+    return res
+
+
+def check_negative_exit(tree, config: ScoringConfig) -> bool:
+    """True when no check-relevant leaf can still reach the acceptance threshold."""
+    return check_negative_exit_many([tree], config)[0]
+
+
+def check_positive_exit(tree, config: ScoringConfig) -> bool:
+    """True once the best completed trajectory meets the exit threshold (scoring.py:178-181)."""
+    _, kinds, _ = _decisions([tree], config, True, False, None, 0)
+    return int(kinds[0]) == 1

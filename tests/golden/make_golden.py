@@ -337,7 +337,156 @@ def gen_targets():
     dump("targets_kats", kats)
 
 
+def _policy_tree_record(tree: SearchTree, configs):
+    """to_dict() plus best score and, per scoring config, the reference's
+    check_negative_exit / decide_exit answers (or the exception it raises)."""
+    from treeserve.scoring import UnsupportedSchemeError, check_negative_exit, decide_exit
+
+    rec = tree.to_dict()
+    rec["nodes"] = [{k: nd[k] for k in ("id", "parent", "reward", "terminal", "depth")} for nd in rec["nodes"]]
+    best = tree.best_trajectory
+    rec["best_score"] = None if best is None else best.aggregate_score
+    answers = []
+    for sc in configs:
+        row = {}
+        try:
+            row["ne"] = check_negative_exit(tree, sc)
+        except UnsupportedSchemeError:
+            row["ne"] = "unsupported"
+        for pe in (True, False):
+            for ne in (True, False):
+                for ex in (False, True):
+                    key = f"{int(pe)}{int(ne)}{int(ex)}"
+                    try:
+                        d = decide_exit(tree, sc, pe, ne, ex)
+                        row[key] = [d.kind.value, d.best_score]
+                    except UnsupportedSchemeError:
+                        row[key] = "unsupported"
+        answers.append(row)
+    rec["answers"] = answers
+    return rec
+
+
+def gen_policy():
+    """Standalone policy operators (csrc/policy.cu): compute_targets on general
+    run queues (unsorted fractional arrivals, shuffled ids), parallelism_score
+    errors, math.log1p values, and check_negative_exit / decide_exit on trees
+    taken mid-search from reference runs and on hand-built deep trees."""
+    import math
+
+    from treeserve.backend import ProblemBackend
+    from treeserve.scheduler import parallelism_score
+    from treeserve.search import finish_rollout
+    from treeserve.tree import (NoExpandableLeafError, SelectionParams, expand, select_leaf,
+                                simulate_to_terminal)
+
+    r = random.Random(11)
+    out = {}
+    # log1p KATs (wait times: non-negative)
+    xs = [0.0, 1e-300, 5e-324, 1e-17, 2.0**-29, 2.0**-28, 1e-5, 0.1, 0.2928, 0.2929, 0.41421, 0.4142135623730950,
+          0.5, 1.0, 2.0, 3.0, 10.0, 1e6, 2.0**53, 1e300, 1.7976931348623157e308]
+    for e in range(-40, 40):
+        for _ in range(25):
+            xs.append(math.ldexp(r.random() + 0.5, e))
+    xs += [r.uniform(0, 50) for _ in range(2000)] + [float(k) for k in range(200)]
+    out["log1p"] = [[x, math.log1p(x)] for x in xs]
+    # general compute_targets
+    kats = []
+    for t in range(300):
+        n = r.randint(1, 40) if t % 5 else r.randint(200, 3000)
+        M = n + r.choice([0, r.randint(0, n), r.randint(0, 6 * n)])
+        cfg = SchedulerConfig(max_concurrency=M, beta=r.choice([2.0, 1.0, 0.5, 3.7]), proximity=r.choice([0.9, 0.5, 0.75]),
+                              obs_threshold=r.choice([1, 2, 3]), boosting_enabled=r.random() > 0.05)
+        theta = r.choice([0.5, 0.6, 0.35])
+        now = r.choice([r.uniform(0, 100), float(r.randint(0, 50))])
+        kind = t % 4
+        ids = r.sample(range(10 * n + 10), n)
+        rows = []
+        state = SchedulerState(now=now)
+        for i in range(n):
+            if kind == 0:
+                arr = r.uniform(0, now)                      # unsorted fractional arrivals
+            elif kind == 1:
+                arr = float(r.randint(0, int(now)))          # integer arrivals, many ties
+            elif kind == 2:
+                arr = 0.0                                    # lock-step pool (all equal scores)
+            else:
+                arr = r.choice([0.0, now, now / 2, r.uniform(0, now)])
+            job = Job(job_id=ids[i], arrival_time=arr, tree=SearchTree(8))
+            job.completed_rollouts = r.randint(0, 5)
+            job.best_score = r.choice([0.0, r.random(), theta * cfg.proximity, theta * 0.95, r.random() * theta * 1.2])
+            job.state = JobState.RUNNING
+            state.run_queue.append(job)
+            rows.append([arr, job.completed_rollouts, job.best_score, ids[i]])
+        targets = compute_targets(state, cfg, theta)
+        scores = None if not cfg.boosting_enabled else [parallelism_score(j, now, theta, cfg) for j in state.run_queue]
+        kats.append({"now": now, "M": M, "beta": cfg.beta, "proximity": cfg.proximity, "obs_threshold": cfg.obs_threshold,
+                     "boosting": cfg.boosting_enabled, "theta_pos": theta, "jobs": rows,
+                     "targets": [targets[j[3]] for j in rows], "scores": scores})
+    out["targets"] = kats
+    # error cases: a job arriving after now
+    errs = []
+    for boosting in (True, False):
+        state = SchedulerState(now=3.0)
+        for i, arr in enumerate([0.0, 1.0, 4.5, 2.0, 7.0]):
+            job = Job(job_id=i, arrival_time=arr, tree=SearchTree(8))
+            job.state = JobState.RUNNING
+            state.run_queue.append(job)
+        cfg = SchedulerConfig(max_concurrency=20, boosting_enabled=boosting)
+        try:
+            res = compute_targets(state, cfg, 0.5)
+            errs.append({"boosting": boosting, "targets": [res[i] for i in range(5)]})
+        except ValueError as e:
+            errs.append({"boosting": boosting, "error": str(e)})
+    out["target_errors"] = errs
+    # trees for the exit policy
+    configs = [ScoringConfig(), ScoringConfig(strict_negative_exit=True),
+               ScoringConfig(futility_bound=FutilityBound.PREFIX_AGGREGATE),
+               ScoringConfig(scheme=AggregationScheme.MINIMUM, futility_bound=FutilityBound.PREFIX_AGGREGATE),
+               ScoringConfig(scheme=AggregationScheme.MINIMUM, strict_negative_exit=True, accept_threshold=0.5),
+               ScoringConfig(accept_threshold=0.6, first_step_threshold=0.5, positive_exit_threshold=0.7),
+               ScoringConfig(scheme=AggregationScheme.AVERAGE), ScoringConfig(scheme=AggregationScheme.CUMULATIVE_SUM)]
+    out["scoring"] = [scoring_record(c) for c in configs]
+    trees = []
+    wl = make_workload(32, MIX, 3, branching=3, depth_ranges={d: (3, 6) for d in Difficulty})
+    wl2 = make_workload(8, MIX, 4, branching=4, depth_ranges={d: (8, 10) for d in Difficulty})
+    for pi, problem in enumerate(list(wl) + list(wl2)):
+        tree = SearchTree(40)
+        backend = ProblemBackend(problem, 4)
+        stops = sorted(r.sample(range(0, 40), 3))
+        k = 0
+        for stop in stops:
+            while k < stop:
+                try:
+                    leaf = select_leaf(tree, SelectionParams())
+                except NoExpandableLeafError:
+                    break
+                term = simulate_to_terminal(tree, leaf, backend, 12)
+                finish_rollout(tree, term, ScoringConfig())
+                k += 1
+            trees.append(_policy_tree_record(tree, configs))
+    # a bare root, a root with only terminal children, and a chain deeper than 64
+    trees.append(_policy_tree_record(SearchTree(4), configs))
+
+    class _C:
+        def __init__(self, ref, reward, term):
+            self.step_ref, self.prior, self.prm_reward, self.is_terminal = ref, 0.5, reward, term
+
+    t = SearchTree(4)
+    expand(t, t.root_id, [_C(0, 0.9, True), _C(1, 0.2, True)])
+    trees.append(_policy_tree_record(t, configs))
+    for chain_rewards in ([0.99] * 90, [0.999] * 70 + [0.2], [0.95] * 80):
+        t = SearchTree(4)
+        node = t.root_id
+        for d, rw in enumerate(chain_rewards):
+            kids = expand(t, node, [_C(0, rw, False), _C(1, r.uniform(0.0, 0.6), d % 3 == 0)])
+            node = kids[0]
+        trees.append(_policy_tree_record(t, configs))
+    out["trees"] = trees
+    dump("policy_kats", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy"]
     for w in which:
         globals()["gen_" + w]()
