@@ -283,6 +283,45 @@ typedef struct ts_forest {
 int ts_exit_policy(const ts_config* cfg, const ts_forest* forest, int32_t* dev_kind, uint8_t* dev_ne,
                    void* stream);
 
+/* ---- beam-search baseline (csrc/beam.cu) ---------------
+ * run_beam_search (beam.py:143-176) for many problems at once, one warp per
+ * problem: every step expands each surviving beam into candidates_per_beam
+ * sampled steps (expand_beams, beam.py:76-104), retires terminal candidates,
+ * keeps the top beam_width of the rest by (-score, candidate order)
+ * (prune_candidates, 107-117), and stops at max_depth, on an empty beam, or
+ * (when enabled) once the best finished score reaches positive_exit_threshold.
+ * This engine runs beam_width * candidates_per_beam <= TS_BEAM_MAX_CANDIDATES. */
+#define TS_BEAM_MAX_CANDIDATES 32
+/* BeamConfig (beam.py:30-41) + the ScoringConfig fields the beam reads. */
+typedef struct ts_beam_config {
+  int32_t beam_width;
+  int32_t candidates_per_beam;
+  int32_t max_depth;
+  int32_t positive_exit_enabled;
+  int32_t scheme;                  /* AggregationScheme of the accumulated score */
+  int32_t _pad;
+  double positive_exit_threshold;
+} ts_beam_config;
+/* BeamResult (beam.py:62-68): best finished beam, or the best surviving partial
+ * (complete = 0), or none (has_best = 0). */
+typedef struct ts_beam_result {
+  int32_t complete;
+  int32_t has_best;
+  int32_t is_terminal;             /* Beam.is_terminal of the best beam */
+  int32_t best_len;                /* len(index_path) */
+  int32_t steps;
+  int32_t status;                  /* ts_status of this problem */
+  int64_t tokens_generated;
+  double best_score;
+  uint8_t best_path[TS_MAX_DEPTH];
+  double best_rewards[TS_MAX_DEPTH];
+} ts_beam_result;
+int ts_beam_search(const ts_beam_config* cfg, const ts_problem* dev_problems, int32_t n,
+                   ts_beam_result* dev_results, void* stream);
+/* End to end: host problems in, host results out (H2D, kernel, D2H). */
+int ts_beam_search_host(const ts_beam_config* cfg, const ts_problem* host_problems, int32_t n,
+                        ts_beam_result* host_results, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,8 @@ def lib() -> ctypes.CDLL:
         L.or_compute_targets_general.argtypes = [P(TsConfig), ctypes.c_double, i32] + [ctypes.c_void_p] * 5
         L.or_forest_policy.restype = None
         L.or_forest_policy.argtypes = [P(TsConfig), i32] + [ctypes.c_void_p] * 12
+        L.or_beam_search.restype = i32
+        L.or_beam_search.argtypes = [P(TsProblem), ctypes.c_void_p, ctypes.c_void_p]
         L.or_run_waves.restype = ctypes.c_void_p
         L.or_run_waves.argtypes = [P(TsProblem), i32, P(TsConfig), i32, i32, P(i32), ctypes.c_int64,
                                    P(ctypes.c_int64)]
@@ -191,6 +193,17 @@ def forest_policy(cfg: TsConfig, off, parent, reward, depth, flags, best, has_be
     ne = np.zeros(max(1, nt), np.uint8)
     lib().or_forest_policy(ctypes.byref(cfg), nt, *[a.ctypes.data for a in arrs], kind.ctypes.data, ne.ctypes.data)
     return kind[:nt], ne[:nt]
+
+
+def beam_search(problem: TsProblem, cfg, out=None):
+    """run_beam_search of one problem; cfg is an _abi.TsBeamConfig."""
+    from paper_2604_00510_b200._abi import TsBeamResult
+
+    r = TsBeamResult() if out is None else out
+    rc = lib().or_beam_search(ctypes.byref(problem), ctypes.addressof(cfg), ctypes.addressof(r))
+    if rc:
+        raise ValueError("beam search: bad arguments")
+    return r
 
 
 class OracleRun:

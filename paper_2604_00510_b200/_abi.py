@@ -118,6 +118,7 @@ EXPORTED = (
     "ts_step_wave", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_read_targets",
     "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
     "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
+    "ts_beam_search", "ts_beam_search_host",
 )
 
 
@@ -152,6 +153,36 @@ class TsForest(ctypes.Structure):
         (name, ctypes.c_void_p)
         for name in ("offsets", "tree_of", "parent", "reward", "depth", "flags", "best_score", "has_best",
                      "completed", "budget", "exhausted")
+    ]
+
+
+TS_BEAM_MAX_CANDIDATES = 32
+
+
+class TsBeamConfig(ctypes.Structure):
+    _fields_ = [
+        ("beam_width", ctypes.c_int32),
+        ("candidates_per_beam", ctypes.c_int32),
+        ("max_depth", ctypes.c_int32),
+        ("positive_exit_enabled", ctypes.c_int32),
+        ("scheme", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("positive_exit_threshold", ctypes.c_double),
+    ]
+
+
+class TsBeamResult(ctypes.Structure):
+    _fields_ = [
+        ("complete", ctypes.c_int32),
+        ("has_best", ctypes.c_int32),
+        ("is_terminal", ctypes.c_int32),
+        ("best_len", ctypes.c_int32),
+        ("steps", ctypes.c_int32),
+        ("status", ctypes.c_int32),
+        ("tokens_generated", ctypes.c_int64),
+        ("best_score", ctypes.c_double),
+        ("best_path", ctypes.c_uint8 * TS_MAX_DEPTH),
+        ("best_rewards", ctypes.c_double * TS_MAX_DEPTH),
     ]
 
 
@@ -197,6 +228,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_compute_targets": (ctypes.c_int, [P(TsSchedParams), ctypes.c_double, vp, vp, vp, vp, i32, vp,
                                               P(TsTargetsInfo), vp]),
         "ts_exit_policy": (ctypes.c_int, [P(TsConfig), P(TsForest), vp, vp, vp]),
+        "ts_beam_search": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp]),
+        "ts_beam_search_host": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

@@ -19,11 +19,16 @@
 
 #include "../../include/treeserve_b200.h"
 #include "exact.cuh"
+#include "rng.cuh"
 
 namespace {
 using tsx::u128;
 using tsx::to_fixed;
 using tsx::fixed_to_double;
+using tsx::MIX_INIT;
+using tsx::sm64;
+using tsx::u53;
+using tsx::Agg;
 
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -109,48 +114,6 @@ struct View {
   long long* g_runWant;
   long long* g_runPW;
   ts_config cfg;
-};
-
-// ---- rng.py ------------------------------------------------------------------
-// _splitmix64 (rng.py:15-19)
-__host__ __device__ __forceinline__ uint64_t sm64(uint64_t x) {
-  x = x + 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
-constexpr uint64_t MIX_INIT = 0x8E12F5A34C29D96Bull;  // mix() initial state (rng.py:24)
-// uniform (rng.py:30-32): top 53 bits scaled by 2^-53 (exact)
-__host__ __device__ __forceinline__ double u53(uint64_t h) { return (double)(h >> 11) * 0x1p-53; }
-
-// ---- aggregate_trajectory (scoring.py:106-116), incremental along a path ----
-struct Agg {
-  double a, c;
-  int n;
-  __device__ __forceinline__ void init() { a = 1.0; c = 0.0; n = 0; }
-  __device__ __forceinline__ void add(double r, int scheme) {
-    if (scheme == TS_SCHEME_PRODUCT) {
-      a = a * r;  // math.prod: 1 * r0 * r1 ... left to right
-    } else if (scheme == TS_SCHEME_MINIMUM) {
-      a = (n == 0 || r < a) ? r : a;
-    } else if (n == 0) {  // builtin sum(): 0 + r0, then Neumaier (CPython >= 3.12)
-      a = r;
-      c = 0.0;
-    } else {
-      double t = a + r;
-      if (fabs(a) >= fabs(r)) c += (a - t) + r;
-      else c += (r - t) + a;
-      a = t;
-    }
-    ++n;
-  }
-  __device__ __forceinline__ double value(int scheme) const {
-    if (scheme == TS_SCHEME_PRODUCT || scheme == TS_SCHEME_MINIMUM) return a;
-    double s = a;
-    if (c != 0.0 && isfinite(c)) s += c;
-    if (scheme == TS_SCHEME_SUM) return s;
-    return s / (double)n;
-  }
 };
 
 // ---- warp helpers ------------------------------------------------------------

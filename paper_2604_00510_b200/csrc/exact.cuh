@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cstring>
 
+#include "../../include/treeserve_b200.h"
+
 namespace tsx {
 
 typedef unsigned __int128 u128;
@@ -150,4 +152,34 @@ __host__ __device__ inline double libm_log1p(double x) {
   return TSX_FMA(dk, ln2_hi, -((hfsq - (TSX_FMA(dk, ln2_lo, c) + sh)) - f));
 #undef TSX_FMA
 }
+// ---- aggregate_trajectory (scoring.py:106-116), incremental along a path ----
+struct Agg {
+  double a, c;
+  int n;
+  __device__ __forceinline__ void init() { a = 1.0; c = 0.0; n = 0; }
+  __device__ __forceinline__ void add(double r, int scheme) {
+    if (scheme == TS_SCHEME_PRODUCT) {
+      a = a * r;  // math.prod: 1 * r0 * r1 ... left to right
+    } else if (scheme == TS_SCHEME_MINIMUM) {
+      a = (n == 0 || r < a) ? r : a;
+    } else if (n == 0) {  // builtin sum(): 0 + r0, then Neumaier (CPython >= 3.12)
+      a = r;
+      c = 0.0;
+    } else {
+      double t = a + r;
+      if (fabs(a) >= fabs(r)) c += (a - t) + r;
+      else c += (r - t) + a;
+      a = t;
+    }
+    ++n;
+  }
+  __device__ __forceinline__ double value(int scheme) const {
+    if (scheme == TS_SCHEME_PRODUCT || scheme == TS_SCHEME_MINIMUM) return a;
+    double s = a;
+    if (c != 0.0 && isfinite(c)) s += c;
+    if (scheme == TS_SCHEME_SUM) return s;
+    return s / (double)n;
+  }
+};
+
 }  // namespace tsx

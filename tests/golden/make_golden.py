@@ -486,7 +486,60 @@ def gen_policy():
     dump("policy_kats", out)
 
 
+def gen_beam():
+    """run_beam_search (beam.py:143-176) on committed workloads under several
+    BeamConfigs and schemes; problems are referenced by (workload, index)."""
+    from treeserve.beam import BeamConfig, run_beam_search
+
+    D7 = {d: (7, 7) for d in Difficulty}
+    D15 = {d: (15, 15) for d in Difficulty}
+    wls = {
+        "c1": list(make_workload(64, MIX, SEED, branching=4, depth_ranges=D7)),
+        "c2": list(make_workload(4096, MIX, SEED, branching=4, depth_ranges=D15))[:256],
+        "cli_default": list(make_workload(500, MIX, 20260810)),
+        "mixed_b3": list(make_workload(
+            97, (0.5, 0.3, 0.2), 77, branching=3,
+            depth_ranges={Difficulty.EASY: (3, 9), Difficulty.HARD_SOLVABLE: (4, 10), Difficulty.UNSOLVABLE: (2, 6)},
+            accept_threshold=0.35)),
+        "c4_stagnation": [make_problem(f"s{i:04d}", rng.mix(SEED, 8, i), Difficulty.HARD_SOLVABLE, (31, 31), 8,
+                                       STAGNATION) for i in range(16)],
+    }
+    cases = [
+        ("c1", BeamConfig(), ScoringConfig()),
+        ("c1", BeamConfig(beam_width=2, candidates_per_beam=4, max_depth=5), ScoringConfig()),
+        ("c1", BeamConfig(positive_exit_enabled=False), ScoringConfig()),
+        ("c2", BeamConfig(), ScoringConfig()),
+        ("c2", BeamConfig(beam_width=4, candidates_per_beam=8, max_depth=20, positive_exit_enabled=False),
+         ScoringConfig()),
+        ("cli_default", BeamConfig(), ScoringConfig()),
+        ("cli_default", BeamConfig(beam_width=1, candidates_per_beam=1), ScoringConfig()),
+        ("cli_default", BeamConfig(beam_width=3, candidates_per_beam=4), ScoringConfig(scheme=AggregationScheme.MINIMUM)),
+        ("mixed_b3", BeamConfig(beam_width=16, candidates_per_beam=2), ScoringConfig(scheme=AggregationScheme.AVERAGE)),
+        ("mixed_b3", BeamConfig(beam_width=5, candidates_per_beam=6),
+         ScoringConfig(scheme=AggregationScheme.CUMULATIVE_SUM, positive_exit_threshold=0.9)),
+        ("mixed_b3", BeamConfig(beam_width=32, candidates_per_beam=1, max_depth=3), ScoringConfig()),
+        ("c4_stagnation", BeamConfig(max_depth=40), ScoringConfig()),
+        ("c4_stagnation", BeamConfig(beam_width=2, candidates_per_beam=16, max_depth=40, positive_exit_enabled=False),
+         ScoringConfig(scheme=AggregationScheme.MINIMUM)),
+    ]
+    out = []
+    for wl, bc, sc in cases:
+        results = []
+        for p in wls[wl]:
+            r = run_beam_search(p, bc, sc)
+            b = r.best
+            results.append({
+                "complete": r.complete, "steps": r.steps, "tokens": r.tokens_generated,
+                "best": None if b is None else {"path": list(b.index_path), "rewards": list(b.rewards),
+                                                "score": b.score, "terminal": b.is_terminal},
+            })
+        out.append({"workload": wl, "beam_width": bc.beam_width, "candidates_per_beam": bc.candidates_per_beam,
+                    "max_depth": bc.max_depth, "positive_exit_enabled": bc.positive_exit_enabled,
+                    "scoring": scoring_record(sc), "results": results})
+    dump("beam", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam"]
     for w in which:
         globals()["gen_" + w]()
