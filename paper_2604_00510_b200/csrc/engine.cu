@@ -76,7 +76,7 @@ struct Counters {
   int heavy_count, heavy_next;  // searches with >= HEAVY_P rollouts this wave (pipelined CTA mode)
   int sum_fallbacks, sched_error;
   unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
-  unsigned long long prof[16];  // TS_HEAVY_PROF diagnostics (cycles), zero otherwise
+  unsigned long long prof[32];  // TS_HEAVY_PROF diagnostics (cycles), zero otherwise
 };
 
 // Kernel-side view of one engine.
@@ -1384,7 +1384,8 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   int k = 0;
   unsigned long long scored = 0, levels = 0;
 #ifdef TS_HEAVY_PROF
-  long long p_total = 0, p_risky = 0, p_infl = 0, p_ring = 0, p_load = 0, p_math = 0, p_lvls = 0;
+  long long p_total = 0, p_risky = 0, p_infl = 0, p_ring = 0, p_load = 0, p_math = 0;
+  long long q_l1 = 0, q_l2 = 0, q_sc = 0, q_t1 = 0, q_l2t = 0, q_rounds = 0;
   HPROF_T0(p_start);
 #endif
   for (; k < count; ++k) {
@@ -1463,6 +1464,9 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         const int fc = nfc;
         uint64_t xno = 0, xmf = 0;
         double xq = 0.0, xp = 0.0, xr = 0.0;
+#ifdef TS_HEAVY_PROF
+        long long t_a = clock64();
+#endif
         if (l1) {
           const int c = fc + lane;
           xno = NO[c];
@@ -1473,6 +1477,10 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         }
         // the grandchild lanes read their parent child's record
         const int src = l1 ? lane : gj;
+#ifdef TS_HEAVY_PROF
+        if (lane == 0) { q_l1 += clock64() - t_a + (xmf == 7 ? 1 : 0) + (xq == -1.0) + (xp == -1.0) + (xr == -1.0) + (xno == 3); }
+        long long t_b = clock64();
+#endif
         const uint64_t gpmf = __shfl_sync(FULL, xmf, src);
         const uint64_t gpno = __shfl_sync(FULL, xno, src);
         const double gpq = __shfl_sync(FULL, xq, src);
@@ -1486,6 +1494,14 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
           xr = RW[c];
         }
         // the scored node's parent terms: the current node for l1, the child for l2
+#ifdef TS_HEAVY_PROF
+        {
+          const bool used = (xmf == 7) | (xq == -1.0) | (xp == -1.0) | (xr == -1.0) | (xno == 3);
+          if (__any_sync(FULL, used)) q_l1 += 0;
+          if (lane == 0) q_l2 += clock64() - t_b;
+        }
+        long long t_c = clock64();
+#endif
         const unsigned gN = (uint32_t)gpno, gO = (uint32_t)(gpno >> 32);
         const double ppq = l1 ? pq : (gN == 0 ? 0.5 : gpq);
         const double ppsq = l1 ? psq : isqrt_tab(sqt, (long long)gN + gO);
@@ -1504,7 +1520,17 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         scored += __popc(vb1);
         ++levels;
         const int j1 = warp_argmax(sc, valid && l1, 0);
-        if (take(j1, j1, fc, xno, xmf, xr, xnq, xnsq)) continue;  // the group is stale after a commit
+#ifdef TS_HEAVY_PROF
+        if (lane == 0) q_sc += clock64() - t_c;
+        long long t_d = clock64();
+#endif
+        const bool stale1 = take(j1, j1, fc, xno, xmf, xr, xnq, xnsq);
+#ifdef TS_HEAVY_PROF
+        if (lane == 0) q_t1 += clock64() - t_d + (nfc == -7 ? 1 : 0);
+        long long t_e = clock64();
+        ++q_rounds;
+#endif
+        if (stale1) continue;  // the group is stale after a commit
         if (!(nmeta & M_KIDS)) break;
         // level 2, within the group of child j1
         const bool ing = l2lane && gj == j1;
@@ -1515,6 +1541,9 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         ++levels;
         const int s2 = warp_argmax(sc, valid && ing, 0);
         take(s2, (s2 - WT) % WT, nfc, xno, xmf, xr, xnq, xnsq);
+#ifdef TS_HEAVY_PROF
+        if (lane == 0) q_l2t += clock64() - t_e + (nfc == -7 ? 1 : 0);
+#endif
       }
     } else {
     while (nmeta & M_KIDS) {
@@ -1648,6 +1677,12 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     atomicAdd(&v.ctr->prof[6], (unsigned long long)p_load);
     atomicAdd(&v.ctr->prof[7], (unsigned long long)p_math);
     atomicAdd(&v.ctr->prof[12], (unsigned long long)levels);
+    atomicAdd(&v.ctr->prof[16], (unsigned long long)q_l1);
+    atomicAdd(&v.ctr->prof[17], (unsigned long long)q_l2);
+    atomicAdd(&v.ctr->prof[18], (unsigned long long)q_sc);
+    atomicAdd(&v.ctr->prof[19], (unsigned long long)q_t1);
+    atomicAdd(&v.ctr->prof[20], (unsigned long long)q_l2t);
+    atomicAdd(&v.ctr->prof[21], (unsigned long long)q_rounds);
   }
 #endif
   rno_out = rno;

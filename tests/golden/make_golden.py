@@ -539,7 +539,30 @@ def gen_beam():
     dump("beam", out)
 
 
+def gen_metrics():
+    """records_to_csv / summarize (metrics.py:62-128) of the serving wave
+    cases on the wave clock (arrival = arrival_step * dt, completion =
+    (exit_step + 1) * dt), computed by the reference's metrics module."""
+    import gzip as _gz
+
+    from treeserve.metrics import RecordExitKind, RequestRecord, records_to_csv, summarize
+
+    with _gz.open(os.path.join(HERE, "waves.json.gz"), "rt", encoding="utf-8") as f:
+        cases = json.load(f)
+    out = []
+    for c in cases:
+        if not c.get("arrival_steps"):
+            continue
+        for dt in (1.0, 0.05):
+            recs = [RequestRecord(o["problem_id"], a * dt, (o["exit_step"] + 1) * dt, o["rollouts_completed"],
+                                  o["cancelled"], o["tokens_generated"], RecordExitKind(o["exit_kind"]), o["best_score"],
+                                  o["solved"], tuple(o["best_path"]))
+                    for o, a in zip(c["outcomes"], c["arrival_steps"]) if o["exit_kind"] != "continue"]
+            out.append({"case": c["name"], "dt": dt, "csv": records_to_csv(recs), "summary": summarize(recs).to_json()})
+    dump("metrics", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics"]
     for w in which:
         globals()["gen_" + w]()

@@ -1,0 +1,57 @@
+"""Request records, CSV and summaries in the reference's formats (metrics.py),
+against bytes produced by the reference's own metrics module
+(tests/golden/metrics.json.gz)."""
+
+from __future__ import annotations
+
+from types import SimpleNamespace
+
+import pytest
+
+from golden_io import config_from_case, load, table
+from paper_2604_00510_b200.metrics import percentile, records_from_outcomes, records_to_csv, summarize
+from paper_2604_00510_b200.scoring import ExitKind
+
+
+def _case(name):
+    return next(c for c in load("waves") if c["name"] == name)
+
+
+def test_percentile_nearest_rank():
+    assert percentile([5.0, 1.0, 3.0, 2.0, 4.0], 50.0) == 3.0
+    assert percentile([5.0, 1.0, 3.0, 2.0, 4.0], 99.0) == 5.0
+    assert percentile([1.0] * 100 + [9.0], 99.0) == 1.0
+    with pytest.raises(ValueError):
+        percentile([], 50.0)
+    with pytest.raises(ValueError):
+        percentile([1.0], 0.0)
+
+
+def test_records_reproduce_reference_bytes_from_fixture_outcomes():
+    for m in load("metrics"):
+        case = _case(m["case"])
+        outs = [SimpleNamespace(exit_kind=ExitKind(o["exit_kind"]), exit_step=o["exit_step"],
+                                rollouts_completed=o["rollouts_completed"], cancelled=o["cancelled"],
+                                tokens_generated=o["tokens_generated"], best_score=o["best_score"],
+                                solved=o["solved"], best_path=tuple(o["best_path"]))
+                for o in case["outcomes"]]
+        recs = records_from_outcomes(outs, [o["problem_id"] for o in case["outcomes"]], case["arrival_steps"],
+                                     m["dt"])
+        assert records_to_csv(recs) == m["csv"]
+        assert summarize(recs).to_json() == m["summary"]
+
+
+@pytest.mark.gpu
+def test_engine_serving_run_reproduces_reference_csv():
+    from paper_2604_00510_b200.engine import Engine
+
+    for m in load("metrics"):
+        case = _case(m["case"])
+        recs_in = load("workloads")[case["workload"]][: len(case["outcomes"])]
+        with Engine(config_from_case(case), 0) as eng:
+            eng.load(table(recs_in, case["arrival_steps"]))
+            eng.run()
+            outs = eng.outcomes()
+        recs = records_from_outcomes(outs, [r["problem_id"] for r in recs_in], case["arrival_steps"], m["dt"])
+        assert records_to_csv(recs) == m["csv"]
+        assert summarize(recs).to_json() == m["summary"]

@@ -19,7 +19,7 @@ for rep in range(2):
     eng.load(table)
     st = eng.run()
 torch.cuda.synchronize()
-buf = (ctypes.c_uint64 * 16)()
+buf = (ctypes.c_uint64 * 32)()
 eng.lib.ts_debug_prof.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 eng.lib.ts_debug_prof(eng._h, buf)
 p = list(buf)
@@ -31,3 +31,6 @@ print("selector per job: prologue %.0f descent %.0f epilogue %.0f (levels/job %.
 print("max over searches: selector loop %d drain %d finish %d cycles" % (p[13], p[14], p[15]))
 print("simulator cycles/job: wait-issue %.0f compute %.0f wait-commit %.0f commit %.0f" %
       (p[8] / jobs, p[9] / jobs, p[10] / jobs, p[11] / jobs))
+r = max(1, p[21])
+print("two-level rounds %d (%.2f/job): per round l1-load %.0f l2(shfl+load) %.0f score+argmax %.0f take1 %.0f level2 %.0f" %
+      (p[21], p[21] / jobs, p[16] / r, p[17] / r, p[18] / r, p[19] / r, p[20] / r))
