@@ -335,6 +335,8 @@ def bench_ours(args, d: Dist):
                    "wave_frac": b2 / (wms2 / 1e3) / 1e9 / hbm}
         eng2.close()
 
+    extra = other_paths(table, flush, args) if N == 1 else {}
+
     cpu = cpu_baseline(PER_GPU, n_total) if (d.rank == 0 and N == 1 and not args.no_cpu) else None
     if d.rank != 0:
         eng.close()
@@ -368,10 +370,69 @@ def bench_ours(args, d: Dist):
                                      "(profiles/r01_ncu_dram_c2_full.json), per batch like algorithmic_bytes; "
                                      "below the algorithmic bytes because the trees stay L2-resident",
                      "regime": "latency-bound: the boosted tail wave is sequential per search by definition"},
-        "cpu_baseline": cpu, "clocks": clk, "variants": {"exits_off": variant},
+        "cpu_baseline": cpu, "clocks": clk, "variants": {"exits_off": variant, **extra},
     }
     eng.close()
     return line
+
+
+def other_paths(table, flush, args) -> dict:
+    """The other device paths of the boundary on the same 4096 problems: the
+    beam-search baseline (beam.py:143-176, default BeamConfig) and the
+    standalone compute_targets operator on a 32768-job run queue."""
+    import numpy as np
+    import torch
+
+    from paper_2604_00510_b200._abi import TsBeamConfig, TsBeamResult, load_library
+    from paper_2604_00510_b200.policy import compute_targets_arrays
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    lib = load_library()
+    out = {}
+    n = len(table)
+    stream = torch.cuda.current_stream()
+    dprob = torch.frombuffer(bytearray(bytes(table)), dtype=torch.uint8).cuda()
+    dres = torch.empty(n * ctypes.sizeof(TsBeamResult), dtype=torch.uint8, device="cuda")
+    cfg = TsBeamConfig(8, 4, 16, 1, 1, 0, 0.5)
+    launch = lambda: lib.ts_beam_search(ctypes.byref(cfg), ctypes.c_void_p(dprob.data_ptr()), n,  # noqa: E731
+                                        ctypes.c_void_p(dres.data_ptr()), ctypes.c_void_p(stream.cuda_stream))
+    for _ in range(3):
+        launch()
+    ts = []
+    for _ in range(max(5, args.steps // 5)):
+        flush_l2(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        launch()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    res = (TsBeamResult * n).from_buffer_copy(dres.cpu().numpy().tobytes())
+    steps = sum(r.steps for r in res)
+    ms = statistics.median(ts)
+    out["beam_baseline"] = {"workload": f"beam.py run_beam_search, BeamConfig() (8 beams x 4 samples, max depth 16), "
+                                        f"{n} c2 problems", "value": n / (ms / 1e3), "unit": "searches/s",
+                            "ms": ms, "beam_steps": steps, "kernel": "k_beam (one warp per problem)"}
+    # standalone compute_targets on a 32768-job run queue (unsorted fractional arrivals)
+    m = 32768
+    rng = np.random.default_rng(0)
+    arr = torch.tensor(rng.uniform(0, 100, m), device="cuda")
+    best = torch.tensor(rng.choice([0.0, 0.3, 0.46, 0.6], m), device="cuda")
+    comp = torch.tensor(rng.integers(0, 5, m), dtype=torch.int32, device="cuda")
+    ids = torch.arange(m, dtype=torch.int64, device="cuda")
+    sc = SchedulerConfig(max_concurrency=4 * m)
+    for _ in range(3):
+        compute_targets_arrays(arr, best, comp, ids, 100.0, sc, 0.5)
+    ts = []
+    for _ in range(10):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, info = compute_targets_arrays(arr, best, comp, ids, 100.0, sc, 0.5)
+        ts.append(time.perf_counter() - t0)
+    out["compute_targets_standalone"] = {"workload": f"compute_targets on {m} running jobs, M={4 * m}",
+                                         "value": 1e3 * statistics.median(ts), "unit": "ms per call (host-timed, "
+                                         "includes the status read-back)", "kernel_launches": info.kernel_launches}
+    return out
 
 
 # --------------------------------------------------------------------------- CPU
