@@ -1292,8 +1292,13 @@ static const wave_kernel_t kWave[3][4] = {
 //    leaf depth >= min(base_depth, depth_cap) - 1, or width 1 — below that a
 //    fresh expansion always leaves a live child) is committed before the next
 //    selection starts.
-constexpr int HEAVY_SIM = 7;
-constexpr int HEAVY_THREADS = 32 * (HEAVY_SIM + 1);
+// 8 warps: warp 0 selects; warp 4, which shares warp 0's SM sub-partition
+// (scheduler = warp id % 4), stays idle so the latency-bound selection chain
+// never competes for issue slots; the other 6 warps simulate.
+constexpr int HEAVY_SIM = 6;
+constexpr int HEAVY_WARPS = 8;
+constexpr int HEAVY_THREADS = 32 * HEAVY_WARPS;
+__device__ __forceinline__ int heavy_sim_of_warp(int w) { return w < 4 ? w - 1 : w - 2; }
 constexpr int HEAVY_RING = 16;
 
 struct HeavyJob {
@@ -1347,9 +1352,18 @@ __device__ __forceinline__ bool heavy_wait_inflight(HeavyCtl* ctl, int lleaf, in
   return true;
 }
 
+// A reload that must stay behind its (warp-uniform) condition: a plain load
+// would be if-converted into an unconditional load plus a select, putting a
+// memory round trip on the selection chain of every level.
+__device__ __forceinline__ uint64_t reload_u64(const uint64_t* p) { return *(const volatile uint64_t*)p; }
+
 constexpr int SQRT_TAB = 2048;  // sqrt(k) for k < SQRT_TAB in shared memory (IEEE sqrt is exact-rounded)
+// The table load is unconditional (no divergent branch around it, so the
+// shared-memory base is hoisted); IEEE sqrt only for the rare large counts.
 __device__ __forceinline__ double isqrt_tab(const double* sqt, long long n) {
-  return n < SQRT_TAB ? sqt[n] : sqrt((double)n);
+  const double t = sqt[n < SQRT_TAB ? n : 0];
+  if (__builtin_expect(n >= SQRT_TAB, 0)) return sqrt((double)n);
+  return t;
 }
 
 template <int NSLOT, int WT>
@@ -1385,7 +1399,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   unsigned long long scored = 0, levels = 0;
 #ifdef TS_HEAVY_PROF
   long long p_total = 0, p_risky = 0, p_infl = 0, p_ring = 0, p_load = 0, p_math = 0;
-  long long q_l1 = 0, q_l2 = 0, q_sc = 0, q_t1 = 0, q_l2t = 0, q_rounds = 0;
+  long long q_l1 = 0, q_l2 = 0, q_sc = 0, q_t1 = 0, q_l2t = 0, q_rounds = 0, q_math = 0;
   HPROF_T0(p_start);
 #endif
   for (; k < count; ++k) {
@@ -1407,7 +1421,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       }
       root_seen = cs;
       if (heavy_wait_inflight(ctl, lleaf, cs, k, 0)) stale = true;
-      if (stale) rmf = MF[0];
+      if (stale) rmf = reload_u64(MF);
     }
     uint32_t nmeta = (uint32_t)rmf;
     if (!meta_expandable(nmeta)) {  // NoExpandableLeafError (tree.py:273-274)
@@ -1447,7 +1461,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       // are only valid after that job's commit (acquired in the wait)
       const bool waited = heavy_wait_inflight(ctl, lleaf, cs, k, node);
       if (waited) {
-        const uint64_t x = MF[node];
+        const uint64_t x = reload_u64(MF + node);
         nmeta = (uint32_t)x;
         nfc = (int)(x >> 32);
       }
@@ -1478,7 +1492,11 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         // the grandchild lanes read their parent child's record
         const int src = l1 ? lane : gj;
 #ifdef TS_HEAVY_PROF
-        if (lane == 0) { q_l1 += clock64() - t_a + (xmf == 7 ? 1 : 0) + (xq == -1.0) + (xp == -1.0) + (xr == -1.0) + (xno == 3); }
+        {
+          unsigned long long w_;
+          asm volatile("xor.b64 %0, %1, %2;\n\txor.b64 %0, %0, %3;" : "=l"(w_) : "l"(xmf), "l"(xno), "l"(__double_as_longlong(xq + xp + xr)) : "memory");
+          if (lane == 0) q_l1 += clock64() - t_a + (w_ == 12345 ? 1 : 0);
+        }
         long long t_b = clock64();
 #endif
         const uint64_t gpmf = __shfl_sync(FULL, xmf, src);
@@ -1496,9 +1514,9 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         // the scored node's parent terms: the current node for l1, the child for l2
 #ifdef TS_HEAVY_PROF
         {
-          const bool used = (xmf == 7) | (xq == -1.0) | (xp == -1.0) | (xr == -1.0) | (xno == 3);
-          if (__any_sync(FULL, used)) q_l1 += 0;
-          if (lane == 0) q_l2 += clock64() - t_b;
+          unsigned long long w_;
+          asm volatile("xor.b64 %0, %1, %2;\n\txor.b64 %0, %0, %3;" : "=l"(w_) : "l"(xmf), "l"(xno), "l"(__double_as_longlong(xq + xp + xr)) : "memory");
+          if (lane == 0) q_l2 += clock64() - t_b + (w_ == 12345 ? 1 : 0);
         }
         long long t_c = clock64();
 #endif
@@ -1513,6 +1531,14 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         const double q = xN == 0 ? ppq : xq;
         const double sc = valid ? q + c_puct * xp * ppsq / (double)(1u + xN + xO) : -INFINITY;
         const bool bad = valid && (!(q >= 0.0 && q <= 1.0) || !(xp >= 0.0 && xp <= 1.0));
+#ifdef TS_HEAVY_PROF
+        {
+          unsigned long long w_;
+          asm volatile("xor.b64 %0, %1, %2;" : "=l"(w_) : "l"(__double_as_longlong(sc)), "l"(__double_as_longlong(xnsq + ppsq)) : "memory");
+          if (lane == 0) q_math += clock64() - t_c + (w_ == 12345 ? 1 : 0);
+        }
+        t_c = clock64();
+#endif
         // level 1
         const unsigned vb1 = __ballot_sync(FULL, valid && l1);
         if (__ballot_sync(FULL, bad && l1)) { status = TS_INVALID_ARGUMENT; break; }
@@ -1603,7 +1629,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       const bool waited = heavy_wait_inflight(ctl, lleaf, cs, k, node);
       HPROF_ACC(p_infl, t_i);
       if (waited) {
-        const uint64_t x = MF[node];
+        const uint64_t x = reload_u64(MF + node);
         nmeta = (uint32_t)x;
         nfc = (int)(x >> 32);
       }
@@ -1626,7 +1652,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         stale |= jb.leaf == 0 || jb.risky != 0;
       }
       root_seen = k - HEAVY_RING + 1;
-      if (stale) rmf = MF[0];
+      if (stale) rmf = reload_u64(MF);
     }
     HeavyJob& jb = ring[k % HEAVY_RING];
     jb.pnode[lane] = pnode;
@@ -1683,6 +1709,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     atomicAdd(&v.ctr->prof[19], (unsigned long long)q_t1);
     atomicAdd(&v.ctr->prof[20], (unsigned long long)q_l2t);
     atomicAdd(&v.ctr->prof[21], (unsigned long long)q_rounds);
+    atomicAdd(&v.ctr->prof[22], (unsigned long long)q_math);
   }
 #endif
   rno_out = rno;
@@ -2195,9 +2222,10 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
     int decision = TS_EXIT_NONE;
     if (warp == 0) {
       heavy_select<NSLOT, WT>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
-    } else {
-      double* s_raw = hsm + (size_t)(warp - 1) * 2 * 32 * WT;
-      heavy_simulate<NSLOT, WT>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, warp - 1);
+    } else if (warp != 4) {
+      const int si = heavy_sim_of_warp(warp);
+      double* s_raw = hsm + (size_t)si * 2 * 32 * WT;
+      heavy_simulate<NSLOT, WT>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, si);
     }
     __syncthreads();
 #ifdef TS_HEAVY_PROF

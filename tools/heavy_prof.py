@@ -32,5 +32,5 @@ print("max over searches: selector loop %d drain %d finish %d cycles" % (p[13], 
 print("simulator cycles/job: wait-issue %.0f compute %.0f wait-commit %.0f commit %.0f" %
       (p[8] / jobs, p[9] / jobs, p[10] / jobs, p[11] / jobs))
 r = max(1, p[21])
-print("two-level rounds %d (%.2f/job): per round l1-load %.0f l2(shfl+load) %.0f score+argmax %.0f take1 %.0f level2 %.0f" %
-      (p[21], p[21] / jobs, p[16] / r, p[17] / r, p[18] / r, p[19] / r, p[20] / r))
+print("two-level rounds %d (%.2f/job): per round l1-load %.0f l2(shfl+load) %.0f math %.0f ballots+argmax %.0f take1 %.0f level2 %.0f" %
+      (p[21], p[21] / jobs, p[16] / r, p[17] / r, p[22] / r, p[18] / r, p[19] / r, p[20] / r))
