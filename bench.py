@@ -128,15 +128,24 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        self.backend = "nccl"
 
     def init(self):
         import torch
 
+        # TS_BENCH_BACKEND=gloo runs the N>1 path with several ranks on one GPU
+        # (validation of the sharded driver only; the measured path is NCCL)
+        self.backend = os.environ.get("TS_BENCH_BACKEND", "nccl")
+        if self.backend != "nccl":
+            self.local = self.local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(self.local)
         if self.world > 1:
             import torch.distributed as dist
 
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
             self.pg = dist
 
     def barrier(self):
@@ -148,7 +157,7 @@ class Dist:
             return x
         import torch
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if self.backend == "nccl" else "cpu")
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -157,7 +166,7 @@ class Dist:
             return x
         import torch
 
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if self.backend == "nccl" else "cpu")
         self.pg.all_reduce(t)
         return float(t.item())
 
@@ -228,7 +237,8 @@ def bench_ours(args, d: Dist):
     if N > 1:
         from paper_2604_00510_b200.distributed import ShardedRun
 
-        sharded = ShardedRun(eng, d.pg, PER_GPU, n_total, torch.device("cuda", d.local))
+        sharded = ShardedRun(eng, d.pg, PER_GPU, n_total, torch.device("cuda", d.local),
+                             host_staging=d.backend != "nccl")
 
     def one_step():
         if N == 1:
