@@ -1241,7 +1241,10 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
 
 
 template <int NSLOT, int WT>
-__global__ void __launch_bounds__(WAVE_THREADS, 4) k_wave(View v, int step) {
+#ifndef TS_WAVE_MINB
+#define TS_WAVE_MINB 4  // resident CTAs of 4 warps per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int step) {
   constexpr int WS = WT ? WT : TS_MAX_WIDTH;
   extern __shared__ double wsm[];  // per warp: raw priors and rewards, [32 depths][WS]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -29,7 +29,6 @@ using tsx::to_fixed;
 using tsx::u128;
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int CT = 1024;       // threads of the single-CTA phases
 constexpr int SORT_TILE = 1024;  // elements sorted per CTA before the global merge passes
 
 thread_local std::string g_err;
@@ -105,11 +104,27 @@ __global__ void k_scores(int n, double now, double theta, double beta, double pr
 // Σ S over the run queue, equal to CPython's sum() (Neumaier since 3.12):
 // exact in 128-bit fixed point when every compensation term is exact (all
 // scores are multiples of 2^-64 and n * ulp(2T) < 2^-10), else
-// the sequential loop.  Also counts the ungated jobs.
-__global__ void __launch_bounds__(CT) k_sum(int n, int obs, const double* __restrict__ S,
-                                            const int32_t* __restrict__ completed, CtState* st) {
-  __shared__ u128 sq[CT / 32];
-  __shared__ long long su[CT / 32];
+// the sequential loop.  Phase 1: per-CTA partial fixed-point sums and
+// ungated counts; phase 2 (one CTA): the total, its exactness test, and the
+// sequential fallback.
+struct SumPart {
+  uint64_t lo, hi;
+  long long ungated;
+  int bad, _pad;
+};
+
+__device__ __forceinline__ void warp_u128_add(u128& x) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t h = __shfl_down_sync(FULL, (uint64_t)(x >> 64), o);
+    const uint64_t l = __shfl_down_sync(FULL, (uint64_t)x, o);
+    x += ((u128)h << 64) | l;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sum_part(int n, int obs, const double* __restrict__ S,
+                                                  const int32_t* __restrict__ completed, SumPart* part) {
+  __shared__ u128 sq[8];
+  __shared__ long long su[8];
   __shared__ int sbad;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) sbad = 0;
@@ -117,18 +132,14 @@ __global__ void __launch_bounds__(CT) k_sum(int n, int obs, const double* __rest
   u128 fx = 0;
   long long u = 0;
   bool bad = false;
-  for (int i = tid; i < n; i += CT) {
+  for (int i = blockIdx.x * 256 + tid; i < n; i += gridDim.x * 256) {
     u128 q;
     if (to_fixed(S[i], q)) fx += q;
     else bad = true;
     u += completed[i] >= obs ? 1 : 0;
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const uint64_t h = __shfl_down_sync(FULL, (uint64_t)(fx >> 64), o);
-    const uint64_t l = __shfl_down_sync(FULL, (uint64_t)fx, o);
-    fx += ((u128)h << 64) | l;
-    u += __shfl_down_sync(FULL, u, o);
-  }
+  warp_u128_add(fx);
+  for (int o = 16; o > 0; o >>= 1) u += __shfl_down_sync(FULL, u, o);
   if (lane == 0) {
     sq[wid] = fx;
     su[wid] = u;
@@ -136,16 +147,42 @@ __global__ void __launch_bounds__(CT) k_sum(int n, int obs, const double* __rest
   if (bad) sbad = 1;
   __syncthreads();
   if (tid == 0) {
-    u128 s = 0;
+    u128 t = 0;
     long long uu = 0;
-    for (int w = 0; w < CT / 32; ++w) {
-      s += sq[w];
+    for (int w = 0; w < 8; ++w) {
+      t += sq[w];
       uu += su[w];
     }
-    bool fallback = sbad != 0;
+    SumPart r;
+    r.lo = (uint64_t)t;
+    r.hi = (uint64_t)(t >> 64);
+    r.ungated = uu;
+    r.bad = sbad;
+    r._pad = 0;
+    part[blockIdx.x] = r;
+  }
+}
+
+__global__ void __launch_bounds__(32) k_sum_final(int n, int nparts, const SumPart* __restrict__ part,
+                                                  const double* __restrict__ S, CtState* st) {
+  const int lane = threadIdx.x;
+  u128 t = 0;
+  long long uu = 0;
+  int bad = 0;
+  for (int b = lane; b < nparts; b += 32) {
+    const SumPart r = part[b];
+    t += ((u128)r.hi << 64) | r.lo;
+    uu += r.ungated;
+    bad |= r.bad;
+  }
+  warp_u128_add(t);
+  for (int o = 16; o > 0; o >>= 1) uu += __shfl_down_sync(FULL, uu, o);
+  bad = __any_sync(FULL, bad);
+  if (lane == 0) {
+    bool fallback = bad != 0;
     double T = 0.0;
     if (!fallback) {
-      T = fixed_to_double(s);
+      T = fixed_to_double(t);
       const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
       if ((double)n * u2 >= 0x1p-10) fallback = true;
     }
@@ -153,10 +190,10 @@ __global__ void __launch_bounds__(CT) k_sum(int n, int obs, const double* __rest
       double f = 0.0, c = 0.0;
       for (int i = 0; i < n; ++i) {
         const double x = S[i];
-        const double t = f + x;
-        if (fabs(f) >= fabs(x)) c += (f - t) + x;
-        else c += (x - t) + f;
-        f = t;
+        const double y = f + x;
+        if (fabs(f) >= fabs(x)) c += (f - y) + x;
+        else c += (x - y) + f;
+        f = y;
       }
       if (c != 0.0 && isfinite(c)) f += c;
       T = f;
@@ -230,10 +267,16 @@ __device__ __forceinline__ long long want_of(double s, double T, long long M) {
   return f >= 9.2e18 ? (long long)9.2e18 : (long long)f;
 }
 
-// Block-wide exclusive (+) scan of one value per thread.
-__device__ long long scan_excl(long long x, long long* total) {
-  __shared__ long long sw[CT / 32];
-  __shared__ long long stot;
+// The allocation loops of compute_targets (scheduler.py:169-186) in closed
+// form over the sorted ungated jobs: extra_k = clamp(R - Σ_{j<k}(want_j - 1),
+// 0, want_k - 1); the leftover R' = R - Σ extra is dealt round-robin in sorted
+// order: floor(R'/U) + [k < R' mod U].  Gated jobs keep 1.  Three phases: a
+// per-CTA scan of (want - 1) in sorted order, a scan of the CTA totals, and
+// the targets.
+constexpr int AT = 256;
+
+__device__ __forceinline__ long long block_excl_scan(long long x, long long* total) {
+  __shared__ long long sw[AT / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   long long incl = x;
   for (int o = 1; o < 32; o <<= 1) {
@@ -242,54 +285,81 @@ __device__ long long scan_excl(long long x, long long* total) {
   }
   if (lane == 31) sw[wid] = incl;
   __syncthreads();
-  if (wid == 0) {
-    const long long v = sw[lane];
-    long long vi = v;
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(FULL, vi, o);
-      if (lane >= o) vi += y;
-    }
-    sw[lane] = vi - v;
-    if (lane == 31) stot = vi;
+  long long base = 0, tot = 0;
+  for (int w = 0; w < AT / 32; ++w) {
+    if (w < wid) base += sw[w];
+    tot += sw[w];
   }
+  *total = tot;
   __syncthreads();
-  const long long r = sw[wid] + incl - x;
-  *total = stot;
-  __syncthreads();
-  return r;
+  return base + incl - x;
 }
 
-// The allocation loops of compute_targets (scheduler.py:169-186) in closed
-// form over the sorted ungated jobs: extra_k = clamp(R - Σ_{j<k}(want_j - 1),
-// 0, want_k - 1); the leftover R' = R - Σ extra is dealt round-robin in sorted
-// order: floor(R'/U) + [k < R' mod U].  Gated jobs keep 1.
-__global__ void __launch_bounds__(CT) k_alloc(int n, long long M, const CtKey* __restrict__ sorted,
-                                              CtState* st, int32_t* __restrict__ targets) {
-  const int tid = threadIdx.x;
-  const double T = st->T;
+__global__ void __launch_bounds__(AT) k_want_scan(int n, long long M, const CtKey* __restrict__ sorted,
+                                                  const CtState* __restrict__ st, long long* __restrict__ pre,
+                                                  long long* __restrict__ blk) {
   const long long U = st->U;
+  const double T = st->T;
+  const int k = blockIdx.x * AT + threadIdx.x;
+  const long long w = k < U ? want_of(sorted[k].S, T, M) - 1 : 0;
+  long long tot;
+  const long long e = block_excl_scan(w, &tot);
+  if (k < n) pre[k] = e;
+  if (threadIdx.x == 0) blk[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_blk_scan(int nb, long long* __restrict__ blk, CtState* st) {
+  __shared__ long long sw[32];
+  __shared__ long long carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const long long x = i < nb ? blk[i] : 0;
+    long long incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) sw[wid] = incl;
+    __syncthreads();
+    long long off = 0, tot = 0;
+    for (int w = 0; w < 32; ++w) {
+      if (w < wid) off += sw[w];
+      tot += sw[w];
+    }
+    if (i < nb) blk[i] = carry + off + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) st->tw = carry;
+}
+
+__global__ void k_targets_out(int n, long long M, const CtKey* __restrict__ sorted, const CtState* __restrict__ st,
+                              const long long* __restrict__ pre, const long long* __restrict__ blk,
+                              int32_t* __restrict__ targets) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const long long U = st->U;
+  if (k >= U) {
+    targets[sorted[k].idx] = 1;
+    return;
+  }
   const long long R = M - (long long)n;
-  const int per = (int)((U + CT - 1) / CT);
-  const int lo = (int)min((long long)tid * per, U), hi = (int)min((long long)lo + per, U);
-  long long loc = 0;
-  for (int k = lo; k < hi; ++k) loc += want_of(sorted[k].S, T, M) - 1;
-  long long tw;
-  long long pre = scan_excl(loc, &tw);
+  const long long tw = st->tw;
   const long long given = R > 0 ? (tw < R ? tw : R) : 0;
   const long long Rp = R > 0 ? R - given : 0;
-  for (int k = lo; k < hi; ++k) {
-    const long long want = want_of(sorted[k].S, T, M);
-    long long extra = R - pre;
-    if (extra < 0) extra = 0;
-    if (extra > want - 1) extra = want - 1;
-    pre += want - 1;
-    long long rr = 0;
-    if (U > 0 && Rp > 0) rr = Rp / U + ((long long)k < Rp % U ? 1 : 0);
-    const long long t = 1 + extra + rr;
-    targets[sorted[k].idx] = t > 0x7fffffffLL ? 0x7fffffff : (int32_t)t;
-  }
-  for (int k = (int)U + tid; k < n; k += CT) targets[sorted[k].idx] = 1;
-  if (tid == 0) st->tw = tw;
+  const long long want = want_of(sorted[k].S, st->T, M);
+  const long long before = blk[k / AT] + pre[k];
+  long long extra = R - before;
+  if (extra < 0) extra = 0;
+  if (extra > want - 1) extra = want - 1;
+  long long rr = 0;
+  if (U > 0 && Rp > 0) rr = Rp / U + ((long long)k < Rp % U ? 1 : 0);
+  const long long t = 1 + extra + rr;
+  targets[sorted[k].idx] = t > 0x7fffffffLL ? 0x7fffffff : (int32_t)t;
 }
 
 __global__ void k_fill(int n, int32_t v, int32_t* out) {
@@ -405,6 +475,48 @@ __global__ void k_decide(int n_trees, double theta_pos, int pe_on, int ne_on, in
 
 inline int blocks(long long n, int t) { return (int)((n + t - 1) / t); }
 
+// Grow-only per-device workspace of ts_compute_targets (one host thread per
+// engine/device, as everywhere in this ABI).
+struct Workspace {
+  int cap = 0;
+  bool attr = false;
+  CtState* st = nullptr;
+  CtState* host = nullptr;  // pinned read-back of st
+  double* S = nullptr;
+  CtKey *ka = nullptr, *kb = nullptr;
+  long long *pre = nullptr, *blk = nullptr;
+  SumPart* part = nullptr;
+};
+
+int workspace_for(int n, Workspace** out) {
+  static Workspace wss[64];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(TS_INVALID_ARGUMENT, "device index out of range");
+  Workspace& w = wss[dev];
+  if (w.cap < n) {
+    cudaFree(w.st);
+    cudaFree(w.S);
+    cudaFree(w.ka);
+    cudaFree(w.kb);
+    cudaFree(w.pre);
+    cudaFree(w.blk);
+    cudaFree(w.part);
+    if (!w.host) CK(cudaMallocHost((void**)&w.host, sizeof(CtState)));
+    const int cap = n < 4096 ? 4096 : n;
+    CK(cudaMalloc((void**)&w.st, sizeof(CtState)));
+    CK(cudaMalloc((void**)&w.S, sizeof(double) * (size_t)cap));
+    CK(cudaMalloc((void**)&w.ka, sizeof(CtKey) * (size_t)cap));
+    CK(cudaMalloc((void**)&w.kb, sizeof(CtKey) * (size_t)cap));
+    CK(cudaMalloc((void**)&w.pre, sizeof(long long) * (size_t)cap));
+    CK(cudaMalloc((void**)&w.blk, sizeof(long long) * (size_t)((cap + AT - 1) / AT + 1)));
+    CK(cudaMalloc((void**)&w.part, sizeof(SumPart) * 1184));
+    w.cap = cap;
+  }
+  *out = &w;
+  return TS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -450,26 +562,27 @@ int ts_compute_targets(const ts_sched_params* p, double now, const double* dev_a
   if (!p->boosting_enabled) {  // scheduler.py:158-160: no scores are computed
     k_fill<<<blocks(n, 256), 256, 0, s>>>(n, 1, dev_targets);
     CK(cudaGetLastError());
+    info.kernel_launches = 1;
     if (host_info) *host_info = info;
     return TS_OK;
   }
-  CtState* st = nullptr;
-  double* S = nullptr;
-  CtKey *ka = nullptr, *kb = nullptr;
-  CK(cudaMallocAsync((void**)&st, sizeof(CtState), s));
-  CK(cudaMallocAsync((void**)&S, sizeof(double) * n, s));
-  CK(cudaMallocAsync((void**)&ka, sizeof(CtKey) * n, s));
-  CK(cudaMallocAsync((void**)&kb, sizeof(CtKey) * n, s));
-  k_init_state<<<1, 1, 0, s>>>(st, n);
+  Workspace* ws = nullptr;
+  int rc = workspace_for(n, &ws);
+  if (rc) return rc;
+  const int nparts = blocks(n, 256) < 1184 ? blocks(n, 256) : 1184;  // 8 x 148 SMs
+  const int nb = blocks(n, AT);
+  CtKey* ka = ws->ka;
+  CtKey* kb = ws->kb;
+  k_init_state<<<1, 1, 0, s>>>(ws->st, n);
   k_scores<<<blocks(n, 256), 256, 0, s>>>(n, now, p->positive_exit_threshold, p->beta, p->proximity,
-                                          p->obs_threshold, dev_arrival, dev_best, dev_completed, dev_job_id, S,
-                                          ka, st);
-  k_sum<<<1, CT, 0, s>>>(n, p->obs_threshold, S, dev_completed, st);
-  static bool attr = false;
+                                          p->obs_threshold, dev_arrival, dev_best, dev_completed, dev_job_id, ws->S,
+                                          ka, ws->st);
+  k_sum_part<<<nparts, 256, 0, s>>>(n, p->obs_threshold, ws->S, dev_completed, ws->part);
+  k_sum_final<<<1, 32, 0, s>>>(n, nparts, ws->part, ws->S, ws->st);
   const size_t sm = 2 * SORT_TILE * sizeof(CtKey);
-  if (!attr) {
+  if (!ws->attr) {
     CK(cudaFuncSetAttribute(k_sort_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = true;
+    ws->attr = true;
   }
   k_sort_tile<<<blocks(n, SORT_TILE), SORT_TILE, sm, s>>>(n, ka);
   int passes = 0;
@@ -479,20 +592,19 @@ int ts_compute_targets(const ts_sched_params* p, double now, const double* dev_a
     ka = kb;
     kb = t;
   }
-  k_alloc<<<1, CT, 0, s>>>(n, (long long)p->max_concurrency, ka, st, dev_targets);
-  CtState h;
-  CK(cudaMemcpyAsync(&h, st, sizeof(CtState), cudaMemcpyDeviceToHost, s));
-  CK(cudaFreeAsync(st, s));
-  CK(cudaFreeAsync(S, s));
-  CK(cudaFreeAsync(ka, s));
-  CK(cudaFreeAsync(kb, s));
+  const long long M = (long long)p->max_concurrency;
+  k_want_scan<<<nb, AT, 0, s>>>(n, M, ka, ws->st, ws->pre, ws->blk);
+  k_blk_scan<<<1, 1024, 0, s>>>(nb, ws->blk, ws->st);
+  k_targets_out<<<blocks(n, 256), 256, 0, s>>>(n, M, ka, ws->st, ws->pre, ws->blk, dev_targets);
+  CK(cudaMemcpyAsync(ws->host, ws->st, sizeof(CtState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   CK(cudaGetLastError());
+  const CtState h = *ws->host;
   info.first_bad = h.first_bad;
   info.total_score = h.T;
   info.ungated = h.U;
   info.sum_fallback = h.fallback;
-  info.kernel_launches = 5 + passes;
+  info.kernel_launches = 9 + passes;
   if (host_info) *host_info = info;
   if (h.first_bad < n) return fail(TS_INVALID_ARGUMENT, "parallelism_score: now precedes arrival");
   return TS_OK;

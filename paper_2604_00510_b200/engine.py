@@ -128,6 +128,25 @@ class Engine:
                     "ts_dump_tree")
         return out
 
+    def tree_dict(self, i: int) -> dict:
+        """Search i in the SearchTree.to_dict() schema (tree.py:183-203)."""
+        t = self.tree(i)
+        o = self.outcomes(i + 1)[i]
+        nodes = [
+            {"id": k, "parent": None if int(p) < 0 else int(p), "reward": float(r), "prior": float(pr),
+             "N": int(n), "O": int(inf), "W": float(w), "terminal": bool(term), "depth": int(d)}
+            for k, (p, r, pr, n, inf, w, term, d) in enumerate(zip(t["parent"], t["reward"], t["prior"], t["N"],
+                                                                   t["O"], t["W"], t["terminal"], t["depth"]))
+        ]
+        return {"root": 0, "completed_rollouts": int(o.rollouts_completed),
+                "rollout_budget": int(self._cfg.rollout_budget), "nodes": nodes}
+
+    def tree_json(self, i: int) -> str:
+        """SearchTree.to_json() (tree.py:205-206): byte-comparable with the reference's dump."""
+        import json
+
+        return json.dumps(self.tree_dict(i), sort_keys=True)
+
     # ---- step API (multi-GPU drivers, tests) -----------------------------
     def step_counts(self, step: int, dev_counts: int) -> None:
         self._check(self.lib.ts_step_counts(self._h, step, ctypes.c_void_p(dev_counts), self.stream),

@@ -562,7 +562,30 @@ def gen_metrics():
     dump("metrics", out)
 
 
+def gen_tree_json():
+    """SearchTree.to_json() (tree.py:183-206) of finished serial searches: the
+    byte-level dump format the engine's Engine.tree_json reproduces."""
+    D7 = {d: (7, 7) for d in Difficulty}
+    c1 = make_workload(64, MIX, SEED, branching=4, depth_ranges=D7)
+    mixed = make_workload(97, (0.5, 0.3, 0.2), 77, branching=3,
+                          depth_ranges={Difficulty.EASY: (3, 9), Difficulty.HARD_SOLVABLE: (4, 10), Difficulty.UNSOLVABLE: (2, 6)},
+                          accept_threshold=0.35)
+    out = []
+    for wl_name, wl, sc, budget, cap, width, pe, ne in [
+        ("c1", c1, ScoringConfig(), 32, 8, 4, True, True),
+        ("c1", c1, ScoringConfig(), 32, 8, 4, False, False),
+        ("mixed_b3", mixed, ScoringConfig(scheme=AggregationScheme.MINIMUM, positive_exit_threshold=0.6,
+                                          first_step_threshold=0.3), 40, 12, 2, True, True),
+    ]:
+        for idx in (0, 3, 7):
+            tree = serial_tree(wl[idx], sc, budget, cap, width, pe, ne)
+            out.append({"workload": wl_name, "index": idx, "scoring": scoring_record(sc), "budget": budget,
+                        "depth_cap": cap, "expand_width": width, "positive_exit": pe, "negative_exit": ne,
+                        "json": tree.to_json()})
+    dump("tree_json", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json"]
     for w in which:
         globals()["gen_" + w]()

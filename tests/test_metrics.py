@@ -55,3 +55,21 @@ def test_engine_serving_run_reproduces_reference_csv():
         recs = records_from_outcomes(outs, [r["problem_id"] for r in recs_in], case["arrival_steps"], m["dt"])
         assert records_to_csv(recs) == m["csv"]
         assert summarize(recs).to_json() == m["summary"]
+
+
+@pytest.mark.gpu
+def test_engine_tree_json_is_byte_identical_to_reference():
+    """Engine.tree_json vs SearchTree.to_json() of the same serial search (tests/golden/tree_json)."""
+    from golden_io import scoring_from_record
+    from paper_2604_00510_b200.config import serial_config
+    from paper_2604_00510_b200.engine import Engine
+
+    for case in load("tree_json"):
+        rec = load("workloads")[case["workload"]][case["index"]]
+        cfg = serial_config(scoring_from_record(case["scoring"]), rollout_budget=case["budget"],
+                            depth_cap=case["depth_cap"], expand_width=case["expand_width"],
+                            positive_exit=case["positive_exit"], negative_exit=case["negative_exit"])
+        with Engine(cfg, 0) as eng:
+            eng.load(table([rec]))
+            eng.run()
+            assert eng.tree_json(0) == case["json"]
