@@ -6,6 +6,7 @@
 // Numerics: compiled with -fmad=false; every floating-point expression keeps
 // the reference's evaluation order, so results are
 // bit-identical to the CPU reference.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -651,6 +652,988 @@ __device__ __forceinline__ size_t targets_smem_dev() {
 
 __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
   targets_block(v, step, rec, v.n_global, v.goff, v.goff + v.n_local, 0);
+}
+
+// ---- compute_targets over many CTAs (multi-GPU runs: all n_global records) ----
+// The same algorithm as targets_block, with every cross-thread scan split into
+// an in-CTA scan plus a scan over CTA totals in a one-CTA kernel between
+// phases.  Thread t owns records [t*MT_CH, (t+1)*MT_CH); its running state
+// between phases (list positions, run ids, the previous score of each list)
+// lives in a global scratch row.
+constexpr int MT_T = 256, MT_CH = 8, MT_REC = MT_T * MT_CH;
+constexpr int MT_RUNCAP = 256;  // runs per list k_mt_all stages in shared memory (else read from global)
+struct MtBlk1 {
+  long long nrun, cnt0, cnt1;
+  unsigned long long flo, fhi;
+  int bad, _p;
+  double min0, min1;
+};
+struct MtOff1 {
+  long long p0, p1;
+  double prev0, prev1;
+};
+struct MtThr {
+  long long pos0, pos1, rid0, rid1;
+  double prev0, prev1;
+};
+struct MtState {
+  double T;
+  long long tot_run, len0, len1, nr0, nr1, tw0, tw1;
+  int boost_on, _p;
+};
+struct MtLayout {
+  MtBlk1* b1;
+  MtOff1* o1;
+  MtThr* thr;
+  long long* b2;  // run counts per CTA, list 0 then list 1
+  long long* b3;  // Σ cnt*(want-1) per run-CTA, list 0 then list 1
+  MtState* st;
+  uint8_t* hflag; // pipelined-mode flag per local search
+};
+__host__ __device__ inline size_t mt_align(size_t x) { return (x + 255) & ~(size_t)255; }
+__host__ __device__ inline int mt_blocks(int n) { return (n + MT_REC - 1) / MT_REC; }
+__host__ __device__ inline int mt_run_blocks(int n) { return (n + MT_T - 1) / MT_T; }
+__host__ __device__ inline size_t mt_layout(unsigned char* base, int n, int n_local, MtLayout* L) {
+  const int G = mt_blocks(n), G3 = mt_run_blocks(n);
+  size_t o = 0;
+  if (L) L->b1 = (MtBlk1*)(base + o);
+  o = mt_align(o + sizeof(MtBlk1) * G);
+  if (L) L->o1 = (MtOff1*)(base + o);
+  o = mt_align(o + sizeof(MtOff1) * G);
+  if (L) L->thr = (MtThr*)(base + o);
+  o = mt_align(o + sizeof(MtThr) * (size_t)G * MT_T);
+  if (L) L->b2 = (long long*)(base + o);
+  o = mt_align(o + sizeof(long long) * 2 * G);
+  if (L) L->b3 = (long long*)(base + o);
+  o = mt_align(o + sizeof(long long) * 2 * G3);
+  if (L) L->st = (MtState*)(base + o);
+  o = mt_align(o + sizeof(MtState));
+  if (L) L->hflag = (uint8_t*)(base + o);
+  o = mt_align(o + (size_t)n_local);
+  return o;
+}
+
+// Exclusive (+) scans of K values per thread over an MT_T-thread CTA; totals out.
+template <int K>
+__device__ void mt_scan(long long (&x)[K], long long (&tot)[K]) {
+  __shared__ long long sw[K][MT_T / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long incl[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    incl[q] = x[q];
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(FULL, incl[q], o);
+      if (lane >= o) incl[q] += y;
+    }
+    if (lane == 31) sw[q][wid] = incl[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    long long base = 0, t = 0;
+    for (int w = 0; w < MT_T / 32; ++w) {
+      if (w < wid) base += sw[q][w];
+      t += sw[q][w];
+    }
+    tot[q] = t;
+    x[q] = base + incl[q] - x[q];
+  }
+  __syncthreads();
+}
+// Exclusive min-scan of two doubles per thread over the CTA (identity +inf); CTA mins out.
+__device__ void mt_scan_min2(double& a, double& b, double& ta, double& tb) {
+  __shared__ double sw[2][MT_T / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double ia = a, ib = b;
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ya = __shfl_up_sync(FULL, ia, o), yb = __shfl_up_sync(FULL, ib, o);
+    if (lane >= o) {
+      ia = fmin(ia, ya);
+      ib = fmin(ib, yb);
+    }
+  }
+  double ea = __shfl_up_sync(FULL, ia, 1), eb = __shfl_up_sync(FULL, ib, 1);
+  if (lane == 0) ea = eb = INFINITY;
+  if (lane == 31) {
+    sw[0][wid] = ia;
+    sw[1][wid] = ib;
+  }
+  __syncthreads();
+  double pa = INFINITY, pb = INFINITY;
+  ta = tb = INFINITY;
+  for (int w = 0; w < MT_T / 32; ++w) {
+    if (w < wid) {
+      pa = fmin(pa, sw[0][w]);
+      pb = fmin(pb, sw[1][w]);
+    }
+    ta = fmin(ta, sw[0][w]);
+    tb = fmin(tb, sw[1][w]);
+  }
+  a = fmin(pa, ea);
+  b = fmin(pb, eb);
+  __syncthreads();
+}
+
+// phase 1: per-CTA counts, exact partial score sums, list minima
+__global__ void __launch_bounds__(MT_T) k_mt_count(View v, int step, const ts_sched_record* rec, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int n = v.n_global;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
+  const int t = blockIdx.x * MT_T + threadIdx.x;
+  const int lo = min(n, t * MT_CH), hi = min(n, lo + MT_CH);
+  long long c[3] = {0, 0, 0}, tot[3];
+  u128 fx = 0;
+  bool bad = false;
+  double m0 = INFINITY, m1 = INFINITY;
+  for (int i = lo; i < hi; ++i) {
+    const ts_sched_record r = rec[i];
+    if (!(r.flags & 1u)) continue;
+    ++c[0];
+    u128 q;
+    if (to_fixed(r.score, q)) fx += q;
+    else bad = true;
+    if (r.flags & 2u) {
+      if (r.flags & 4u) { ++c[2]; m1 = fmin(m1, r.score); }
+      else { ++c[1]; m0 = fmin(m0, r.score); }
+    }
+  }
+  mt_scan<3>(c, tot);
+  double tm0, tm1;
+  mt_scan_min2(m0, m1, tm0, tm1);
+  __shared__ u128 sq[MT_T / 32];
+  __shared__ int sbad;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) sbad = 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t h = __shfl_down_sync(FULL, (uint64_t)(fx >> 64), o);
+    const uint64_t l = __shfl_down_sync(FULL, (uint64_t)fx, o);
+    fx += ((u128)h << 64) | l;
+  }
+  if (lane == 0) sq[wid] = fx;
+  __syncthreads();
+  if (bad) sbad = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u128 s = 0;
+    for (int w = 0; w < MT_T / 32; ++w) s += sq[w];
+    MtBlk1 b;
+    b.nrun = tot[0];
+    b.cnt0 = tot[1];
+    b.cnt1 = tot[2];
+    b.flo = (unsigned long long)s;
+    b.fhi = (unsigned long long)(s >> 64);
+    b.bad = sbad;
+    b._p = 0;
+    b.min0 = tm0;
+    b.min1 = tm1;
+    L.b1[blockIdx.x] = b;
+  }
+}
+
+// phase 2 (one CTA): CTA offsets, the score sum T, the totals
+__global__ void __launch_bounds__(1024) k_mt_scan1(View v, const ts_sched_record* rec, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int n = v.n_global, G = mt_blocks(n);
+  __shared__ long long shl[264];
+  __shared__ double shd[80];
+  __shared__ u128 sq[32];
+  __shared__ int sbad;
+  const int b = threadIdx.x, lane = b & 31, wid = b >> 5;
+  if (b == 0) sbad = 0;
+  __syncthreads();
+  MtBlk1 x{};
+  x.min0 = x.min1 = INFINITY;
+  if (b < G) x = L.b1[b];
+  long long c4[4] = {x.nrun, x.cnt0, x.cnt1, 0}, t4[4];
+  block_scan_add4(c4, t4, shl);
+  const double p0 = block_scan_min(x.min0, shd);
+  const double p1 = block_scan_min(x.min1, shd);
+  u128 fx = b < G ? (((u128)x.fhi << 64) | x.flo) : 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t h = __shfl_down_sync(FULL, (uint64_t)(fx >> 64), o);
+    const uint64_t l = __shfl_down_sync(FULL, (uint64_t)fx, o);
+    fx += ((u128)h << 64) | l;
+  }
+  if (lane == 0) sq[wid] = fx;
+  if (b < G && x.bad) sbad = 1;
+  __syncthreads();
+  if (b < G) {
+    MtOff1 o;
+    o.p0 = c4[1];
+    o.p1 = c4[2];
+    o.prev0 = p0;
+    o.prev1 = p1;
+    L.o1[b] = o;
+  }
+  if (b == 0) {
+    u128 s = 0;
+    for (int w = 0; w < 32; ++w) s += sq[w];
+    const long long tot_run = t4[0];
+    bool fallback = sbad != 0;
+    double T = 0.0;
+    if (!fallback) {
+      T = fixed_to_double(s);
+      const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
+      if ((double)tot_run * u2 >= 0x1p-10) fallback = true;
+    }
+    if (fallback) {  // sequential Neumaier sum in run-queue order
+      double f = 0.0, cc = 0.0;
+      bool first = true;
+      for (int i = 0; i < n; ++i) {
+        const ts_sched_record r = rec[i];
+        if (!(r.flags & 1u)) continue;
+        const double x2 = r.score;
+        if (first) { f = x2; first = false; continue; }
+        const double y = f + x2;
+        if (fabs(f) >= fabs(x2)) cc += (f - y) + x2;
+        else cc += (x2 - y) + f;
+        f = y;
+      }
+      if (cc != 0.0 && isfinite(cc)) f += cc;
+      T = f;
+      atomicAdd(&v.ctr->sum_fallbacks, 1);
+    }
+    MtState st{};
+    st.T = T;
+    st.tot_run = tot_run;
+    st.len0 = t4[1];
+    st.len1 = t4[2];
+    const long long R = (long long)v.cfg.max_concurrency - tot_run;
+    st.boost_on = (v.cfg.boosting_enabled != 0 && tot_run > 0 && R > 0 && t4[1] + t4[2] > 0) ? 1 : 0;
+    *L.st = st;
+  }
+}
+
+// phase 3: per-thread list positions and previous scores; runs of equal score
+__global__ void __launch_bounds__(MT_T) k_mt_runs(View v, const ts_sched_record* rec, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int n = v.n_global;
+  const int t = blockIdx.x * MT_T + threadIdx.x;
+  const int lo = min(n, t * MT_CH), hi = min(n, lo + MT_CH);
+  const bool boost_on = L.st->boost_on != 0;
+  long long c[2] = {0, 0}, tot[2];
+  double m0 = INFINITY, m1 = INFINITY;
+  for (int i = lo; i < hi; ++i) {
+    const ts_sched_record r = rec[i];
+    if ((r.flags & 3u) != 3u) continue;
+    if (r.flags & 4u) { ++c[1]; m1 = fmin(m1, r.score); }
+    else { ++c[0]; m0 = fmin(m0, r.score); }
+  }
+  mt_scan<2>(c, tot);
+  double tm0, tm1;
+  mt_scan_min2(m0, m1, tm0, tm1);
+  const MtOff1 o = L.o1[blockIdx.x];
+  MtThr th;
+  th.pos0 = o.p0 + c[0];
+  th.pos1 = o.p1 + c[1];
+  th.prev0 = fmin(o.prev0, m0);
+  th.prev1 = fmin(o.prev1, m1);
+  long long rs[2] = {0, 0};
+  if (boost_on) {
+    double p0 = th.prev0, p1 = th.prev1;
+    for (int i = lo; i < hi; ++i) {
+      const ts_sched_record r = rec[i];
+      if ((r.flags & 3u) != 3u) continue;
+      if (r.flags & 4u) { if (r.score != p1) ++rs[1]; if (r.score > p1) v.ctr->sched_error = 1; p1 = r.score; }
+      else { if (r.score != p0) ++rs[0]; if (r.score > p0) v.ctr->sched_error = 1; p0 = r.score; }
+    }
+  }
+  long long rt[2];
+  mt_scan<2>(rs, rt);
+  th.rid0 = rs[0];
+  th.rid1 = rs[1];
+  L.thr[t] = th;
+  if (threadIdx.x == 0) {
+    L.b2[blockIdx.x] = rt[0];
+    L.b2[gridDim.x + blockIdx.x] = rt[1];
+  }
+}
+
+// phase 4 (one CTA): run offsets of the CTAs; run totals
+__global__ void __launch_bounds__(1024) k_mt_scan2(View v, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int G = mt_blocks(v.n_global);
+  __shared__ long long shl[264];
+  const int b = threadIdx.x;
+  long long c4[4] = {b < G ? L.b2[b] : 0, b < G ? L.b2[G + b] : 0, 0, 0}, t4[4];
+  block_scan_add4(c4, t4, shl);
+  if (b < G) {
+    L.b2[b] = c4[0];
+    L.b2[G + b] = c4[1];
+  }
+  if (b == 0) {
+    L.st->nr0 = t4[0];
+    L.st->nr1 = t4[1];
+  }
+}
+
+// phase 5: run records (score, start position) of the runs starting in each chunk
+__global__ void __launch_bounds__(MT_T) k_mt_write_runs(View v, const ts_sched_record* rec, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int n = v.n_global, G = gridDim.x;
+  const int t = blockIdx.x * MT_T + threadIdx.x;
+  MtThr th = L.thr[t];
+  th.rid0 += L.b2[blockIdx.x];
+  th.rid1 += L.b2[G + blockIdx.x];
+  L.thr[t] = th;
+  if (!L.st->boost_on) return;
+  const int lo = min(n, t * MT_CH), hi = min(n, lo + MT_CH);
+  const int stride = n;
+  double p0 = th.prev0, p1 = th.prev1;
+  long long q0 = th.pos0, q1 = th.pos1, k0 = th.rid0, k1 = th.rid1;
+  for (int i = lo; i < hi; ++i) {
+    const ts_sched_record r = rec[i];
+    if ((r.flags & 3u) != 3u) continue;
+    if (r.flags & 4u) {
+      if (r.score != p1) { v.g_runS[stride + k1] = r.score; v.g_runStart[stride + k1] = (int)q1; ++k1; }
+      p1 = r.score;
+      ++q1;
+    } else {
+      if (r.score != p0) { v.g_runS[k0] = r.score; v.g_runStart[k0] = (int)q0; ++k0; }
+      p0 = r.score;
+      ++q0;
+    }
+  }
+}
+
+__device__ __forceinline__ long long mt_want(double s, double T, long long M) {
+  long long want = 1;
+  if (T > 0.0) {
+    const double f = floor(s / T * (double)M);
+    want = f > 1.0 ? (long long)f : 1;
+  }
+  return want;
+}
+
+// phase 6: want per run and the per-CTA sums of cnt*(want-1) (one run per thread, both lists)
+__global__ void __launch_bounds__(MT_T) k_mt_want(View v, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int n = v.n_global, G3 = gridDim.x;
+  const MtState st = *L.st;
+  const long long M = v.cfg.max_concurrency;
+  const int k = blockIdx.x * MT_T + threadIdx.x;
+  long long w[2] = {0, 0}, tot[2];
+  if (st.boost_on) {
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const long long nr = b ? st.nr1 : st.nr0, len = b ? st.len1 : st.len0;
+      const int off = b ? n : 0;
+      if (k < nr) {
+        const long long want = mt_want(v.g_runS[off + k], st.T, M);
+        const long long cnt = (k + 1 < nr ? v.g_runStart[off + k + 1] : len) - v.g_runStart[off + k];
+        v.g_runWant[off + k] = want;
+        w[b] = cnt * (want - 1);
+      }
+    }
+  }
+  mt_scan<2>(w, tot);
+  if (st.boost_on) {
+    if (k < st.nr0) v.g_runPW[k] = w[0];
+    if (k < st.nr1) v.g_runPW[n + k] = w[1];
+  }
+  if (threadIdx.x == 0) {
+    L.b3[blockIdx.x] = tot[0];
+    L.b3[G3 + blockIdx.x] = tot[1];
+  }
+}
+
+// phase 7 (one CTA): scan of the run-CTA sums; tw0, tw1
+__global__ void __launch_bounds__(1024) k_mt_scan3(View v, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int G3 = mt_run_blocks(v.n_global);
+  __shared__ long long shl[264];
+  __shared__ long long carry[2];
+  if (threadIdx.x == 0) carry[0] = carry[1] = 0;
+  __syncthreads();
+  for (int base = 0; base < G3; base += 1024) {
+    const int b = base + threadIdx.x;
+    long long c4[4] = {b < G3 ? L.b3[b] : 0, b < G3 ? L.b3[G3 + b] : 0, 0, 0}, t4[4];
+    block_scan_add4(c4, t4, shl);
+    if (b < G3) {
+      L.b3[b] = carry[0] + c4[0];
+      L.b3[G3 + b] = carry[1] + c4[1];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      carry[0] += t4[0];
+      carry[1] += t4[1];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    L.st->tw0 = carry[0];
+    L.st->tw1 = carry[1];
+  }
+}
+
+// phase 8: targets of the local slice (closed-form clamp + round-robin, merge
+// rank by binary search in the other list's runs); pipelined-mode flags
+__global__ void __launch_bounds__(MT_T) k_mt_targets(View v, const ts_sched_record* rec, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  const int n = v.n_global, G3 = mt_run_blocks(n);
+  const int t = blockIdx.x * MT_T + threadIdx.x;
+  const int lo = min(n, t * MT_CH), hi = min(n, lo + MT_CH);
+  const int glo = v.goff, ghi = v.goff + v.n_local;
+  if (hi <= glo || lo >= ghi) return;  // no local search in this chunk: nothing to write
+  const MtState st = *L.st;
+  const MtThr th = L.thr[t];
+  const ts_config& cf = v.cfg;
+  const long long M = cf.max_concurrency, R = M - st.tot_run;
+  const long long U = st.len0 + st.len1;
+  long long Rp = R - (st.tw0 + st.tw1);
+  if (Rp < 0) Rp = 0;
+  const int stride = n;
+  const double* runS = v.g_runS;
+  const int32_t* runStart = v.g_runStart;
+  const long long* runWant = v.g_runWant;
+  const long long* runPWl = v.g_runPW;
+  auto runPW = [&](int off, long long k) { return runPWl[off + k] + L.b3[(off ? G3 : 0) + k / MT_T]; };
+  long long q0 = th.pos0, q1 = th.pos1, k0 = th.rid0 - 1, k1 = th.rid1 - 1;
+  double p0 = th.prev0, p1 = th.prev1;
+  for (int i = lo; i < hi; ++i) {
+    const ts_sched_record r = rec[i];
+    const bool local = i >= glo && i < ghi;
+    if (!(r.flags & 1u)) {
+      if (local) {
+        v.st[i - glo].target = 0;
+        L.hflag[i - glo] = 0;
+      }
+      continue;
+    }
+    long long tgt = 1;
+    if ((r.flags & 2u) && st.boost_on) {
+      const int b = (r.flags & 4u) ? 1 : 0;
+      long long pos, k;
+      if (b) { if (r.score != p1) ++k1; p1 = r.score; pos = q1++; k = k1; }
+      else { if (r.score != p0) ++k0; p0 = r.score; pos = q0++; k = k0; }
+      if (local) {
+        const int off = b ? stride : 0, oo = b ? 0 : stride;
+        const long long want = runWant[off + k];
+        long long before = runPW(off, k) + (pos - runStart[off + k]) * (want - 1);
+        const long long nro = b ? st.nr0 : st.nr1, leno = b ? st.len0 : st.len1, two = b ? st.tw0 : st.tw1;
+        const long long obefore = b ? q0 : q1;
+        int lo2 = 0, hi2 = (int)nro;  // first run of the other list with runS <= S
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          if (runS[oo + mid] > r.score) lo2 = mid + 1;
+          else hi2 = mid;
+        }
+        const int kk = lo2;
+        long long c, cw;
+        if (kk < nro && runS[oo + kk] == r.score) {
+          const long long st0 = runStart[oo + kk];
+          const long long cntk = (kk + 1 < nro ? runStart[oo + kk + 1] : leno) - st0;
+          long long part = obefore - st0;
+          if (part < 0) part = 0;
+          if (part > cntk) part = cntk;
+          c = st0 + part;
+          cw = runPW(oo, kk) + part * (runWant[oo + kk] - 1);
+        } else if (kk < nro) {
+          c = runStart[oo + kk];
+          cw = runPW(oo, kk);
+        } else {
+          c = leno;
+          cw = two;
+        }
+        const long long spos = pos + c;
+        before += cw;
+        long long extra = R - before;
+        if (extra < 0) extra = 0;
+        if (extra > want - 1) extra = want - 1;
+        long long rr = 0;
+        if (U > 0) rr = Rp / U + (spos < Rp % U ? 1 : 0);
+        tgt = 1 + extra + rr;
+      }
+    }
+    if (local) {
+      v.st[i - glo].target = (int)tgt;
+      L.hflag[i - glo] = (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P) ? 1 : 0;
+    }
+  }
+}
+
+// phase 9 (one CTA over the local slice): single-warp and pipelined work lists
+__global__ void __launch_bounds__(TT) k_mt_split(View v, int step, const ts_sched_record* rec, unsigned char* mt) {
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  __shared__ long long shl[264];
+  const int tid = threadIdx.x, nl = v.n_local, glo = v.goff;
+  const int per = (nl + TT - 1) / TT;
+  const int lo = min(nl, tid * per), hi = min(nl, lo + per);
+  long long nh = 0, nlt = 0;
+  for (int i = lo; i < hi; ++i) {
+    if (!(rec[i + glo].flags & 1u)) continue;
+    if (L.hflag[i]) ++nh;
+    else ++nlt;
+  }
+  long long sc2[4] = {nh, nlt, 0, 0}, tt2[4];
+  block_scan_add4(sc2, tt2, shl);
+  long long ph = sc2[0], pl = sc2[1];
+  for (int i = lo; i < hi; ++i) {
+    if (!(rec[i + glo].flags & 1u)) continue;
+    if (L.hflag[i]) v.work_heavy[ph++] = i;
+    else v.work[pl++] = i;
+  }
+  if (tid == 0) {
+    v.ctr->work_count = (int)tt2[1];
+    v.ctr->work_next = 0;
+    v.ctr->heavy_count = (int)tt2[0];
+    v.ctr->heavy_next = 0;
+    v.ctr->cur_step = step;
+  }
+}
+
+// All phases of the multi-CTA targets in ONE cooperative launch (grid-wide
+// barriers between phases; every CTA keeps its 2048 records in shared memory
+// across phases, read from HBM once).  Used when the grid (one CTA per 2048
+// records) fits on the device at once; the per-phase kernels above are the
+// fallback.
+__global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sched_record* rec, unsigned char* mt) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  MtLayout L;
+  mt_layout(mt, v.n_global, v.n_local, &L);
+  __shared__ ts_sched_record srec[MT_REC];
+  __shared__ long long sfl[4];
+  __shared__ double s_runS[2 * MT_RUNCAP];
+  __shared__ int32_t s_runStart[2 * MT_RUNCAP];
+  __shared__ long long s_runWant[2 * MT_RUNCAP];
+  __shared__ long long s_runPW[2 * MT_RUNCAP];
+  const int n = v.n_global, G = gridDim.x, G3 = mt_run_blocks(n);
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int base = b * MT_REC;
+  const int nb = min(MT_REC, n - base);
+  for (int i = tid; i < nb; i += MT_T) srec[i] = rec[base + i];
+  if (b == 0 && tid == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
+  __syncthreads();
+#ifdef TS_HEAVY_PROF
+  const long long t_mt0 = clock64();
+#endif
+  const int lo = min(nb, tid * MT_CH), hi = min(nb, lo + MT_CH);  // this thread's records, CTA-local
+  const ts_config& cf = v.cfg;
+
+  // ---- phase 1: CTA counts, exact partial sums, list minima
+  {
+    long long c[3] = {0, 0, 0}, tot[3];
+    u128 fx = 0;
+    bool bad = false;
+    double m0 = INFINITY, m1 = INFINITY;
+    for (int i = lo; i < hi; ++i) {
+      const ts_sched_record r = srec[i];
+      if (!(r.flags & 1u)) continue;
+      ++c[0];
+      u128 q;
+      if (to_fixed(r.score, q)) fx += q;
+      else bad = true;
+      if (r.flags & 2u) {
+        if (r.flags & 4u) { ++c[2]; m1 = fmin(m1, r.score); }
+        else { ++c[1]; m0 = fmin(m0, r.score); }
+      }
+    }
+    mt_scan<3>(c, tot);
+    double tm0, tm1;
+    mt_scan_min2(m0, m1, tm0, tm1);
+    __shared__ u128 sq[MT_T / 32];
+    __shared__ int sbad;
+    if (tid == 0) sbad = 0;
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t h = __shfl_down_sync(FULL, (uint64_t)(fx >> 64), o);
+      const uint64_t l = __shfl_down_sync(FULL, (uint64_t)fx, o);
+      fx += ((u128)h << 64) | l;
+    }
+    if (lane == 0) sq[wid] = fx;
+    __syncthreads();
+    if (bad) sbad = 1;
+    __syncthreads();
+    if (tid == 0) {
+      u128 s = 0;
+      for (int w = 0; w < MT_T / 32; ++w) s += sq[w];
+      MtBlk1 x;
+      x.nrun = tot[0];
+      x.cnt0 = tot[1];
+      x.cnt1 = tot[2];
+      x.flo = (unsigned long long)s;
+      x.fhi = (unsigned long long)(s >> 64);
+      x.bad = sbad;
+      x._p = 0;
+      x.min0 = tm0;
+      x.min1 = tm1;
+      L.b1[b] = x;
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[23], (unsigned long long)(clock64() - t_mt0));
+#endif
+  // ---- phase 2 (CTA 0): CTA offsets, T, totals
+  if (b == 0) {
+    MtBlk1 x{};
+    x.min0 = x.min1 = INFINITY;
+    if (tid < G) x = L.b1[tid];
+    long long c[3] = {x.nrun, x.cnt0, x.cnt1}, tot[3];
+    mt_scan<3>(c, tot);
+    double m0 = x.min0, m1 = x.min1, tm0, tm1;
+    mt_scan_min2(m0, m1, tm0, tm1);
+    __shared__ u128 sq2[MT_T / 32];
+    __shared__ int sbad2;
+    if (tid == 0) sbad2 = 0;
+    u128 fx = tid < G ? (((u128)x.fhi << 64) | x.flo) : 0;
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t h = __shfl_down_sync(FULL, (uint64_t)(fx >> 64), o);
+      const uint64_t l = __shfl_down_sync(FULL, (uint64_t)fx, o);
+      fx += ((u128)h << 64) | l;
+    }
+    if (lane == 0) sq2[wid] = fx;
+    __syncthreads();
+    if (tid < G && x.bad) sbad2 = 1;
+    __syncthreads();
+    if (tid < G) {
+      MtOff1 o;
+      o.p0 = c[1];
+      o.p1 = c[2];
+      o.prev0 = m0;
+      o.prev1 = m1;
+      L.o1[tid] = o;
+    }
+    if (tid == 0) {
+      u128 s = 0;
+      for (int w = 0; w < MT_T / 32; ++w) s += sq2[w];
+      const long long tot_run = tot[0];
+      bool fallback = sbad2 != 0;
+      double T = 0.0;
+      if (!fallback) {
+        T = fixed_to_double(s);
+        const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
+        if ((double)tot_run * u2 >= 0x1p-10) fallback = true;
+      }
+      if (fallback) {  // sequential Neumaier sum in run-queue order
+        double f = 0.0, cc = 0.0;
+        bool first = true;
+        for (int i = 0; i < n; ++i) {
+          const ts_sched_record r = rec[i];
+          if (!(r.flags & 1u)) continue;
+          const double x2 = r.score;
+          if (first) { f = x2; first = false; continue; }
+          const double y = f + x2;
+          if (fabs(f) >= fabs(x2)) cc += (f - y) + x2;
+          else cc += (x2 - y) + f;
+          f = y;
+        }
+        if (cc != 0.0 && isfinite(cc)) f += cc;
+        T = f;
+        atomicAdd(&v.ctr->sum_fallbacks, 1);
+      }
+      MtState st{};
+      st.T = T;
+      st.tot_run = tot_run;
+      st.len0 = tot[1];
+      st.len1 = tot[2];
+      const long long R = (long long)cf.max_concurrency - tot_run;
+      st.boost_on = (cf.boosting_enabled != 0 && tot_run > 0 && R > 0 && tot[1] + tot[2] > 0) ? 1 : 0;
+      *L.st = st;
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[24], (unsigned long long)(clock64() - t_mt0));
+#endif
+  const bool boost_on = L.st->boost_on != 0;
+  // ---- phase 3: positions, previous scores, run counts
+  MtThr th;
+  {
+    long long c[2] = {0, 0}, tot[2];
+    double m0 = INFINITY, m1 = INFINITY;
+    for (int i = lo; i < hi; ++i) {
+      const ts_sched_record r = srec[i];
+      if ((r.flags & 3u) != 3u) continue;
+      if (r.flags & 4u) { ++c[1]; m1 = fmin(m1, r.score); }
+      else { ++c[0]; m0 = fmin(m0, r.score); }
+    }
+    mt_scan<2>(c, tot);
+    double tm0, tm1;
+    mt_scan_min2(m0, m1, tm0, tm1);
+    const MtOff1 o = L.o1[b];
+    th.pos0 = o.p0 + c[0];
+    th.pos1 = o.p1 + c[1];
+    th.prev0 = fmin(o.prev0, m0);
+    th.prev1 = fmin(o.prev1, m1);
+    long long rs[2] = {0, 0};
+    if (boost_on) {
+      double p0 = th.prev0, p1 = th.prev1;
+      for (int i = lo; i < hi; ++i) {
+        const ts_sched_record r = srec[i];
+        if ((r.flags & 3u) != 3u) continue;
+        if (r.flags & 4u) { if (r.score != p1) ++rs[1]; if (r.score > p1) v.ctr->sched_error = 1; p1 = r.score; }
+        else { if (r.score != p0) ++rs[0]; if (r.score > p0) v.ctr->sched_error = 1; p0 = r.score; }
+      }
+    }
+    long long rt[2];
+    mt_scan<2>(rs, rt);
+    th.rid0 = rs[0];
+    th.rid1 = rs[1];
+    if (tid == 0) {
+      L.b2[b] = rt[0];
+      L.b2[G + b] = rt[1];
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[25], (unsigned long long)(clock64() - t_mt0));
+#endif
+  // ---- phase 4 (CTA 0): run offsets of the CTAs
+  if (b == 0) {
+    long long c[2] = {tid < G ? L.b2[tid] : 0, tid < G ? L.b2[G + tid] : 0}, tot[2];
+    mt_scan<2>(c, tot);
+    if (tid < G) {
+      L.b2[tid] = c[0];
+      L.b2[G + tid] = c[1];
+    }
+    if (tid == 0) {
+      L.st->nr0 = tot[0];
+      L.st->nr1 = tot[1];
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[26], (unsigned long long)(clock64() - t_mt0));
+#endif
+  // ---- phase 5: run records
+  th.rid0 += L.b2[b];
+  th.rid1 += L.b2[G + b];
+  if (boost_on) {
+    double p0 = th.prev0, p1 = th.prev1;
+    long long q0 = th.pos0, q1 = th.pos1, k0 = th.rid0, k1 = th.rid1;
+    for (int i = lo; i < hi; ++i) {
+      const ts_sched_record r = srec[i];
+      if ((r.flags & 3u) != 3u) continue;
+      if (r.flags & 4u) {
+        if (r.score != p1) { v.g_runS[n + k1] = r.score; v.g_runStart[n + k1] = (int)q1; ++k1; }
+        p1 = r.score;
+        ++q1;
+      } else {
+        if (r.score != p0) { v.g_runS[k0] = r.score; v.g_runStart[k0] = (int)q0; ++k0; }
+        p0 = r.score;
+        ++q0;
+      }
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[27], (unsigned long long)(clock64() - t_mt0));
+#endif
+  const long long M = cf.max_concurrency;
+  // ---- phase 6: want per run, per-run-block sums
+  if (boost_on) {
+    const MtState st = *L.st;
+    const long long nrmax = st.nr0 > st.nr1 ? st.nr0 : st.nr1;
+    const int g3 = (int)((nrmax + MT_T - 1) / MT_T);
+    for (int rb = b; rb < g3; rb += G) {
+      const long long k = (long long)rb * MT_T + tid;
+      long long w[2] = {0, 0}, tot[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const long long nr = q ? st.nr1 : st.nr0, len = q ? st.len1 : st.len0;
+        const int off = q ? n : 0;
+        if (k < nr) {
+          const long long want = mt_want(v.g_runS[off + k], st.T, M);
+          const long long cnt = (k + 1 < nr ? v.g_runStart[off + k + 1] : len) - v.g_runStart[off + k];
+          v.g_runWant[off + k] = want;
+          w[q] = cnt * (want - 1);
+        }
+      }
+      mt_scan<2>(w, tot);
+      if (k < st.nr0) v.g_runPW[k] = w[0];
+      if (k < st.nr1) v.g_runPW[n + k] = w[1];
+      if (tid == 0) {
+        L.b3[rb] = tot[0];
+        L.b3[G3 + rb] = tot[1];
+      }
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[28], (unsigned long long)(clock64() - t_mt0));
+#endif
+  // ---- phase 7 (CTA 0): run-block offsets, tw0/tw1
+  if (b == 0) {
+    const MtState st = *L.st;
+    const long long nrmax = st.nr0 > st.nr1 ? st.nr0 : st.nr1;
+    const int g3 = boost_on ? (int)((nrmax + MT_T - 1) / MT_T) : 0;
+    long long carry0 = 0, carry1 = 0;
+    for (int base3 = 0; base3 < g3; base3 += MT_T) {
+      const int rb = base3 + tid;
+      long long c[2] = {rb < g3 ? L.b3[rb] : 0, rb < g3 ? L.b3[G3 + rb] : 0}, tot[2];
+      mt_scan<2>(c, tot);
+      if (rb < g3) {
+        L.b3[rb] = carry0 + c[0];
+        L.b3[G3 + rb] = carry1 + c[1];
+      }
+      carry0 += tot[0];
+      carry1 += tot[1];
+    }
+    if (tid == 0) {
+      L.st->tw0 = carry0;
+      L.st->tw1 = carry1;
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[29], (unsigned long long)(clock64() - t_mt0));
+#endif
+  // ---- phase 8: targets of the local records, pipelined-mode flags, per-CTA list counts
+  const int glo = v.goff, ghi = v.goff + v.n_local;
+  long long nh = 0, nlt = 0;
+  if (base + nb > glo && base < ghi) {  // this CTA holds local records (CTA-uniform: the staging syncs)
+    const MtState st = *L.st;
+    const long long R = M - st.tot_run, U = st.len0 + st.len1;
+    long long Rp = R - (st.tw0 + st.tw1);
+    if (Rp < 0) Rp = 0;
+    // the runs of both lists (score, start, want, Σ before) in shared memory when
+    // they fit: the binary searches below then never leave the SM
+    const bool in_smem = st.nr0 <= MT_RUNCAP && st.nr1 <= MT_RUNCAP;
+    const double* runS = v.g_runS;
+    const int32_t* runStart = v.g_runStart;
+    const long long* runWant = v.g_runWant;
+    const long long* runPWg = v.g_runPW;
+    int off1 = n;
+    if (in_smem) {
+      off1 = MT_RUNCAP;
+      for (int q = 0; q < 2; ++q) {
+        const long long nr = q ? st.nr1 : st.nr0;
+        const int go = q ? n : 0, so = q ? MT_RUNCAP : 0;
+        for (int k = tid; k < nr; k += MT_T) {
+          s_runS[so + k] = v.g_runS[go + k];
+          s_runStart[so + k] = v.g_runStart[go + k];
+          s_runWant[so + k] = v.g_runWant[go + k];
+          s_runPW[so + k] = v.g_runPW[go + k] + L.b3[(q ? G3 : 0) + k / MT_T];
+        }
+      }
+      runS = s_runS;
+      runStart = s_runStart;
+      runWant = s_runWant;
+      runPWg = s_runPW;
+    }
+    __syncthreads();
+    auto runPW = [&](int off, long long k) {
+      return in_smem ? runPWg[off + k] : runPWg[off + k] + L.b3[(off ? G3 : 0) + k / MT_T];
+    };
+    long long q0 = th.pos0, q1 = th.pos1, k0 = th.rid0 - 1, k1 = th.rid1 - 1;
+    double p0 = th.prev0, p1 = th.prev1;
+    for (int ii = lo; ii < hi; ++ii) {
+      const ts_sched_record r = srec[ii];
+      const int i = base + ii;
+      const bool local = i >= glo && i < ghi;
+      if (!(r.flags & 1u)) {
+        if (local) {
+          v.st[i - glo].target = 0;
+          L.hflag[i - glo] = 0;
+        }
+        continue;
+      }
+      long long tgt = 1;
+      if ((r.flags & 2u) && boost_on) {
+        const int lb = (r.flags & 4u) ? 1 : 0;
+        long long pos, k;
+        if (lb) { if (r.score != p1) ++k1; p1 = r.score; pos = q1++; k = k1; }
+        else { if (r.score != p0) ++k0; p0 = r.score; pos = q0++; k = k0; }
+        if (local) {
+          const int off = lb ? off1 : 0, oo = lb ? 0 : off1;
+          const long long want = runWant[off + k];
+          long long before = runPW(off, k) + (pos - runStart[off + k]) * (want - 1);
+          const long long nro = lb ? st.nr0 : st.nr1, leno = lb ? st.len0 : st.len1, two = lb ? st.tw0 : st.tw1;
+          const long long obefore = lb ? q0 : q1;
+          int lo2 = 0, hi2 = (int)nro;
+          while (lo2 < hi2) {
+            const int mid = (lo2 + hi2) >> 1;
+            if (runS[oo + mid] > r.score) lo2 = mid + 1;
+            else hi2 = mid;
+          }
+          const int kk = lo2;
+          long long c, cw;
+          if (kk < nro && runS[oo + kk] == r.score) {
+            const long long st0 = runStart[oo + kk];
+            const long long cntk = (kk + 1 < nro ? runStart[oo + kk + 1] : leno) - st0;
+            long long part = obefore - st0;
+            if (part < 0) part = 0;
+            if (part > cntk) part = cntk;
+            c = st0 + part;
+            cw = runPW(oo, kk) + part * (runWant[oo + kk] - 1);
+          } else if (kk < nro) {
+            c = runStart[oo + kk];
+            cw = runPW(oo, kk);
+          } else {
+            c = leno;
+            cw = two;
+          }
+          const long long spos = pos + c;
+          before += cw;
+          long long extra = R - before;
+          if (extra < 0) extra = 0;
+          if (extra > want - 1) extra = want - 1;
+          long long rr = 0;
+          if (U > 0) rr = Rp / U + (spos < Rp % U ? 1 : 0);
+          tgt = 1 + extra + rr;
+        }
+      }
+      if (local) {
+        v.st[i - glo].target = (int)tgt;
+        const bool hv = v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P;
+        L.hflag[i - glo] = hv ? 1 : 0;
+        if (hv) ++nh;
+        else ++nlt;
+      }
+    }
+  }
+  {
+    long long c[2] = {nh, nlt}, tot[2];
+    mt_scan<2>(c, tot);
+    nh = c[0];
+    nlt = c[1];
+    if (tid == 0) {
+      L.b1[b].nrun = tot[0];  // b1 is free after phase 2: per-CTA list counts
+      L.b1[b].cnt0 = tot[1];
+    }
+  }
+  grid.sync();
+#ifdef TS_HEAVY_PROF
+  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[30], (unsigned long long)(clock64() - t_mt0));
+#endif
+  // ---- phase 9: work lists in run-queue order
+  {
+    if (tid == 0) {
+      long long h = 0, l = 0;
+      for (int j = 0; j < b; ++j) {
+        h += L.b1[j].nrun;
+        l += L.b1[j].cnt0;
+      }
+      sfl[0] = h;
+      sfl[1] = l;
+      if (b == G - 1) {
+        v.ctr->heavy_count = (int)(h + L.b1[b].nrun);
+        v.ctr->work_count = (int)(l + L.b1[b].cnt0);
+        v.ctr->work_next = 0;
+        v.ctr->heavy_next = 0;
+        v.ctr->cur_step = step;
+      }
+    }
+    __syncthreads();
+    long long ph = sfl[0] + nh, pl = sfl[1] + nlt;
+    for (int ii = lo; ii < hi; ++ii) {
+      const int i = base + ii;
+      if (i < glo || i >= ghi || !(srec[ii].flags & 1u)) continue;
+      if (L.hflag[i - glo]) v.work_heavy[ph++] = i - glo;
+      else v.work[pl++] = i - glo;
+    }
+  }
 }
 
 // Number of requests with arrival_step <= step (arrivals are non-decreasing),
@@ -2320,6 +3303,8 @@ struct ts_engine {
   int wave_blocks[12] = {0};
   int wkind = 3;
   bool heavy_off = false;  // TS_NO_PIPELINE=1 disables the pipelined CTA mode (diagnostics)
+  int mt_min = 6144;       // TS_MT_MIN: largest run queue for the one-CTA targets kernel
+  int coop_ctas = -1;      // co-resident CTAs of k_mt_all (cooperative launch), 0 = unavailable
   bool heavy_sync = false; // TS_PIPELINE_SYNC=1 serialises it (diagnostics)
   // sizes
   int n_local = 0, goff = 0, n_global = 0, cap_searches = 0, cap_global = 0;
@@ -2353,6 +3338,8 @@ struct ts_engine {
   int32_t* g_runStart = nullptr;
   long long* g_runWant = nullptr;
   long long* g_runPW = nullptr;
+  unsigned char* mt = nullptr;      // multi-CTA targets scratch (mt_layout)
+  size_t mt_bytes = 0;
   long long* counts = nullptr;      // 3
   ts_sched_record* records = nullptr;
   ts_outcome* outcomes = nullptr;
@@ -2721,6 +3708,15 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     const char* env = getenv("TS_NO_PIPELINE");
     e->heavy_off = env && env[0] == '1';
     const char* env2 = getenv("TS_PIPELINE_SYNC");
+    const char* env3 = getenv("TS_MT_MIN");
+    if (env3) e->mt_min = atoi(env3);
+    int coop = 0, per = 0, sms = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)k_mt_all, MT_T, 0) != cudaSuccess) per = 0;
+    const char* env4 = getenv("TS_MT_COOP");
+    e->coop_ctas = (coop && !(env4 && env4[0] == '0')) ? per * sms : 0;
+    cudaGetLastError();
     e->heavy_sync = env2 && env2[0] == '1';
   }
   if (cr != cudaSuccess) {
@@ -2736,7 +3732,7 @@ int ts_engine_destroy(ts_engine* e) {
   void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
-                  e->work_heavy};
+                  e->work_heavy, e->mt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
@@ -2835,6 +3831,15 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
       return rc;
     e->cap_global = n_global;
   }
+  {
+    const size_t need = mt_layout(nullptr, n_global, n_local, nullptr);
+    if (need > e->mt_bytes) {
+      if (e->mt) cudaFree(e->mt);
+      e->mt = nullptr;
+      TS_CUDA_TRY(e, cudaMalloc((void**)&e->mt, need));
+      e->mt_bytes = need;
+    }
+  }
   e->n_local = n_local;
   e->goff = global_offset;
   e->n_global = n_global;
@@ -2905,8 +3910,35 @@ int ts_step_targets(ts_engine* e, int32_t step, const ts_sched_record* dev_all, 
   int rc;
   if ((rc = ensure_step_times(e, step + 1, s))) return rc;
   View v = make_view(e);
-  k_targets<<<1, TT, targets_smem(), s>>>(v, step, dev_all);
-  TS_LAUNCH_CHECK(e, "k_targets");
+  if (v.n_global <= e->mt_min) {
+    k_targets<<<1, TT, targets_smem(), s>>>(v, step, dev_all);
+    TS_LAUNCH_CHECK(e, "k_targets");
+    return TS_OK;
+  }
+  // many CTAs: the run queue of a multi-GPU job (every rank scans all records)
+  const int G = mt_blocks(v.n_global), G3 = mt_run_blocks(v.n_global);
+  unsigned char* mt = e->mt;
+  if (G <= e->coop_ctas) {  // one cooperative launch, grid-wide barriers between phases
+    void* args[] = {(void*)&v, (void*)&step, (void*)&dev_all, (void*)&mt};
+    const cudaError_t rc2 = cudaLaunchCooperativeKernel((const void*)k_mt_all, dim3(G), dim3(MT_T), args, 0, s);
+    if (rc2 == cudaSuccess) {
+      TS_LAUNCH_CHECK(e, "k_mt_all");
+      return TS_OK;
+    }
+    cudaGetLastError();
+    e->coop_ctas = 0;  // not available: per-phase kernels from now on
+  }
+  k_mt_count<<<G, MT_T, 0, s>>>(v, step, dev_all, mt);
+  k_mt_scan1<<<1, 1024, 0, s>>>(v, dev_all, mt);
+  k_mt_runs<<<G, MT_T, 0, s>>>(v, dev_all, mt);
+  k_mt_scan2<<<1, 1024, 0, s>>>(v, mt);
+  k_mt_write_runs<<<G, MT_T, 0, s>>>(v, dev_all, mt);
+  k_mt_want<<<G3, MT_T, 0, s>>>(v, mt);
+  k_mt_scan3<<<1, 1024, 0, s>>>(v, mt);
+  k_mt_targets<<<G, MT_T, 0, s>>>(v, dev_all, mt);
+  k_mt_split<<<1, TT, 0, s>>>(v, step, dev_all, mt);
+  e->launches += 8;
+  TS_LAUNCH_CHECK(e, "k_mt_*");
   return TS_OK;
 }
 
