@@ -3178,15 +3178,21 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
   __shared__ HeavyJob ring[HEAVY_RING];
   __shared__ int s_item;
   __shared__ double sqt[SQRT_TAB];
-  for (int i = threadIdx.x; i < SQRT_TAB; i += HEAVY_THREADS) sqt[i] = sqrt((double)i);
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WaveStats ws = {0, 0, 0, 0, 0, 0};
   const int count_items = v.ctr->heavy_count;
+  if (count_items == 0) return;  // most waves have no pipelined-mode search
   if (step < 0) step = v.ctr->cur_step;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
-    __syncthreads();
+  if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
+  __syncthreads();
+  if (s_item >= count_items) return;  // no item for this CTA: skip the table set-up
+  for (int i = threadIdx.x; i < SQRT_TAB; i += HEAVY_THREADS) sqt[i] = sqrt((double)i);
+  __syncthreads();
+  for (bool first = true;; first = false) {
+    if (!first) {
+      if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
+      __syncthreads();
+    }
     const int item = s_item;
     if (item >= count_items) break;
     const int s = v.work_heavy[item];
