@@ -322,6 +322,38 @@ int ts_beam_search(const ts_beam_config* cfg, const ts_problem* dev_problems, in
 int ts_beam_search_host(const ts_beam_config* cfg, const ts_problem* host_problems, int32_t n,
                         ts_beam_result* host_results, void* stream);
 
+/* Step-level beam operators (beam.py:44-131) for callers that drive the loop
+ * themselves: expand_beams + prune_candidates for many problems at once. */
+typedef struct ts_beam {          /* Beam (beam.py:44-51) */
+  int32_t len;                    /* len(index_path) */
+  int32_t is_terminal;
+  double score;
+  uint8_t path[TS_MAX_DEPTH];
+  double rewards[TS_MAX_DEPTH];
+} ts_beam;
+typedef struct ts_beam_candidate { /* BeamCandidate (beam.py:54-59) + the pruning result */
+  int32_t beam;                   /* index of the extended input beam */
+  int32_t order;                  /* candidate index within the step (tie-break) */
+  int32_t step_ref;
+  int32_t token_count;
+  double prm_reward;
+  double score;                   /* aggregate_trajectory of the extended rewards */
+  int32_t is_terminal;
+  int32_t rank;                   /* prune_candidates: survivor slot, -1 pruned, -2 finished */
+} ts_beam_candidate;
+/* expand_beams (beam.py:76-104) then prune_candidates (107-117) for problem i:
+ * input beams dev_beams[i * TS_BEAM_MAX_CANDIDATES + b], b < dev_counts[i]
+ * (counts * candidates_per_beam <= TS_BEAM_MAX_CANDIDATES); candidates out in
+ * dev_cands[i * TS_BEAM_MAX_CANDIDATES + j], beam-major, each with its rank
+ * among the non-terminal candidates under (-score, order) (rank < beam_width
+ * survives).  Per-problem status (ValueError on a terminal or too-deep
+ * context, generate_steps backend.py:244-246) in dev_status[i]. */
+int ts_beam_expand(const ts_beam_config* cfg, const ts_problem* dev_problems, int32_t n, const ts_beam* dev_beams,
+                   const int32_t* dev_counts, ts_beam_candidate* dev_cands, int32_t* dev_status, void* stream);
+/* prune_candidates (beam.py:107-117) over caller candidates (score, order,
+ * is_terminal used; rank written): n <= 1024 candidates of one problem. */
+int ts_beam_prune(ts_beam_candidate* dev_cands, int32_t n, int32_t beam_width, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,7 +118,7 @@ EXPORTED = (
     "ts_step_wave", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_read_targets",
     "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
     "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
-    "ts_beam_search", "ts_beam_search_host",
+    "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
 )
 
 
@@ -186,6 +186,29 @@ class TsBeamResult(ctypes.Structure):
     ]
 
 
+class TsBeam(ctypes.Structure):
+    _fields_ = [
+        ("len", ctypes.c_int32),
+        ("is_terminal", ctypes.c_int32),
+        ("score", ctypes.c_double),
+        ("path", ctypes.c_uint8 * TS_MAX_DEPTH),
+        ("rewards", ctypes.c_double * TS_MAX_DEPTH),
+    ]
+
+
+class TsBeamCandidate(ctypes.Structure):
+    _fields_ = [
+        ("beam", ctypes.c_int32),
+        ("order", ctypes.c_int32),
+        ("step_ref", ctypes.c_int32),
+        ("token_count", ctypes.c_int32),
+        ("prm_reward", ctypes.c_double),
+        ("score", ctypes.c_double),
+        ("is_terminal", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+    ]
+
+
 _lib = None
 
 
@@ -230,6 +253,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_exit_policy": (ctypes.c_int, [P(TsConfig), P(TsForest), vp, vp, vp]),
         "ts_beam_search": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp]),
         "ts_beam_search_host": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp]),
+        "ts_beam_expand": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp, vp, vp, vp]),
+        "ts_beam_prune": (ctypes.c_int, [vp, i32, i32, vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

@@ -227,6 +227,122 @@ __global__ void __launch_bounds__(32 * BEAM_WARPS) k_beam(ts_beam_config cfg, co
   }
 }
 
+
+// ---- step-level operators -------------------------------------------------------
+
+// expand_beams + prune ranks for one problem per warp (candidate j in lane j).
+__global__ void __launch_bounds__(32 * BEAM_WARPS) k_beam_expand(ts_beam_config cfg, const ts_problem* __restrict__ probs,
+                                                                 int n, const ts_beam* __restrict__ beams,
+                                                                 const int32_t* __restrict__ counts,
+                                                                 ts_beam_candidate* __restrict__ out,
+                                                                 int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int pi = blockIdx.x * BEAM_WARPS + wid;
+  if (pi >= n) return;
+  const ts_problem& P = probs[pi];
+  const int C = cfg.candidates_per_beam, nb = counts[pi], nc = nb * C;
+  const int branching = P.branching, base = P.base_depth, glen = P.golden_len;
+  const bool act = lane < nc;
+  const int b = act ? lane / C : 0;
+  const ts_beam& bm = beams[(size_t)pi * MAXB + b];
+  const int L = bm.len;
+  // generate_steps raises on a terminal or too-deep context (backend.py:244-246)
+  bool bad = act && (L > base + 1 || L < 0 || L >= TS_MAX_DEPTH);
+  bool pgold = glen >= 0 && L <= glen;
+  uint64_t he0 = fold3(P.seed, 6, (uint64_t)L);
+  for (int d = 0; d < L && !bad; ++d) {
+    const uint64_t s = bm.path[d];
+    he0 = sm64(he0 ^ s);
+    if (pgold && P.golden_path[d] != bm.path[d]) pgold = false;
+  }
+  if (act && !bad && L > 0) {  // _is_terminal(context)
+    bool term;
+    if (L < base) term = false;
+    else if (L >= base + 1) term = true;
+    else if (pgold) term = true;
+    else term = !((he0 % 2u) == 0u);
+    bad = term;
+  }
+  const unsigned badm = __ballot_sync(FULL, bad);
+  if (lane == 0) status[pi] = badm ? TS_INVALID_ARGUMENT : TS_OK;
+  if (badm) return;
+  const int idx = (lane % C) % branching;
+  const int depth = L + 1;
+  uint64_t hr = fold3(P.seed, 1, depth), ht = fold3(P.seed, 3, depth), he = fold3(P.seed, 6, depth);
+  Agg g;
+  g.init();
+  for (int d = 0; act && d < L; ++d) {
+    const uint64_t s = bm.path[d];
+    hr = sm64(hr ^ s);
+    ht = sm64(ht ^ s);
+    he = sm64(he ^ s);
+    g.add(bm.rewards[d], cfg.scheme);
+  }
+  hr = sm64(hr ^ (uint64_t)idx);
+  ht = sm64(ht ^ (uint64_t)idx);
+  he = sm64(he ^ (uint64_t)idx);
+  const bool gold = pgold && depth <= glen && idx == (int)P.golden_path[depth - 1];
+  double reward;
+  if (gold) {
+    reward = P.golden_rewards[depth - 1];
+  } else {
+    const bool sr = P.has_shared && depth <= P.hidden_until_depth;
+    const double lo = sr ? P.shared_lo : P.off_lo, hi = sr ? P.shared_hi : P.off_hi;
+    reward = lo + (hi - lo) * u53(hr);
+  }
+  bool term;
+  if (depth < base) term = false;
+  else if (depth >= base + 1) term = true;
+  else if (gold) term = true;
+  else term = !((he % 2u) == 0u);
+  g.add(reward, cfg.scheme);
+  const double score = g.value(cfg.scheme);
+  const bool open = act && !term;
+  const unsigned om = __ballot_sync(FULL, open);
+  int rank = 0;
+  for (int k = 0; k < nc; ++k) {
+    const double sk = __shfl_sync(FULL, score, k);
+    rank += (((om >> k) & 1u) && (sk > score || (sk == score && k < lane))) ? 1 : 0;
+  }
+  if (act) {
+    ts_beam_candidate c;
+    c.beam = b;
+    c.order = lane;
+    c.step_ref = idx;
+    c.token_count = 40 + (int)(ht % 81u);
+    c.prm_reward = reward;
+    c.score = score;
+    c.is_terminal = term ? 1 : 0;
+    c.rank = term ? -2 : (rank < cfg.beam_width ? rank : -1);
+    out[(size_t)pi * MAXB + lane] = c;
+  }
+}
+
+// prune_candidates over caller candidates: rank among the open ones by (-score, order).
+__global__ void __launch_bounds__(1024) k_beam_prune(ts_beam_candidate* c, int n, int width) {
+  __shared__ double ss[1024];
+  __shared__ int so[1024];
+  __shared__ unsigned char sopen[1024];
+  const int t = threadIdx.x;
+  if (t < n) {
+    ss[t] = c[t].score;
+    so[t] = c[t].order;
+    sopen[t] = c[t].is_terminal ? 0 : 1;
+  }
+  __syncthreads();
+  if (t >= n) return;
+  if (!sopen[t]) {
+    c[t].rank = -2;
+    return;
+  }
+  const double s = ss[t];
+  const int o = so[t];
+  int rank = 0;
+  for (int k = 0; k < n; ++k)
+    rank += (sopen[k] && (ss[k] > s || (ss[k] == s && (so[k] < o || (so[k] == o && k < t))))) ? 1 : 0;
+  c[t].rank = rank < width ? rank : -1;
+}
+
 thread_local std::string g_beam_err;
 
 int beam_check(const ts_beam_config* c) {
@@ -291,6 +407,25 @@ int ts_beam_search_host(const ts_beam_config* cfg, const ts_problem* host_proble
   cudaFreeAsync(dr, s);
   const cudaError_t e = cudaStreamSynchronize(s);
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? TS_OK : TS_CUDA;
+}
+
+int ts_beam_expand(const ts_beam_config* cfg, const ts_problem* dev_problems, int32_t n, const ts_beam* dev_beams,
+                   const int32_t* dev_counts, ts_beam_candidate* dev_cands, int32_t* dev_status, void* stream) {
+  int rc = beam_check(cfg);
+  if (rc) return rc;
+  if (n < 0 || (n > 0 && (!dev_problems || !dev_beams || !dev_counts || !dev_cands || !dev_status)))
+    return TS_INVALID_ARGUMENT;
+  if (n == 0) return TS_OK;
+  k_beam_expand<<<(n + BEAM_WARPS - 1) / BEAM_WARPS, 32 * BEAM_WARPS, 0, (cudaStream_t)stream>>>(
+      *cfg, dev_problems, n, dev_beams, dev_counts, dev_cands, dev_status);
+  return cudaGetLastError() == cudaSuccess ? TS_OK : TS_CUDA;
+}
+
+int ts_beam_prune(ts_beam_candidate* dev_cands, int32_t n, int32_t beam_width, void* stream) {
+  if (n < 0 || n > 1024 || beam_width < 1 || (n > 0 && !dev_cands)) return TS_INVALID_ARGUMENT;
+  if (n == 0) return TS_OK;
+  k_beam_prune<<<1, 1024, 0, (cudaStream_t)stream>>>(dev_cands, n, beam_width);
+  return cudaGetLastError() == cudaSuccess ? TS_OK : TS_CUDA;
 }
 
 }  // extern "C"

@@ -585,7 +585,44 @@ def gen_tree_json():
     dump("tree_json", out)
 
 
+def gen_beam_steps():
+    """beam_step / expand_beams / prune_candidates (beam.py:76-131) on beams taken
+    from reference beam searches mid-run."""
+    from treeserve.beam import Beam, BeamConfig, beam_step, expand_beams, prune_candidates
+
+    def brec(b):
+        return {"path": list(b.index_path), "rewards": list(b.rewards), "score": b.score, "terminal": b.is_terminal}
+
+    wl = list(make_workload(24, MIX, 5, branching=3, depth_ranges={d: (4, 9) for d in Difficulty}))
+    wl2 = list(make_workload(8, MIX, 6, branching=2, depth_ranges={d: (3, 5) for d in Difficulty}))
+    out = []
+    for pi, problem in enumerate(wl + wl2):
+        for bc, sc in [(BeamConfig(beam_width=8, candidates_per_beam=4), ScoringConfig()),
+                       (BeamConfig(beam_width=3, candidates_per_beam=4), ScoringConfig(scheme=AggregationScheme.MINIMUM)),
+                       (BeamConfig(beam_width=5, candidates_per_beam=6), ScoringConfig(scheme=AggregationScheme.AVERAGE))]:
+            active = [Beam(index_path=(), rewards=(), score=0.0)]
+            steps = []
+            for _ in range(4):
+                if not active:
+                    break
+                cands = expand_beams(active, bc, sc, problem)
+                res = beam_step(active, bc, sc, problem)
+                surv, fin = prune_candidates(cands, bc.beam_width)
+                steps.append({"beams": [brec(b) for b in active],
+                              "candidates": [{"beam": brec(c.beam), "order": c.order, "tokens": c.token_count}
+                                             for c in cands],
+                              "survivors": [brec(b) for b in res.survivors], "finished": [brec(b) for b in res.finished],
+                              "tokens": res.tokens_generated, "prune_survivors": [brec(b) for b in surv],
+                              "prune_finished": [brec(b) for b in fin]})
+                active = res.survivors
+            out.append({"workload": "w5" if pi < len(wl) else "w6", "index": pi if pi < len(wl) else pi - len(wl),
+                        "beam_width": bc.beam_width, "candidates_per_beam": bc.candidates_per_beam,
+                        "max_depth": bc.max_depth, "positive_exit_enabled": bc.positive_exit_enabled,
+                        "scoring": scoring_record(sc), "problem": problem_record(problem), "steps": steps})
+    dump("beam_steps", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps"]
     for w in which:
         globals()["gen_" + w]()

@@ -106,3 +106,86 @@ def test_device_beam_rejects_oversized_candidate_sets():
         run_beam_searches_raw(p, TsBeamConfig(9, 4, 16, 1, 1, 0, 0.5))
     assert len(run_beam_searches_raw([], TsBeamConfig(8, 4, 16, 1, 1, 0, 0.5))) == 0
     _ = np  # keep numpy import for parity with other suites
+
+
+def _beam(rec):
+    from paper_2604_00510_b200.beam import Beam
+
+    return Beam(tuple(rec["path"]), tuple(rec["rewards"]), rec["score"], rec["terminal"])
+
+
+def _rec(b):
+    return {"path": list(b.index_path), "rewards": list(b.rewards), "score": b.score, "terminal": b.is_terminal}
+
+
+@pytest.mark.gpu
+def test_device_beam_steps_match_reference():
+    """expand_beams / prune_candidates / beam_step vs the reference on mid-run beams."""
+    from paper_2604_00510_b200.beam import BeamConfig, beam_step, expand_beams, prune_candidates
+
+    for case in load("beam_steps"):
+        prob = problem_from_record(case["problem"])
+        cfg = BeamConfig(case["beam_width"], case["candidates_per_beam"], case["max_depth"],
+                         case["positive_exit_enabled"])
+        sc = scoring_from_record(case["scoring"])
+        for st in case["steps"]:
+            beams = [_beam(b) for b in st["beams"]]
+            cands = expand_beams(beams, cfg, sc, prob)
+            assert [{"beam": _rec(c.beam), "order": c.order, "tokens": c.token_count} for c in cands] == st["candidates"]
+            res = beam_step(beams, cfg, sc, prob)
+            assert [_rec(b) for b in res.survivors] == st["survivors"]
+            assert [_rec(b) for b in res.finished] == st["finished"]
+            assert res.tokens_generated == st["tokens"]
+            surv, fin = prune_candidates(cands, cfg.beam_width)
+            assert [_rec(b) for b in surv] == st["prune_survivors"]
+            assert [_rec(b) for b in fin] == st["prune_finished"]
+
+
+@pytest.mark.gpu
+def test_reference_beam_step_unit_cases_on_device():
+    """test_beam.py TestBeamStep / TestRunBeamSearch through the drop-in API."""
+    from paper_2604_00510_b200.backend import Difficulty, make_problem
+    from paper_2604_00510_b200.beam import Beam, BeamConfig, beam_step, run_beam_search
+    from paper_2604_00510_b200.scoring import ScoringConfig
+
+    def problem_of(difficulty, seed=11, depth=(3, 3), branching=2):
+        return make_problem("b", seed=seed, difficulty=difficulty, depth_range=depth, branching=branching)
+
+    root = Beam(index_path=(), rewards=(), score=0.0)
+    sc = ScoringConfig()
+    p = problem_of(Difficulty.EASY, depth=(4, 4))
+    cfg = BeamConfig(beam_width=2, candidates_per_beam=4)
+    r1 = beam_step([root], cfg, sc, p)
+    r2 = beam_step(r1.survivors, cfg, sc, p)
+    assert len(r2.survivors) == 2 and r2.tokens_generated > 0
+    assert len(beam_step([root], BeamConfig(beam_width=1, candidates_per_beam=1), sc, problem_of(Difficulty.EASY)).survivors) == 1
+    res = beam_step([root], cfg, sc, p)  # duplicate sampling keeps both copies of the best
+    assert len(res.survivors) == 2 and res.survivors[0].index_path == res.survivors[1].index_path
+    assert res.survivors[0].score == max(b.score for b in res.survivors)
+    res = beam_step([root], BeamConfig(beam_width=3, candidates_per_beam=4), sc, p)  # ties by candidate index
+    paths = [b.index_path for b in res.survivors]
+    assert paths[0] == paths[1] and paths[2] != paths[0]
+    pu = problem_of(Difficulty.UNSOLVABLE, depth=(4, 4))
+    cfg8 = BeamConfig(beam_width=8, candidates_per_beam=4)
+    active = [root]
+    for _ in range(3):
+        expected = cfg8.candidates_per_beam * len(active)
+        r = beam_step(active, cfg8, sc, pu)
+        assert len(r.survivors) == min(cfg8.beam_width, expected - len(r.finished))
+        assert 40 * expected <= r.tokens_generated <= 120 * expected
+        active = r.survivors
+        if not active:
+            break
+    with pytest.raises(ValueError):
+        beam_step([root] * 3, BeamConfig(beam_width=2, candidates_per_beam=2), sc, problem_of(Difficulty.EASY))
+    easy = problem_of(Difficulty.EASY, seed=23, depth=(3, 3))
+    r = run_beam_search(easy, BeamConfig(), sc)
+    assert r.complete and r.best.score >= sc.positive_exit_threshold and r.steps <= easy.base_depth
+    without = run_beam_search(easy, BeamConfig(positive_exit_enabled=False), sc)
+    assert without.steps >= r.steps and without.tokens_generated >= r.tokens_generated
+    un = run_beam_search(problem_of(Difficulty.UNSOLVABLE, seed=5, depth=(3, 3)), BeamConfig(), sc)
+    assert un.best.score < sc.accept_threshold
+    solved = problem_of(Difficulty.EASY, seed=31, depth=(2, 4))
+    assert run_beam_search(solved, BeamConfig(), sc).best.index_path == tuple(solved.golden_path)
+    hard = problem_of(Difficulty.HARD_SOLVABLE, seed=13)
+    assert run_beam_search(hard, BeamConfig(), sc) == run_beam_search(hard, BeamConfig(), sc)
