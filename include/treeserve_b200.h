@@ -354,6 +354,23 @@ int ts_beam_expand(const ts_beam_config* cfg, const ts_problem* dev_problems, in
  * is_terminal used; rank written): n <= 1024 candidates of one problem. */
 int ts_beam_prune(ts_beam_candidate* dev_cands, int32_t n, int32_t beam_width, void* stream);
 
+/* ---- the synthetic backend as an operator (csrc/steps.cu) -------------------
+ * generate_steps (backend.py:230-269) for n (problem, context path) pairs:
+ * candidate j of pair i in dev_out[i * width + j].  dev_paths holds
+ * TS_MAX_DEPTH bytes per pair, dev_lens the context lengths; dev_status[i] =
+ * TS_INVALID_ARGUMENT where the reference raises ValueError (terminal or
+ * too-deep context).  width <= TS_MAX_WIDTH. */
+typedef struct ts_step_candidate { /* StepCandidate (backend.py:62-70) */
+  int32_t step_ref;
+  int32_t token_count;
+  double prior;
+  double prm_reward;
+  int32_t is_terminal;
+  int32_t _pad;
+} ts_step_candidate;
+int ts_generate_steps(const ts_problem* dev_problems, int32_t n, const uint8_t* dev_paths, const int32_t* dev_lens,
+                      int32_t width, ts_step_candidate* dev_out, int32_t* dev_status, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

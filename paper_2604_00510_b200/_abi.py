@@ -119,6 +119,7 @@ EXPORTED = (
     "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
     "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
     "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
+    "ts_generate_steps",
 )
 
 
@@ -209,6 +210,17 @@ class TsBeamCandidate(ctypes.Structure):
     ]
 
 
+class TsStepCandidate(ctypes.Structure):
+    _fields_ = [
+        ("step_ref", ctypes.c_int32),
+        ("token_count", ctypes.c_int32),
+        ("prior", ctypes.c_double),
+        ("prm_reward", ctypes.c_double),
+        ("is_terminal", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+    ]
+
+
 _lib = None
 
 
@@ -255,6 +267,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_beam_search_host": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp]),
         "ts_beam_expand": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp, vp, vp, vp]),
         "ts_beam_prune": (ctypes.c_int, [vp, i32, i32, vp]),
+        "ts_generate_steps": (ctypes.c_int, [vp, i32, vp, vp, i32, vp, vp, vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

@@ -254,3 +254,140 @@ def problem_table(specs: Sequence, arrival_steps: Optional[Sequence[int]] = None
                 p.golden_path[d] = int(step)
                 p.golden_rewards[d] = float(r)
     return arr
+
+
+# ---- generate_steps and the cost model (backend.py:62-70, 230-311) -------------------
+
+@dataclass(frozen=True)
+class StepCandidate:
+    """One generated reasoning step with its verifier reward (backend.py:62-70)."""
+
+    step_ref: int
+    token_count: int
+    prior: float
+    prm_reward: float
+    is_terminal: bool
+
+
+def generate_steps_many(problems: Sequence, context_paths: Sequence[Sequence[int]], width: int) -> list:
+    """generate_steps for many (problem, context path) pairs in one kernel
+    (csrc/steps.cu).  Returns one candidate list per pair; raises ValueError
+    (like the reference) if any context is terminal or too deep."""
+    import torch
+
+    from ._abi import TS_MAX_WIDTH, TsStepCandidate, load_library, raise_for_status
+
+    if width < 1:
+        raise ValueError("width must be >= 1")
+    if width > TS_MAX_WIDTH:
+        raise ValueError(f"width above {TS_MAX_WIDTH} is not supported by this engine")
+    if not torch.cuda.is_available():
+        raise RuntimeError("generate_steps runs on the CUDA device; no CUDA device is available")
+    n = len(problems)
+    if n == 0:
+        return []
+    paths = np.zeros((n, TS_MAX_DEPTH), np.uint8)
+    lens = np.zeros(n, np.int32)
+    for i, cp in enumerate(context_paths):
+        cp = tuple(cp)
+        if len(cp) >= TS_MAX_DEPTH:
+            raise ValueError(f"context {cp} is terminal")
+        paths[i, : len(cp)] = cp
+        lens[i] = len(cp)
+    if isinstance(problems, ctypes.Array):
+        table = problems
+    elif isinstance(problems[0], TsProblem):  # ts_problem rows already
+        table = (TsProblem * n)(*problems)
+    else:
+        table = problem_table(list(problems))
+    dev = torch.device("cuda")
+    dprob = torch.frombuffer(bytearray(bytes(table)), dtype=torch.uint8).to(dev)
+    dpath = torch.from_numpy(paths).to(dev)
+    dlen = torch.from_numpy(lens).to(dev)
+    dout = torch.zeros(n * width * ctypes.sizeof(TsStepCandidate), dtype=torch.uint8, device=dev)
+    dstat = torch.zeros(n, dtype=torch.int32, device=dev)
+    rc = load_library().ts_generate_steps(ctypes.c_void_p(dprob.data_ptr()), n, ctypes.c_void_p(dpath.data_ptr()),
+                                          ctypes.c_void_p(dlen.data_ptr()), width, ctypes.c_void_p(dout.data_ptr()),
+                                          ctypes.c_void_p(dstat.data_ptr()),
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    raise_for_status(rc, "ts_generate_steps")
+    bad = dstat.cpu().numpy()
+    if bad.any():
+        i = int(np.flatnonzero(bad)[0])
+        raise ValueError(f"context {tuple(context_paths[i])} is terminal")
+    raw = (TsStepCandidate * (n * width)).from_buffer_copy(dout.cpu().numpy().tobytes())
+    return [[StepCandidate(c.step_ref, c.token_count, c.prior, c.prm_reward, bool(c.is_terminal))
+             for c in raw[i * width:(i + 1) * width]] for i in range(n)]
+
+
+def generate_steps(problem, context_path: Sequence[int], width: int) -> list:
+    """``width`` child steps below ``context_path`` (backend.py:230-269), on the device."""
+    return generate_steps_many([problem], [tuple(context_path)], width)[0]
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """Token-latency model with a concurrency knee (backend.py:287-300)."""
+
+    per_token_latency: float = 0.002
+    engine_capacity: int = 32
+    reward_latency: float = 0.01
+
+    def __post_init__(self) -> None:
+        if not (self.per_token_latency > 0 and self.engine_capacity >= 1 and self.reward_latency >= 0):
+            raise ValueError("cost model parameters must be positive")
+
+
+def service_time(token_count: int, model: CostModel, inflight_load: int) -> float:
+    """Generation latency of one request under load (backend.py:303-311): the
+    per-token latency stretched by the overload ratio past engine_capacity."""
+    if token_count < 1:
+        raise ValueError("token_count must be >= 1")
+    if inflight_load < 0:
+        raise ValueError("inflight_load must be >= 0")
+    stretch = max(1.0, inflight_load / model.engine_capacity)
+    return token_count * model.per_token_latency * stretch
+
+
+# ---- workload replay files (backend.py:359-410) ----------------------------------------
+
+def _spec_doc(spec) -> dict:
+    prof = spec.reward_profile
+    shared = prof.shared_range
+    return {
+        "branching": spec.branching,
+        "depth_range": [int(x) for x in spec.depth_range],
+        "difficulty": spec.difficulty.value,
+        "golden_path": [int(x) for x in spec.golden_path] if spec.golden_path else None,
+        "problem_id": spec.problem_id,
+        "reward_profile": {
+            "golden_range": [float(x) for x in prof.golden_range],
+            "hidden_until_depth": prof.hidden_until_depth,
+            "off_path_range": [float(x) for x in prof.off_path_range],
+            "shared_range": [float(x) for x in shared] if shared else None,
+            "target_aggregate": prof.target_aggregate,
+        },
+        "seed": int(spec.seed),
+    }
+
+
+def workload_to_json(specs: Sequence) -> str:
+    """The reference's workload replay format: sorted keys, indent 2 (byte-identical)."""
+    import json
+
+    return json.dumps([_spec_doc(s) for s in specs], indent=2, sort_keys=True)
+
+
+def workload_from_json(text: str) -> list:
+    """Specs back from :func:`workload_to_json` (or the reference's file)."""
+    import json
+
+    out = []
+    for doc in json.loads(text):
+        p = doc["reward_profile"]
+        prof = RewardProfile(tuple(p["golden_range"]), tuple(p["off_path_range"]), p["hidden_until_depth"],
+                             tuple(p["shared_range"]) if p["shared_range"] else None, p["target_aggregate"])
+        golden = tuple(doc["golden_path"]) if doc["golden_path"] else None
+        out.append(SyntheticProblemSpec(doc["problem_id"], doc["seed"], Difficulty(doc["difficulty"]),
+                                        tuple(doc["depth_range"]), doc["branching"], prof, golden))
+    return out

@@ -13,6 +13,7 @@ expandable leaves, one per tree decides.
 from __future__ import annotations
 
 import enum
+import math
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -90,6 +91,39 @@ def check_scheme_for_pruning(config: ScoringConfig) -> None:
         raise UnsupportedSchemeError(
             f"negative exit is unsound under {config.scheme.value} aggregation"
         )
+
+
+class LeafClass(enum.Enum):
+    VIABLE = "viable"
+    FUTILE = "futile"
+
+
+def aggregate_trajectory(rewards, scheme: AggregationScheme) -> float:
+    """One trajectory score from per-step rewards (scoring.py:106-116): min,
+    left-to-right product, CPython float sum, or that sum over the length.
+    (The engine computes the same incrementally on the device, `Agg`.)"""
+    values = list(rewards)
+    if len(values) == 0:
+        raise ValueError("rewards must be non-empty")
+    table = {
+        AggregationScheme.MINIMUM: lambda v: min(v),
+        AggregationScheme.CUMULATIVE_PRODUCT: lambda v: math.prod(v),
+        AggregationScheme.CUMULATIVE_SUM: lambda v: sum(v),
+    }
+    if scheme in table:
+        return table[scheme](values)
+    return sum(values) / len(values)
+
+
+def classify_leaf(leaf_reward: float, prefix_aggregate: float, config: ScoringConfig) -> LeafClass:
+    """FUTILE iff the futility bound is below the acceptance threshold
+    (scoring.py:119-134); only the minimum and product schemes admit a bound."""
+    check_scheme_for_pruning(config)
+    if config.futility_bound is FutilityBound.LEAF_REWARD:
+        bound = leaf_reward
+    else:
+        bound = min(leaf_reward, prefix_aggregate)
+    return LeafClass.FUTILE if bound < config.accept_threshold else LeafClass.VIABLE
 
 
 _KIND_OF_CODE = EXIT_FROM_CODE

@@ -622,7 +622,17 @@ def gen_beam_steps():
     dump("beam_steps", out)
 
 
+def gen_workload_json():
+    """workload_to_json (backend.py:359-384) of two workloads: the replay-file bytes."""
+    from treeserve.backend import workload_to_json
+
+    D7 = {d: (7, 7) for d in Difficulty}
+    out = {"c1": workload_to_json(make_workload(64, MIX, SEED, branching=4, depth_ranges=D7)),
+           "cli_default": workload_to_json(make_workload(40, MIX, 20260810))}
+    dump("workload_json", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps", "workload_json"]
     for w in which:
         globals()["gen_" + w]()
