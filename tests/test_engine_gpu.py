@@ -179,20 +179,29 @@ def test_compute_targets_random_vs_oracle(n):
             assert eng.read_targets() == want, (n, trial)
 
 
-def test_sharded_engines_match_single():
+@pytest.mark.parametrize("name,multi_cta", [("c1_M48_admission", False), ("c1_M48_admission", True),
+                                             ("cli_serving_pe_ne_boost", False), ("cli_serving_pe_ne_boost", True),
+                                             ("c2_s512_M2048", True)])
+def test_sharded_engines_match_single(name, multi_cta, monkeypatch):
     """Block sharding of the run queue over 3 engines (one 'rank' each) with the
-    exchanges done by device copies == one engine: the multi-GPU step contract."""
+    exchanges done by device copies == one engine: the multi-GPU step contract
+    (FIFO admission across ranks, Poisson arrivals, the boosting exchange),
+    with the one-CTA or the many-CTA scheduler step."""
     import torch
 
-    case = next(c for c in load("waves") if c["name"] == "c1_M48_admission")
-    recs = load("workloads")[case["workload"]]
+    if multi_cta:
+        monkeypatch.setenv("TS_MT_MIN", "0")
+    case = next(c for c in load("waves") if c["name"] == name)
+    recs = load("workloads")[case["workload"]][: len(case["outcomes"])]
     cfg = config_from_case(case)
     n = len(recs)
-    bounds = [0, 20, 41, n]
+    bounds = [0, n // 3, (2 * n) // 3 + 1, n]
+    arr = case.get("arrival_steps")
     engines = []
     for r in range(3):
         e = _engine(cfg)
-        e.load(table(recs[bounds[r]:bounds[r + 1]]), global_offset=bounds[r], n_global=n)
+        lo, hi = bounds[r], bounds[r + 1]
+        e.load(table(recs[lo:hi], arr[lo:hi] if arr else None), global_offset=lo, n_global=n)
         engines.append(e)
     counts = [torch.zeros(3, dtype=torch.int64, device="cuda") for _ in engines]
     recbufs = [torch.zeros((bounds[r + 1] - bounds[r]) * 16, dtype=torch.uint8, device="cuda") for r in range(3)]
