@@ -86,28 +86,60 @@ class ShardedRun:
         if parts[0].data_ptr() != out.data_ptr():  # backend returned fresh tensors
             out.copy_(__import__("torch").cat(parts))
 
+    def _global_max(self, x: int) -> int:
+        import torch
+
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.int64, device="cpu" if self.host else self.counts.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+    def _any_running(self) -> bool:
+        """Some search of the job is running (records gathered this wave)."""
+        flags = self.all_records.view(-1, RECORD_BYTES)[:, 8]  # low byte of ts_sched_record.flags
+        return bool((flags & 1).any().item())
+
     def run(self, max_steps: int = 1 << 30, wave_events: Optional[list] = None) -> int:
         """Advance waves until every search of every rank has exited; returns
-        the number of loop iterations (the reference loop's ``steps`` when it
-        breaks exactly at the first all-finished check).  ``wave_events``
-        collects (start, stop) CUDA events around every wave launch."""
+        the number of waves (the reference loop's ``steps``).  ``wave_events``
+        collects (start, stop) CUDA events around every wave launch.
+
+        Admission needs the counts exchange only while a search can still be
+        waiting: with M >= the whole run queue, after the last arrival step
+        nothing is ever pending, so those waves skip it (admit_jobs with no
+        pending search admits nothing) and the loop test reads the running
+        flags of the records every wave instead; otherwise the counts are
+        exchanged every wave and tested every ``check_every`` waves."""
+        import torch
+
         eng = self.engine
+        table = getattr(eng, "_table", None)
+        local_max = max((int(p.arrival_step) for p in table), default=0) if table is not None else 1 << 30
+        last_arrival = self._global_max(local_max)
+        cfg = getattr(eng, "_cfg", None)
+        capacity = int(cfg.max_concurrency) if cfg is not None else 0  # unknown: always exchange counts
+        no_pending = torch.zeros(COUNT_WORDS * self.world, dtype=torch.int64, device=self.counts.device)
         for step in range(max_steps):
-            eng.step_counts(step, self.counts.data_ptr())
-            self._gather(self.all_counts, self.counts)
-            if step % self.check_every == 0:
-                unfinished = int(self.all_counts.view(-1, COUNT_WORDS)[:, 2].sum().item())
-                if unfinished == 0:
-                    return step
-            eng.step_admit(step, self.all_counts.data_ptr(), self.world, self.rank)
+            admission = capacity < self.n_total or step <= last_arrival
+            if admission:
+                eng.step_counts(step, self.counts.data_ptr())
+                self._gather(self.all_counts, self.counts)
+                if step % self.check_every == 0:
+                    unfinished = int(self.all_counts.view(-1, COUNT_WORDS)[:, 2].sum().item())
+                    if unfinished == 0:
+                        return step
+                eng.step_admit(step, self.all_counts.data_ptr(), self.world, self.rank)
+            else:
+                eng.step_admit(step, no_pending.data_ptr(), self.world, self.rank)
             eng.step_records(step, self.records.data_ptr())
             self._gather(self.all_records, self.records)
+            if not admission and not self._any_running():
+                return step
             eng.step_targets(step, self.all_records.data_ptr())
             if wave_events is None:
                 eng.step_wave(step)
             else:
-                import torch
-
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 eng.step_wave(step)

@@ -91,11 +91,18 @@ class MockEngine:
                     self.running -= 1
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, batch=False):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     arrivals, lifetimes = _workload()
+    if batch:  # all requests at step 0, budget for all: the loop skips the counts exchange
+        global M
+        M = N_TOTAL
+        arrivals = [0] * N_TOTAL
     lo, hi = shard_bounds(N_TOTAL, world, rank)
     eng = MockEngine(arrivals[lo:hi], lifetimes[lo:hi], lo)
+    if batch:
+        eng._cfg = type("Cfg", (), {"max_concurrency": M})()
+        eng._table = [type("P", (), {"arrival_step": a})() for a in arrivals[lo:hi]]
     steps = run_sharded(eng, dist, hi - lo, N_TOTAL, "cpu", check_every=1)
     out[rank] = (steps, eng.admit, eng.exit)
     dist.destroy_process_group()
@@ -109,10 +116,10 @@ def _free_port():
     return p
 
 
-def _run(world):
+def _run(world, batch=False):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, batch), nprocs=world, join=True)
     steps = {out[r][0] for r in range(world)}
     assert len(steps) == 1
     admit = [a for r in range(world) for a in out[r][1]]
@@ -136,3 +143,14 @@ def test_gloo_world2_matches_single_rank():
     for step in range(s1):
         running = sum(1 for a, e in zip(a1, e1) if a <= step <= e and a >= 0)
         assert running <= M
+
+
+def test_gloo_world2_batch_mode_skips_counts_exchange():
+    """M >= the run queue and every request at step 0: after the first wave the
+    loop skips the counts exchange and stops on the gathered running flags,
+    with the same decisions as one rank and no extra (empty) waves."""
+    s1, a1, e1 = _run(1, batch=True)
+    s2, a2, e2 = _run(2, batch=True)
+    assert (s1, a1, e1) == (s2, a2, e2)
+    assert all(a == 0 for a in a1)
+    assert s1 == max(e1) + 1
