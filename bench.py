@@ -467,10 +467,17 @@ def cpu_baseline(per_gpu: int, n_total: int, target_s: float = 12.0):
         if dt > target_s / 4 or sample >= per_gpu:
             break
         sample = min(per_gpu, sample * 4)
+    # one host core on the same sample (single core and all cores)
+    t1 = time.perf_counter()
+    r1 = oracle.OracleRun(t, cfg, threads=1)
+    dt1 = time.perf_counter() - t1
+    ro1 = r1.stats.rollouts
+    r1.close()
     return {"value": ro / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"first {sample} of the {per_gpu} searches, M={sample}, same budget/exits/boosting; "
                       f"{ro} rollouts in {dt:.2f} s",
-            "p99_search_latency_ms": percentile(lat, 99)}
+            "p99_search_latency_ms": percentile(lat, 99),
+            "single_core_value": ro1 / dt1}
 
 
 def bench_reference(args):
