@@ -661,7 +661,8 @@ __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched
 // between phases (list positions, run ids, the previous score of each list)
 // lives in a global scratch row.
 constexpr int MT_T = 256, MT_CH = 8, MT_REC = MT_T * MT_CH;
-constexpr int MT_RUNCAP = 256;  // runs per list k_mt_all stages in shared memory (else read from global)
+constexpr int MT_RUNCAP = 128;  // runs per list k_mt_all stages in shared memory (else read from global)
+constexpr int MT_RB = 256;      // run blocks per list whose offsets k_mt_all keeps in shared memory
 struct MtBlk1 {
   long long nrun, cnt0, cnt1;
   unsigned long long flo, fhi;
@@ -1274,8 +1275,11 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
 #ifdef TS_HEAVY_PROF
   if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[23], (unsigned long long)(clock64() - t_mt0));
 #endif
-  // ---- phase 2 (CTA 0): CTA offsets, T, totals
-  if (b == 0) {
+  // ---- phase 2 (every CTA, redundantly): CTA offsets, T, totals from the
+  // G summaries (no further grid barrier: each CTA keeps its own copy)
+  __shared__ MtOff1 s_off;
+  __shared__ MtState s_st;
+  {
     MtBlk1 x{};
     x.min0 = x.min1 = INFINITY;
     if (tid < G) x = L.b1[tid];
@@ -1295,23 +1299,23 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     if (lane == 0) sq2[wid] = fx;
     __syncthreads();
     if (tid < G && x.bad) sbad2 = 1;
-    __syncthreads();
-    if (tid < G) {
+    if (tid == b) {
       MtOff1 o;
       o.p0 = c[1];
       o.p1 = c[2];
       o.prev0 = m0;
       o.prev1 = m1;
-      L.o1[tid] = o;
+      s_off = o;
     }
+    __syncthreads();
     if (tid == 0) {
-      u128 s = 0;
-      for (int w = 0; w < MT_T / 32; ++w) s += sq2[w];
+      u128 sum = 0;
+      for (int w = 0; w < MT_T / 32; ++w) sum += sq2[w];
       const long long tot_run = tot[0];
       bool fallback = sbad2 != 0;
       double T = 0.0;
       if (!fallback) {
-        T = fixed_to_double(s);
+        T = fixed_to_double(sum);
         const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
         if ((double)tot_run * u2 >= 0x1p-10) fallback = true;
       }
@@ -1330,7 +1334,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
         }
         if (cc != 0.0 && isfinite(cc)) f += cc;
         T = f;
-        atomicAdd(&v.ctr->sum_fallbacks, 1);
+        if (b == 0) atomicAdd(&v.ctr->sum_fallbacks, 1);
       }
       MtState st{};
       st.T = T;
@@ -1339,14 +1343,11 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
       st.len1 = tot[2];
       const long long R = (long long)cf.max_concurrency - tot_run;
       st.boost_on = (cf.boosting_enabled != 0 && tot_run > 0 && R > 0 && tot[1] + tot[2] > 0) ? 1 : 0;
-      *L.st = st;
+      s_st = st;
     }
+    __syncthreads();
   }
-  grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[24], (unsigned long long)(clock64() - t_mt0));
-#endif
-  const bool boost_on = L.st->boost_on != 0;
+  const bool boost_on = s_st.boost_on != 0;
   // ---- phase 3: positions, previous scores, run counts
   MtThr th;
   {
@@ -1361,7 +1362,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     mt_scan<2>(c, tot);
     double tm0, tm1;
     mt_scan_min2(m0, m1, tm0, tm1);
-    const MtOff1 o = L.o1[b];
+    const MtOff1 o = s_off;
     th.pos0 = o.p0 + c[0];
     th.pos1 = o.p1 + c[1];
     th.prev0 = fmin(o.prev0, m0);
@@ -1389,26 +1390,24 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
 #ifdef TS_HEAVY_PROF
   if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[25], (unsigned long long)(clock64() - t_mt0));
 #endif
-  // ---- phase 4 (CTA 0): run offsets of the CTAs
-  if (b == 0) {
+  // ---- phase 4 (every CTA): run offsets of the CTAs, run totals
+  {
     long long c[2] = {tid < G ? L.b2[tid] : 0, tid < G ? L.b2[G + tid] : 0}, tot[2];
     mt_scan<2>(c, tot);
-    if (tid < G) {
-      L.b2[tid] = c[0];
-      L.b2[G + tid] = c[1];
+    __shared__ long long s_roff[2];
+    if (tid == b) {
+      s_roff[0] = c[0];
+      s_roff[1] = c[1];
     }
     if (tid == 0) {
-      L.st->nr0 = tot[0];
-      L.st->nr1 = tot[1];
+      s_st.nr0 = tot[0];
+      s_st.nr1 = tot[1];
     }
+    __syncthreads();
+    th.rid0 += s_roff[0];
+    th.rid1 += s_roff[1];
   }
-  grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[26], (unsigned long long)(clock64() - t_mt0));
-#endif
   // ---- phase 5: run records
-  th.rid0 += L.b2[b];
-  th.rid1 += L.b2[G + b];
   if (boost_on) {
     double p0 = th.prev0, p1 = th.prev1;
     long long q0 = th.pos0, q1 = th.pos1, k0 = th.rid0, k1 = th.rid1;
@@ -1433,7 +1432,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
   const long long M = cf.max_concurrency;
   // ---- phase 6: want per run, per-run-block sums
   if (boost_on) {
-    const MtState st = *L.st;
+    const MtState st = s_st;
     const long long nrmax = st.nr0 > st.nr1 ? st.nr0 : st.nr1;
     const int g3 = (int)((nrmax + MT_T - 1) / MT_T);
     for (int rb = b; rb < g3; rb += G) {
@@ -1463,9 +1462,11 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
 #ifdef TS_HEAVY_PROF
   if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[28], (unsigned long long)(clock64() - t_mt0));
 #endif
-  // ---- phase 7 (CTA 0): run-block offsets, tw0/tw1
-  if (b == 0) {
-    const MtState st = *L.st;
+  // ---- phase 7 (every CTA): run-block offsets into shared memory, tw0/tw1
+  __shared__ long long s_b3[2 * MT_RB];
+  const bool b3_smem = G3 <= MT_RB;
+  {
+    const MtState st = s_st;
     const long long nrmax = st.nr0 > st.nr1 ? st.nr0 : st.nr1;
     const int g3 = boost_on ? (int)((nrmax + MT_T - 1) / MT_T) : 0;
     long long carry0 = 0, carry1 = 0;
@@ -1474,26 +1475,29 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
       long long c[2] = {rb < g3 ? L.b3[rb] : 0, rb < g3 ? L.b3[G3 + rb] : 0}, tot[2];
       mt_scan<2>(c, tot);
       if (rb < g3) {
-        L.b3[rb] = carry0 + c[0];
-        L.b3[G3 + rb] = carry1 + c[1];
+        if (b3_smem) {
+          s_b3[rb] = carry0 + c[0];
+          s_b3[MT_RB + rb] = carry1 + c[1];
+        } else if (b == 0) {
+          L.b3[rb] = carry0 + c[0];
+          L.b3[G3 + rb] = carry1 + c[1];
+        }
       }
       carry0 += tot[0];
       carry1 += tot[1];
     }
     if (tid == 0) {
-      L.st->tw0 = carry0;
-      L.st->tw1 = carry1;
+      s_st.tw0 = carry0;
+      s_st.tw1 = carry1;
     }
+    __syncthreads();
   }
-  grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[29], (unsigned long long)(clock64() - t_mt0));
-#endif
+  if (!b3_smem) grid.sync();  // CTA 0 rewrote the global run-block offsets
   // ---- phase 8: targets of the local records, pipelined-mode flags, per-CTA list counts
   const int glo = v.goff, ghi = v.goff + v.n_local;
   long long nh = 0, nlt = 0;
   if (base + nb > glo && base < ghi) {  // this CTA holds local records (CTA-uniform: the staging syncs)
-    const MtState st = *L.st;
+    const MtState st = s_st;
     const long long R = M - st.tot_run, U = st.len0 + st.len1;
     long long Rp = R - (st.tw0 + st.tw1);
     if (Rp < 0) Rp = 0;
@@ -1514,7 +1518,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
           s_runS[so + k] = v.g_runS[go + k];
           s_runStart[so + k] = v.g_runStart[go + k];
           s_runWant[so + k] = v.g_runWant[go + k];
-          s_runPW[so + k] = v.g_runPW[go + k] + L.b3[(q ? G3 : 0) + k / MT_T];
+          s_runPW[so + k] = v.g_runPW[go + k] + (b3_smem ? s_b3[(q ? MT_RB : 0) + k / MT_T] : L.b3[(q ? G3 : 0) + k / MT_T]);
         }
       }
       runS = s_runS;
@@ -1524,7 +1528,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
     __syncthreads();
     auto runPW = [&](int off, long long k) {
-      return in_smem ? runPWg[off + k] : runPWg[off + k] + L.b3[(off ? G3 : 0) + k / MT_T];
+      if (in_smem) return runPWg[off + k];
+      const long long blk = b3_smem ? s_b3[(off ? MT_RB : 0) + k / MT_T] : L.b3[(off ? G3 : 0) + k / MT_T];
+      return runPWg[off + k] + blk;
     };
     long long q0 = th.pos0, q1 = th.pos1, k0 = th.rid0 - 1, k1 = th.rid1 - 1;
     double p0 = th.prev0, p1 = th.prev1;
