@@ -95,11 +95,6 @@ class ShardedRun:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return int(t.item())
 
-    def _any_running(self) -> bool:
-        """Some search of the job is running (records gathered this wave)."""
-        flags = self.all_records.view(-1, RECORD_BYTES)[:, 8]  # low byte of ts_sched_record.flags
-        return bool((flags & 1).any().item())
-
     def run(self, max_steps: int = 1 << 30, wave_events: Optional[list] = None) -> int:
         """Advance waves until every search of every rank has exited; returns
         the number of waves (the reference loop's ``steps``).  ``wave_events``
@@ -120,6 +115,9 @@ class ShardedRun:
         cfg = getattr(eng, "_cfg", None)
         capacity = int(cfg.max_concurrency) if cfg is not None else 0  # unknown: always exchange counts
         no_pending = torch.zeros(COUNT_WORDS * self.world, dtype=torch.int64, device=self.counts.device)
+        on_gpu = self.counts.device.type == "cuda"
+        self._flag_host = torch.zeros(1, dtype=torch.int32, pin_memory=on_gpu)
+        self._flag_event = torch.cuda.Event() if on_gpu else _HostEvent()
         for step in range(max_steps):
             admission = capacity < self.n_total or step <= last_arrival
             if admission:
@@ -134,8 +132,13 @@ class ShardedRun:
                 eng.step_admit(step, no_pending.data_ptr(), self.world, self.rank)
             eng.step_records(step, self.records.data_ptr())
             self._gather(self.all_records, self.records)
-            if not admission and not self._any_running():
-                return step
+            if not admission:
+                # the loop test reads this wave's running flags, but only after
+                # the wave is queued: the GPU never idles on the host's check
+                # (a finished job costs one empty scheduler step instead)
+                flags = self.all_records.view(-1, RECORD_BYTES)[:, 8]
+                self._flag_host.copy_((flags & 1).any().to(torch.int32).view(1), non_blocking=True)
+                self._flag_event.record()
             eng.step_targets(step, self.all_records.data_ptr())
             if wave_events is None:
                 eng.step_wave(step)
@@ -145,7 +148,21 @@ class ShardedRun:
                 eng.step_wave(step)
                 e1.record()
                 wave_events.append((e0, e1))
+            if not admission:
+                self._flag_event.synchronize()
+                if int(self._flag_host[0]) == 0:
+                    return step
         return max_steps
+
+
+class _HostEvent:
+    """Stand-in for a CUDA event when the exchange runs on CPU tensors."""
+
+    def record(self):
+        pass
+
+    def synchronize(self):
+        pass
 
 
 def run_sharded(engine, dist, n_local: int, n_total: int, device, group=None,
