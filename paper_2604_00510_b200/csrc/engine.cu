@@ -134,6 +134,19 @@ __device__ __forceinline__ int warp_argmax(double v, bool valid, int /*wp2*/) {
   return __ffs(win) - 1;
 }
 
+// warp_argmax for values that are never -0.0 (WU-PUCT scores: q >= +0 and the
+// exploration term >= +0), without the fold of -0.0 into +0.0.
+__device__ __forceinline__ int warp_argmax_nonneg(double v, bool valid) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const uint64_t key = (b >> 63) ? ~b : (b | (1ull << 63));
+  const unsigned hi = valid ? (unsigned)(key >> 32) : 0u;
+  const unsigned lo = valid ? (unsigned)key : 0u;
+  const unsigned mh = __reduce_max_sync(FULL, hi);
+  const unsigned ml = __reduce_max_sync(FULL, hi == mh ? lo : 0u);
+  const unsigned win = __ballot_sync(FULL, valid && hi == mh && lo == ml);
+  return __ffs(win) - 1;
+}
+
 // Running splitmix64 folds: for every expansion depth d a rollout can reach,
 // the lanes hold fold(seed, TAG, len, path[0:depth]) for the four key tags of
 // generate_steps (backend.py:230-269): prior (2, d), reward (1, d+1), tokens
@@ -2358,7 +2371,7 @@ __device__ __forceinline__ double isqrt_tab(const double* sqt, long long n) {
   return t;
 }
 
-template <int NSLOT, int WT>
+template <int NSLOT, int WT, bool PROD>
 __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, const double* sqt, int count,
                              WaveStats& ws, uint64_t& rno_out, double& rW_out, int& decision_out) {
   const int lane = threadIdx.x & 31;
@@ -2445,9 +2458,14 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       const uint64_t nno = __shfl_sync(FULL, xno, src);
       pq = __shfl_sync(FULL, xnq, src);
       psq = __shfl_sync(FULL, xnsq, src);
-      agg.add(nrew, scheme);
+      if constexpr (PROD) {
+        agg.a = agg.a * nrew;
+        ++agg.n;
+      } else {
+        agg.add(nrew, scheme);
+      }
       if (depth == 1) d1r = nrew;
-      golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == child_index;
+      if (golden) golden = depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == child_index;
       if (lane == depth - 1) { pnode = node; pno = nno; pj = child_index; }
       // entering a leaf whose expansion may be in flight: its word and children
       // are only valid after that job's commit (acquired in the wait)
@@ -2537,7 +2555,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         if (!vb1) { status = TS_EXHAUSTED; break; }
         scored += __popc(vb1);
         ++levels;
-        const int j1 = warp_argmax(sc, valid && l1, 0);
+        const int j1 = warp_argmax_nonneg(sc, valid && l1);
 #ifdef TS_HEAVY_PROF
         if (lane == 0) q_sc += clock64() - t_c;
         long long t_d = clock64();
@@ -2557,7 +2575,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         if (!vb2) { status = TS_EXHAUSTED; break; }
         scored += __popc(vb2);
         ++levels;
-        const int s2 = warp_argmax(sc, valid && ing, 0);
+        const int s2 = warp_argmax_nonneg(sc, valid && ing);
         take(s2, (s2 - WT) % WT, nfc, xno, xmf, xr, xnq, xnsq);
 #ifdef TS_HEAVY_PROF
         if (lane == 0) q_l2t += clock64() - t_e + (nfc == -7 ? 1 : 0);
@@ -2598,7 +2616,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       if (!vb) { status = TS_EXHAUSTED; break; }
       scored += __popc(vb);
       ++levels;
-      const int j = warp_argmax(sc, valid, 0);
+      const int j = warp_argmax_nonneg(sc, valid);
 #ifdef TS_HEAVY_PROF
       if (lane == 0) p_math += clock64() - t_l0;
 #endif
@@ -2611,9 +2629,14 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       const uint64_t nno = __shfl_sync(FULL, cno, j);
       pq = __shfl_sync(FULL, nq, j);
       psq = __shfl_sync(FULL, nsq, j);
-      agg.add(nrew, scheme);
+      if constexpr (PROD) {
+        agg.a = agg.a * nrew;
+        ++agg.n;
+      } else {
+        agg.add(nrew, scheme);
+      }
       if (depth == 1) d1r = nrew;
-      golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
+      if (golden) golden = depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
       if (lane == depth - 1) { pnode = node; pno = nno; pj = j; }
       // entering a leaf whose expansion may be in flight: its word and children
       // are only valid after that job's commit (acquired in the wait)
@@ -3219,7 +3242,10 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
     double rW = 0.0;
     int decision = TS_EXIT_NONE;
     if (warp == 0) {
-      heavy_select<NSLOT, WT>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
+      if (v.cfg.scheme == TS_SCHEME_PRODUCT)
+        heavy_select<NSLOT, WT, true>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
+      else
+        heavy_select<NSLOT, WT, false>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
     } else if (warp != 4) {
       const int si = heavy_sim_of_warp(warp);
       double* s_raw = hsm + (size_t)si * 2 * 32 * WT;
