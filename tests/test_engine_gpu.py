@@ -304,22 +304,29 @@ def test_invalid_config_raises():
         Engine(c, 0)
 
 
-@pytest.mark.parametrize("seed,M,budget,cap,b,base", [(0, 256, 32, 8, 4, 7), (5, 4096, 128, 16, 4, 15),
-                                                      (9, 512, 64, 12, 8, 11), (3, 1024, 48, 6, 2, 7)])
-def test_pipelined_mode_matches_single_warp_mode(seed, M, budget, cap, b, base, monkeypatch):
+@pytest.mark.parametrize("seed,M,budget,cap,b,base,scheme", [
+    (0, 256, 32, 8, 4, 7, "cumulative_product"), (5, 4096, 128, 16, 4, 15, "cumulative_product"),
+    (9, 512, 64, 12, 8, 11, "cumulative_product"), (3, 1024, 48, 6, 2, 7, "cumulative_product"),
+    (11, 512, 64, 24, 4, 23, "cumulative_product"), (13, 512, 64, 12, 4, 11, "minimum"),
+    (17, 256, 48, 10, 3, 9, "average")])
+def test_pipelined_mode_matches_single_warp_mode(seed, M, budget, cap, b, base, scheme, monkeypatch):
     """Searches with many rollouts per wave run in the pipelined CTA mode
     (selector warp + simulator warps, in-order commits); the result must equal
-    the single-warp mode bit for bit — outcomes and whole trees."""
+    the single-warp mode bit for bit — outcomes and whole trees (all fold
+    layouts, widths 2-8, and the product / minimum / average aggregations)."""
     from paper_2604_00510_b200 import backend as B
     from paper_2604_00510_b200.config import SearchConfig
     from paper_2604_00510_b200.scheduler import SchedulerConfig
+    from paper_2604_00510_b200.scoring import AggregationScheme, ScoringConfig
 
     n = M // 4
     specs = B.make_workload(n, (0.5, 0.3, 0.2), seed, branching=b,
                             depth_ranges={d: (base, base) for d in B.Difficulty})
     t = B.problem_table(specs)
-    cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=M), rollout_budget=budget, depth_cap=cap,
-                       expand_width=b)
+    sc = AggregationScheme(scheme)
+    cfg = SearchConfig(scoring=ScoringConfig(scheme=sc), scheduler=SchedulerConfig(max_concurrency=M),
+                       rollout_budget=budget, depth_cap=cap, expand_width=b,
+                       negative_exit=sc in (AggregationScheme.CUMULATIVE_PRODUCT, AggregationScheme.MINIMUM))
     res = {}
     for mode in ("0", "1"):
         monkeypatch.setenv("TS_NO_PIPELINE", mode)
