@@ -2315,8 +2315,11 @@ struct HeavyJob {
   int pj[32];      // child index chosen at depth l
 };
 
+constexpr int HEAVY_ZERO_O_MAX = 1 << 16;  // trees up to this size clear O with the whole CTA at an exit
+
 struct HeavyCtl {
   volatile int issued, committed, done, status;
+  int zero_o;  // set by heavy_finish: clear O of every node of the search (exit with cancellations)
   volatile int nnodes, viable;
   unsigned long long created, tokens;
 };
@@ -3140,7 +3143,28 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
     pathn += pl;
     if (status == TS_OK) decision = decide(false);
     __syncwarp();
-    if (status == TS_OK && nb < nl) {
+    if (status == TS_OK && nb < nl && ctl->nnodes <= HEAVY_ZERO_O_MAX) {
+      // cancel_inflight (tree.py:374-380) for the wave's remaining rollouts,
+      // at an exit.  Every wave ends with no rollout in flight, so O was 0 on
+      // every node when this wave started; after the backups above the only
+      // in-flight counts left are exactly the cancelled rollouts', and
+      // removing them returns every node to O = 0.  The whole CTA clears the
+      // O half of the search's N|O words after this call (coalesced), instead
+      // of one warp decrementing ~17 scattered nodes per cancelled rollout.
+      const int first = nb, ncan = nl - first;
+      long long pc = 0;
+      for (int r2 = first + lane; r2 < nl; r2 += 32) pc += SLs[r2] + 1;
+      for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(FULL, pc, o);
+      if ((long long)(rno >> 32) < ncan) status = TS_ACCOUNTING;
+      rno -= (uint64_t)ncan * O_ONE;
+      if (lane == 0) {
+        NO[0] = rno;
+        ctl->zero_o = 1;
+      }
+      __syncwarp();
+      cancelled += ncan;
+      pathn += (unsigned long long)pc;
+    } else if (status == TS_OK && nb < nl) {
       // cancel_inflight (tree.py:374-380) for the wave's remaining rollouts.
       // Their order does not matter (O -= 1 on each path node), so lanes take
       // whole rollouts and decrement with atomics; a node's in-flight count
@@ -3231,6 +3255,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
       ctl.issued = 0;
       ctl.committed = 0;
       ctl.done = 0;
+      ctl.zero_o = 0;
       ctl.status = TS_OK;
       ctl.nnodes = S->nodes;
       ctl.viable = S->viable;
@@ -3256,6 +3281,12 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
     long long t_fin = clock64();
 #endif
     if (warp == 0) heavy_finish(v, s, step, &ctl, ctl.issued, rno, rW, decision, ws);
+    __syncthreads();
+    if (ctl.zero_o) {  // the cancellation of an exit: O back to 0 on every node but the root
+      uint64_t* NO = v.no + (size_t)s * (size_t)v.cap;
+      const int nn = ctl.nnodes;
+      for (int i = 1 + threadIdx.x; i < nn; i += HEAVY_THREADS) NO[i] &= 0xffffffffull;
+    }
 #ifdef TS_HEAVY_PROF
     if (threadIdx.x == 0) atomicMax(&v.ctr->prof[15], (unsigned long long)(clock64() - t_fin));
 #endif
