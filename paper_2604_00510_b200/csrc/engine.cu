@@ -3285,7 +3285,21 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
     if (ctl.zero_o) {  // the cancellation of an exit: O back to 0 on every node but the root
       uint64_t* NO = v.no + (size_t)s * (size_t)v.cap;
       const int nn = ctl.nnodes;
-      for (int i = 1 + threadIdx.x; i < nn; i += HEAVY_THREADS) NO[i] &= 0xffffffffull;
+      // 8 independent loads in flight per thread, then the stores
+      constexpr int U = 8;
+      for (int i0 = 1 + threadIdx.x; i0 < nn; i0 += U * HEAVY_THREADS) {
+        uint64_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * HEAVY_THREADS;
+          w[u] = i < nn ? NO[i] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = i0 + u * HEAVY_THREADS;
+          if (i < nn && (w[u] >> 32)) NO[i] = w[u] & 0xffffffffull;
+        }
+      }
     }
 #ifdef TS_HEAVY_PROF
     if (threadIdx.x == 0) atomicMax(&v.ctr->prof[15], (unsigned long long)(clock64() - t_fin));
