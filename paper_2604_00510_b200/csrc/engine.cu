@@ -1229,9 +1229,6 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
   for (int i = tid; i < nb; i += MT_T) srec[i] = rec[base + i];
   if (b == 0 && tid == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
   __syncthreads();
-#ifdef TS_HEAVY_PROF
-  const long long t_mt0 = clock64();
-#endif
   const int lo = min(nb, tid * MT_CH), hi = min(nb, lo + MT_CH);  // this thread's records, CTA-local
   const ts_config& cf = v.cfg;
 
@@ -1285,9 +1282,6 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[23], (unsigned long long)(clock64() - t_mt0));
-#endif
   // ---- phase 2 (every CTA, redundantly): CTA offsets, T, totals from the
   // G summaries (no further grid barrier: each CTA keeps its own copy)
   __shared__ MtOff1 s_off;
@@ -1400,9 +1394,6 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[25], (unsigned long long)(clock64() - t_mt0));
-#endif
   // ---- phase 4 (every CTA): run offsets of the CTAs, run totals
   {
     long long c[2] = {tid < G ? L.b2[tid] : 0, tid < G ? L.b2[G + tid] : 0}, tot[2];
@@ -1439,9 +1430,6 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[27], (unsigned long long)(clock64() - t_mt0));
-#endif
   const long long M = cf.max_concurrency;
   // ---- phase 6: want per run, per-run-block sums
   if (boost_on) {
@@ -1472,9 +1460,6 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[28], (unsigned long long)(clock64() - t_mt0));
-#endif
   // ---- phase 7 (every CTA): run-block offsets into shared memory, tw0/tw1
   __shared__ long long s_b3[2 * MT_RB];
   const bool b3_smem = G3 <= MT_RB;
@@ -1623,9 +1608,6 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
-#ifdef TS_HEAVY_PROF
-  if (b == 0 && tid == 0) atomicAdd(&v.ctr->prof[30], (unsigned long long)(clock64() - t_mt0));
-#endif
   // ---- phase 9: work lists in run-queue order
   {
     if (tid == 0) {
@@ -2672,6 +2654,9 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       root_seen = k - HEAVY_RING + 1;
       if (stale) rmf = reload_u64(MF);
     }
+#ifdef TS_HEAVY_PROF
+    const long long e0 = clock64();
+#endif
     HeavyJob& jb = ring[k % HEAVY_RING];
     jb.pnode[lane] = pnode;
     jb.pj[lane] = pj;
@@ -2688,7 +2673,13 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       jb.d1r = d1r;
     }
     __syncwarp();
+#ifdef TS_HEAVY_PROF
+    const long long e1 = clock64();
+#endif
     if (lane == 0) st_release_cta(&ctl->issued, k + 1);
+#ifdef TS_HEAVY_PROF
+    const long long e2 = clock64();
+#endif
     if (width == 1 || depth >= risky_depth || v.heavy_sync) last_risky = k;
     // in-flight registration of root..leaf (tree.py:282-283); only this warp
     // reads N|O of pre-existing nodes during the wave
@@ -2698,6 +2689,14 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     lleaf = __shfl_up_sync(FULL, lleaf, 1);
     if (lane == 0) lleaf = node;
     __syncwarp();
+#ifdef TS_HEAVY_PROF
+    if (lane == 0) {
+      const long long e3 = clock64();
+      atomicAdd(&v.ctr->prof[23], (unsigned long long)(e1 - e0));
+      atomicAdd(&v.ctr->prof[24], (unsigned long long)(e2 - e1));
+      atomicAdd(&v.ctr->prof[25], (unsigned long long)(e3 - e2));
+    }
+#endif
     HPROF_ACC(p_infl, t_epi);
   }
   if (lane == 0) ctl->done = 1;

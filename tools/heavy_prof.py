@@ -34,3 +34,4 @@ print("simulator cycles/job: wait-issue %.0f compute %.0f wait-commit %.0f commi
 r = max(1, p[21])
 print("two-level rounds %d (%.2f/job): per round l1-load %.0f l2(shfl+load) %.0f math %.0f ballots+argmax %.0f take1 %.0f level2 %.0f" %
       (p[21], p[21] / jobs, p[16] / r, p[17] / r, p[22] / r, p[18] / r, p[19] / r, p[20] / r))
+print("selector epilogue per job: ring writes %.0f release %.0f registration %.0f" % (p[23] / jobs, p[24] / jobs, p[25] / jobs))
