@@ -3100,34 +3100,69 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
     // backpropagate (tree.py:352-371) of rollouts [0, nb): lane i owns depth
     // i+1 (a node has one depth, so lanes never share a node) and adds the
     // scores in launch order, keeping runs of the same node in registers
+    // The rollouts are read 4 at a time: their lengths, scores, this lane's
+    // node ids and those nodes' N|O and W load together (independent, one
+    // round trip); a node this lane already wrote back in the same batch is
+    // re-read after its write-back instead (the prefetched copy is older).
     bool bad = false;
     int cur = -1;
     uint64_t cno = 0;
     double cw = 0.0;
     unsigned long long pl = 0;
-#pragma unroll 4
-    for (int r = 0; r < nb; ++r) {
-      const int len = SLs[r];
-      const double sc = SSs[r];
-      pl += len + 1;
-      if ((rno >> 32) < 1) bad = true;
-      rno = rno + 1 - O_ONE;
-      rW += sc;
-      if (lane < len) {
-        const int nd = SPs[(size_t)r * 32 + lane];
-        if (nd != cur) {
-          if (cur >= 0) {
-            NO[cur] = cno;
-            Wv[cur] = cw;
-            QQ[cur] = cw / (double)(uint32_t)cno;
+    constexpr int BB = 4;
+    for (int r0 = 0; r0 < nb; r0 += BB) {
+      int lenb[BB], idb[BB];
+      double scb[BB], wb[BB];
+      uint64_t nob[BB];
+#pragma unroll
+      for (int k = 0; k < BB; ++k) {
+        const int r = min(r0 + k, nb - 1);
+        lenb[k] = SLs[r];
+        scb[k] = SSs[r];
+        idb[k] = SPs[(size_t)r * 32 + lane];
+      }
+#pragma unroll
+      for (int k = 0; k < BB; ++k) {
+        const bool use = r0 + k < nb && lane < lenb[k];
+        if (!use) idb[k] = -1;
+        nob[k] = use ? NO[idb[k]] : 0ull;
+        wb[k] = use ? Wv[idb[k]] : 0.0;
+      }
+      const int cur0 = cur;  // the run carried into this batch (written back in it if left)
+#pragma unroll
+      for (int k = 0; k < BB; ++k) {
+        if (r0 + k >= nb) break;
+        const double sc = scb[k];
+        pl += lenb[k] + 1;
+        if ((rno >> 32) < 1) bad = true;
+        rno = rno + 1 - O_ONE;
+        rW += sc;
+        const int nd = idb[k];
+        if (nd >= 0) {
+          if (nd != cur) {
+            if (cur >= 0) {
+              NO[cur] = cno;
+              Wv[cur] = cw;
+              QQ[cur] = cw / (double)(uint32_t)cno;
+            }
+            // the carried run or a node seen earlier in this batch, left since:
+            // written back after the prefetch
+            bool again = nd == cur0;
+#pragma unroll
+            for (int j = 0; j < k; ++j) again |= idb[j] == nd;
+            cur = nd;
+            if (again) {  // written back earlier in this batch: the prefetched copy is stale
+              cno = NO[nd];
+              cw = Wv[nd];
+            } else {
+              cno = nob[k];
+              cw = wb[k];
+            }
           }
-          cur = nd;
-          cno = NO[nd];
-          cw = Wv[nd];
+          if ((cno >> 32) < 1) bad = true;
+          cno = cno + 1 - O_ONE;
+          cw += sc;
         }
-        if ((cno >> 32) < 1) bad = true;
-        cno = cno + 1 - O_ONE;
-        cw += sc;
       }
     }
     if (cur >= 0) {
