@@ -2390,6 +2390,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
 #ifdef TS_HEAVY_PROF
   long long p_total = 0, p_risky = 0, p_infl = 0, p_ring = 0, p_load = 0, p_math = 0;
   long long q_l1 = 0, q_l2 = 0, q_sc = 0, q_t1 = 0, q_l2t = 0, q_rounds = 0, q_math = 0;
+  long long q_root_l1 = 0, q_root_l2 = 0, q_root_rounds = 0;
   HPROF_T0(p_start);
 #endif
   for (; k < count; ++k) {
@@ -2490,7 +2491,11 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         {
           unsigned long long w_;
           asm volatile("xor.b64 %0, %1, %2;\n\txor.b64 %0, %0, %3;" : "=l"(w_) : "l"(xmf), "l"(xno), "l"(__double_as_longlong(xq + xp + xr)) : "memory");
-          if (lane == 0) q_l1 += clock64() - t_a + (w_ == 12345 ? 1 : 0);
+          if (lane == 0) {
+            const long long dt_ = clock64() - t_a + (w_ == 12345 ? 1 : 0);
+            q_l1 += dt_;
+            if (depth == 0) q_root_l1 += dt_;
+          }
         }
         long long t_b = clock64();
 #endif
@@ -2511,7 +2516,11 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         {
           unsigned long long w_;
           asm volatile("xor.b64 %0, %1, %2;\n\txor.b64 %0, %0, %3;" : "=l"(w_) : "l"(xmf), "l"(xno), "l"(__double_as_longlong(xq + xp + xr)) : "memory");
-          if (lane == 0) q_l2 += clock64() - t_b + (w_ == 12345 ? 1 : 0);
+          if (lane == 0) {
+            const long long dt_ = clock64() - t_b + (w_ == 12345 ? 1 : 0);
+            q_l2 += dt_;
+            if (depth == 0) { q_root_l2 += dt_; ++q_root_rounds; }
+          }
         }
         long long t_c = clock64();
 #endif
@@ -2727,6 +2736,9 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     atomicAdd(&v.ctr->prof[20], (unsigned long long)q_l2t);
     atomicAdd(&v.ctr->prof[21], (unsigned long long)q_rounds);
     atomicAdd(&v.ctr->prof[22], (unsigned long long)q_math);
+    atomicAdd(&v.ctr->prof[26], (unsigned long long)q_root_l1);
+    atomicAdd(&v.ctr->prof[27], (unsigned long long)q_root_l2);
+    atomicAdd(&v.ctr->prof[28], (unsigned long long)q_root_rounds);
   }
 #endif
   rno_out = rno;

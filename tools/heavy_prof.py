@@ -35,3 +35,6 @@ r = max(1, p[21])
 print("two-level rounds %d (%.2f/job): per round l1-load %.0f l2(shfl+load) %.0f math %.0f ballots+argmax %.0f take1 %.0f level2 %.0f" %
       (p[21], p[21] / jobs, p[16] / r, p[17] / r, p[22] / r, p[18] / r, p[19] / r, p[20] / r))
 print("selector epilogue per job: ring writes %.0f release %.0f registration %.0f" % (p[23] / jobs, p[24] / jobs, p[25] / jobs))
+rr = max(1, p[28])
+print("root rounds %d: l1-load %.0f l2 %.0f per root round; other rounds: l1 %.0f l2 %.0f" % (
+    p[28], p[26] / rr, p[27] / rr, (p[16] - p[26]) / max(1, p[21] - p[28]), (p[17] - p[27]) / max(1, p[21] - p[28])))
