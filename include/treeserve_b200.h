@@ -163,6 +163,10 @@ int ts_step_records(ts_engine* eng, int32_t step, ts_sched_record* dev_records, 
  * run-queue order); keeps this rank's P_i and builds the wave's work list. */
 int ts_step_targets(ts_engine* eng, int32_t step, const ts_sched_record* dev_all_records,
                     void* stream);
+/* An external scheduler's targets instead of ts_step_targets: dev_targets[i]
+ * = P_i for local search i (call after ts_step_records, which marks this
+ * step's admissions as running); running searches get max(1, P_i). */
+int ts_step_set_targets(ts_engine* eng, int32_t step, const int32_t* dev_targets, void* stream);
 /* One wave for every running search with its target P_i: select_leaf →
  * simulate_to_terminal ×min(P_i, budget-completed), then finish_rollout →
  * decide_exit per rollout in launch order, cancel_inflight on exit

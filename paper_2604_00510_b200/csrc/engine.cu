@@ -1637,6 +1637,46 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
   }
 }
 
+// Caller-provided parallelism targets (an external scheduler): P_i for every
+// local search, then the work lists of the wave exactly as compute_targets'
+// phase 5 builds them.  Running searches get max(1, P_i), others 0.
+__global__ void __launch_bounds__(TT) k_set_targets(View v, int step, const int32_t* __restrict__ P) {
+  __shared__ long long shl[264];
+  const int tid = threadIdx.x, nl = v.n_local;
+  if (tid == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
+  const int per = (nl + TT - 1) / TT;
+  const int lo = min(nl, tid * per), hi = min(nl, lo + per);
+  const ts_config& cf = v.cfg;
+  long long nh = 0, nlt = 0;
+  for (int i = lo; i < hi; ++i) {
+    SearchState* st = v.st + i;
+    if (st->state != ST_RUNNING) {
+      st->target = 0;
+      continue;
+    }
+    const int t = max(1, P[i]);
+    st->target = t;
+    if (v.heavy_on && min(t, cf.rollout_budget - st->completed) >= HEAVY_P) ++nh;
+    else ++nlt;
+  }
+  long long sc2[4] = {nh, nlt, 0, 0}, tt2[4];
+  block_scan_add4(sc2, tt2, shl);
+  long long ph = sc2[0], pl = sc2[1];
+  for (int i = lo; i < hi; ++i) {
+    const SearchState* st = v.st + i;
+    if (st->state != ST_RUNNING) continue;
+    if (v.heavy_on && min(st->target, cf.rollout_budget - st->completed) >= HEAVY_P) v.work_heavy[ph++] = i;
+    else v.work[pl++] = i;
+  }
+  if (tid == 0) {
+    v.ctr->work_count = (int)tt2[1];
+    v.ctr->work_next = 0;
+    v.ctr->heavy_count = (int)tt2[0];
+    v.ctr->heavy_next = 0;
+    v.ctr->cur_step = step;
+  }
+}
+
 // Number of requests with arrival_step <= step (arrivals are non-decreasing),
 // by one warp: a 32-way split per round instead of a binary search.
 __device__ int arrived_count(const View& v, int step) {
@@ -4068,6 +4108,18 @@ int ts_step_targets(ts_engine* e, int32_t step, const ts_sched_record* dev_all, 
   k_mt_split<<<1, TT, 0, s>>>(v, step, dev_all, mt);
   e->launches += 8;
   TS_LAUNCH_CHECK(e, "k_mt_*");
+  return TS_OK;
+}
+
+int ts_step_set_targets(ts_engine* e, int32_t step, const int32_t* dev_targets, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!dev_targets || step < 0) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  if ((rc = ensure_step_times(e, step + 1, s))) return rc;
+  View v = make_view(e);
+  k_set_targets<<<1, TT, 0, s>>>(v, step, dev_targets);
+  TS_LAUNCH_CHECK(e, "k_set_targets");
   return TS_OK;
 }
 

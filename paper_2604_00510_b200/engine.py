@@ -164,6 +164,11 @@ class Engine:
         self._check(self.lib.ts_step_targets(self._h, step, ctypes.c_void_p(dev_all_records), self.stream),
                     "ts_step_targets")
 
+    def step_set_targets(self, step: int, dev_targets: int) -> None:
+        """Targets from an external scheduler (int32 device array, one per local search)."""
+        self._check(self.lib.ts_step_set_targets(self._h, step, ctypes.c_void_p(dev_targets), self.stream),
+                    "ts_step_set_targets")
+
     def step_wave(self, step: int) -> None:
         self._check(self.lib.ts_step_wave(self._h, step, self.stream), "ts_step_wave")
 

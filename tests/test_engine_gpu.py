@@ -405,3 +405,52 @@ def test_serving_arrivals_vs_oracle(boost):
         for i in (0, 1234, n - 1):
             assert_tree_equal(eng.tree(i), ref.tree(i), f"serving[{i}]")
     ref.close()
+
+
+def test_external_scheduler_targets():
+    """ts_step_set_targets: the targets k_targets computes, replayed into a second
+    engine through the external-scheduler hook, give the same batch bit for bit;
+    all-ones targets give run_tree_search per problem (the serial fixtures)."""
+    import torch
+
+    case = next(c for c in load("waves") if c["name"] == "c1_M256")
+    recs = load("workloads")[case["workload"]][: len(case["outcomes"])]
+    cfg = config_from_case(case)
+    n = len(recs)
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    records = torch.zeros(n * 16, dtype=torch.uint8, device="cuda")
+    with _engine(cfg) as a, _engine(cfg) as b:
+        a.load(table(recs))
+        b.load(table(recs))
+        for step in range(case["steps"]):
+            for e in (a, b):
+                e.step_counts(step, counts.data_ptr())
+                e.step_admit(step, counts.data_ptr(), 1, 0)
+                e.step_records(step, records.data_ptr())
+            a.step_targets(step, records.data_ptr())
+            t = torch.tensor(a.read_targets(), dtype=torch.int32, device="cuda")
+            b.step_set_targets(step, t.data_ptr())
+            a.step_wave(step)
+            b.step_wave(step)
+        for i in range(n):
+            assert outcome_dict(a.outcomes()[i]) == outcome_dict(b.outcomes()[i]), i
+        for i in (0, 7, 33):
+            assert_tree_equal(b.tree(i), {k: v.tolist() for k, v in a.tree(i).items()}, f"external[{i}]")
+    serial = next(c for c in load("serial") if c["name"] == "c1_default")
+    srecs = load("workloads")[serial["workload"]]
+    scfg = config_from_case(serial)
+    ones = torch.ones(len(srecs), dtype=torch.int32, device="cuda")
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    records = torch.zeros(len(srecs) * 16, dtype=torch.uint8, device="cuda")
+    with _engine(scfg) as e:
+        e.load(table(srecs))
+        for step in range(serial["budget"] + 2):
+            e.step_counts(step, counts.data_ptr())
+            e.step_admit(step, counts.data_ptr(), 1, 0)
+            e.step_records(step, records.data_ptr())
+            e.step_set_targets(step, ones.data_ptr())
+            e.step_wave(step)
+        outs = e.outcomes()
+    for i, want in enumerate(serial["outcomes"]):
+        got = outcome_dict(outs[i])
+        assert {k: got[k] for k in want if k in got} == {k: want[k] for k in want if k in got}, i
