@@ -167,6 +167,10 @@ int ts_step_targets(ts_engine* eng, int32_t step, const ts_sched_record* dev_all
  * = P_i for local search i (call after ts_step_records, which marks this
  * step's admissions as running); running searches get max(1, P_i). */
 int ts_step_set_targets(ts_engine* eng, int32_t step, const int32_t* dev_targets, void* stream);
+/* The Job fields an external scheduler needs (scheduler.py:63-74), per local
+ * search, into device arrays (any may be NULL): running (1/0),
+ * completed_rollouts, best_score.  Call after ts_step_records. */
+int ts_read_jobs(ts_engine* eng, int32_t* dev_running, int32_t* dev_completed, double* dev_best, void* stream);
 /* One wave for every running search with its target P_i: select_leaf →
  * simulate_to_terminal ×min(P_i, budget-completed), then finish_rollout →
  * decide_exit per rollout in launch order, cancel_inflight on exit

@@ -115,7 +115,7 @@ class TsRunStats(ctypes.Structure):
 EXPORTED = (
     "ts_engine_create", "ts_engine_destroy", "ts_last_error", "ts_abi_version",
     "ts_load_problems", "ts_step_counts", "ts_step_admit", "ts_step_records", "ts_step_targets",
-    "ts_step_set_targets", "ts_step_wave", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_read_targets",
+    "ts_step_set_targets", "ts_read_jobs", "ts_step_wave", "ts_run", "ts_read_outcomes", "ts_read_stats", "ts_read_targets",
     "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
     "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
     "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
@@ -249,6 +249,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_step_records": (ctypes.c_int, [vp, i32, vp, vp]),
         "ts_step_targets": (ctypes.c_int, [vp, i32, vp, vp]),
         "ts_step_set_targets": (ctypes.c_int, [vp, i32, vp, vp]),
+        "ts_read_jobs": (ctypes.c_int, [vp, vp, vp, vp, vp]),
         "ts_step_wave": (ctypes.c_int, [vp, i32, vp]),
         "ts_run": (ctypes.c_int, [vp, i32, P(TsRunStats), vp]),
         "ts_read_outcomes": (ctypes.c_int, [vp, P(TsOutcome), i32, vp]),

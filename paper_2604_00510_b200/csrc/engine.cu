@@ -1677,6 +1677,17 @@ __global__ void __launch_bounds__(TT) k_set_targets(View v, int step, const int3
   }
 }
 
+// The scheduler's view of the local searches (Job fields, scheduler.py:63-74)
+// for an external scheduler: running flag, completed_rollouts, best_score.
+__global__ void k_read_jobs(View v, int32_t* running, int32_t* completed, double* best) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v.n_local) return;
+  const SearchState* st = v.st + i;
+  if (running) running[i] = st->state == ST_RUNNING ? 1 : 0;
+  if (completed) completed[i] = st->completed;
+  if (best) best[i] = st->job_best;
+}
+
 // Number of requests with arrival_step <= step (arrivals are non-decreasing),
 // by one warp: a 32-way split per round instead of a binary search.
 __device__ int arrived_count(const View& v, int step) {
@@ -4120,6 +4131,15 @@ int ts_step_set_targets(ts_engine* e, int32_t step, const int32_t* dev_targets, 
   View v = make_view(e);
   k_set_targets<<<1, TT, 0, s>>>(v, step, dev_targets);
   TS_LAUNCH_CHECK(e, "k_set_targets");
+  return TS_OK;
+}
+
+int ts_read_jobs(ts_engine* e, int32_t* dev_running, int32_t* dev_completed, double* dev_best, void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  View v = make_view(e);
+  if (v.n_local == 0) return TS_OK;
+  k_read_jobs<<<(v.n_local + 255) / 256, 256, 0, (cudaStream_t)stream>>>(v, dev_running, dev_completed, dev_best);
+  TS_LAUNCH_CHECK(e, "k_read_jobs");
   return TS_OK;
 }
 

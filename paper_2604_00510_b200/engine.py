@@ -169,6 +169,21 @@ class Engine:
         self._check(self.lib.ts_step_set_targets(self._h, step, ctypes.c_void_p(dev_targets), self.stream),
                     "ts_step_set_targets")
 
+    def read_jobs(self):
+        """(running int32, completed int32, best float64) device tensors of the
+        local searches: the Job fields an external scheduler works on."""
+        import torch
+
+        n = max(1, self.n)
+        dev = torch.device("cuda", self.device)
+        running = torch.empty(n, dtype=torch.int32, device=dev)
+        completed = torch.empty(n, dtype=torch.int32, device=dev)
+        best = torch.empty(n, dtype=torch.float64, device=dev)
+        self._check(self.lib.ts_read_jobs(self._h, ctypes.c_void_p(running.data_ptr()),
+                                          ctypes.c_void_p(completed.data_ptr()), ctypes.c_void_p(best.data_ptr()),
+                                          self.stream), "ts_read_jobs")
+        return running[: self.n], completed[: self.n], best[: self.n]
+
     def step_wave(self, step: int) -> None:
         self._check(self.lib.ts_step_wave(self._h, step, self.stream), "ts_step_wave")
 

@@ -454,3 +454,44 @@ def test_external_scheduler_targets():
     for i, want in enumerate(serial["outcomes"]):
         got = outcome_dict(outs[i])
         assert {k: got[k] for k in want if k in got} == {k: want[k] for k in want if k in got}, i
+
+
+@pytest.mark.parametrize("name", ["c1_M256", "mixed_M200_obs3", "c2_s512_M2048"])
+def test_policy_operator_drives_the_engine(name):
+    """The standalone compute_targets operator (csrc/policy.cu, any run-queue
+    order, device log1p) as the engine's external scheduler: fed the engine's
+    own job state every wave, it reproduces the reference-composed wave oracle."""
+    import torch
+
+    from paper_2604_00510_b200.policy import compute_targets_arrays
+
+    case = next(c for c in load("waves") if c["name"] == name)
+    recs = load("workloads")[case["workload"]][: len(case["outcomes"])]
+    cfg = config_from_case(case)
+    sched = cfg.scheduler
+    n = len(recs)
+    arrivals = case.get("arrival_steps") or [0] * n
+    arr_t = torch.tensor(arrivals, dtype=torch.float64, device="cuda")
+    ids = torch.arange(n, dtype=torch.int64, device="cuda")
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    records = torch.zeros(n * 16, dtype=torch.uint8, device="cuda")
+    with _engine(cfg) as e:
+        e.load(table(recs, case.get("arrival_steps")))
+        for step in range(case["steps"]):
+            e.step_counts(step, counts.data_ptr())
+            e.step_admit(step, counts.data_ptr(), 1, 0)
+            e.step_records(step, records.data_ptr())
+            running, completed, best = e.read_jobs()
+            idx = torch.nonzero(running, as_tuple=False).flatten()  # run queue = index order
+            targets = torch.zeros(n, dtype=torch.int32, device="cuda")
+            if idx.numel():
+                t, _ = compute_targets_arrays(arr_t[idx], best[idx], completed[idx], ids[idx], float(step), sched,
+                                              cfg.scoring.positive_exit_threshold)
+                targets[idx] = t
+            e.step_set_targets(step, targets.data_ptr())
+            e.step_wave(step)
+        outs = e.outcomes()
+    for i, want in enumerate(case["outcomes"]):
+        got = outcome_dict(outs[i])
+        for k in got:
+            assert got[k] == want[k], (name, i, k)
