@@ -506,3 +506,41 @@ def test_device_exit_policy_on_engine_trees_vs_oracle():
         kinds, nes = exit_policy(Forest(trees), sc, True, True)
         assert kinds.tolist() == want_k.tolist()
         assert nes.tolist() == want_ne.tolist()
+
+
+@pytest.mark.gpu
+def test_engine_exit_decisions_agree_with_forest_policy():
+    """The engine decides negative exit with an incremental viable-leaf count;
+    the forest kernels of the standalone policy do the reference's full scan.
+    On the engine's final trees (an exit happens after every expansion of its
+    wave) both must give the engine's exit kind for every search."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.engine import Engine
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+    from paper_2604_00510_b200.scoring import decide_exits
+
+    kinds = {1: ExitKind.POSITIVE_EXIT, 2: ExitKind.NEGATIVE_EXIT, 3: ExitKind.BUDGET_EXHAUSTED}
+    for scoring, b, depth, budget in ((ScoringConfig(), 4, 9, 48),
+                                      (ScoringConfig(futility_bound=FutilityBound.PREFIX_AGGREGATE,
+                                                     accept_threshold=0.35), 3, 7, 40),
+                                      (ScoringConfig(scheme=AggregationScheme.MINIMUM, strict_negative_exit=True,
+                                                     accept_threshold=0.4), 2, 6, 32)):
+        specs = B.make_workload(256, (0.5, 0.3, 0.2), 21, branching=b, depth_ranges={d: (depth, depth)
+                                                                                    for d in B.Difficulty})
+        cfg = SearchConfig(scoring=scoring, scheduler=SchedulerConfig(max_concurrency=512), rollout_budget=budget,
+                           depth_cap=depth + 1, expand_width=b)
+        with Engine(cfg, 0) as eng:
+            eng.load(B.problem_table(specs))
+            eng.run()
+            outs = eng.outcomes()
+            trees = []
+            for i, o in enumerate(outs):
+                d = eng.tree(i)
+                d["best_score"] = o.best_score if o.best_len > 0 else None
+                d["completed_rollouts"] = o.rollouts_completed
+                d["rollout_budget"] = budget
+                trees.append(d)
+        exhausted = [o.exit_kind == 3 and o.rollouts_completed < budget for o in outs]
+        got = decide_exits(trees, scoring, True, True, exhausted)
+        assert [g.kind for g in got] == [kinds[o.exit_kind] for o in outs]
