@@ -57,15 +57,18 @@ enum { ST_PENDING = 0, ST_RUNNING = 1, ST_FINISHED = 2 };
 
 // Per-search state (SoA would split one warp's scalar reads over many lines;
 // a search's row is touched only by its owning warp and the scheduler).
-struct SearchState {
-  int32_t state, completed, launched, cancelled;
+struct __align__(16) SearchState {
+  // the scheduler's inputs share the first 16 bytes (one vector load in k_sched)
+  int32_t state, completed;
+  double job_best;  // Job.best_score (scheduler.py:71, refreshed by on_rollout_complete)
+  int32_t launched, cancelled;
   int32_t nodes, viable, best_term, exit_kind;
-  int32_t exit_step, admit_step, status, target;
+  int32_t exit_step, admit_step, status, _pad;
   int64_t tokens;
   double best;      // best trajectory score, valid iff best_term >= 0
-  double job_best;  // Job.best_score (scheduler.py:71, refreshed by on_rollout_complete)
   unsigned long long t_exit;  // %globaltimer at the exit decision
 };
+static_assert(sizeof(SearchState) == 80, "SearchState layout");
 
 struct Counters {
   long long running, head, finished, last_exit_step;
@@ -98,6 +101,7 @@ struct View {
   Counters* ctr;
   int32_t* work;           // this wave's running local searches (single-warp mode)
   int32_t* work_heavy;     // this wave's searches for the pipelined CTA mode
+  int32_t* tgt;            // P_i of this wave per local search (compute_targets)
   int32_t heavy_on;        // pipelined mode available (uniform width 2/4/8)
   int32_t heavy_sync;      // diagnostics: commit every job before the next selection
   int32_t max_arrival;     // last arrival step of the loaded requests
@@ -174,6 +178,24 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// TS_SCHED_PROF (diagnostics build): %globaltimer phase stamps of the graph
+// loop in Counters::prof, read by tools/sched_prof.py.  Slots: 0 wave end ->
+// k_sched start, 1 wave span, 2 k_sched end -> first wave CTA, 3-9 k_sched
+// phases, 10 passes, 20/21/22 the current wave's last end / first start and
+// the last k_sched end.
+#ifdef TS_SCHED_PROF
+#define SP_MARK(slot, t0)                                                       \
+  do {                                                                          \
+    if (threadIdx.x == 0) {                                                     \
+      const unsigned long long t_ = globaltimer();                              \
+      atomicAdd(&v.ctr->prof[slot], t_ - (t0));                                 \
+      (t0) = t_;                                                                \
+    }                                                                           \
+  } while (0)
+#else
+#define SP_MARK(slot, t0) do { } while (0)
+#endif
+
 // ---- kernels -------------------------------------------------------------------
 
 // SearchTree.__init__ (tree.py:120-128): bare root, reward 1.0, prior 1.0.
@@ -198,7 +220,8 @@ __global__ void k_init(View v) {
   z.exit_step = -1;
   z.admit_step = -1;
   z.status = TS_OK;
-  z.target = 0;
+  z._pad = 0;
+  v.tgt[s] = 0;
   z.tokens = 0;
   z.best = 0.0;
   z.job_best = 0.0;
@@ -284,6 +307,7 @@ constexpr int HEAVY_P = 8;  // rollouts in one wave from which a search runs in 
 constexpr int HBITS_WORDS = 2048;  // run-queue slots with a pipelined-mode flag bit (65536)
 constexpr int SREC_MAX = 4096;     // k_sched keeps the records of up to this many searches in shared memory
 constexpr int RUNCAP = 1536;  // runs per list kept in shared memory
+constexpr size_t TGT_SCR = (96 + 96 + 32 + 64) * 8;  // targets_block scan scratch (bytes)
 
 // Block-wide exclusive scan (+) of one value per thread; returns the prefix,
 // writes the block total.  All threads must call.
@@ -404,183 +428,309 @@ __device__ __forceinline__ int runs_lower(const double* runS, int nr, double s) 
 // below); it is computed exactly in 128-bit fixed point.
 // rec holds n records in global run-queue order; records [glo, ghi) are this
 // engine's searches base + (i - glo).
+// Exclusive (+) scans of N values per thread with ONE barrier: lane 31 of each
+// warp publishes the warp's inclusive totals, then every warp rescans the 32
+// warp totals itself instead of waiting for one warp to publish offsets.  `sh`
+// (32*N long longs) may be reused two calls later: the intervening call's
+// barrier orders every read of this one before the next write.
+template <int N>
+__device__ __forceinline__ void scan1_add(long long (&x)[N], long long (&tot)[N], long long* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long inc[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    inc[q] = x[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(FULL, inc[q], o);
+      if (lane >= o) inc[q] += y;
+    }
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int q = 0; q < N; ++q) sh[q * 32 + wid] = inc[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    const long long w = lane < TT / 32 ? sh[q * 32 + lane] : 0;
+    long long wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(FULL, wi, o);
+      if (lane >= o) wi += y;
+    }
+    tot[q] = __shfl_sync(FULL, wi, 31);
+    x[q] = __shfl_sync(FULL, wi - w, wid) + inc[q] - x[q];
+  }
+}
+
+// compute_targets over the global run queue (records in global id order).
+// The reference sorts ungated jobs by (-S, arrival, id).  Because arrivals
+// are non-decreasing in run-queue order and S = log1p(now - arrival) + boost,
+// the unboosted and the boosted jobs each form a list already sorted by
+// (-S, id) in run-queue order; the sorted order is their merge.  Within a
+// list, equal scores form runs with one `want` each; a job's sorted position
+// and the Σ(want-1) before it follow from run prefix sums plus a binary
+// search in the other list.  The clamp loop (scheduler.py:169-180) then has
+// the closed form extra_k = clamp(R - Σ_{j<k}(want_j-1), 0, want_k-1), and the
+// round-robin leftover gives floor(R'/U) + [pos < R' mod U] (181-186).
+// The score sum Σ S (scheduler.py:165, CPython's Neumaier sum) equals the
+// correctly rounded exact sum when all compensation terms are exact (checked
+// below); it is computed exactly in 128-bit fixed point.
+// rec holds n records in global run-queue order; records [glo, ghi) are this
+// engine's searches base + (i - glo).  Thread t owns records
+// [t*ceil(n/TT), ...) in every pass, so a caller that wrote them with the same
+// partition needs no barrier before the call.  Six barriers in all: the
+// counts/sum/min scan, the run-count scan, the run table, the want-prefix
+// scan, the run prefixes, the work-list scan.
 __device__ void targets_block(const View& v, int step, const ts_sched_record* rec, int n, int glo, int ghi,
                               int base) {
   extern __shared__ __align__(16) unsigned char smem[];
-  long long* shl = (long long*)smem;                 // 264 long longs of scan scratch
-  double* shd = (double*)(smem + 264 * 8);           // 80 doubles
-  u128* shq = (u128*)(smem + 344 * 8);               // 32 u128
-  uint32_t* hbits = (uint32_t*)(smem + 344 * 8 + 32 * 16);  // pipelined-mode flag per run-queue slot
-  double* s_runS = (double*)(smem + 344 * 8 + 32 * 16 + HBITS_WORDS * 4);
+  long long* shA = (long long*)smem;                  // 96: scan scratch (even calls)
+  long long* shB = shA + 96;                          // 96: scan scratch (odd calls)
+  long long* shF = shB + 96;                          // 32: per-warp fallback flags
+  double* shD = (double*)(shF + 32);                  // 64: per-warp list minima
+  u128* shq = (u128*)(smem + TGT_SCR);                // 32: per-warp partial sums
+  uint32_t* hbits = (uint32_t*)(smem + TGT_SCR + 32 * 16);  // pipelined-mode flag per run-queue slot
+  double* s_runS = (double*)(smem + TGT_SCR + 32 * 16 + HBITS_WORDS * 4);
   int32_t* s_runStart = (int32_t*)(s_runS + 2 * RUNCAP);
   long long* s_runWant = (long long*)(s_runStart + 2 * RUNCAP);
   long long* s_runPW = s_runWant + 2 * RUNCAP;
   __shared__ double sT;
-  __shared__ int sBad;
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const ts_config& cf = v.cfg;
   if (tid == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
+#ifdef TS_SCHED_PROF
+  unsigned long long sp_t = globaltimer();
+#endif
   const int per = (n + TT - 1) / TT;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
   for (int w = tid; w < (ghi - glo + 31) / 32 && w < HBITS_WORDS; w += TT) hbits[w] = 0u;
 
-  // phase 1: counts, exact score sum, list positions
+  // phase 1: counts, exact score sum, list positions, list minima before each
+  // thread (the lists are non-increasing, so the last score before a thread's
+  // range is the minimum over the threads before it)
   u128 fx = 0;
   bool bad = false;
-  long long nrun = 0, cnt0 = 0, cnt1 = 0, nloc = 0;
+  long long c3[3] = {0, 0, 0};  // running, gated-in unboosted (list 0), boosted (list 1)
   double min0 = INFINITY, min1 = INFINITY;
   for (int i = lo; i < hi; ++i) {
-    ts_sched_record r = rec[i];
+    const ts_sched_record r = rec[i];
     if (!(r.flags & 1u)) continue;
-    ++nrun;
-    if (i >= glo && i < ghi) ++nloc;
+    ++c3[0];
     u128 q;
     if (to_fixed(r.score, q)) fx += q;
     else bad = true;
     if (r.flags & 2u) {
-      if (r.flags & 4u) { ++cnt1; min1 = fmin(min1, r.score); }
-      else { ++cnt0; min0 = fmin(min0, r.score); }
+      if (r.flags & 4u) { ++c3[2]; min1 = fmin(min1, r.score); }
+      else { ++c3[1]; min0 = fmin(min0, r.score); }
     }
   }
-  long long sc4[4] = {nrun, cnt0, cnt1, nloc}, tt4[4];
-  block_scan_add4(sc4, tt4, shl);
-  const long long tot_run = tt4[0], len0 = tt4[1], len1 = tt4[2], tot_loc = tt4[3];
-  const long long pos0 = sc4[1], pos1 = sc4[2], wpos = sc4[3];
-  (void)tot_loc;
-  // u128 reduction
+  long long t3[3];
+  double prev0, prev1;
+  u128 fsum;
+  bool anybad;
   {
-    const int lane = tid & 31, wid = tid >> 5;
+    long long inc[3];
+    double m0 = min0, m1 = min1;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) inc[q] = c3[q];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const long long y = __shfl_up_sync(FULL, inc[q], o);
+        if (lane >= o) inc[q] += y;
+      }
+      const double y0 = __shfl_up_sync(FULL, m0, o), y1 = __shfl_up_sync(FULL, m1, o);
+      if (lane >= o) { m0 = fmin(m0, y0); m1 = fmin(m1, y1); }
+    }
+    double e0 = __shfl_up_sync(FULL, m0, 1), e1 = __shfl_up_sync(FULL, m1, 1);
+    if (lane == 0) e0 = e1 = INFINITY;
     u128 x = fx;
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      uint64_t h = __shfl_down_sync(FULL, (uint64_t)(x >> 64), o);
-      uint64_t l = __shfl_down_sync(FULL, (uint64_t)x, o);
+      const uint64_t h = __shfl_xor_sync(FULL, (uint64_t)(x >> 64), o);
+      const uint64_t l = __shfl_xor_sync(FULL, (uint64_t)x, o);
       x += ((u128)h << 64) | l;
     }
-    if (lane == 0) shq[wid] = x;
-    if (tid == 0) sBad = 0;
-    __syncthreads();
-    if (bad) sBad = 1;
-    __syncthreads();
-    if (tid == 0) {
-      u128 s = 0;
-      for (int w = 0; w < TT / 32; ++w) s += shq[w];
-      double T;
-      bool fallback = sBad != 0;
-      if (!fallback) {
-        T = fixed_to_double(s);
-        // compensation exactness: n * ulp(2T) < 2^-10
-        double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
-        if ((double)tot_run * u2 >= 0x1p-10) fallback = true;
-      }
-      if (fallback) {  // sequential Neumaier sum in run-queue order
-        double f = 0.0, c = 0.0;
-        bool first = true;
-        for (int i = 0; i < n; ++i) {
-          ts_sched_record r = rec[i];
-          if (!(r.flags & 1u)) continue;
-          double x2 = r.score;
-          if (first) { f = x2; first = false; continue; }
-          double t = f + x2;
-          if (fabs(f) >= fabs(x2)) c += (f - t) + x2;
-          else c += (x2 - t) + f;
-          f = t;
-        }
-        if (c != 0.0 && isfinite(c)) f += c;
-        T = f;
-        atomicAdd(&v.ctr->sum_fallbacks, 1);
-      }
-      sT = T;
+    const bool wbad = __any_sync(FULL, bad);
+    if (lane == 31) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) shA[q * 32 + wid] = inc[q];
+      shD[wid] = m0;
+      shD[32 + wid] = m1;
+    }
+    if (lane == 0) {
+      shq[wid] = x;
+      shF[wid] = wbad;
     }
     __syncthreads();
+    // every warp: scans of the warp totals, the block sum, the fallback flag
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const long long w = shA[q * 32 + lane];
+      long long wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(FULL, wi, o);
+        if (lane >= o) wi += y;
+      }
+      t3[q] = __shfl_sync(FULL, wi, 31);
+      c3[q] = __shfl_sync(FULL, wi - w, wid) + inc[q] - c3[q];
+    }
+    double w0 = shD[lane], w1 = shD[32 + lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y0 = __shfl_up_sync(FULL, w0, o), y1 = __shfl_up_sync(FULL, w1, o);
+      if (lane >= o) { w0 = fmin(w0, y0); w1 = fmin(w1, y1); }
+    }
+    const double b0 = __shfl_sync(FULL, w0, (wid + 31) & 31), b1 = __shfl_sync(FULL, w1, (wid + 31) & 31);
+    prev0 = wid == 0 ? e0 : fmin(b0, e0);
+    prev1 = wid == 0 ? e1 : fmin(b1, e1);
+    fsum = shq[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t h = __shfl_xor_sync(FULL, (uint64_t)(fsum >> 64), o);
+      const uint64_t l = __shfl_xor_sync(FULL, (uint64_t)fsum, o);
+      fsum += ((u128)h << 64) | l;
+    }
+    anybad = __any_sync(FULL, shF[lane] != 0);
   }
-  const double T = sT;
+  const long long tot_run = t3[0], len0 = t3[1], len1 = t3[2];
+  const long long pos0 = c3[1], pos1 = c3[2];
+  double T = 0.0;
+  bool fallback = anybad;
+  if (!fallback) {
+    T = fixed_to_double(fsum);
+    // compensation exactness: n * ulp(2T) < 2^-10
+    const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
+    if ((double)tot_run * u2 >= 0x1p-10) fallback = true;
+  }
+  if (fallback) {  // block-uniform: sequential Neumaier sum in run-queue order
+    if (tid == 0) {
+      double f = 0.0, c = 0.0;
+      bool first = true;
+      for (int i = 0; i < n; ++i) {
+        const ts_sched_record r = rec[i];
+        if (!(r.flags & 1u)) continue;
+        const double x2 = r.score;
+        if (first) { f = x2; first = false; continue; }
+        const double t = f + x2;
+        if (fabs(f) >= fabs(x2)) c += (f - t) + x2;
+        else c += (x2 - t) + f;
+        f = t;
+      }
+      if (c != 0.0 && isfinite(c)) f += c;
+      sT = f;
+      atomicAdd(&v.ctr->sum_fallbacks, 1);
+    }
+    __syncthreads();
+    T = sT;
+  }
+  SP_MARK(5, sp_t);
   const long long M = cf.max_concurrency;
   const long long R = M - tot_run;
   // no free slot or nobody past the observation gate: every running job gets 1
   const bool boost_on = cf.boosting_enabled != 0 && tot_run > 0 && R > 0 && len0 + len1 > 0;
 
   // phase 2: runs of equal score in each list (lists are non-increasing)
-  double prev0 = block_scan_min(min0, shd);
-  double prev1 = block_scan_min(min1, shd);
-  long long rs0 = 0, rs1 = 0;
+  long long rid[2] = {0, 0}, nrr[2] = {0, 0};
   if (boost_on) {
     double p0 = prev0, p1 = prev1;
     for (int i = lo; i < hi; ++i) {
-      ts_sched_record r = rec[i];
+      const ts_sched_record r = rec[i];
       if ((r.flags & 3u) != 3u) continue;
-      if (r.flags & 4u) { if (r.score != p1) ++rs1; if (r.score > p1) v.ctr->sched_error = 1; p1 = r.score; }
-      else { if (r.score != p0) ++rs0; if (r.score > p0) v.ctr->sched_error = 1; p0 = r.score; }
+      if (r.flags & 4u) { if (r.score != p1) ++rid[1]; if (r.score > p1) v.ctr->sched_error = 1; p1 = r.score; }
+      else { if (r.score != p0) ++rid[0]; if (r.score > p0) v.ctr->sched_error = 1; p0 = r.score; }
     }
+    scan1_add<2>(rid, nrr, shB);
   }
-  long long nr0, nr1;
-  long long rid0 = block_scan_add(rs0, &nr0, shl);
-  long long rid1 = block_scan_add(rs1, &nr1, shl);
+  const long long nr0 = nrr[0], nr1 = nrr[1];
   const bool in_smem = nr0 <= RUNCAP && nr1 <= RUNCAP;
   double* runS = in_smem ? s_runS : v.g_runS;
   int32_t* runStart = in_smem ? s_runStart : v.g_runStart;
   long long* runWant = in_smem ? s_runWant : v.g_runWant;
   long long* runPW = in_smem ? s_runPW : v.g_runPW;
   const int stride = in_smem ? RUNCAP : v.n_global;  // list 1 offset
-  if (boost_on) {
-    double p0 = prev0, p1 = prev1;
-    long long q0 = pos0, q1 = pos1, k0 = rid0, k1 = rid1;
-    for (int i = lo; i < hi; ++i) {
-      ts_sched_record r = rec[i];
-      if ((r.flags & 3u) != 3u) continue;
-      if (r.flags & 4u) {
-        if (r.score != p1) { runS[stride + k1] = r.score; runStart[stride + k1] = (int)q1; ++k1; }
-        p1 = r.score;
-        ++q1;
-      } else {
-        if (r.score != p0) { runS[k0] = r.score; runStart[k0] = (int)q0; ++k0; }
-        p0 = r.score;
-        ++q0;
-      }
-    }
-  }
-  __syncthreads();
-  // phase 3: want per run, prefix Σ cnt*(want-1) over runs
   long long tw0 = 0, tw1 = 0;
-  for (int b = 0; b < 2 && boost_on; ++b) {
-    const long long nr = b ? nr1 : nr0;
-    const long long len = b ? len1 : len0;
-    const int off = b ? stride : 0;
-    const int per2 = (int)((nr + TT - 1) / TT);
-    const int a0 = (int)min((long long)tid * per2, nr), a1 = (int)min((long long)a0 + per2, nr);
-    long long loc = 0;
-    for (int k = a0; k < a1; ++k) {
-      double s = runS[off + k];
-      long long want = 1;
-      if (T > 0.0) {
-        double f = floor(s / T * (double)M);
-        want = f > 1.0 ? (long long)f : 1;
+  if (boost_on) {
+    {
+      double p0 = prev0, p1 = prev1;
+      long long q0 = pos0, q1 = pos1, k0 = rid[0], k1 = rid[1];
+      for (int i = lo; i < hi; ++i) {
+        const ts_sched_record r = rec[i];
+        if ((r.flags & 3u) != 3u) continue;
+        if (r.flags & 4u) {
+          if (r.score != p1) { runS[stride + k1] = r.score; runStart[stride + k1] = (int)q1; ++k1; }
+          p1 = r.score;
+          ++q1;
+        } else {
+          if (r.score != p0) { runS[k0] = r.score; runStart[k0] = (int)q0; ++k0; }
+          p0 = r.score;
+          ++q0;
+        }
       }
-      long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
-      runWant[off + k] = want;
-      loc += cnt * (want - 1);
     }
-    long long tw;
-    long long pre = block_scan_add(loc, &tw, shl);
-    for (int k = a0; k < a1; ++k) {
-      runPW[off + k] = pre;
-      long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
-      pre += cnt * (runWant[off + k] - 1);
+    __syncthreads();
+    SP_MARK(6, sp_t);
+    // phase 3: want per run, prefix Σ cnt*(want-1) over runs (both lists in one scan)
+    long long pre[2] = {0, 0}, tw[2];
+    int a0[2], a1[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const long long nr = b ? nr1 : nr0;
+      const long long len = b ? len1 : len0;
+      const int off = b ? stride : 0;
+      const int per2 = (int)((nr + TT - 1) / TT);
+      a0[b] = (int)min((long long)tid * per2, nr);
+      a1[b] = (int)min((long long)a0[b] + per2, nr);
+      for (int k = a0[b]; k < a1[b]; ++k) {
+        const double sc = runS[off + k];
+        long long want = 1;
+        if (T > 0.0) {
+          const double f = floor(sc / T * (double)M);
+          want = f > 1.0 ? (long long)f : 1;
+        }
+        const long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
+        runWant[off + k] = want;
+        pre[b] += cnt * (want - 1);
+      }
     }
-    if (b) tw1 = tw; else tw0 = tw;
+    scan1_add<2>(pre, tw, shA);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const long long nr = b ? nr1 : nr0;
+      const long long len = b ? len1 : len0;
+      const int off = b ? stride : 0;
+      long long q = pre[b];
+      for (int k = a0[b]; k < a1[b]; ++k) {
+        runPW[off + k] = q;
+        const long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
+        q += cnt * (runWant[off + k] - 1);
+      }
+    }
+    tw0 = tw[0];
+    tw1 = tw[1];
+    __syncthreads();
   }
-  __syncthreads();
-  // phase 4: targets
+  SP_MARK(7, sp_t);
+  // phase 4: targets; each thread counts its local searches per work list
   const long long U = len0 + len1;
   long long Rp = R - (tw0 + tw1);
   if (Rp < 0) Rp = 0;
+  const long long rr_q = U > 0 ? Rp / U : 0, rr_r = U > 0 ? Rp % U : 0;
+  long long nl2[2] = {0, 0};  // pipelined-mode, single-warp
   {
-    long long q0 = pos0, q1 = pos1, k0 = rid0 - 1, k1 = rid1 - 1;
+    long long q0 = pos0, q1 = pos1, k0 = rid[0] - 1, k1 = rid[1] - 1;
     double p0 = prev0, p1 = prev1;
     for (int i = lo; i < hi; ++i) {
-      ts_sched_record r = rec[i];
+      const ts_sched_record r = rec[i];
+      const bool local = i >= glo && i < ghi;
       if (!(r.flags & 1u)) {
-        if (i >= glo && i < ghi) v.st[base + i - glo].target = 0;
+        if (local) v.tgt[base + i - glo] = 0;
         continue;
       }
       long long tgt = 1;
@@ -595,11 +745,11 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
         // cross list: elements with S' > S, or S' == S and smaller id
         const long long nro = b ? nr0 : nr1, leno = b ? len0 : len1, two = b ? tw0 : tw1;
         const long long obefore = b ? q0 : q1;  // other-list elements with id < i
-        int kk = runs_lower(runS + oo, (int)nro, r.score);
+        const int kk = runs_lower(runS + oo, (int)nro, r.score);
         long long c, cw;
         if (kk < nro && runS[oo + kk] == r.score) {
-          long long st0 = runStart[oo + kk];
-          long long cntk = (kk + 1 < nro ? runStart[oo + kk + 1] : leno) - st0;
+          const long long st0 = runStart[oo + kk];
+          const long long cntk = (kk + 1 < nro ? runStart[oo + kk + 1] : leno) - st0;
           long long part = obefore - st0;
           if (part < 0) part = 0;
           if (part > cntk) part = cntk;
@@ -617,50 +767,47 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
         long long extra = R - before;
         if (extra < 0) extra = 0;
         if (extra > want - 1) extra = want - 1;
-        long long rr = 0;
-        if (U > 0) rr = Rp / U + (spos < Rp % U ? 1 : 0);
-        tgt = 1 + extra + rr;
-      } else if ((r.flags & 2u) == 0 && boost_on) {
-        // gated: stays serial; advance nothing
+        tgt = 1 + extra + rr_q + (spos < rr_r ? 1 : 0);
       }
-      if (i >= glo && i < ghi) {
-        v.st[base + i - glo].target = (int)tgt;
+      if (local) {
+        v.tgt[base + i - glo] = (int)tgt;
         // rollouts this wave = min(P_i, budget - completed); `_pad` carries completed
-        if (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P)
+        if (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P) {
           atomicOr(&hbits[(i - glo) >> 5], 1u << ((i - glo) & 31));
+          ++nl2[0];
+        } else {
+          ++nl2[1];
+        }
       }
     }
   }
-  (void)wpos;
-  __syncthreads();
-  // phase 5: split the local running searches into the single-warp and the
-  // pipelined (many rollouts this wave) work lists, in run-queue order
-  long long nh = 0, nlt = 0;
-  const int loc_lo = max(lo, glo) - glo, loc_hi = max(loc_lo, min(hi, ghi) - glo);
-  for (int i = loc_lo; i < loc_hi; ++i) {
-    if (!(rec[i + glo].flags & 1u)) continue;
-    if ((hbits[i >> 5] >> (i & 31)) & 1u) ++nh;
-    else ++nlt;
-  }
-  long long sc2[4] = {nh, nlt, 0, 0}, tt2[4];
-  block_scan_add4(sc2, tt2, shl);
-  long long ph = sc2[0], pl = sc2[1];
-  for (int i = loc_lo; i < loc_hi; ++i) {
-    if (!(rec[i + glo].flags & 1u)) continue;
-    if ((hbits[i >> 5] >> (i & 31)) & 1u) v.work_heavy[ph++] = base + i;
-    else v.work[pl++] = base + i;
+  SP_MARK(8, sp_t);
+  // phase 5: the local running searches split into the single-warp and the
+  // pipelined (many rollouts this wave) work lists, in run-queue order.  A
+  // thread reads back only the flag bits it set itself.
+  long long tl2[2];
+  scan1_add<2>(nl2, tl2, shB);
+  {
+    long long ph = nl2[0], pl = nl2[1];
+    const int loc_lo = max(lo, glo) - glo, loc_hi = max(loc_lo, min(hi, ghi) - glo);
+    for (int i = loc_lo; i < loc_hi; ++i) {
+      if (!(rec[i + glo].flags & 1u)) continue;
+      if ((hbits[i >> 5] >> (i & 31)) & 1u) v.work_heavy[ph++] = base + i;
+      else v.work[pl++] = base + i;
+    }
   }
   if (tid == 0) {
-    v.ctr->work_count = (int)tt2[1];
+    v.ctr->work_count = (int)tl2[1];
     v.ctr->work_next = 0;
-    v.ctr->heavy_count = (int)tt2[0];
+    v.ctr->heavy_count = (int)tl2[0];
     v.ctr->heavy_next = 0;
     v.ctr->cur_step = step;
   }
+  SP_MARK(9, sp_t);
 }
 
 __device__ __forceinline__ size_t targets_smem_dev() {
-  return 344 * 8 + 32 * 16 + HBITS_WORDS * 4 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8);
+  return TGT_SCR + 32 * 16 + HBITS_WORDS * 4 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8);
 }
 
 __global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
@@ -1118,7 +1265,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_targets(View v, const ts_sched_reco
     const bool local = i >= glo && i < ghi;
     if (!(r.flags & 1u)) {
       if (local) {
-        v.st[i - glo].target = 0;
+        v.tgt[i - glo] = 0;
         L.hflag[i - glo] = 0;
       }
       continue;
@@ -1169,7 +1316,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_targets(View v, const ts_sched_reco
       }
     }
     if (local) {
-      v.st[i - glo].target = (int)tgt;
+      v.tgt[i - glo] = (int)tgt;
       L.hflag[i - glo] = (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P) ? 1 : 0;
     }
   }
@@ -1538,7 +1685,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
       const bool local = i >= glo && i < ghi;
       if (!(r.flags & 1u)) {
         if (local) {
-          v.st[i - glo].target = 0;
+          v.tgt[i - glo] = 0;
           L.hflag[i - glo] = 0;
         }
         continue;
@@ -1589,7 +1736,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
         }
       }
       if (local) {
-        v.st[i - glo].target = (int)tgt;
+        v.tgt[i - glo] = (int)tgt;
         const bool hv = v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P;
         L.hflag[i - glo] = hv ? 1 : 0;
         if (hv) ++nh;
@@ -1651,11 +1798,11 @@ __global__ void __launch_bounds__(TT) k_set_targets(View v, int step, const int3
   for (int i = lo; i < hi; ++i) {
     SearchState* st = v.st + i;
     if (st->state != ST_RUNNING) {
-      st->target = 0;
+      v.tgt[i] = 0;
       continue;
     }
     const int t = max(1, P[i]);
-    st->target = t;
+    v.tgt[i] = t;
     if (v.heavy_on && min(t, cf.rollout_budget - st->completed) >= HEAVY_P) ++nh;
     else ++nlt;
   }
@@ -1665,7 +1812,7 @@ __global__ void __launch_bounds__(TT) k_set_targets(View v, int step, const int3
   for (int i = lo; i < hi; ++i) {
     const SearchState* st = v.st + i;
     if (st->state != ST_RUNNING) continue;
-    if (v.heavy_on && min(st->target, cf.rollout_budget - st->completed) >= HEAVY_P) v.work_heavy[ph++] = i;
+    if (v.heavy_on && min(v.tgt[i], cf.rollout_budget - st->completed) >= HEAVY_P) v.work_heavy[ph++] = i;
     else v.work[pl++] = i;
   }
   if (tid == 0) {
@@ -1713,8 +1860,16 @@ __device__ int arrived_count(const View& v, int step) {
 // {k_sched, k_wave} runs a whole batch without host round trips.
 __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cudaGraphConditionalHandle cond,
                                               int use_cond) {
-  __shared__ int s_go;
+  __shared__ int s_go, s_min;
   Counters* c = v.ctr;
+#ifdef TS_SCHED_PROF
+  unsigned long long sp_t = globaltimer();
+  if (threadIdx.x == 0 && c->prof[20]) {
+    c->prof[0] += sp_t - c->prof[20];
+    c->prof[1] += c->prof[20] - c->prof[21];
+    c->prof[2] += c->prof[21] - c->prof[22];
+  }
+#endif
   const int step = (int)c->step;
   int arrived = 0;
   if (threadIdx.x < 32) arrived = arrived_count(v, step);
@@ -1730,17 +1885,22 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
       c->admit_hi = c->head + q;
       c->head += q;
       c->running += q;
+      s_min = (int)c->head;
     } else {
       c->work_count = 0;
       c->work_next = 0;
       c->heavy_count = 0;
       c->heavy_next = 0;
       if (use_cond) cudaGraphSetConditional(cond, 0);
+#ifdef TS_SCHED_PROF
+      c->prof[20] = 0;
+#endif
     }
     s_go = go;
   }
   __syncthreads();
   if (!s_go) return;
+  SP_MARK(3, sp_t);
   const long long alo = c->admit_lo, ahi = c->admit_hi;
   const ts_config& cf = v.cfg;
   // the run queue is the window [win_lo, head): searches below win_lo have
@@ -1750,41 +1910,70 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
   // one GPU: the window's records stay in shared memory when they fit
   extern __shared__ __align__(16) unsigned char smem[];
   ts_sched_record* srec = nw <= SREC_MAX ? (ts_sched_record*)(smem + targets_smem_dev()) : rec;
-  __shared__ int s_min;
-  if (threadIdx.x == 0) s_min = whi;
-  __syncthreads();
+  // Records.  targets_block gives thread t the records [t*per, (t+1)*per), so
+  // warp w's threads own the chunk [32*w*per, 32*(w+1)*per): the warp fills
+  // its chunk with lane-consecutive (coalesced) loads, four in flight per
+  // lane, and a warp barrier replaces a block barrier before the call.
+  const int per = (nw + TT - 1) / TT;
+  const int lane = threadIdx.x & 31;
+  const int c0 = min(nw, (int)(threadIdx.x >> 5) * 32 * per), c1 = min(nw, c0 + 32 * per);
   int my_min = whi;
-#pragma unroll 4
-  for (int i = wlo + threadIdx.x; i < whi; i += TT) {
-    SearchState* st = v.st + i;
-    int state = st->state;
-    if (i >= alo && i < ahi) {
-      state = ST_RUNNING;
-      st->state = ST_RUNNING;
-      st->admit_step = step;
+  for (int j0 = c0; j0 < c1; j0 += 4 * 32) {
+    int state[4], done[4], arr[4];
+    double jb[4], lt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * 32 + lane, i = wlo + j;
+      state[u] = ST_PENDING;
+      done[u] = arr[u] = 0;
+      jb[u] = 0.0;
+      if (j < c1) {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(v.st + i);
+        state[u] = (i >= alo && i < ahi) ? (int)ST_RUNNING : (int)(uint32_t)w.x;
+        done[u] = (int)(uint32_t)(w.x >> 32);
+        jb[u] = __longlong_as_double((long long)w.y);
+        arr[u] = v.arrival[i];
+      }
     }
-    ts_sched_record r;
-    r.score = 0.0;
-    r.flags = 0;
-    r._pad = 0;
-    if (state == ST_RUNNING) {
-      my_min = min(my_min, i);
-      const double ratio = st->job_best / cf.positive_exit_threshold;
-      const bool boosted = ratio > cf.proximity;
-      r.score = v.log1p_tab[step - v.arrival[i]] + (boosted ? cf.beta : 0.0);
-      const int done = st->completed;
-      r.flags = 1u | (done >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
-      r._pad = (uint32_t)done;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) lt[u] = state[u] == ST_RUNNING ? v.log1p_tab[step - arr[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * 32 + lane, i = wlo + j;
+      if (j >= c1) break;
+      if (i >= alo && i < ahi) {
+        v.st[i].state = ST_RUNNING;
+        v.st[i].admit_step = step;
+      }
+      ts_sched_record r;
+      r.score = 0.0;
+      r.flags = 0;
+      r._pad = 0;
+      if (state[u] == ST_RUNNING) {
+        my_min = min(my_min, i);
+        const double ratio = jb[u] / cf.positive_exit_threshold;
+        const bool boosted = ratio > cf.proximity;
+        r.score = lt[u] + (boosted ? cf.beta : 0.0);
+        r.flags = 1u | (done[u] >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
+        r._pad = (uint32_t)done[u];
+      }
+      srec[j] = r;
     }
-    srec[i - wlo] = r;
   }
+  __syncwarp();
   for (int o = 16; o > 0; o >>= 1) my_min = min(my_min, __shfl_xor_sync(FULL, my_min, o));
   if ((threadIdx.x & 31) == 0) atomicMin(&s_min, my_min);
-  __syncthreads();
+  SP_MARK(4, sp_t);
   targets_block(v, step, srec, nw, 0, nw, wlo);
   if (threadIdx.x == 0) {
     c->win_lo = s_min;  // no running search below this index
     c->step = step + 1;
+#ifdef TS_SCHED_PROF
+    c->prof[10] += 1;
+    c->prof[20] = 0;
+    c->prof[21] = ~0ull;
+    c->prof[22] = globaltimer();
+#endif
   }
 }
 
@@ -1855,7 +2044,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
   int launched = S->launched, cancelled = S->cancelled;
   int status = TS_OK;
   const int budget = cf.rollout_budget;
-  const int count = min(S->target, budget - completed);
+  const int count = min(v.tgt[s], budget - completed);
   const bool multi = count > 1;
   int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
   double* SSs = v.ss + (size_t)s * budget;
@@ -2286,6 +2475,9 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
   double* s_raw = wsm + (size_t)warp * 2 * 32 * WS;
   double* s_rew = s_raw + 32 * WS;
   WaveStats ws = {0, 0, 0, 0, 0, 0};
+#ifdef TS_SCHED_PROF
+  if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
+#endif
   const int count = v.ctr->work_count;
   if (step < 0) step = v.ctr->cur_step;
   for (;;) {
@@ -2295,6 +2487,9 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
     if (item >= count) break;
     search_wave<NSLOT, WT>(v, v.work[item], step, ws, s_raw, s_rew);
   }
+#ifdef TS_SCHED_PROF
+  if (lane == 0) atomicMax(&v.ctr->prof[20], globaltimer());
+#endif
   if (lane == 0 && ws.launched) {
     atomicAdd(&v.ctr->rollouts, ws.rollouts);
     atomicAdd(&v.ctr->launched, ws.launched);
@@ -3335,6 +3530,9 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
   if (step < 0) step = v.ctr->cur_step;
   if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
   __syncthreads();
+#ifdef TS_SCHED_PROF
+  if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
+#endif
   if (s_item >= count_items) return;  // no item for this CTA: skip the table set-up
   for (int i = threadIdx.x; i < SQRT_TAB; i += HEAVY_THREADS) sqt[i] = sqrt((double)i);
   __syncthreads();
@@ -3347,7 +3545,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
     if (item >= count_items) break;
     const int s = v.work_heavy[item];
     const SearchState* S = v.st + s;
-    const int count = min(S->target, v.cfg.rollout_budget - S->completed);
+    const int count = min(v.tgt[s], v.cfg.rollout_budget - S->completed);
     if (threadIdx.x == 0) {
       ctl.issued = 0;
       ctl.committed = 0;
@@ -3403,6 +3601,9 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
 #endif
     __syncthreads();
   }
+#ifdef TS_SCHED_PROF
+  if (threadIdx.x == 0) atomicMax(&v.ctr->prof[20], globaltimer());
+#endif
   if (lane == 0 && warp == 0 && ws.launched) {
     atomicAdd(&v.ctr->rollouts, ws.rollouts);
     atomicAdd(&v.ctr->launched, ws.launched);
@@ -3505,6 +3706,7 @@ struct ts_engine {
   Counters* ctr = nullptr;
   int32_t* work = nullptr;
   int32_t* work_heavy = nullptr;
+  int32_t* tgt = nullptr;
   int heavy_blocks = 0;
   int32_t* sp = nullptr;
   double* ss = nullptr;
@@ -3590,6 +3792,7 @@ View make_view(ts_engine* e) {
   v.ctr = e->ctr;
   v.work = e->work;
   v.work_heavy = e->work_heavy;
+  v.tgt = e->tgt;
   v.heavy_on = (e->wkind != 3 && !e->heavy_off && e->n_local <= HBITS_WORDS * 32) ? 1 : 0;
   v.heavy_sync = e->heavy_sync ? 1 : 0;
   v.max_arrival = e->max_arrival;
@@ -3611,7 +3814,7 @@ View make_view(ts_engine* e) {
   return v;
 }
 
-size_t targets_smem() { return 344 * 8 + 32 * 16 + HBITS_WORDS * 4 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8); }
+size_t targets_smem() { return TGT_SCR + 32 * 16 + HBITS_WORDS * 4 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8); }
 size_t sched_smem() { return targets_smem() + (size_t)SREC_MAX * sizeof(ts_sched_record); }
 
 // log1p(k) for k < n from the host libm (the reference calls math.log1p,
@@ -3912,7 +4115,7 @@ int ts_engine_destroy(ts_engine* e) {
   void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
-                  e->work_heavy, e->mt};
+                  e->work_heavy, e->mt, e->tgt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
@@ -3979,12 +4182,13 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   }
   e->cap = cap;
   if (n_local > e->cap_searches || !e->st) {
-    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0, h6 = 0;
+    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0, h6 = 0, h7 = 0;
     if ((rc = grow(e, e->st, n_local, h0, "search state")) ||
         (rc = grow(e, e->prob, n_local, h1, "problem table")) ||
         (rc = grow(e, e->arrival, n_local, h2, "arrivals")) ||
         (rc = grow(e, e->work, n_local, h3, "work list")) ||
         (rc = grow(e, e->work_heavy, n_local, h6, "work list")) ||
+        (rc = grow(e, e->tgt, n_local, h7, "targets")) ||
         (rc = grow(e, e->records, n_local, h4, "records")) ||
         (rc = grow(e, e->outcomes, n_local, h5, "outcomes")))
       return rc;
@@ -4254,16 +4458,14 @@ int ts_read_outcomes(ts_engine* e, ts_outcome* host_out, int32_t n, void* stream
 int ts_read_targets(ts_engine* e, int32_t* host_out, int32_t n, void* stream) {
   if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
   if (!host_out || n < 0 || n > e->n_local) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
-  std::vector<SearchState> st(n);
   cudaStream_t s = (cudaStream_t)stream;
-  TS_CUDA_TRY(e, cudaMemcpyAsync(st.data(), e->st, sizeof(SearchState) * n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, e->tgt, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
   TS_CUDA_TRY(e, cudaStreamSynchronize(s));
-  for (int i = 0; i < n; ++i) host_out[i] = st[i].target;
   return TS_OK;
 }
 
-#ifdef TS_HEAVY_PROF
-// diagnostics build only (not part of the C-ABI): the pipelined-mode phase counters
+#if defined(TS_HEAVY_PROF) || defined(TS_SCHED_PROF)
+// diagnostics build only (not part of the C-ABI): the phase counters
 int ts_debug_prof(ts_engine* e, uint64_t* host16) {
   Counters c;
   TS_CUDA_TRY(e, cudaMemcpy(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost));
