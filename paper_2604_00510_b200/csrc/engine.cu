@@ -102,6 +102,7 @@ struct View {
   int32_t* work;           // this wave's running local searches (single-warp mode)
   int32_t* work_heavy;     // this wave's searches for the pipelined CTA mode
   int32_t* tgt;            // P_i of this wave per local search (compute_targets)
+  ts_sched_record* nrec;   // next wave's scheduler record per search, written by the wave (see k_sched)
   int32_t heavy_on;        // pipelined mode available (uniform width 2/4/8)
   int32_t heavy_sync;      // diagnostics: commit every job before the next selection
   int32_t max_arrival;     // last arrival step of the loaded requests
@@ -198,6 +199,32 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 // ---- kernels -------------------------------------------------------------------
 
+// The record of search s for the scheduler pass of step+1, written by the
+// search's own wave: the fields k_sched would otherwise gather from the
+// SearchState, the arrival and the log1p table (parallelism_score,
+// scheduler.py:118-128, the same expressions as the gather).  Bits 8..31 of
+// flags tag the step the record is for; NREC_FINAL (an exited search) is valid
+// at every later step, NREC_NONE at none.
+constexpr uint32_t NREC_FINAL = 0xFFFFFFu, NREC_NONE = 0xFFFFFEu;
+__device__ __forceinline__ void write_next_record(const View& v, int s, int step, bool finished, int completed,
+                                                  double job_best) {
+  ts_sched_record r;
+  r.score = 0.0;
+  r._pad = 0;
+  r.flags = NREC_NONE << 8;
+  const int ns = step + 1;
+  if (finished) {
+    r.flags = NREC_FINAL << 8;
+  } else if (ns < v.log1p_n) {
+    const ts_config& cf = v.cfg;
+    const bool boosted = job_best / cf.positive_exit_threshold > cf.proximity;
+    r.score = v.log1p_tab[ns - v.arrival[s]] + (boosted ? cf.beta : 0.0);
+    r.flags = 1u | (completed >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u) | ((uint32_t)ns << 8);
+    r._pad = (uint32_t)completed;
+  }
+  v.nrec[s] = r;
+}
+
 // SearchTree.__init__ (tree.py:120-128): bare root, reward 1.0, prior 1.0.
 __global__ void k_init(View v) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -222,6 +249,11 @@ __global__ void k_init(View v) {
   z.status = TS_OK;
   z._pad = 0;
   v.tgt[s] = 0;
+  ts_sched_record nr0;
+  nr0.score = 0.0;
+  nr0._pad = 0;
+  nr0.flags = NREC_NONE << 8;
+  v.nrec[s] = nr0;
   z.tokens = 0;
   z.best = 0.0;
   z.job_best = 0.0;
@@ -303,6 +335,10 @@ __global__ void k_records(View v, int step, ts_sched_record* rec) {
 
 // ---- compute_targets (scheduler.py:143-187) in one CTA ------------------------
 constexpr int TT = 1024;
+// k_sched and k_targets (targets_block): one CTA whose time is the instruction
+// issue of one SM, dominated by the block scans every warp performs, so fewer
+// warps with more records each
+constexpr int SCHED_T = 1024, SCHED_W = SCHED_T / 32;
 constexpr int HEAVY_P = 8;  // rollouts in one wave from which a search runs in pipelined CTA mode
 constexpr int HBITS_WORDS = 2048;  // run-queue slots with a pipelined-mode flag bit (65536)
 constexpr int SREC_MAX = 4096;     // k_sched keeps the records of up to this many searches in shared memory
@@ -433,16 +469,16 @@ __device__ __forceinline__ int runs_lower(const double* runS, int nr, double s) 
 // warp totals itself instead of waiting for one warp to publish offsets.  `sh`
 // (32*N long longs) may be reused two calls later: the intervening call's
 // barrier orders every read of this one before the next write.
-template <int N>
-__device__ __forceinline__ void scan1_add(long long (&x)[N], long long (&tot)[N], long long* sh) {
+template <int N, typename T>
+__device__ __forceinline__ void scan1_add(T (&x)[N], T (&tot)[N], T* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  long long inc[N];
+  T inc[N];
 #pragma unroll
   for (int q = 0; q < N; ++q) {
     inc[q] = x[q];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(FULL, inc[q], o);
+      const T y = __shfl_up_sync(FULL, inc[q], o);
       if (lane >= o) inc[q] += y;
     }
   }
@@ -453,11 +489,11 @@ __device__ __forceinline__ void scan1_add(long long (&x)[N], long long (&tot)[N]
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < N; ++q) {
-    const long long w = lane < TT / 32 ? sh[q * 32 + lane] : 0;
-    long long wi = w;
+    const T w = lane < SCHED_W ? sh[q * 32 + lane] : (T)0;
+    T wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const long long y = __shfl_up_sync(FULL, wi, o);
+      const T y = __shfl_up_sync(FULL, wi, o);
       if (lane >= o) wi += y;
     }
     tot[q] = __shfl_sync(FULL, wi, 31);
@@ -490,6 +526,8 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   long long* shA = (long long*)smem;                  // 96: scan scratch (even calls)
   long long* shB = shA + 96;                          // 96: scan scratch (odd calls)
   long long* shF = shB + 96;                          // 32: per-warp fallback flags
+  int* shA32 = (int*)shA;                             // 32-bit views of the scan scratch
+  int* shB32 = (int*)shB;
   double* shD = (double*)(shF + 32);                  // 64: per-warp list minima
   u128* shq = (u128*)(smem + TGT_SCR);                // 32: per-warp partial sums
   uint32_t* hbits = (uint32_t*)(smem + TGT_SCR + 32 * 16);  // pipelined-mode flag per run-queue slot
@@ -505,16 +543,16 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
 #ifdef TS_SCHED_PROF
   unsigned long long sp_t = globaltimer();
 #endif
-  const int per = (n + TT - 1) / TT;
+  const int per = (n + SCHED_T - 1) / SCHED_T;
   const int lo = min(n, tid * per), hi = min(n, lo + per);
-  for (int w = tid; w < (ghi - glo + 31) / 32 && w < HBITS_WORDS; w += TT) hbits[w] = 0u;
+  for (int w = tid; w < (ghi - glo + 31) / 32 && w < HBITS_WORDS; w += SCHED_T) hbits[w] = 0u;
 
   // phase 1: counts, exact score sum, list positions, list minima before each
   // thread (the lists are non-increasing, so the last score before a thread's
   // range is the minimum over the threads before it)
   u128 fx = 0;
   bool bad = false;
-  long long c3[3] = {0, 0, 0};  // running, gated-in unboosted (list 0), boosted (list 1)
+  int c3[3] = {0, 0, 0};  // running, gated-in unboosted (list 0), boosted (list 1)
   double min0 = INFINITY, min1 = INFINITY;
   for (int i = lo; i < hi; ++i) {
     const ts_sched_record r = rec[i];
@@ -528,12 +566,12 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
       else { ++c3[1]; min0 = fmin(min0, r.score); }
     }
   }
-  long long t3[3];
+  int t3[3];
   double prev0, prev1;
   u128 fsum;
   bool anybad;
   {
-    long long inc[3];
+    int inc[3];
     double m0 = min0, m1 = min1;
 #pragma unroll
     for (int q = 0; q < 3; ++q) inc[q] = c3[q];
@@ -541,7 +579,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        const long long y = __shfl_up_sync(FULL, inc[q], o);
+        const int y = __shfl_up_sync(FULL, inc[q], o);
         if (lane >= o) inc[q] += y;
       }
       const double y0 = __shfl_up_sync(FULL, m0, o), y1 = __shfl_up_sync(FULL, m1, o);
@@ -559,7 +597,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     const bool wbad = __any_sync(FULL, bad);
     if (lane == 31) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) shA[q * 32 + wid] = inc[q];
+      for (int q = 0; q < 3; ++q) shA32[q * 32 + wid] = inc[q];
       shD[wid] = m0;
       shD[32 + wid] = m1;
     }
@@ -571,17 +609,17 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     // every warp: scans of the warp totals, the block sum, the fallback flag
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-      const long long w = shA[q * 32 + lane];
-      long long wi = w;
+      const int w = lane < SCHED_W ? shA32[q * 32 + lane] : 0;
+      int wi = w;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const long long y = __shfl_up_sync(FULL, wi, o);
+        const int y = __shfl_up_sync(FULL, wi, o);
         if (lane >= o) wi += y;
       }
       t3[q] = __shfl_sync(FULL, wi, 31);
       c3[q] = __shfl_sync(FULL, wi - w, wid) + inc[q] - c3[q];
     }
-    double w0 = shD[lane], w1 = shD[32 + lane];
+    double w0 = lane < SCHED_W ? shD[lane] : INFINITY, w1 = lane < SCHED_W ? shD[32 + lane] : INFINITY;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double y0 = __shfl_up_sync(FULL, w0, o), y1 = __shfl_up_sync(FULL, w1, o);
@@ -590,17 +628,17 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     const double b0 = __shfl_sync(FULL, w0, (wid + 31) & 31), b1 = __shfl_sync(FULL, w1, (wid + 31) & 31);
     prev0 = wid == 0 ? e0 : fmin(b0, e0);
     prev1 = wid == 0 ? e1 : fmin(b1, e1);
-    fsum = shq[lane];
+    fsum = lane < SCHED_W ? shq[lane] : (u128)0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const uint64_t h = __shfl_xor_sync(FULL, (uint64_t)(fsum >> 64), o);
       const uint64_t l = __shfl_xor_sync(FULL, (uint64_t)fsum, o);
       fsum += ((u128)h << 64) | l;
     }
-    anybad = __any_sync(FULL, shF[lane] != 0);
+    anybad = __any_sync(FULL, lane < SCHED_W && shF[lane] != 0);
   }
   const long long tot_run = t3[0], len0 = t3[1], len1 = t3[2];
-  const long long pos0 = c3[1], pos1 = c3[2];
+  const int pos0 = c3[1], pos1 = c3[2];
   double T = 0.0;
   bool fallback = anybad;
   if (!fallback) {
@@ -637,7 +675,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   const bool boost_on = cf.boosting_enabled != 0 && tot_run > 0 && R > 0 && len0 + len1 > 0;
 
   // phase 2: runs of equal score in each list (lists are non-increasing)
-  long long rid[2] = {0, 0}, nrr[2] = {0, 0};
+  int rid[2] = {0, 0}, nrr[2] = {0, 0};
   if (boost_on) {
     double p0 = prev0, p1 = prev1;
     for (int i = lo; i < hi; ++i) {
@@ -646,9 +684,9 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
       if (r.flags & 4u) { if (r.score != p1) ++rid[1]; if (r.score > p1) v.ctr->sched_error = 1; p1 = r.score; }
       else { if (r.score != p0) ++rid[0]; if (r.score > p0) v.ctr->sched_error = 1; p0 = r.score; }
     }
-    scan1_add<2>(rid, nrr, shB);
+    scan1_add<2>(rid, nrr, shB32);
   }
-  const long long nr0 = nrr[0], nr1 = nrr[1];
+  const int nr0 = nrr[0], nr1 = nrr[1];
   const bool in_smem = nr0 <= RUNCAP && nr1 <= RUNCAP;
   double* runS = in_smem ? s_runS : v.g_runS;
   int32_t* runStart = in_smem ? s_runStart : v.g_runStart;
@@ -659,7 +697,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   if (boost_on) {
     {
       double p0 = prev0, p1 = prev1;
-      long long q0 = pos0, q1 = pos1, k0 = rid[0], k1 = rid[1];
+      int q0 = pos0, q1 = pos1, k0 = rid[0], k1 = rid[1];
       for (int i = lo; i < hi; ++i) {
         const ts_sched_record r = rec[i];
         if ((r.flags & 3u) != 3u) continue;
@@ -681,12 +719,12 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     int a0[2], a1[2];
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-      const long long nr = b ? nr1 : nr0;
-      const long long len = b ? len1 : len0;
+      const int nr = b ? nr1 : nr0;
+      const int len = (int)(b ? len1 : len0);
       const int off = b ? stride : 0;
-      const int per2 = (int)((nr + TT - 1) / TT);
-      a0[b] = (int)min((long long)tid * per2, nr);
-      a1[b] = (int)min((long long)a0[b] + per2, nr);
+      const int per2 = (nr + SCHED_T - 1) / SCHED_T;
+      a0[b] = min(tid * per2, nr);
+      a1[b] = min(a0[b] + per2, nr);
       for (int k = a0[b]; k < a1[b]; ++k) {
         const double sc = runS[off + k];
         long long want = 1;
@@ -694,7 +732,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
           const double f = floor(sc / T * (double)M);
           want = f > 1.0 ? (long long)f : 1;
         }
-        const long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
+        const int cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
         runWant[off + k] = want;
         pre[b] += cnt * (want - 1);
       }
@@ -702,13 +740,13 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     scan1_add<2>(pre, tw, shA);
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-      const long long nr = b ? nr1 : nr0;
-      const long long len = b ? len1 : len0;
+      const int nr = b ? nr1 : nr0;
+      const int len = (int)(b ? len1 : len0);
       const int off = b ? stride : 0;
       long long q = pre[b];
       for (int k = a0[b]; k < a1[b]; ++k) {
         runPW[off + k] = q;
-        const long long cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
+        const int cnt = (k + 1 < nr ? runStart[off + k + 1] : len) - runStart[off + k];
         q += cnt * (runWant[off + k] - 1);
       }
     }
@@ -722,9 +760,9 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   long long Rp = R - (tw0 + tw1);
   if (Rp < 0) Rp = 0;
   const long long rr_q = U > 0 ? Rp / U : 0, rr_r = U > 0 ? Rp % U : 0;
-  long long nl2[2] = {0, 0};  // pipelined-mode, single-warp
+  int nl2[2] = {0, 0};  // pipelined-mode, single-warp
   {
-    long long q0 = pos0, q1 = pos1, k0 = rid[0] - 1, k1 = rid[1] - 1;
+    int q0 = pos0, q1 = pos1, k0 = rid[0] - 1, k1 = rid[1] - 1;
     double p0 = prev0, p1 = prev1;
     for (int i = lo; i < hi; ++i) {
       const ts_sched_record r = rec[i];
@@ -736,25 +774,27 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
       long long tgt = 1;
       if ((r.flags & 2u) && boost_on) {
         const int b = (r.flags & 4u) ? 1 : 0;
-        long long pos, k;
+        int pos, k;
         if (b) { if (r.score != p1) ++k1; p1 = r.score; pos = q1++; k = k1; }
         else { if (r.score != p0) ++k0; p0 = r.score; pos = q0++; k = k0; }
         const int off = b ? stride : 0, oo = b ? 0 : stride;
         const long long want = runWant[off + k];
-        long long before = runPW[off + k] + (pos - runStart[off + k]) * (want - 1);
+        long long before = runPW[off + k] + (long long)(pos - runStart[off + k]) * (want - 1);
         // cross list: elements with S' > S, or S' == S and smaller id
-        const long long nro = b ? nr0 : nr1, leno = b ? len0 : len1, two = b ? tw0 : tw1;
-        const long long obefore = b ? q0 : q1;  // other-list elements with id < i
-        const int kk = runs_lower(runS + oo, (int)nro, r.score);
-        long long c, cw;
+        const int nro = b ? nr0 : nr1, leno = (int)(b ? len0 : len1);
+        const long long two = b ? tw0 : tw1;
+        const int obefore = b ? q0 : q1;  // other-list elements with id < i
+        const int kk = runs_lower(runS + oo, nro, r.score);
+        int c;
+        long long cw;
         if (kk < nro && runS[oo + kk] == r.score) {
-          const long long st0 = runStart[oo + kk];
-          const long long cntk = (kk + 1 < nro ? runStart[oo + kk + 1] : leno) - st0;
-          long long part = obefore - st0;
+          const int st0 = runStart[oo + kk];
+          const int cntk = (kk + 1 < nro ? runStart[oo + kk + 1] : leno) - st0;
+          int part = obefore - st0;
           if (part < 0) part = 0;
           if (part > cntk) part = cntk;
           c = st0 + part;
-          cw = runPW[oo + kk] + part * (runWant[oo + kk] - 1);
+          cw = runPW[oo + kk] + (long long)part * (runWant[oo + kk] - 1);
         } else if (kk < nro) {
           c = runStart[oo + kk];
           cw = runPW[oo + kk];
@@ -762,7 +802,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
           c = leno;
           cw = two;
         }
-        const long long spos = pos + c;
+        const int spos = pos + c;
         before += cw;
         long long extra = R - before;
         if (extra < 0) extra = 0;
@@ -785,10 +825,10 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
   // phase 5: the local running searches split into the single-warp and the
   // pipelined (many rollouts this wave) work lists, in run-queue order.  A
   // thread reads back only the flag bits it set itself.
-  long long tl2[2];
-  scan1_add<2>(nl2, tl2, shB);
+  int tl2[2];
+  scan1_add<2>(nl2, tl2, shB32);
   {
-    long long ph = nl2[0], pl = nl2[1];
+    int ph = nl2[0], pl = nl2[1];
     const int loc_lo = max(lo, glo) - glo, loc_hi = max(loc_lo, min(hi, ghi) - glo);
     for (int i = loc_lo; i < loc_hi; ++i) {
       if (!(rec[i + glo].flags & 1u)) continue;
@@ -810,7 +850,7 @@ __device__ __forceinline__ size_t targets_smem_dev() {
   return TGT_SCR + 32 * 16 + HBITS_WORDS * 4 + (size_t)2 * RUNCAP * (8 + 4 + 8 + 8);
 }
 
-__global__ void __launch_bounds__(TT) k_targets(View v, int step, const ts_sched_record* rec) {
+__global__ void __launch_bounds__(SCHED_T) k_targets(View v, int step, const ts_sched_record* rec) {
   targets_block(v, step, rec, v.n_global, v.goff, v.goff + v.n_local, 0);
 }
 
@@ -1858,7 +1898,7 @@ __device__ int arrived_count(const View& v, int step) {
 // driver, admit_jobs, parallelism_score records and compute_targets.  The
 // step counter lives on the device, so a CUDA-graph while-loop of
 // {k_sched, k_wave} runs a whole batch without host round trips.
-__global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cudaGraphConditionalHandle cond,
+__global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec, cudaGraphConditionalHandle cond,
                                               int use_cond) {
   __shared__ int s_go, s_min;
   Counters* c = v.ctr;
@@ -1914,50 +1954,62 @@ __global__ void __launch_bounds__(TT) k_sched(View v, ts_sched_record* rec, cuda
   // warp w's threads own the chunk [32*w*per, 32*(w+1)*per): the warp fills
   // its chunk with lane-consecutive (coalesced) loads, four in flight per
   // lane, and a warp barrier replaces a block barrier before the call.
-  const int per = (nw + TT - 1) / TT;
+  const int per = (nw + SCHED_T - 1) / SCHED_T;
   const int lane = threadIdx.x & 31;
   const int c0 = min(nw, (int)(threadIdx.x >> 5) * 32 * per), c1 = min(nw, c0 + 32 * per);
   int my_min = whi;
   for (int j0 = c0; j0 < c1; j0 += 4 * 32) {
-    int state[4], done[4], arr[4];
-    double jb[4], lt[4];
+    // the record the search's last wave wrote, else (admitted now, or written
+    // for another step by the step API) gathered from the SearchState
+    ts_sched_record rr[4];
+    bool slow[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = j0 + u * 32 + lane, i = wlo + j;
-      state[u] = ST_PENDING;
-      done[u] = arr[u] = 0;
-      jb[u] = 0.0;
-      if (j < c1) {
-        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(v.st + i);
-        state[u] = (i >= alo && i < ahi) ? (int)ST_RUNNING : (int)(uint32_t)w.x;
-        done[u] = (int)(uint32_t)(w.x >> 32);
-        jb[u] = __longlong_as_double((long long)w.y);
-        arr[u] = v.arrival[i];
-      }
+      slow[u] = false;
+      if (j < c1) rr[u] = v.nrec[i];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) lt[u] = state[u] == ST_RUNNING ? v.log1p_tab[step - arr[u]] : 0.0;
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * 32 + lane, i = wlo + j;
+      const uint32_t tag = rr[u].flags >> 8;
+      slow[u] = j < c1 && ((i >= alo && i < ahi) || (tag != (uint32_t)step && tag != NREC_FINAL));
+    }
+    if (slow[0] | slow[1] | slow[2] | slow[3]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!slow[u]) continue;
+        const int i = wlo + j0 + u * 32 + lane;
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(v.st + i);
+        const bool adm = i >= alo && i < ahi;
+        const int state = adm ? (int)ST_RUNNING : (int)(uint32_t)w.x;
+        const int done = (int)(uint32_t)(w.x >> 32);
+        const double jb = __longlong_as_double((long long)w.y);
+        if (adm) {
+          v.st[i].state = ST_RUNNING;
+          v.st[i].admit_step = step;
+        }
+        ts_sched_record r;
+        r.score = 0.0;
+        r.flags = 0;
+        r._pad = 0;
+        if (state == ST_RUNNING) {
+          const double ratio = jb / cf.positive_exit_threshold;
+          const bool boosted = ratio > cf.proximity;
+          r.score = v.log1p_tab[step - v.arrival[i]] + (boosted ? cf.beta : 0.0);
+          r.flags = 1u | (done >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
+          r._pad = (uint32_t)done;
+        }
+        rr[u] = r;
+      }
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int j = j0 + u * 32 + lane, i = wlo + j;
       if (j >= c1) break;
-      if (i >= alo && i < ahi) {
-        v.st[i].state = ST_RUNNING;
-        v.st[i].admit_step = step;
-      }
-      ts_sched_record r;
-      r.score = 0.0;
-      r.flags = 0;
-      r._pad = 0;
-      if (state[u] == ST_RUNNING) {
-        my_min = min(my_min, i);
-        const double ratio = jb[u] / cf.positive_exit_threshold;
-        const bool boosted = ratio > cf.proximity;
-        r.score = lt[u] + (boosted ? cf.beta : 0.0);
-        r.flags = 1u | (done[u] >= cf.obs_threshold ? 2u : 0u) | (boosted ? 4u : 0u);
-        r._pad = (uint32_t)done[u];
-      }
-      srec[j] = r;
+      rr[u].flags &= 7u;
+      if (rr[u].flags & 1u) my_min = min(my_min, i);
+      srec[j] = rr[u];
     }
   }
   __syncwarp();
@@ -2442,7 +2494,9 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     S->launched = launched;
     S->cancelled = cancelled;
     // on_rollout_complete (scheduler.py:217-233): refresh Job.best_score
-    if (best_term >= 0 && best > S->job_best) S->job_best = best;
+    double jb = S->job_best;
+    if (best_term >= 0 && best > jb) S->job_best = jb = best;
+    write_next_record(v, s, step, status != TS_OK || decision != TS_EXIT_NONE, completed, jb);
     if (status != TS_OK || decision != TS_EXIT_NONE) {
       S->state = ST_FINISHED;
       S->exit_kind = status == TS_OK ? decision : TS_EXIT_NONE;
@@ -3498,7 +3552,9 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
     atomicAdd(&v.ctr->tokens, ctl->tokens);
     S->launched = launched;
     S->cancelled = cancelled;
-    if (best_term >= 0 && best > S->job_best) S->job_best = best;
+    double jb = S->job_best;
+    if (best_term >= 0 && best > jb) S->job_best = jb = best;
+    write_next_record(v, s, step, status != TS_OK || decision != TS_EXIT_NONE, completed, jb);
     if (status != TS_OK || decision != TS_EXIT_NONE) {
       S->state = ST_FINISHED;
       S->exit_kind = status == TS_OK ? decision : TS_EXIT_NONE;
@@ -3707,6 +3763,7 @@ struct ts_engine {
   int32_t* work = nullptr;
   int32_t* work_heavy = nullptr;
   int32_t* tgt = nullptr;
+  ts_sched_record* nrec = nullptr;
   int heavy_blocks = 0;
   int32_t* sp = nullptr;
   double* ss = nullptr;
@@ -3793,6 +3850,7 @@ View make_view(ts_engine* e) {
   v.work = e->work;
   v.work_heavy = e->work_heavy;
   v.tgt = e->tgt;
+  v.nrec = e->nrec;
   v.heavy_on = (e->wkind != 3 && !e->heavy_off && e->n_local <= HBITS_WORDS * 32) ? 1 : 0;
   v.heavy_sync = e->heavy_sync ? 1 : 0;
   v.max_arrival = e->max_arrival;
@@ -3984,7 +4042,7 @@ int build_run_graph(ts_engine* e, const View& v) {
   memset(&k1, 0, sizeof(k1));
   k1.func = (void*)k_sched;
   k1.gridDim = dim3(1);
-  k1.blockDim = dim3(TT);
+  k1.blockDim = dim3(SCHED_T);
   k1.sharedMemBytes = (unsigned)sched_smem();
   k1.kernelParams = a1;
   cudaGraphNode_t n1, n2;
@@ -4101,6 +4159,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     e->coop_ctas = (coop && !(env4 && env4[0] == '0')) ? per * sms : 0;
     cudaGetLastError();
     e->heavy_sync = env2 && env2[0] == '1';
+    const char* env5 = getenv("TS_NO_GRAPH");  // host-driven stepping (diagnostics: ncu cannot see graph kernels)
+    e->graph_failed = env5 && env5[0] == '1';
   }
   if (cr != cudaSuccess) {
     *out = e;
@@ -4115,7 +4175,7 @@ int ts_engine_destroy(ts_engine* e) {
   void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
-                  e->work_heavy, e->mt, e->tgt};
+                  e->work_heavy, e->mt, e->tgt, e->nrec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
@@ -4182,13 +4242,14 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   }
   e->cap = cap;
   if (n_local > e->cap_searches || !e->st) {
-    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0, h6 = 0, h7 = 0;
+    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0, h6 = 0, h7 = 0, h8 = 0;
     if ((rc = grow(e, e->st, n_local, h0, "search state")) ||
         (rc = grow(e, e->prob, n_local, h1, "problem table")) ||
         (rc = grow(e, e->arrival, n_local, h2, "arrivals")) ||
         (rc = grow(e, e->work, n_local, h3, "work list")) ||
         (rc = grow(e, e->work_heavy, n_local, h6, "work list")) ||
         (rc = grow(e, e->tgt, n_local, h7, "targets")) ||
+        (rc = grow(e, e->nrec, n_local, h8, "records")) ||
         (rc = grow(e, e->records, n_local, h4, "records")) ||
         (rc = grow(e, e->outcomes, n_local, h5, "outcomes")))
       return rc;
@@ -4295,7 +4356,7 @@ int ts_step_targets(ts_engine* e, int32_t step, const ts_sched_record* dev_all, 
   if ((rc = ensure_step_times(e, step + 1, s))) return rc;
   View v = make_view(e);
   if (v.n_global <= e->mt_min) {
-    k_targets<<<1, TT, targets_smem(), s>>>(v, step, dev_all);
+    k_targets<<<1, SCHED_T, targets_smem(), s>>>(v, step, dev_all);
     TS_LAUNCH_CHECK(e, "k_targets");
     return TS_OK;
   }
@@ -4384,7 +4445,7 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
       int blocks = 0;
       if ((rc = wave_grid(e, blocks))) return rc;
       for (int it = 0;; ++it) {
-        k_sched<<<1, TT, sched_smem(), s>>>(v, e->records, cudaGraphConditionalHandle(), 0);
+        k_sched<<<1, SCHED_T, sched_smem(), s>>>(v, e->records, cudaGraphConditionalHandle(), 0);
         TS_LAUNCH_CHECK(e, "k_sched");
         if ((rc = launch_wave(e, v, -1, s))) return rc;
         if (it % 8 == 7) {

@@ -19,10 +19,7 @@ from paper_2604_00510_b200.backend import problem_table  # noqa: E402
 from paper_2604_00510_b200.engine import Engine  # noqa: E402
 
 exits_off = len(sys.argv) > 1 and sys.argv[1] == "exits_off"
-cfg = bench.search_config(bench.PER_GPU)
-if exits_off:
-    cfg.positive_exit_enabled = False
-    cfg.negative_exit_enabled = False
+cfg = bench.search_config(bench.PER_GPU, exits=not exits_off)
 table = problem_table(bench.workload(bench.PER_GPU))
 eng = Engine(cfg, 0)
 eng.lib.ts_debug_prof.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
