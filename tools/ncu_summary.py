@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches <launches.csv> <out.json> <note>
     python tools/ncu_summary.py dram <dram.csv> <out.json> <note>
+    python tools/ncu_summary.py capture <rep.ncu-rep> <out.json> <note> <key>   (adds/replaces entry <key>)
 """
 import collections
 import csv
@@ -55,13 +56,6 @@ def dram(path):
             for k, (n, r, w) in agg.items()}
 
 
-if __name__ == "__main__":
-    mode, src, dst, note = sys.argv[1:5]
-    out = {"note": note, "kernels": launches(src) if mode == "launches" else dram(src)}
-    json.dump(out, open(dst, "w"), indent=1)
-    print(json.dumps(out, indent=1)[:1500])
-
-
 def details(rep):
     """Key metrics of one `ncu --set full` capture (ncu -i <rep> --page details)."""
     import subprocess
@@ -105,5 +99,15 @@ def stalls(rep):
     return {k: round(v / tot, 3) for k, v in agg.most_common(8)}
 
 
-if __name__ == "__main__" and sys.argv[1] == "capture":
-    pass
+if __name__ == "__main__":
+    mode, src, dst, note = sys.argv[1:5]
+    if mode == "capture":
+        import os
+
+        key = sys.argv[5]
+        out = json.load(open(dst)) if os.path.exists(dst) else {}
+        out[key] = {"note": note, "metrics": details(src), "stall_share": stalls(src)}
+    else:
+        out = {"note": note, "kernels": launches(src) if mode == "launches" else dram(src)}
+    json.dump(out, open(dst, "w"), indent=1)
+    print(json.dumps(out if mode != "capture" else out[key], indent=1)[:1500])
