@@ -183,7 +183,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // loop in Counters::prof, read by tools/sched_prof.py.  Slots: 0 wave end ->
 // k_sched start, 1 wave span, 2 k_sched end -> first wave CTA, 3-9 k_sched
 // phases, 10 passes, 20/21/22 the current wave's last end / first start and
-// the last k_sched end.
+// the last k_sched end, 30 the batch has ended.
 #ifdef TS_SCHED_PROF
 #define SP_MARK(slot, t0)                                                       \
   do {                                                                          \
@@ -1904,7 +1904,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
   Counters* c = v.ctr;
 #ifdef TS_SCHED_PROF
   unsigned long long sp_t = globaltimer();
-  if (threadIdx.x == 0 && c->prof[20]) {
+  if (threadIdx.x == 0 && c->prof[20] && !c->prof[30]) {  // 30: the batch has ended (empty passes follow)
     c->prof[0] += sp_t - c->prof[20];
     c->prof[1] += c->prof[20] - c->prof[21];
     c->prof[2] += c->prof[21] - c->prof[22];
@@ -1933,7 +1933,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
       c->heavy_next = 0;
       if (use_cond) cudaGraphSetConditional(cond, 0);
 #ifdef TS_SCHED_PROF
-      c->prof[20] = 0;
+      c->prof[30] = 1;
 #endif
     }
     s_go = go;
@@ -3795,6 +3795,7 @@ struct ts_engine {
   cudaGraphExec_t run_exec = nullptr;
   View run_view;
   bool graph_failed = false;
+  int graph_unroll = 3;  // scheduler passes + waves per iteration of the graph's while loop (TS_GRAPH_UNROLL)
 };
 
 namespace {
@@ -4045,8 +4046,6 @@ int build_run_graph(ts_engine* e, const View& v) {
   k1.blockDim = dim3(SCHED_T);
   k1.sharedMemBytes = (unsigned)sched_smem();
   k1.kernelParams = a1;
-  cudaGraphNode_t n1, n2;
-  TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n1, body, nullptr, 0, &k1));
   void* a2[] = {(void*)&vv, (void*)&stepm1};
   cudaKernelNodeParams k2;
   memset(&k2, 0, sizeof(k2));
@@ -4055,17 +4054,31 @@ int build_run_graph(ts_engine* e, const View& v) {
   k2.blockDim = dim3(WAVE_THREADS);
   k2.sharedMemBytes = (unsigned)wave_smem_of(e->wkind);
   k2.kernelParams = a2;
-  TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
+  cudaKernelNodeParams k3 = k2;
   if (v.heavy_on) {
     int hb = 0;
     if ((rc = heavy_grid(e, hb))) return rc;
-    cudaKernelNodeParams k3 = k2;
     k3.func = heavy_fn(e);
     k3.gridDim = dim3(hb);
     k3.blockDim = dim3(HEAVY_THREADS);
     k3.sharedMemBytes = (unsigned)heavy_smem_of(e->wkind);
-    cudaGraphNode_t n3;
-    TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n3, body, &n1, 1, &k3));
+  }
+  // The body holds `graph_unroll` scheduler passes and waves: an edge inside
+  // the body is cheaper than the loop's back edge (conditional node + launch).
+  // A pass after the batch is done finds nothing to do (empty work lists).
+  cudaGraphNode_t prev[2];
+  int nprev = 0;
+  for (int u = 0; u < e->graph_unroll; ++u) {
+    cudaGraphNode_t n1, n2, n3;
+    TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n1, body, nprev ? prev : nullptr, nprev, &k1));
+    TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
+    prev[0] = n2;
+    nprev = 1;
+    if (v.heavy_on) {
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n3, body, &n1, 1, &k3));
+      prev[1] = n3;
+      nprev = 2;
+    }
   }
   TS_CUDA_TRY(e, cudaGraphInstantiate(&e->run_exec, g, 0));
   e->run_view = v;
@@ -4161,6 +4174,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     e->heavy_sync = env2 && env2[0] == '1';
     const char* env5 = getenv("TS_NO_GRAPH");  // host-driven stepping (diagnostics: ncu cannot see graph kernels)
     e->graph_failed = env5 && env5[0] == '1';
+    const char* env6 = getenv("TS_GRAPH_UNROLL");
+    if (env6) e->graph_unroll = std::max(1, std::min(8, atoi(env6)));
   }
   if (cr != cudaSuccess) {
     *out = e;
@@ -4422,6 +4437,7 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
   if ((rc = ensure_log1p(e, 1 << 16, s))) return rc;
   if ((rc = ensure_step_times(e, e->log1p_n + 1, s))) return rc;
   Counters c;
+  long long step0 = 0;  // device step count before this graph launch
   for (;;) {
     k_set_max_steps<<<1, 1, 0, s>>>(e->ctr, max_steps);
     TS_LAUNCH_CHECK(e, "k_set_max_steps");
@@ -4455,11 +4471,17 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
         }
       }
     } else {
-      e->launches += 2;  // per-step kernels counted from the device step count below
+      e->launches += 1;  // k_set_max_steps; the loop's kernels are counted from the device step count below
     }
     TS_CUDA_TRY(e, cudaMemcpyAsync(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(e, cudaStreamSynchronize(s));
-    if (graphed) e->launches += 2 * c.step;
+    if (graphed) {
+      // every iteration runs graph_unroll passes of {k_sched, k_wave[, k_heavy]}; the
+      // last one contains the pass that ended the loop
+      const long long iters = (c.step - step0) / e->graph_unroll + 1;
+      e->launches += iters * e->graph_unroll * (v.heavy_on ? 3 : 2);
+    }
+    step0 = c.step;
     if (c.finished >= e->n_local || c.step >= max_steps) break;
     // the log1p table bounds the device loop: grow it and continue
     if ((rc = ensure_log1p(e, e->log1p_n * 2, s))) return rc;
