@@ -1900,7 +1900,7 @@ __device__ int arrived_count(const View& v, int step) {
 // {k_sched, k_wave} runs a whole batch without host round trips.
 __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec, cudaGraphConditionalHandle cond,
                                               int use_cond) {
-  __shared__ int s_go, s_min;
+  __shared__ int s_go, s_min, s_fast;
   Counters* c = v.ctr;
 #ifdef TS_SCHED_PROF
   unsigned long long sp_t = globaltimer();
@@ -1926,6 +1926,10 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
       c->head += q;
       c->running += q;
       s_min = (int)c->head;
+      // no free slot, or boosting off: compute_targets gives every running job
+      // P = 1 (scheduler.py:160-163) whatever the scores, so the pass only
+      // needs the list of running searches
+      s_fast = (long long)v.cfg.max_concurrency - c->running <= 0 || v.cfg.boosting_enabled == 0;
     } else {
       c->work_count = 0;
       c->work_next = 0;
@@ -2016,7 +2020,40 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
   for (int o = 16; o > 0; o >>= 1) my_min = min(my_min, __shfl_xor_sync(FULL, my_min, o));
   if ((threadIdx.x & 31) == 0) atomicMin(&s_min, my_min);
   SP_MARK(4, sp_t);
-  targets_block(v, step, srec, nw, 0, nw, wlo);
+  static_assert(HEAVY_P > 1, "P = 1 searches run in single-warp mode");
+  if (s_fast) {
+    // the running searches of the warp's chunk, in run-queue order, onto the
+    // single-warp work list
+    __shared__ int s_wcnt[SCHED_W];
+    const int wid = threadIdx.x >> 5;
+    int cnt = 0;
+    for (int j = c0 + lane; j < c1; j += 32) cnt += (int)(srec[j].flags & 1u);
+    cnt = __reduce_add_sync(FULL, cnt);
+    if (lane == 0) s_wcnt[wid] = cnt;
+    if (threadIdx.x == 0 && step < v.step_times_cap) v.step_times[step] = globaltimer();
+    __syncthreads();
+    const int wt = lane < SCHED_W ? s_wcnt[lane] : 0;
+    int pos = __reduce_add_sync(FULL, lane < wid ? wt : 0);
+    const int total = __reduce_add_sync(FULL, wt);
+    for (int j0 = c0; j0 < c1; j0 += 32) {
+      const int j = j0 + lane;
+      const bool run = j < c1 && (srec[j].flags & 1u);
+      const unsigned b = __ballot_sync(FULL, run);
+      if (run) v.work[pos + __popc(b & ((1u << lane) - 1u))] = wlo + j;
+      if (j < c1) v.tgt[wlo + j] = run ? 1 : 0;
+      pos += __popc(b);
+    }
+    if (threadIdx.x == 0) {
+      c->work_count = total;
+      c->work_next = 0;
+      c->heavy_count = 0;
+      c->heavy_next = 0;
+      c->cur_step = step;
+    }
+    SP_MARK(9, sp_t);
+  } else {
+    targets_block(v, step, srec, nw, 0, nw, wlo);
+  }
   if (threadIdx.x == 0) {
     c->win_lo = s_min;  // no running search below this index
     c->step = step + 1;

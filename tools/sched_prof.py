@@ -34,7 +34,7 @@ n = max(1, p[10])
 names = ["wave end -> k_sched start", "wave span (first CTA start -> last CTA end)",
          "k_sched end -> first wave CTA start", "k_sched: loop test + admission", "k_sched: records",
          "targets: counts + exact sum", "targets: runs", "targets: want per run", "targets: per-search targets",
-         "targets: work lists"]
+         "targets: work lists (or the P = 1 fast path)"]
 print(f"{'exits off' if exits_off else 'PE+NE+boost'}: {n} scheduler passes, {st.steps} waves")
 for i, nm in enumerate(names):
     print(f"  {nm:48s} {p[i] / n / 1000.0:8.2f} us/pass")
