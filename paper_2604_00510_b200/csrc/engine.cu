@@ -2571,12 +2571,14 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
 #endif
   const int count = v.ctr->work_count;
   if (step < 0) step = v.ctr->cur_step;
-  for (;;) {
-    int item = 0;
-    if (lane == 0) item = atomicAdd(&v.ctr->work_next, 1);
-    item = __shfl_sync(FULL, item, 0);
-    if (item >= count) break;
+  // the first item of every warp is its global warp index (no burst of
+  // same-address atomics at launch); later items come from the shared counter
+  const int nwarps = gridDim.x * WAVE_WARPS;
+  int item = blockIdx.x * WAVE_WARPS + warp;
+  while (item < count) {
     search_wave<NSLOT, WT>(v, v.work[item], step, ws, s_raw, s_rew);
+    if (lane == 0) item = nwarps + atomicAdd(&v.ctr->work_next, 1);
+    item = __shfl_sync(FULL, item, 0);
   }
 #ifdef TS_SCHED_PROF
   if (lane == 0) atomicMax(&v.ctr->prof[20], globaltimer());
