@@ -495,3 +495,30 @@ def test_policy_operator_drives_the_engine(name):
         got = outcome_dict(outs[i])
         for k in got:
             assert got[k] == want[k], (name, i, k)
+
+
+@pytest.mark.parametrize("unroll,no_graph", [(1, False), (2, False), (4, False), (3, True)])
+def test_graph_loop_variants_match_oracle(unroll, no_graph, monkeypatch):
+    """The graph loop with 1-4 passes per while-loop iteration (a batch that
+    ends mid-body runs empty passes) and host-driven stepping give the oracle's
+    outcomes; the batch mixes the P = 1 fast path (no free slot) with boosted
+    passes (slots freed by exits) and a second batch reuses the instantiated graph."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    monkeypatch.setenv("TS_GRAPH_UNROLL", str(unroll))
+    if no_graph:
+        monkeypatch.setenv("TS_NO_GRAPH", "1")
+    specs = B.make_workload(512, (0.6, 0.25, 0.15), 17, branching=4, depth_ranges={d: (11, 11) for d in B.Difficulty})
+    cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=512), rollout_budget=64, depth_cap=12,
+                       expand_width=4)
+    t = B.problem_table(specs)
+    ref = oracle.OracleRun(t, cfg.to_c(), threads=8)
+    with _engine(cfg) as eng:
+        for rep in range(2):
+            eng.load(t)
+            st = eng.run()
+            _cmp_outcomes(eng.outcomes(), ref.outcomes, f"unroll{unroll}{'-nograph' if no_graph else ''}#{rep}")
+            assert st.steps == ref.steps and st.rollouts == ref.stats.rollouts
+    ref.close()
