@@ -237,6 +237,7 @@ __global__ void k_init(View v) {
   v.reward[r] = 1.0;
   v.mf[r] = mk_mf(-1, 0);
   v.parent[r] = -1;
+  const_cast<int32_t*>(v.arrival)[s] = v.prob[s].arrival_step;  // the run queue's arrival column
   SearchState z;
   z.state = ST_PENDING;
   z.completed = z.launched = z.cancelled = 0;
@@ -345,33 +346,6 @@ constexpr int SREC_MAX = 4096;     // k_sched keeps the records of up to this ma
 constexpr int RUNCAP = 1536;  // runs per list kept in shared memory
 constexpr size_t TGT_SCR = (96 + 96 + 32 + 64) * 8;  // targets_block scan scratch (bytes)
 
-// Block-wide exclusive scan (+) of one value per thread; returns the prefix,
-// writes the block total.  All threads must call.
-__device__ long long block_scan_add(long long x, long long* total, long long* sh) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  long long incl = x;
-  for (int o = 1; o < 32; o <<= 1) {
-    long long y = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) sh[wid] = incl;
-  __syncthreads();
-  if (wid == 0) {
-    long long w = sh[lane];
-    long long wi = w;
-    for (int o = 1; o < 32; o <<= 1) {
-      long long y = __shfl_up_sync(FULL, wi, o);
-      if (lane >= o) wi += y;
-    }
-    sh[32 + lane] = wi - w;
-    if (lane == 31) sh[64] = wi;
-  }
-  __syncthreads();
-  long long res = sh[32 + wid] + incl - x;
-  if (total) *total = sh[64];
-  __syncthreads();
-  return res;
-}
 // Four exclusive (+) scans in one pass; totals in tot[4].  All threads must call.
 __device__ void block_scan_add4(long long (&x)[4], long long (&tot)[4], long long* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -3822,11 +3796,13 @@ struct ts_engine {
   ts_sched_record* records = nullptr;
   ts_outcome* outcomes = nullptr;
   int outcomes_cap = 0;
-  std::vector<int32_t> h_arrival;
   int max_arrival = 0;
   long long launches = 0;
   void* pin = nullptr;  // pinned staging for host tables (problems in, outcomes out)
   size_t pin_bytes = 0;
+  void* pin_out = nullptr;  // pinned staging of ts_run_batch_host's outcomes
+  size_t pin_out_bytes = 0;
+  Counters* pin_ctr = nullptr;  // pinned copy of the counters read after a run
   std::vector<cudaEvent_t> wave_ev;  // start/stop pairs of every wave since load
   size_t wave_ev_used = 0;
   // ts_run: CUDA graph with a device-driven while loop over {k_sched, k_wave}
@@ -4235,6 +4211,8 @@ int ts_engine_destroy(ts_engine* e) {
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
   destroy_run_graph(e);
   if (e->pin) cudaFreeHost(e->pin);
+  if (e->pin_out) cudaFreeHost(e->pin_out);
+  if (e->pin_ctr) cudaFreeHost(e->pin_ctr);
   delete e;
   return TS_OK;
 }
@@ -4249,7 +4227,6 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   TS_CUDA_TRY(e, cudaSetDevice(e->device));
   const ts_config& c = e->cfg;
   int max_len = 1, max_width = 1, prev_arr = 0;
-  e->h_arrival.resize(n_local);
   for (int i = 0; i < n_local; ++i) {
     const ts_problem& p = hp[i];
     if (p.branching < 1 || p.branching > TS_MAX_WIDTH)
@@ -4260,7 +4237,6 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
     if (p.arrival_step < 0 || p.arrival_step < prev_arr)
       return fail(e, TS_INVALID_ARGUMENT, "arrival steps must be non-negative and non-decreasing");
     prev_arr = p.arrival_step;
-    e->h_arrival[i] = p.arrival_step;
     max_len = std::max(max_len, std::min(c.depth_cap, p.base_depth + 1));
     max_width = std::max(max_width, std::min(c.expand_width, p.branching));
   }
@@ -4354,8 +4330,6 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
       TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, e->pin, bytes, cudaMemcpyHostToDevice, s));
     }
   }
-  TS_CUDA_TRY(e, cudaMemcpyAsync(e->arrival, e->h_arrival.data(), sizeof(int32_t) * n_local,
-                                 cudaMemcpyHostToDevice, s));
   if ((rc = ensure_log1p(e, 1024, s))) return rc;
   if ((rc = ensure_step_times(e, 4096, s))) return rc;
   View v = make_view(e);
@@ -4468,11 +4442,24 @@ int ts_step_wave(ts_engine* e, int32_t step, void* stream) {
   return launch_wave(e, v, step, (cudaStream_t)stream);
 }
 
-int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* stream) {
+// ts_run, and with host_out the outcome readout too: k_outcomes and both
+// device-to-host copies (outcomes, counters; pinned) are queued behind the
+// graph launch so the batch ends in one stream synchronisation.
+static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cudaStream_t s, ts_outcome* host_out,
+             int32_t n_out) {
   if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
   if (max_steps < 0) return fail(e, TS_INVALID_ARGUMENT, "max_steps must be >= 0");
-  cudaStream_t s = (cudaStream_t)stream;
   int rc;
+  const size_t out_bytes = sizeof(ts_outcome) * (size_t)std::max(0, n_out);
+  const bool out_direct = host_out && is_pinned(host_out);
+  if (host_out && n_out > 0 && !out_direct && out_bytes > e->pin_out_bytes) {
+    if (e->pin_out) cudaFreeHost(e->pin_out);
+    e->pin_out = nullptr;
+    e->pin_out_bytes = 0;
+    TS_CUDA_TRY(e, cudaMallocHost(&e->pin_out, out_bytes));
+    e->pin_out_bytes = out_bytes;
+  }
+  if (!e->pin_ctr) TS_CUDA_TRY(e, cudaMallocHost((void**)&e->pin_ctr, sizeof(Counters)));
   if ((rc = ensure_log1p(e, 1 << 16, s))) return rc;
   if ((rc = ensure_step_times(e, e->log1p_n + 1, s))) return rc;
   Counters c;
@@ -4512,8 +4499,15 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
     } else {
       e->launches += 1;  // k_set_max_steps; the loop's kernels are counted from the device step count below
     }
-    TS_CUDA_TRY(e, cudaMemcpyAsync(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
+    if (host_out && n_out > 0) {
+      k_outcomes<<<(n_out + 127) / 128, 128, 0, s>>>(v, e->outcomes, n_out);
+      TS_LAUNCH_CHECK(e, "k_outcomes");
+      TS_CUDA_TRY(e, cudaMemcpyAsync(out_direct ? (void*)host_out : e->pin_out, e->outcomes, out_bytes,
+                                     cudaMemcpyDeviceToHost, s));
+    }
+    TS_CUDA_TRY(e, cudaMemcpyAsync(e->pin_ctr, e->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
     TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+    c = *e->pin_ctr;
     if (graphed) {
       // every iteration runs graph_unroll passes of {k_sched, k_wave[, k_heavy]}; the
       // last one contains the pass that ended the loop
@@ -4533,7 +4527,12 @@ int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* strea
     stats_out->wave_ms = 0.0;
     if (c.sched_error) return fail(e, TS_INVALID_ARGUMENT, "run queue scores not ordered by arrival");
   }
+  if (host_out && n_out > 0 && !out_direct) memcpy(host_out, e->pin_out, out_bytes);
   return TS_OK;
+}
+
+int ts_run(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, void* stream) {
+  return run_impl(e, max_steps, stats_out, (cudaStream_t)stream, nullptr, 0);
 }
 
 int ts_read_stats(ts_engine* e, ts_run_stats* o, void* stream) {
@@ -4624,8 +4623,8 @@ int ts_run_batch_host(ts_engine* e, const ts_problem* hp, int32_t n, int32_t max
                       ts_run_stats* stats_out, void* stream) {
   int rc;
   if ((rc = ts_load_problems(e, hp, n, 0, n, stream))) return rc;
-  if ((rc = ts_run(e, max_steps, stats_out, stream))) return rc;
-  return ts_read_outcomes(e, host_out, n, stream);
+  if (!host_out) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  return run_impl(e, max_steps, stats_out, (cudaStream_t)stream, host_out, n);
 }
 
 int ts_tree_size(ts_engine* e, int32_t search, int32_t* nodes_out) {
