@@ -228,6 +228,10 @@ __device__ __forceinline__ void write_next_record(const View& v, int s, int step
 // SearchTree.__init__ (tree.py:120-128): bare root, reward 1.0, prior 1.0.
 __global__ void k_init(View v) {
   int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0) {  // the run's counters (nothing reads them before the next kernel)
+    memset(v.ctr, 0, sizeof(Counters));
+    v.ctr->last_exit_step = -1;
+  }
   if (s >= v.n_local) return;
   size_t r = (size_t)s * (size_t)v.cap;
   v.no[r] = 0;
@@ -262,10 +266,6 @@ __global__ void k_init(View v) {
   v.st[s] = z;
 }
 
-__global__ void k_reset_counters(Counters* c) {
-  memset(c, 0, sizeof(Counters));
-  c->last_exit_step = -1;
-}
 
 __global__ void k_set_max_steps(Counters* c, int max_steps) { c->max_steps = max_steps; }
 
@@ -4335,9 +4335,8 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   View v = make_view(e);
   e->launches = 0;
   e->wave_ev_used = 0;
-  k_reset_counters<<<1, 1, 0, s>>>(e->ctr);
-  TS_LAUNCH_CHECK(e, "k_reset_counters");
-  k_init<<<(n_local + 255) / 256, 256, 0, s>>>(v);
+  // 64-thread CTAs: the root records are scattered stores, spread them over more SMs
+  k_init<<<(n_local + 63) / 64, 64, 0, s>>>(v);
   TS_LAUNCH_CHECK(e, "k_init");
   e->loaded = true;
   (void)have;
@@ -4496,9 +4495,7 @@ static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cu
           if (c.finished >= e->n_local || c.step >= max_steps || c.step >= e->log1p_n) break;
         }
       }
-    } else {
-      e->launches += 1;  // k_set_max_steps; the loop's kernels are counted from the device step count below
-    }
+    }  // graphed: the loop's kernels are counted from the device step count below
     if (host_out && n_out > 0) {
       k_outcomes<<<(n_out + 127) / 128, 128, 0, s>>>(v, e->outcomes, n_out);
       TS_LAUNCH_CHECK(e, "k_outcomes");
