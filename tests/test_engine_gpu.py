@@ -181,7 +181,7 @@ def test_compute_targets_random_vs_oracle(n):
 
 @pytest.mark.parametrize("name,multi_cta", [("c1_M48_admission", False), ("c1_M48_admission", True),
                                              ("cli_serving_pe_ne_boost", False), ("cli_serving_pe_ne_boost", True),
-                                             ("c2_s512_M2048", True)])
+                                             ("c2_s512_M2048", True), ("c2_s512_M2048", "nocoop")])
 def test_sharded_engines_match_single(name, multi_cta, monkeypatch):
     """Block sharding of the run queue over 3 engines (one 'rank' each) with the
     exchanges done by device copies == one engine: the multi-GPU step contract
@@ -191,6 +191,8 @@ def test_sharded_engines_match_single(name, multi_cta, monkeypatch):
 
     if multi_cta:
         monkeypatch.setenv("TS_MT_MIN", "0")
+    if multi_cta == "nocoop":  # the many-CTA step as separate kernels instead of one cooperative launch
+        monkeypatch.setenv("TS_MT_COOP", "0")
     case = next(c for c in load("waves") if c["name"] == name)
     recs = load("workloads")[case["workload"]][: len(case["outcomes"])]
     cfg = config_from_case(case)
@@ -328,19 +330,24 @@ def test_pipelined_mode_matches_single_warp_mode(seed, M, budget, cap, b, base, 
                        rollout_budget=budget, depth_cap=cap, expand_width=b,
                        negative_exit=sc in (AggregationScheme.CUMULATIVE_PRODUCT, AggregationScheme.MINIMUM))
     res = {}
-    for mode in ("0", "1"):
-        monkeypatch.setenv("TS_NO_PIPELINE", mode)
+    # "sync": the pipelined mode with every rollout committed before the next selection
+    for mode in ("0", "1", "sync") if seed in (0, 13) else ("0", "1"):
+        monkeypatch.setenv("TS_NO_PIPELINE", "0" if mode == "sync" else mode)
+        monkeypatch.setenv("TS_PIPELINE_SYNC", "1" if mode == "sync" else "0")
         with _engine(cfg) as eng:
             eng.load(t)
             st = eng.run()
             outs = eng.outcomes()
             trees = [eng.tree(i) for i in range(0, n, max(1, n // 16))]
             res[mode] = (st.steps, st.rollouts, st.launched, st.nodes, outs, trees)
-    a, c = res["0"], res["1"]
-    assert a[:4] == c[:4]
-    _cmp_outcomes(a[4], c[4], f"pipelined[{seed}]")
-    for x, y in zip(a[5], c[5]):
-        assert_tree_equal(x, {k: v.tolist() for k, v in y.items()}, "pipelined tree")
+    c = res["1"]
+    for mode, a in res.items():
+        if mode == "1":
+            continue
+        assert a[:4] == c[:4]
+        _cmp_outcomes(a[4], c[4], f"pipelined[{seed}/{mode}]")
+        for x, y in zip(a[5], c[5]):
+            assert_tree_equal(x, {k: v.tolist() for k, v in y.items()}, f"pipelined tree ({mode})")
 
 
 def test_sum_scheme_q_out_of_range_raises_like_reference():
