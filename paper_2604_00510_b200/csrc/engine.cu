@@ -1375,6 +1375,10 @@ __global__ void __launch_bounds__(TT) k_mt_split(View v, int step, const ts_sche
 __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sched_record* rec, unsigned char* mt) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
+#ifdef TS_SCHED_PROF
+  const unsigned long long mt_t0 = globaltimer();
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11] += 1;
+#endif
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   __shared__ ts_sched_record srec[MT_REC];
@@ -1443,6 +1447,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
+#ifdef TS_SCHED_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11 + 1] += globaltimer() - mt_t0;
+#endif
   // ---- phase 2 (every CTA, redundantly): CTA offsets, T, totals from the
   // G summaries (no further grid barrier: each CTA keeps its own copy)
   __shared__ MtOff1 s_off;
@@ -1555,6 +1562,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
+#ifdef TS_SCHED_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11 + 2] += globaltimer() - mt_t0;
+#endif
   // ---- phase 4 (every CTA): run offsets of the CTAs, run totals
   {
     long long c[2] = {tid < G ? L.b2[tid] : 0, tid < G ? L.b2[G + tid] : 0}, tot[2];
@@ -1591,6 +1601,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
+#ifdef TS_SCHED_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11 + 3] += globaltimer() - mt_t0;
+#endif
   const long long M = cf.max_concurrency;
   // ---- phase 6: want per run, per-run-block sums
   if (boost_on) {
@@ -1621,6 +1634,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
+#ifdef TS_SCHED_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11 + 4] += globaltimer() - mt_t0;
+#endif
   // ---- phase 7 (every CTA): run-block offsets into shared memory, tw0/tw1
   __shared__ long long s_b3[2 * MT_RB];
   const bool b3_smem = G3 <= MT_RB;
@@ -1652,6 +1668,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     __syncthreads();
   }
   if (!b3_smem) grid.sync();  // CTA 0 rewrote the global run-block offsets
+#ifdef TS_SCHED_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11 + 5] += globaltimer() - mt_t0;
+#endif
   // ---- phase 8: targets of the local records, pipelined-mode flags, per-CTA list counts
   const int glo = v.goff, ghi = v.goff + v.n_local;
   long long nh = 0, nlt = 0;
@@ -1769,6 +1788,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
   }
   grid.sync();
+#ifdef TS_SCHED_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11 + 6] += globaltimer() - mt_t0;
+#endif
   // ---- phase 9: work lists in run-queue order
   {
     if (tid == 0) {
@@ -1796,6 +1818,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
       else v.work[pl++] = i - glo;
     }
   }
+#ifdef TS_SCHED_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[18] += globaltimer() - mt_t0;
+#endif
 }
 
 // Caller-provided parallelism targets (an external scheduler): P_i for every

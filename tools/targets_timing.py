@@ -18,7 +18,7 @@ from paper_2604_00510_b200.scheduler import SchedulerConfig  # noqa: E402
 
 rng = random.Random(0)
 dummy = load("workloads")["c1"][0]
-for n in (4096, 16384, 32768, 65536):
+for n in [int(x) for x in os.environ.get("TT_SIZES", "4096,16384,32768,65536").split(",")]:
     M = 4 * n
     now = 30
     sch = SchedulerConfig(max_concurrency=M)
@@ -44,7 +44,27 @@ for n in (4096, 16384, 32768, 65536):
         ts.append(e0.elapsed_time(e1))
     print(f"n={n}: k_targets {1e3 * min(ts[1:]):.1f} us", flush=True)
     eng.close()
-if os.environ.get("TS_LIB_PATH", "").endswith("_prof.so"):
+if os.environ.get("TS_LIB_PATH", "").endswith("_sprof.so"):
+    # -DTS_SCHED_PROF build: %globaltimer at each grid barrier of k_mt_all (CTA 0)
+    import ctypes
+    n = int(os.environ.get("TT_PROF_N", "32768"))
+    eng = Engine(SearchConfig(scheduler=SchedulerConfig(max_concurrency=4 * n)), 0)
+    eng.load(table([dummy] * n))
+    recs = (TsSchedRecord * n)()
+    for i in range(n):
+        recs[i].score = math.log1p(30 - (i * 31) // n)
+        recs[i].flags = 3
+    dev = torch.frombuffer(bytearray(bytes(recs)), dtype=torch.uint8).cuda()
+    for r in range(10):
+        eng.step_targets(30, dev.data_ptr())
+    torch.cuda.synchronize()
+    buf = (ctypes.c_uint64 * 32)()
+    eng.lib.ts_debug_prof.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+    eng.lib.ts_debug_prof(eng._h, buf)
+    calls = max(1, buf[11])
+    print(f"k_mt_all n={n}, {calls} calls: us since kernel start at grid barriers 1-6 and at the end:",
+          [round(buf[i] / calls / 1e3, 2) for i in range(12, 19)])
+elif os.environ.get("TS_LIB_PATH", "").endswith("_prof.so"):
     import ctypes
     eng = Engine(SearchConfig(scheduler=SchedulerConfig(max_concurrency=4 * 32768)), 0)
     buf = (ctypes.c_uint64 * 32)()
