@@ -1899,7 +1899,8 @@ __device__ int arrived_count(const View& v, int step) {
 // {k_sched, k_wave} runs a whole batch without host round trips.
 __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec, cudaGraphConditionalHandle cond,
                                               int use_cond) {
-  __shared__ int s_go, s_min, s_fast;
+  __shared__ int s_go, s_min, s_fast, s_wlo, s_whi;
+  __shared__ long long s_alo, s_ahi;
   Counters* c = v.ctr;
 #ifdef TS_SCHED_PROF
   unsigned long long sp_t = globaltimer();
@@ -1914,21 +1915,29 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
   if (threadIdx.x < 32) arrived = arrived_count(v, step);
   if (threadIdx.x == 0) {
     const int lo = arrived;
-    const long long unfinished = (long long)v.n_local - c->finished;
-    const bool go = unfinished > 0 && step < c->max_steps && step < v.log1p_n;
+    // every counter in one round of loads; the pass's bounds go to the other
+    // threads through shared memory
+    const long long fin = c->finished, max_steps = c->max_steps, running = c->running, head = c->head,
+                    win_lo = c->win_lo;
+    const long long unfinished = (long long)v.n_local - fin;
+    const bool go = unfinished > 0 && step < max_steps && step < v.log1p_n;
     if (go) {
-      long long q = (long long)v.cfg.max_concurrency - c->running;
-      if (q > (long long)lo - c->head) q = (long long)lo - c->head;
+      long long q = (long long)v.cfg.max_concurrency - running;
+      if (q > (long long)lo - head) q = (long long)lo - head;
       if (q < 0) q = 0;
-      c->admit_lo = c->head;
-      c->admit_hi = c->head + q;
-      c->head += q;
-      c->running += q;
-      s_min = (int)c->head;
+      c->admit_lo = head;
+      c->admit_hi = head + q;
+      c->head = head + q;
+      c->running = running + q;
+      s_alo = head;
+      s_ahi = head + q;
+      s_wlo = (int)win_lo;
+      s_whi = (int)(head + q);
+      s_min = (int)(head + q);
       // no free slot, or boosting off: compute_targets gives every running job
       // P = 1 (scheduler.py:160-163) whatever the scores, so the pass only
       // needs the list of running searches
-      s_fast = (long long)v.cfg.max_concurrency - c->running <= 0 || v.cfg.boosting_enabled == 0;
+      s_fast = (long long)v.cfg.max_concurrency - (running + q) <= 0 || v.cfg.boosting_enabled == 0;
     } else {
       c->work_count = 0;
       c->work_next = 0;
@@ -1944,11 +1953,11 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
   __syncthreads();
   if (!s_go) return;
   SP_MARK(3, sp_t);
-  const long long alo = c->admit_lo, ahi = c->admit_hi;
+  const long long alo = s_alo, ahi = s_ahi;
   const ts_config& cf = v.cfg;
   // the run queue is the window [win_lo, head): searches below win_lo have
   // exited, searches from head on are not admitted yet
-  const int wlo = (int)c->win_lo, whi = (int)c->head;
+  const int wlo = s_wlo, whi = s_whi;
   const int nw = whi - wlo;
   // one GPU: the window's records stay in shared memory when they fit
   extern __shared__ __align__(16) unsigned char smem[];
