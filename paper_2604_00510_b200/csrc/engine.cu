@@ -2651,6 +2651,10 @@ struct HeavyCtl {
   int zero_o;  // set by heavy_finish: clear O of every node of the search (exit with cancellations)
   volatile int nnodes, viable;
   unsigned long long created, tokens;
+  // the root's word (meta | first child << 32) after the commits so far: the
+  // committing simulator updates it with MF[0], so the selector refreshes its
+  // copy from shared memory instead of global memory
+  volatile unsigned long long root_mf;
 };
 
 // CTA-scope acquire load / release store on shared-memory counters
@@ -2759,7 +2763,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       }
       root_seen = cs;
       if (heavy_wait_inflight(ctl, lleaf, cs, k, 0)) stale = true;
-      if (stale) rmf = reload_u64(MF);
+      if (stale) rmf = ctl->root_mf;
     }
     uint32_t nmeta = (uint32_t)rmf;
     if (!meta_expandable(nmeta)) {  // NoExpandableLeafError (tree.py:273-274)
@@ -3008,7 +3012,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         stale |= jb.leaf == 0 || jb.risky != 0;
       }
       root_seen = k - HEAVY_RING + 1;
-      if (stale) rmf = reload_u64(MF);
+      if (stale) rmf = ctl->root_mf;
     }
 #ifdef TS_HEAVY_PROF
     const long long e0 = clock64();
@@ -3302,7 +3306,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     if (ok) {
       if (lane >= d0 && lane < dend) pnode += cbase;  // final ids of the new path nodes
       const int fc0 = cbase;
-      uint32_t root_meta = ME[0];
+      uint32_t root_meta = (uint32_t)ctl->root_mf;
       if (d0 == 0 && lane == 0) meta_l |= root_meta;  // the root was the selected leaf
       if (risky && lane < d0 - 1) pmeta = ME[2 * pnode];  // current metas for the propagation
       const int up_node = __shfl_up_sync(FULL, pnode, 1);
@@ -3334,6 +3338,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
       }
       // the selector reads this job's nodes only after acquiring its commit
       if (act) MF[lane == d0 ? leaf : node_l] = mk_mf(fc0 + (lane - d0) * width, meta_l);
+      if (d0 == 0 && nlev > 0 && lane == 0) ctl->root_mf = mk_mf(fc0, meta_l);
       {
         const uint32_t dn = __shfl_down_sync(FULL, meta_l, 1);
         const bool dn_act = (lane + 1) >= d0 && (lane + 1) < d0 + nlev;
@@ -3356,6 +3361,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
           const int pid = i == 0 ? 0 : __shfl_sync(FULL, pnode, i - 1);
           m -= NEXP_ONE;
           if (lane == 0) ME[2 * pid] = m;
+          if (i == 0 && lane == 0) ctl->root_mf = (ctl->root_mf & 0xFFFFFFFF00000000ull) | m;
           if (i == 0) root_meta = m;
           else if (lane == i - 1) pmeta = m;
           if (meta_nexp(m) > 0) break;
@@ -3659,6 +3665,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
       ctl.viable = S->viable;
       ctl.created = 0;
       ctl.tokens = 0;
+      ctl.root_mf = v.mf[(size_t)s * (size_t)v.cap];
     }
     __syncthreads();
     uint64_t rno = 0;
