@@ -1970,6 +1970,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
   const int lane = threadIdx.x & 31;
   const int c0 = min(nw, (int)(threadIdx.x >> 5) * 32 * per), c1 = min(nw, c0 + 32 * per);
   int my_min = whi;
+  bool ungated = false;  // a running search past the observation gate
   for (int j0 = c0; j0 < c1; j0 += 4 * 32) {
     // the record the search's last wave wrote, else (admitted now, or written
     // for another step by the step API) gathered from the SearchState
@@ -2021,6 +2022,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
       if (j >= c1) break;
       rr[u].flags &= 7u;
       if (rr[u].flags & 1u) my_min = min(my_min, i);
+      ungated |= (rr[u].flags & 3u) == 3u;
       srec[j] = rr[u];
     }
   }
@@ -2029,7 +2031,10 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
   if ((threadIdx.x & 31) == 0) atomicMin(&s_min, my_min);
   SP_MARK(4, sp_t);
   static_assert(HEAVY_P > 1, "P = 1 searches run in single-warp mode");
-  if (s_fast) {
+  // nobody past the observation gate: the extra and leftover loops of
+  // compute_targets run over an empty list (scheduler.py:166-186), P = 1 again
+  const bool fast = __syncthreads_or(ungated) == 0 || s_fast;
+  if (fast) {
     // the running searches of the warp's chunk, in run-queue order, onto the
     // single-warp work list
     __shared__ int s_wcnt[SCHED_W];
