@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 3
+#define TS_ABI_VERSION 4
 #define TS_MAX_DEPTH 32 /* golden path / reward table length; base_depth <= 31 */
 #define TS_MAX_WIDTH 32 /* branching <= one warp                                */
 
@@ -180,6 +180,27 @@ int ts_step_wave(ts_engine* eng, int32_t step, void* stream);
 /* Whole batch on one GPU: the five calls above per step until every search
  * has exited (or max_steps).  stats_out may be NULL. */
 int ts_run(ts_engine* eng, int32_t max_steps, ts_run_stats* stats_out, void* stream);
+
+/* ---- run-time invariants (checked mode) ---------------------------------- */
+/* The reference asserts these while it runs (Engine._check_capacity and the
+ * conservation check, simulator.py:252-260; test_acceptance.py:167-187,
+ * test_simulator.py:58-64).  With checks enabled, two extra kernels bracket
+ * every wave (ts_run's graph loop and ts_step_wave alike) and count
+ * violations on the device; ts_read_invariants reads the counts since the
+ * last ts_load_problems.  All *_violations / inflight_nodes / root_mismatches
+ * are 0 on a correct run. */
+typedef struct ts_invariants {
+  int64_t waves;                   /* waves checked */
+  int64_t capacity_violations;     /* waves with Σ min(P_i, budget-completed_i) > M, or |running| > M */
+  int64_t gate_violations;         /* searches below obs_threshold given P_i > 1 */
+  int64_t inflight_nodes;          /* nodes with O != 0 after a wave (every launch backed up or cancelled) */
+  int64_t conservation_violations; /* searches with launched != completed + cancelled after a wave */
+  int64_t root_mismatches;         /* searches whose root N != completed_rollouts after a wave */
+  int64_t max_wave_launched;       /* largest number of rollouts in flight in one wave */
+  int64_t max_running;             /* largest run queue */
+} ts_invariants;
+int ts_engine_set_checks(ts_engine* eng, int32_t enable);
+int ts_read_invariants(ts_engine* eng, ts_invariants* host_out, void* stream);
 
 /* ---- readout ------------------------------------------------------------ */
 /* Device→host SearchOutcome records for local searches [0, n). */

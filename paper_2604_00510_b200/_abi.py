@@ -12,7 +12,7 @@ import os
 
 TS_MAX_DEPTH = 32
 TS_MAX_WIDTH = 32
-TS_ABI_VERSION = 3
+TS_ABI_VERSION = 4
 
 TS_OK = 0
 TS_INVALID_ARGUMENT = 1
@@ -111,6 +111,15 @@ class TsRunStats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class TsInvariants(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int64) for name in (
+        "waves", "capacity_violations", "gate_violations", "inflight_nodes", "conservation_violations",
+        "root_mismatches", "max_wave_launched", "max_running")]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 # Every symbol include/treeserve_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
     "ts_engine_create", "ts_engine_destroy", "ts_last_error", "ts_abi_version",
@@ -119,7 +128,7 @@ EXPORTED = (
     "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
     "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
     "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
-    "ts_generate_steps",
+    "ts_generate_steps", "ts_engine_set_checks", "ts_read_invariants",
 )
 
 
@@ -270,6 +279,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_beam_expand": (ctypes.c_int, [P(TsBeamConfig), vp, i32, vp, vp, vp, vp, vp]),
         "ts_beam_prune": (ctypes.c_int, [vp, i32, i32, vp]),
         "ts_generate_steps": (ctypes.c_int, [vp, i32, vp, vp, i32, vp, vp, vp]),
+        "ts_engine_set_checks": (ctypes.c_int, [vp, i32]),
+        "ts_read_invariants": (ctypes.c_int, [vp, P(TsInvariants), vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

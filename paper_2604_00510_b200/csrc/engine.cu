@@ -81,6 +81,10 @@ struct Counters {
   int sum_fallbacks, sched_error;
   unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
   unsigned long long prof[32];  // TS_HEAVY_PROF diagnostics (cycles), zero otherwise
+  // invariant checks (ts_engine_set_checks): ts_invariants in order, and the
+  // current wave's Σ launched rollouts
+  long long inv[8];
+  long long inv_wave;
 };
 
 // Kernel-side view of one engine.
@@ -111,6 +115,7 @@ struct View {
   int32_t* sl;             // scratch lengths
   const double* log1p_tab; // log1p(k) computed by the host libm, k < log1p_n
   int32_t log1p_n;
+  int32_t checks;          // ts_engine_set_checks: invariant kernels around every wave
   int32_t n_local, goff, n_global;
   unsigned long long* step_times;
   int32_t step_times_cap;
@@ -862,6 +867,7 @@ struct MtLayout {
   MtThr* thr;
   long long* b2;  // run counts per CTA, list 0 then list 1
   long long* b3;  // Σ cnt*(want-1) per run-CTA, list 0 then list 1
+  long long* b3p; // exclusive prefixes of b3 (k_mt_all with more run blocks than MT_RB)
   MtState* st;
   uint8_t* hflag; // pipelined-mode flag per local search
 };
@@ -880,6 +886,8 @@ __host__ __device__ inline size_t mt_layout(unsigned char* base, int n, int n_lo
   if (L) L->b2 = (long long*)(base + o);
   o = mt_align(o + sizeof(long long) * 2 * G);
   if (L) L->b3 = (long long*)(base + o);
+  o = mt_align(o + sizeof(long long) * 2 * G3);
+  if (L) L->b3p = (long long*)(base + o);
   o = mt_align(o + sizeof(long long) * 2 * G3);
   if (L) L->st = (MtState*)(base + o);
   o = mt_align(o + sizeof(MtState));
@@ -1654,8 +1662,9 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
           s_b3[rb] = carry0 + c[0];
           s_b3[MT_RB + rb] = carry1 + c[1];
         } else if (b == 0) {
-          L.b3[rb] = carry0 + c[0];
-          L.b3[G3 + rb] = carry1 + c[1];
+          // a separate array: the other CTAs are still reading the totals in b3
+          L.b3p[rb] = carry0 + c[0];
+          L.b3p[G3 + rb] = carry1 + c[1];
         }
       }
       carry0 += tot[0];
@@ -1667,7 +1676,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     }
     __syncthreads();
   }
-  if (!b3_smem) grid.sync();  // CTA 0 rewrote the global run-block offsets
+  if (!b3_smem) grid.sync();  // CTA 0 wrote the global run-block offsets
 #ifdef TS_SCHED_PROF
   if (blockIdx.x == 0 && threadIdx.x == 0) v.ctr->prof[11 + 5] += globaltimer() - mt_t0;
 #endif
@@ -1696,7 +1705,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
           s_runS[so + k] = v.g_runS[go + k];
           s_runStart[so + k] = v.g_runStart[go + k];
           s_runWant[so + k] = v.g_runWant[go + k];
-          s_runPW[so + k] = v.g_runPW[go + k] + (b3_smem ? s_b3[(q ? MT_RB : 0) + k / MT_T] : L.b3[(q ? G3 : 0) + k / MT_T]);
+          s_runPW[so + k] = v.g_runPW[go + k] + (b3_smem ? s_b3[(q ? MT_RB : 0) + k / MT_T] : L.b3p[(q ? G3 : 0) + k / MT_T]);
         }
       }
       runS = s_runS;
@@ -1707,7 +1716,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
     __syncthreads();
     auto runPW = [&](int off, long long k) {
       if (in_smem) return runPWg[off + k];
-      const long long blk = b3_smem ? s_b3[(off ? MT_RB : 0) + k / MT_T] : L.b3[(off ? G3 : 0) + k / MT_T];
+      const long long blk = b3_smem ? s_b3[(off ? MT_RB : 0) + k / MT_T] : L.b3p[(off ? G3 : 0) + k / MT_T];
       return runPWg[off + k] + blk;
     };
     long long q0 = th.pos0, q1 = th.pos1, k0 = th.rid0 - 1, k1 = th.rid1 - 1;
@@ -3786,6 +3795,79 @@ __global__ void k_outcomes(View v, ts_outcome* out, int n) {
   out[s] = o;
 }
 
+// ---- invariant checks (ts_engine_set_checks) ----------------------------------
+// The reference's run-time invariants, asserted on the device state of every
+// wave (test_acceptance.py:167-187, test_simulator.py:58-64, simulator.py:252-260):
+//  * capacity: Σ_i min(P_i, budget - completed_i) <= M rollouts in flight per
+//    wave (Engine._check_capacity), and |running| <= M;
+//  * serial gate: a search below the observation gate runs one rollout;
+//  * every wave ends with no rollout in flight: O == 0 on every node of every
+//    search the wave touched (each launch is backed up or cancelled);
+//  * conservation: launched == completed + cancelled per search, root N ==
+//    completed_rollouts.
+enum { INV_WAVES = 0, INV_CAPACITY, INV_GATE, INV_INFLIGHT, INV_CONSERVATION, INV_ROOT, INV_MAX_LAUNCH,
+       INV_MAX_RUNNING };
+
+__global__ void __launch_bounds__(1024) k_check_pre(View v) {
+  Counters* c = v.ctr;
+  const int nw = c->work_count, nh = c->heavy_count;
+  long long sum = 0, gate = 0;
+  for (int i = threadIdx.x; i < nw + nh; i += blockDim.x) {
+    const int s = i < nw ? v.work[i] : v.work_heavy[i - nw];
+    const int done = v.st[s].completed;
+    const int P = v.tgt[s];
+    sum += min(P, v.cfg.rollout_budget - done);
+    if (done < v.cfg.obs_threshold && P > 1) ++gate;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    sum += __shfl_xor_sync(FULL, sum, o);
+    gate += __shfl_xor_sync(FULL, gate, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd((unsigned long long*)&c->inv_wave, (unsigned long long)sum);
+    if (gate) atomicAdd((unsigned long long*)&c->inv[INV_GATE], (unsigned long long)gate);
+  }
+  if (threadIdx.x == 0 && nw + nh > 0) {
+    const long long run = c->running;
+    if (run > c->inv[INV_MAX_RUNNING]) c->inv[INV_MAX_RUNNING] = run;
+    if (run > v.cfg.max_concurrency) c->inv[INV_CAPACITY] += 1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_check_post(View v) {
+  Counters* c = v.ctr;
+  const int nw = c->work_count, nh = c->heavy_count;
+  __shared__ unsigned long long s_bad;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && nw + nh > 0) {
+    const long long w = c->inv_wave;
+    c->inv_wave = 0;
+    c->inv[INV_WAVES] += 1;
+    if (w > c->inv[INV_MAX_LAUNCH]) c->inv[INV_MAX_LAUNCH] = w;
+    if (w > v.cfg.max_concurrency) c->inv[INV_CAPACITY] += 1;
+  }
+  for (int i = blockIdx.x; i < nw + nh; i += gridDim.x) {
+    const int s = i < nw ? v.work[i] : v.work_heavy[i - nw];
+    const SearchState st = v.st[s];
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    const size_t base = (size_t)s * (size_t)v.cap;
+    unsigned long long bad = 0;
+    for (int k = threadIdx.x; k < st.nodes; k += blockDim.x) bad += (v.no[base + k] >> 32) != 0 ? 1 : 0;
+    bad = __reduce_add_sync(FULL, (unsigned)bad);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&s_bad, bad);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_bad) atomicAdd((unsigned long long*)&c->inv[INV_INFLIGHT], s_bad);
+      if (st.status == TS_OK) {
+        if (st.launched != st.completed + st.cancelled)
+          atomicAdd((unsigned long long*)&c->inv[INV_CONSERVATION], 1ull);
+        if ((int)(uint32_t)v.no[base] != st.completed) atomicAdd((unsigned long long*)&c->inv[INV_ROOT], 1ull);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 // ============================================================================
@@ -3856,6 +3938,7 @@ struct ts_engine {
   cudaGraphExec_t run_exec = nullptr;
   View run_view;
   bool graph_failed = false;
+  int checks = 0;        // ts_engine_set_checks
   int graph_unroll = 3;  // scheduler passes + waves per iteration of the graph's while loop (TS_GRAPH_UNROLL)
 };
 
@@ -3921,6 +4004,7 @@ View make_view(ts_engine* e) {
   v.sl = e->sl;
   v.log1p_tab = e->log1p_tab;
   v.log1p_n = e->log1p_n;
+  v.checks = e->checks;
   v.n_local = e->n_local;
   v.goff = e->goff;
   v.n_global = e->n_global;
@@ -4127,11 +4211,29 @@ int build_run_graph(ts_engine* e, const View& v) {
   // The body holds `graph_unroll` scheduler passes and waves: an edge inside
   // the body is cheaper than the loop's back edge (conditional node + launch).
   // A pass after the batch is done finds nothing to do (empty work lists).
+  // invariant checks (ts_engine_set_checks): k_check_pre after the pass,
+  // k_check_post after the wave kernels
+  void* a4[] = {(void*)&vv};
+  cudaKernelNodeParams kc1;
+  memset(&kc1, 0, sizeof(kc1));
+  kc1.func = (void*)k_check_pre;
+  kc1.gridDim = dim3(1);
+  kc1.blockDim = dim3(1024);
+  kc1.kernelParams = a4;
+  cudaKernelNodeParams kc2 = kc1;
+  kc2.func = (void*)k_check_post;
+  kc2.gridDim = dim3(2 * e->sm_count);
+  kc2.blockDim = dim3(256);
   cudaGraphNode_t prev[2];
   int nprev = 0;
   for (int u = 0; u < e->graph_unroll; ++u) {
     cudaGraphNode_t n1, n2, n3;
     TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n1, body, nprev ? prev : nullptr, nprev, &k1));
+    if (v.checks) {
+      cudaGraphNode_t nc;
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nc, body, &n1, 1, &kc1));
+      n1 = nc;
+    }
     TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
     prev[0] = n2;
     nprev = 1;
@@ -4139,6 +4241,12 @@ int build_run_graph(ts_engine* e, const View& v) {
       TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n3, body, &n1, 1, &k3));
       prev[1] = n3;
       nprev = 2;
+    }
+    if (v.checks) {
+      cudaGraphNode_t nc;
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nc, body, prev, nprev, &kc2));
+      prev[0] = nc;
+      nprev = 1;
     }
   }
   TS_CUDA_TRY(e, cudaGraphInstantiate(&e->run_exec, g, 0));
@@ -4156,6 +4264,10 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
       e->wave_ev.push_back(ev);
     }
   }
+  if (v.checks) {
+    k_check_pre<<<1, 1024, 0, s>>>(v);
+    TS_LAUNCH_CHECK(e, "k_check_pre");
+  }
   cudaEventRecord(e->wave_ev[e->wave_ev_used], s);
   const int k = wave_index(e);
   kWave[k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
@@ -4163,6 +4275,10 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   if ((rc = launch_heavy(e, v, step, s))) return rc;
   cudaEventRecord(e->wave_ev[e->wave_ev_used + 1], s);
   e->wave_ev_used += 2;
+  if (v.checks) {
+    k_check_post<<<2 * e->sm_count, 256, 0, s>>>(v);
+    TS_LAUNCH_CHECK(e, "k_check_post");
+  }
   return TS_OK;
 }
 
@@ -4555,7 +4671,7 @@ static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cu
       // every iteration runs graph_unroll passes of {k_sched, k_wave[, k_heavy]}; the
       // last one contains the pass that ended the loop
       const long long iters = (c.step - step0) / e->graph_unroll + 1;
-      e->launches += iters * e->graph_unroll * (v.heavy_on ? 3 : 2);
+      e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.checks ? 2 : 0));
     }
     step0 = c.step;
     if (c.finished >= e->n_local || c.step >= max_steps) break;
@@ -4701,6 +4817,29 @@ int ts_dump_tree(ts_engine* e, int32_t search, int32_t* parent, double* reward, 
     if (depth) depth[i] = (int32_t)(m & M_DEPTH);
     if (step_ref) step_ref[i] = i == 0 ? -1 : (int32_t)((m >> SH_REF) & 31u);
   }
+  return TS_OK;
+}
+
+int ts_engine_set_checks(ts_engine* e, int32_t enable) {
+  if (!e) return TS_INVALID_ARGUMENT;
+  e->checks = enable ? 1 : 0;
+  return TS_OK;
+}
+
+int ts_read_invariants(ts_engine* e, ts_invariants* o, void* stream) {
+  if (!e || !o) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  if (!e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  Counters c;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  TS_CUDA_TRY(e, cudaStreamSynchronize((cudaStream_t)stream));
+  o->waves = c.inv[INV_WAVES];
+  o->capacity_violations = c.inv[INV_CAPACITY];
+  o->gate_violations = c.inv[INV_GATE];
+  o->inflight_nodes = c.inv[INV_INFLIGHT];
+  o->conservation_violations = c.inv[INV_CONSERVATION];
+  o->root_mismatches = c.inv[INV_ROOT];
+  o->max_wave_launched = c.inv[INV_MAX_LAUNCH];
+  o->max_running = c.inv[INV_MAX_RUNNING];
   return TS_OK;
 }
 

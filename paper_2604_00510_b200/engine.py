@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 from . import _abi
-from ._abi import TsConfig, TsOutcome, TsProblem, TsRunStats, load_library, raise_for_status
+from ._abi import TsConfig, TsInvariants, TsOutcome, TsProblem, TsRunStats, load_library, raise_for_status
 from .config import SearchConfig
 
 
@@ -106,6 +106,16 @@ class Engine:
         st = TsRunStats()
         self._check(self.lib.ts_read_stats(self._h, ctypes.byref(st), self.stream), "ts_read_stats")
         return st
+
+    def set_checks(self, enable: bool = True) -> None:
+        """Run the invariant kernels around every wave (ts_engine_set_checks)."""
+        self._check(self.lib.ts_engine_set_checks(self._h, 1 if enable else 0), "ts_engine_set_checks")
+
+    def invariants(self) -> dict:
+        """Violation counts of the checked mode since the last load (ts_read_invariants)."""
+        inv = TsInvariants()
+        self._check(self.lib.ts_read_invariants(self._h, ctypes.byref(inv), self.stream), "ts_read_invariants")
+        return inv.as_dict()
 
     def outcomes(self, n: Optional[int] = None):
         n = self.n if n is None else n

@@ -632,7 +632,23 @@ def gen_workload_json():
     dump("workload_json", out)
 
 
+def gen_arrivals():
+    """Config-5 arrival steps at full size (65,536 Poisson arrivals, simulator.py:193-200):
+    the reference generator's cumulative times t_i (``rng.exponential(rate, seed, 21, i)``)
+    quantised to waves as int(t_i * steps_per_unit); the first 256 times are stored too."""
+    out = {}
+    for name, n, rate, seed, spu in (("c5", 65536, 1.0, 20260810, 1.0 / 2800.0), ("cli_500", 500, 5.0, 20260810, 20.0)):
+        t, times, steps = 0.0, [], []
+        for i in range(n):
+            t += rng.exponential(rate, seed, 21, i)
+            times.append(t)
+            steps.append(int(t * spu))
+        out[name] = {"n": n, "rate": rate, "seed": seed, "steps_per_unit": spu, "times_head": times[:256],
+                     "steps": steps}
+    dump("arrivals", out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps", "workload_json"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps", "workload_json", "arrivals"]
     for w in which:
         globals()["gen_" + w]()

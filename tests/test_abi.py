@@ -35,7 +35,7 @@ def test_header_and_mirror_agree():
 def test_library_exports_every_declared_symbol(lib):
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.ts_abi_version() == 3
+    assert lib.ts_abi_version() == 4
 
 
 def test_struct_layouts_match_header():

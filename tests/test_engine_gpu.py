@@ -149,10 +149,12 @@ def _random_targets_case(rng, n, lockstep):
     return M, now, rows
 
 
-@pytest.mark.parametrize("n", [1, 7, 300, 1025, 5000, 20000])
+@pytest.mark.parametrize("n", [1, 7, 300, 1025, 5000, 20000, 70000, 140000])
 def test_compute_targets_random_vs_oracle(n):
     """Larger pools (multi-chunk scans, long runs, lock-step ties) vs the oracle's
-    literal sorted loop (scheduler.py:143-187 restated in oracle/ts_oracle.c)."""
+    literal sorted loop (scheduler.py:143-187 restated in oracle/ts_oracle.c).
+    Above 65,536 records the cooperative k_mt_all keeps its run-block offsets
+    in global memory (the phase-7 path)."""
     import torch
 
     from paper_2604_00510_b200._abi import TsConfig, TsSchedRecord

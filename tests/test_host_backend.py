@@ -64,3 +64,18 @@ def test_make_workload_validation():
         B.make_workload(0, MIX, 0)
     with pytest.raises(ValueError):
         B.make_workload(5, (0.5, 0.5, 0.5), 0)
+
+
+def test_serving_arrival_steps_match_reference_generator():
+    """backend.serving_arrival_steps (config 5: 65,536 Poisson arrivals) equals
+    the reference generator's cumulative exponential times quantised to waves
+    (simulator.py:193-200; fixture from tests/golden/make_golden.py gen_arrivals)."""
+    from paper_2604_00510_b200 import keyed
+
+    for name, case in load("arrivals").items():
+        got = B.serving_arrival_steps(case["n"], case["rate"], case["seed"], case["steps_per_unit"])
+        assert got == case["steps"], name
+        t = 0.0
+        for i, want in enumerate(case["times_head"]):
+            t += keyed.exponential_draw(case["rate"], case["seed"], B.TAG_ARRIVAL, i)
+            assert t == want, (name, i)
