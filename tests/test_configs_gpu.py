@@ -111,7 +111,8 @@ def assert_negative_exit_on_unsolvable(specs, outs, cfg, label):
     from paper_2604_00510_b200 import backend as B
 
     unsolvable = [i for i, s in enumerate(specs) if s.difficulty is B.Difficulty.UNSOLVABLE]
-    assert unsolvable, label
+    if not unsolvable:  # config 4 is all HARD_SOLVABLE (stagnation profile)
+        return
     bad = [i for i in unsolvable if outs[i].exit_kind != 2]
     assert not bad, f"{label}: unsolvable searches without a negative exit: {bad[:10]}"
 
