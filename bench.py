@@ -44,6 +44,15 @@ def workload(n_total: int):
     return B.make_workload(n_total, (0.6, 0.25, 0.15), 0, branching=BRANCH, depth_ranges=D)
 
 
+def config_dict(n_total: int, n_gpus: int) -> dict:
+    """The workload description, identical in both arms (--impl ours|reference)."""
+    return {"workload": f"c2: {PER_GPU}/GPU searches, b={BRANCH}, depth {BASE + 1}, budget {BUDGET}, "
+                        f"PE+NE+boost, M={n_total}",
+            "searches": n_total, "branching": BRANCH, "depth": BASE + 1, "rollout_budget": BUDGET,
+            "max_concurrency": n_total, "parallelism": f"search-sharded x{n_gpus}",
+            "l2": "flushed (512 MiB write) before every timed step; node pool > L2"}
+
+
 def search_config(M: int, exits: bool = True):
     from paper_2604_00510_b200.config import SearchConfig
     from paper_2604_00510_b200.scheduler import SchedulerConfig
@@ -136,6 +145,9 @@ class Dist:
         # TS_BENCH_BACKEND=gloo runs the N>1 path with several ranks on one GPU
         # (validation of the sharded driver only; the measured path is NCCL)
         self.backend = os.environ.get("TS_BENCH_BACKEND", "nccl")
+        if self.backend == "nccl" and self.world > torch.cuda.device_count():
+            raise SystemExit(f"bench.py: {self.world} ranks over NCCL need {self.world} GPUs, this node has "
+                             f"{torch.cuda.device_count()} (TS_BENCH_BACKEND=gloo validates N ranks on one GPU)")
         if self.backend != "nccl":
             self.local = self.local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(self.local)
@@ -345,30 +357,31 @@ def bench_ours(args, d: Dist):
                    "wave_frac": b2 / (wms2 / 1e3) / 1e9 / hbm}
         eng2.close()
 
+    c3 = c3_rollout_step(table, lo, n_total, d, flush, args)
     extra = other_paths(table, flush, args) if N == 1 else {}
 
-    cpu = cpu_baseline(PER_GPU, n_total) if (d.rank == 0 and N == 1 and not args.no_cpu) else None
+    cpu = cpu_baseline(n_total, args.steps, args.warmup) if (d.rank == 0 and N == 1 and not args.no_cpu) else None
     if d.rank != 0:
         eng.close()
         return None
     hbm, src = peaks()
     achieved = byte_total / (wave_ms / 1e3) / 1e9 if wave_ms > 0 else 0.0
-    traffic = None
-    try:  # DRAM bytes of the same wave kernels over one batch, from the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_dram_c2_full.json")) as f:
-            kk = json.load(f)["kernels"]
-        traffic = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in kk.values())
-    except Exception:
-        pass
+    traffic, traffic_src = None, None
+    for rnd in ("r02", "r01"):  # DRAM bytes of the same wave kernels over one batch, newest ncu capture
+        path = os.path.join(ROOT, "profiles", f"{rnd}_ncu_dram_c2_full.json")
+        try:
+            with open(path) as f:
+                kk = json.load(f)["kernels"]
+            traffic = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in kk.values())
+            traffic_src = os.path.relpath(path, ROOT)
+            break
+        except Exception:
+            continue
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64+u64", "data": "synthetic (reference make_workload generator, seed 0)",
-        "config": {"workload": f"c2: {PER_GPU}/GPU searches, b={BRANCH}, depth {BASE + 1}, budget {BUDGET}, "
-                               f"PE+NE+boost, M={n_total}",
-                   "searches": n_total, "branching": BRANCH, "depth": BASE + 1, "rollout_budget": BUDGET,
-                   "max_concurrency": n_total, "parallelism": f"search-sharded x{N}",
-                   "l2": "flushed (512 MiB write) before every timed step; node pool > L2"},
+        "config": config_dict(n_total, N),
         "p99_search_latency_ms": percentile(lat, 99), "p50_search_latency_ms": percentile(lat, 50),
         "rollouts_per_step": rollouts_all / args.steps, "exits": exits,
         "e2e": e2e,
@@ -376,14 +389,58 @@ def bench_ours(args, d: Dist):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                      "traffic": traffic, "kernel": "k_wave + k_heavy (the wave phase of one batch)",
                      "peak_source": src, "algorithmic_bytes": byte_total, "wave_ms": wave_ms,
-                     "traffic_note": "ncu dram__bytes_read+write of every k_wave/k_heavy launch of one batch "
-                                     "(profiles/r01_ncu_dram_c2_full.json), per batch like algorithmic_bytes; "
+                     "traffic_note": f"ncu dram__bytes_read+write of every k_wave/k_heavy launch of one batch "
+                                     f"({traffic_src}, tools/profile_round.sh on the benchmarked build), per batch "
+                                     "like algorithmic_bytes; "
                                      "below the algorithmic bytes because the trees stay L2-resident",
                      "regime": "latency-bound: the boosted tail wave is sequential per search by definition"},
-        "cpu_baseline": cpu, "clocks": clk, "variants": {"exits_off": variant, **extra},
+        "cpu_baseline": cpu, "clocks": clk, "variants": {"exits_off": variant, "c3_rollout_step": c3, **extra},
     }
     eng.close()
     return line
+
+
+def c3_rollout_step(table, lo, n_total, d: Dist, flush, args) -> dict:
+    """Config 3's shape on N GPUs: 4096 searches per GPU of a 4096*N run queue,
+    M = 4 * 4096 * N (4 parallel rollouts per ungated search with virtual
+    loss), exits off so every wave advances every search; `ms_per_wave` is the
+    north star's "one rollout step" (max over ranks, device-timed)."""
+    import torch
+
+    from paper_2604_00510_b200.engine import Engine
+
+    N = d.world
+    eng = Engine(search_config(4 * n_total, exits=False), d.local)
+    sharded = None
+    if N > 1:
+        from paper_2604_00510_b200.distributed import ShardedRun
+
+        sharded = ShardedRun(eng, d.pg, PER_GPU, n_total, torch.device("cuda", d.local),
+                             host_staging=d.backend != "nccl")
+    run = (lambda: eng.run()) if N == 1 else (lambda: sharded.run())  # noqa: E731
+    eng.load(table, lo, n_total)
+    run()
+    stream = torch.cuda.current_stream()
+    ts, waves, ro = [], 0, 0
+    for _ in range(max(3, min(args.steps, 5))):
+        eng.load(table, lo, n_total)
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        d.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        w = run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(d.max(e0.elapsed_time(e1)))
+        st = eng.stats()
+        waves = st.steps if N == 1 else w
+        ro = d.sum(st.rollouts)
+    eng.close()
+    ms = statistics.median(ts)
+    return {"workload": f"c3 shape: {PER_GPU}/GPU searches of {n_total}, M={4 * n_total} (P=4), exits off",
+            "value": ro / (ms / 1e3), "unit": UNIT, "ms_per_batch": ms, "waves": waves,
+            "ms_per_wave": ms / max(1, waves), "rollouts_per_batch": ro}
 
 
 def other_paths(table, flush, args) -> dict:
@@ -446,74 +503,106 @@ def other_paths(table, flush, args) -> dict:
 
 
 # --------------------------------------------------------------------------- CPU
-def cpu_baseline(per_gpu: int, n_total: int, target_s: float = 12.0):
-    """The C oracle (a restatement of the reference, oracle/) on the host cores:
-    a bounded sample of the same workload (the first S searches, M scaled)."""
-    from oracle import oracle
-    from paper_2604_00510_b200.backend import problem_table
-
-    threads = os.cpu_count() or 1
-    specs = workload(n_total)
-    sample = 256
-    while True:
-        t = problem_table(specs[:sample])
-        cfg = search_config(sample).to_c()
-        t0 = time.perf_counter()
-        r = oracle.OracleRun(t, cfg, threads=threads)
-        dt = time.perf_counter() - t0
-        ro = r.stats.rollouts
-        lat = (r.latencies_s() * 1e3).tolist()
-        r.close()
-        if dt > target_s / 4 or sample >= per_gpu:
-            break
-        sample = min(per_gpu, sample * 4)
-    # one host core on the same sample (SURVEY §8(d): single core and all cores)
-    t1 = time.perf_counter()
-    r1 = oracle.OracleRun(t, cfg, threads=1)
-    dt1 = time.perf_counter() - t1
-    ro1 = r1.stats.rollouts
-    r1.close()
-    return {"value": ro / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {sample} of the {per_gpu} searches, M={sample}, same budget/exits/boosting; "
-                      f"{ro} rollouts in {dt:.2f} s",
-            "p99_search_latency_ms": percentile(lat, 99),
-            "single_core_value": ro1 / dt1}
-
-
-def bench_reference(args):
-    """--impl reference: the reference algorithm on the host cores (oracle port;
-    the Python reference itself is not present on the GPU box)."""
+def oracle_batches(n_total: int, steps: int, warmup: int, threads: int):
+    """The reference algorithm (the C restatement in oracle/, test
+    infrastructure) over the whole n_total-search batch on `threads` host
+    threads: `warmup` untimed batches, then `steps` timed ones.  Both arms
+    time the CPU this way (same batch, warm-up and repetitions; median)."""
     from oracle import oracle
     from paper_2604_00510_b200.backend import problem_table
 
     oracle.build()
-    threads = os.cpu_count() or 1
-    specs = workload(PER_GPU)
-    sample = PER_GPU  # the whole config-2 batch: ~30 ms per step on 16 host threads
-    t = problem_table(specs[:sample])
-    cfg = search_config(sample).to_c()
-    for _ in range(args.warmup):
+    t = problem_table(workload(n_total))
+    cfg = search_config(n_total).to_c()
+    for _ in range(warmup):
         oracle.OracleRun(t, cfg, threads=threads).close()
     times, ro, lat = [], 0, []
-    for _ in range(args.steps):
+    for _ in range(steps):
         t0 = time.perf_counter()
         r = oracle.OracleRun(t, cfg, threads=threads)
         times.append(time.perf_counter() - t0)
-        ro += r.stats.rollouts
+        ro = r.stats.rollouts
         lat.extend((r.latencies_s() * 1e3).tolist())
         r.close()
-    value = ro / sum(times)
+    med = statistics.median(times)
+    return {"value": ro / med, "ms_per_step": 1e3 * med, "rollouts_per_step": ro,
+            "p99_search_latency_ms": percentile(lat, 99)}
+
+
+def python_reference_sample(n: int = 64):
+    """The UNMODIFIED Python reference (treeserve, installed into baseline/_ref)
+    on the first n searches of the same workload, composed into waves only of
+    reference calls (tests/golden/wave_ref.py); one host core.  None when the
+    reference is not importable on this machine."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(ref) and ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        import wave_ref
+        from treeserve.backend import Difficulty, make_workload
+        from treeserve.scheduler import SchedulerConfig as RefSched
+    except Exception as e:  # pragma: no cover - reference absent
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    finally:
+        sys.path.pop(0)
+    specs = make_workload(PER_GPU, (0.6, 0.25, 0.15), 0, branching=BRANCH,
+                          depth_ranges={d: (BASE, BASE) for d in Difficulty})[:n]
+    t0 = time.perf_counter()
+    recs, info = wave_ref.run_waves(specs, sched=RefSched(max_concurrency=n), rollout_budget=BUDGET,
+                                    depth_cap=DEPTH_CAP, expand_width=WIDTH)
+    dt = time.perf_counter() - t0
+    ro = sum(r["rollouts_completed"] for r in recs)
+    return {"value": ro / dt, "unit": UNIT, "cores": 1, "rollouts": ro, "s": dt,
+            "sample": f"first {n} searches of the same workload, M={n}, unmodified Python reference"}
+
+
+def cpu_baseline(n_total: int, steps: int, warmup: int):
+    """The CPU oracle timed like the reference arm, plus one-core and
+    Python-reference samples for context."""
+    threads = os.cpu_count() or 1
+    full = oracle_batches(n_total, steps, warmup, threads)
+    one = oracle_batches(n_total, max(1, min(steps, 3)), 1, 1)
+    return {"value": full["value"], "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"the whole {n_total}-search batch per step, {warmup} warm-up + {steps} timed batches, "
+                      f"median ({full['ms_per_step']:.1f} ms per batch)",
+            "p99_search_latency_ms": full["p99_search_latency_ms"],
+            "single_core_value": one["value"],
+            "python_reference": python_reference_sample()}
+
+
+def bench_reference(args):
+    """--impl reference: the reference algorithm on the host cores (oracle port;
+    the reference is pure Python and is not what a CPU deployment of this path
+    would time) over the same batch as our arm, all host threads."""
+    N = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    n_total = PER_GPU * N
+    threads = os.cpu_count() or 1
+    r = oracle_batches(n_total, args.steps, args.warmup, threads)
     return {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64", "data": "synthetic",
-        "config": {"workload": f"c2: {PER_GPU}/GPU searches, b={BRANCH}, depth {BASE + 1}, budget {BUDGET}, "
-                               f"PE+NE+boost, M={PER_GPU}", "searches": sample},
-        "p99_search_latency_ms": percentile(lat, 99),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"the full batch of {sample} searches per step"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64+u64",
+        "data": "synthetic (reference make_workload generator, seed 0)",
+        "config": config_dict(n_total, N),
+        "p99_search_latency_ms": r["p99_search_latency_ms"], "rollouts_per_step": r["rollouts_per_step"],
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"the whole {n_total}-search batch per step, median of {args.steps}"},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` without a torchrun environment: re-exec this script
+    as N ranks (one process per GPU) on 127.0.0.1 and pass rank 0's line on."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -524,11 +613,16 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    world = os.environ.get("WORLD_SIZE")
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return
         print(json.dumps(bench_reference(args)))
         return
+    if world is None and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    if world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch N ranks for --gpus N")
     import __graft_entry__
 
     __graft_entry__.build()

@@ -105,7 +105,9 @@ class ShardedRun:
         nothing is ever pending, so those waves skip it (admit_jobs with no
         pending search admits nothing) and the loop test reads the running
         flags of the records every wave instead; otherwise the counts are
-        exchanged every wave and tested every ``check_every`` waves."""
+        exchanged and tested every wave.  Either test is read back after the
+        wave is queued (a finished run costs one empty wave, never a wrong
+        step count).  ``check_every`` is kept for API compatibility."""
         import torch
 
         eng = self.engine
@@ -123,10 +125,12 @@ class ShardedRun:
             if admission:
                 eng.step_counts(step, self.counts.data_ptr())
                 self._gather(self.all_counts, self.counts)
-                if step % self.check_every == 0:
-                    unfinished = int(self.all_counts.view(-1, COUNT_WORDS)[:, 2].sum().item())
-                    if unfinished == 0:
-                        return step
+                # the loop test (no unfinished search on any rank) is read back
+                # after this wave is queued, like the running flags below: the
+                # returned step count is exact and the GPU never idles on it
+                unfinished = self.all_counts.view(-1, COUNT_WORDS)[:, 2].sum()
+                self._flag_host.copy_((unfinished > 0).to(torch.int32).view(1), non_blocking=True)
+                self._flag_event.record()
                 eng.step_admit(step, self.all_counts.data_ptr(), self.world, self.rank)
             else:
                 eng.step_admit(step, no_pending.data_ptr(), self.world, self.rank)
@@ -148,10 +152,9 @@ class ShardedRun:
                 eng.step_wave(step)
                 e1.record()
                 wave_events.append((e0, e1))
-            if not admission:
-                self._flag_event.synchronize()
-                if int(self._flag_host[0]) == 0:
-                    return step
+            self._flag_event.synchronize()
+            if int(self._flag_host[0]) == 0:
+                return step
         return max_steps
 
 

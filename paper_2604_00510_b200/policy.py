@@ -50,6 +50,16 @@ def sched_params(config, positive_exit_threshold: float) -> TsSchedParams:
                          float(positive_exit_threshold))
 
 
+def _torch_stream(stream, device):
+    """The torch stream object for a caller's stream argument (None: current)."""
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(getattr(stream, "cuda_stream", stream)), device=device)
+
+
 def _dev(a, dtype, torch, device):
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=dtype).contiguous()
@@ -64,7 +74,8 @@ def compute_targets_arrays(arrival, best, completed, job_id, now: float, config,
     torch = _torch()
     lib = load_library()
     dev = torch.device("cuda", device)
-    with torch.cuda.device(dev):
+    # the H2D copies and the output live on the stream the kernels run on
+    with torch.cuda.device(dev), torch.cuda.stream(_torch_stream(stream, dev)):
         arr = _dev(arrival, torch.float64, torch, dev)
         bst = _dev(best, torch.float64, torch, dev)
         cmp = _dev(completed, torch.int32, torch, dev)
@@ -89,7 +100,7 @@ def parallelism_scores_arrays(arrival, best, now: float, positive_exit_threshold
     torch = _torch()
     lib = load_library()
     dev = torch.device("cuda", device)
-    with torch.cuda.device(dev):
+    with torch.cuda.device(dev), torch.cuda.stream(_torch_stream(stream, dev)):
         arr = _dev(arrival, torch.float64, torch, dev)
         bst = _dev(best, torch.float64, torch, dev)
         n = int(arr.numel())

@@ -116,7 +116,14 @@ def run_tree_search(
     positive_exit: bool = True,
     negative_exit: bool = True,
 ) -> SearchOutcome:
-    """Reference-signature serial search (search.py:79-88)."""
+    """Reference-signature serial search (search.py:79-88).
+
+    One deviation: with negative exit on, a CUMULATIVE_SUM or AVERAGE scheme
+    raises ``UnsupportedSchemeError`` up front (SearchConfig), where the
+    reference raises lazily inside ``classify_leaf`` (scoring.py:119-127) and
+    so returns normally for a search whose tree never holds a check-relevant
+    expandable leaf when an exit check runs (e.g. every depth-1 step below
+    ``first_step_threshold``, or a positive exit at the first rollout)."""
     return run_tree_searches([problem], scoring, selection, rollout_budget, depth_cap, expand_width,
                              positive_exit, negative_exit)[0]
 

@@ -1,15 +1,18 @@
-"""All five BASELINE.json configs on one B200, each with the CPU oracle timed
-beside it on a bounded sample.  Writes one JSON object per config.
+"""Every BASELINE.json config at its STATED size on one B200, with the CPU
+oracle run over the same whole batch on all host threads: the oracle run is
+both the parity check (every outcome field and best path, bit for bit) and the
+CPU baseline.  Writes one JSON object per config.
 
     python tools/bench_configs.py [--out profiles/rNN_configs.json] [--only c1,c2,...]
 
-c1  reference CPU demo: 64 searches, b=4, depth 8, 32 rollouts, PE+NE+boost, M=64
-c2  4096 searches, b=4, depth 16, 128 rollouts, PE+NE+boost, M=4096 (also exits off)
-c3  one GPU's shard of config 3: 4096 searches, M = 4x4096 (4 parallel rollouts per
-    ungated search with virtual loss), exits off so every search runs its budget
-c4  deep-tree stress: 1024 searches, b=8, depth 32, 1024 rollouts, stagnation profile
-c5  serving: 65536 Poisson arrivals (reference generator, step-quantised), M=4096,
-    arms pe (positive exit only, no boosting) vs pe_ne_boost; p99 arrival→exit latency
+c1      reference CPU demo: 64 searches, b=4, depth 8, 32 rollouts, PE+NE+boost, M=64
+c2      4096 searches, b=4, depth 16, 128 rollouts, PE+NE+boost, M=4096
+c2off   the same, exits off (every search runs its budget)
+c3      32,768 searches, M = 4 x 32,768 (P = 4 per ungated search, virtual loss), PE+NE+boost
+c3off   the same, exits off
+c4      deep-tree stress: 1024 searches, b=8, depth 32, 1024 rollouts, stagnation profile
+c5_*    serving: 65,536 Poisson arrivals (reference generator, step-quantised), M=4096,
+        arms pe (positive exit only, no boosting) and pe_ne_boost; p99 arrival→exit latency
 """
 
 from __future__ import annotations
@@ -23,17 +26,13 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import torch  # noqa: E402
 
 from oracle import oracle  # noqa: E402
-from paper_2604_00510_b200 import backend as B  # noqa: E402
-from paper_2604_00510_b200 import keyed  # noqa: E402
-from paper_2604_00510_b200.config import SearchConfig  # noqa: E402
 from paper_2604_00510_b200.engine import Engine  # noqa: E402
-from paper_2604_00510_b200.scheduler import SchedulerConfig  # noqa: E402
 
-MIX = (0.6, 0.25, 0.15)
 THREADS = os.cpu_count() or 1
 
 
@@ -88,84 +87,42 @@ def cpu_run(table, cfg, arrivals=None):
     return res, outs
 
 
+OUT_KEYS = ("exit_kind", "rollouts_completed", "tokens_generated", "best_score", "best_len", "solved",
+            "exit_step", "admit_step", "launched", "cancelled", "nodes", "status")
+
+
 def parity(g, c, n):
-    keys = ("exit_kind", "rollouts_completed", "tokens_generated", "best_score", "exit_step", "launched", "nodes")
-    return all(getattr(g[i], k) == getattr(c[i], k) for i in range(n) for k in keys)
+    """Every outcome field and best path of all n searches, bit for bit."""
+    return all(getattr(g[i], k) == getattr(c[i], k) for i in range(n) for k in OUT_KEYS) and all(
+        bytes(g[i].best_path[: g[i].best_len]) == bytes(c[i].best_path[: c[i].best_len]) for i in range(n))
 
 
-def cfg_of(M, budget, cap, width, pe=True, ne=True, boost=True):
-    return SearchConfig(scheduler=SchedulerConfig(max_concurrency=M, boosting_enabled=boost), rollout_budget=budget,
-                        depth_cap=cap, expand_width=width, positive_exit=pe, negative_exit=ne)
+def run_config(name, reps=3):
+    """A BASELINE config at its stated size (tests/test_configs_gpu.config_case):
+    the engine's timed batch, and the oracle over the WHOLE batch on all host
+    threads, which is both the parity check and the CPU baseline."""
+    from test_configs_gpu import config_case
 
-
-def c1():
-    specs = B.make_workload(64, MIX, 0, branching=4, depth_ranges={d: (7, 7) for d in B.Difficulty})
-    t = B.problem_table(specs)
-    cfg = cfg_of(64, 32, 8, 4)
-    g, go = gpu_run(t, cfg)
+    specs, t, cfg = config_case(name)
+    arrivals = [int(p.arrival_step) for p in t] if name.startswith("c5") else None
+    g, go = gpu_run(t, cfg, arrivals, reps=reps)
     c, co = cpu_run(t, cfg)
-    return {"gpu": g, "cpu": c, "cpu_sample": "all 64", "parity_vs_oracle": parity(go, co, 64)}
-
-
-def c2(exits=True):
-    specs = B.make_workload(4096, MIX, 0, branching=4, depth_ranges={d: (15, 15) for d in B.Difficulty})
-    t = B.problem_table(specs)
-    cfg = cfg_of(4096, 128, 16, 4, exits, exits)
-    g, go = gpu_run(t, cfg)
-    n = 4096 if exits else 512
-    cs = B.problem_table(specs[:n])
-    c, co = cpu_run(cs, cfg_of(n, 128, 16, 4, exits, exits))
-    return {"gpu": g, "cpu": c, "cpu_sample": f"first {n} searches, M={n}",
-            "parity_vs_oracle": parity(go, co, n) if n == 4096 else None}
-
-
-def c3():
-    specs = B.make_workload(4096, MIX, 0, branching=4, depth_ranges={d: (15, 15) for d in B.Difficulty})
-    t = B.problem_table(specs)
-    g, go = gpu_run(t, cfg_of(4 * 4096, 128, 16, 4, False, False))
-    cs = B.problem_table(specs[:256])
-    c, co = cpu_run(cs, cfg_of(4 * 256, 128, 16, 4, False, False))
-    return {"gpu": g, "cpu": c, "cpu_sample": "first 256 searches, M=1024", "note": "one GPU's shard of config 3"}
-
-
-def c4(n=1024):
-    specs = [B.make_problem(f"s{i:04d}", keyed.mix(0, 8, i), B.Difficulty.HARD_SOLVABLE, (31, 31), 8,
-                            B.stagnation_profile()) for i in range(n)]
-    t = B.problem_table(specs)
-    g, go = gpu_run(t, cfg_of(n, 1024, 32, 8), reps=1)
-    cs = B.problem_table(specs[:16])
-    c, co = cpu_run(cs, cfg_of(16, 1024, 32, 8))
-    return {"gpu": g, "cpu": c, "cpu_sample": "first 16 searches, M=16"}
-
-
-def c5(n=65536, per_wave=2800.0, M=4096):
-    specs = B.make_workload(n, MIX, 20260810)
-    arrivals = B.serving_arrival_steps(n, 1.0, 20260810, 1.0 / per_wave)
-    t = B.problem_table(specs, arrivals)
-    out = {"arrivals_per_wave": per_wave, "M": M, "arrival_waves": arrivals[-1] + 1}
-    for arm, pe, ne, boost in (("pe", True, False, False), ("pe_ne_boost", True, True, True)):
-        cfg = cfg_of(M, 32, 16, 4, pe, ne, boost)
-        g, go = gpu_run(t, cfg, arrivals, reps=1)
-        ns = 8192
-        cs = B.problem_table(specs[:ns], arrivals[:ns])
-        c, co = cpu_run(cs, cfg)
-        out[arm] = {"gpu": g, "cpu": c, "cpu_sample": f"first {ns} arrivals, same M",
-                    "parity_vs_oracle_first_8192": None}
-    return out
+    n = len(specs)
+    return {"searches": n, "M": cfg.scheduler.max_concurrency, "gpu": g, "cpu": c,
+            "cpu_sample": f"the whole batch ({n} searches) on {THREADS} threads",
+            "parity_vs_oracle": parity(go, co, n), "waves_match": g["waves"] == c["waves"],
+            "speedup": c["s"] * 1e3 / g["ms"]}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
-    ap.add_argument("--only", default="c1,c2,c2off,c3,c4,c5")
+    ap.add_argument("--only", default="c1,c2,c2off,c3,c3off,c4,c5_pe,c5_pe_ne_boost")
     args = ap.parse_args()
     res = {"gpu": torch.cuda.get_device_name(0), "cpu_threads": THREADS}
     for name in args.only.split(","):
         t0 = time.time()
-        if name == "c2off":
-            res[name] = c2(False)
-        else:
-            res[name] = globals()[name]()
+        res[name] = run_config(name, reps=1 if name in ("c3", "c3off", "c4") else 3)
         res[name]["wall_s"] = round(time.time() - t0, 1)
         print(name, json.dumps(res[name]), flush=True)
     if args.out:
