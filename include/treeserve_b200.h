@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 4
+#define TS_ABI_VERSION 5
 #define TS_MAX_DEPTH 32 /* golden path / reward table length; base_depth <= 31 */
 #define TS_MAX_WIDTH 32 /* branching <= one warp                                */
 
@@ -202,6 +202,30 @@ typedef struct ts_invariants {
 int ts_engine_set_checks(ts_engine* eng, int32_t enable);
 int ts_read_invariants(ts_engine* eng, ts_invariants* host_out, void* stream);
 
+/* ---- allocation trace ------------------------------------------------------
+ * Replaces the reference's per-pass trace records (simulator.py:314-341,
+ * written to <preset>_<rate>_trace.jsonl by cli.py:263-265): with a trace
+ * buffer set, one row per running search per scheduler pass is written between
+ * the pass and its wave (ts_run's graph loop and ts_step_wave alike).  The
+ * row holds the "allocation" record's fields; the "action" record follows
+ * from them (reconcile, scheduler.py:199-214: every wave starts with no rollout
+ * in flight, so the action is launch(target)).  Rows are in completion order
+ * of the writing threads; sort by (step, job) for run-queue order. */
+typedef struct ts_trace_row {
+  int32_t step;   /* the pass's step (now = step * dt) */
+  int32_t job;    /* global run-queue index (job_id) */
+  int32_t target; /* compute_targets(...)[job] */
+  int32_t active; /* len(job.active_rollouts) at the pass: 0 in the wave model */
+  double score;   /* parallelism_score(job, now, θ_pos, config) (scheduler.py:118-128) */
+} ts_trace_row;
+/* capacity = rows kept per run (0 frees the buffer and disables the trace);
+ * rows past it are counted as dropped. */
+int ts_engine_set_trace(ts_engine* eng, int64_t capacity);
+/* Rows of the run since the last ts_load_problems: copies min(n, cap) rows,
+ * *n_out = rows held, *dropped = rows lost to a full buffer (may be NULL). */
+int ts_read_trace(ts_engine* eng, ts_trace_row* host_out, int64_t cap, int64_t* n_out, int64_t* dropped,
+                  void* stream);
+
 /* ---- readout ------------------------------------------------------------ */
 /* Device→host SearchOutcome records for local searches [0, n). */
 int ts_read_outcomes(ts_engine* eng, ts_outcome* host_out, int32_t n, void* stream);
@@ -280,6 +304,20 @@ int ts_parallelism_scores(double now, double positive_exit_threshold, double bet
 int ts_compute_targets(const ts_sched_params* params, double now, const double* dev_arrival,
                        const double* dev_best, const int32_t* dev_completed, const int64_t* dev_job_id,
                        int32_t n, int32_t* dev_targets, ts_targets_info* host_info, void* stream);
+
+/* reconcile (scheduler.py:199-214) with choose_preemption_victims (190-196)
+ * over a run queue of n_jobs jobs in run-queue order: job j's in-flight
+ * rollouts (Job.active_rollouts) are entries [offsets[j], offsets[j+1]) of
+ * prefix_score / rollout_id (InflightRollout, scheduler.py:59-62).  Outputs:
+ * launch[j] = target - active when a running job is below its target
+ * (LaunchAction), else 0; victim_rank[r] = the rank of rollout r among its
+ * job's in-flight rollouts by (prefix_score, rollout_id) when it is one of
+ * the active - target victims of a running job above its target
+ * (PreemptAction, emitted in rank order), else -1.  dev_running may be NULL
+ * (every job running; the reference skips jobs whose state is not RUNNING). */
+int ts_reconcile(const int32_t* dev_running, const int32_t* dev_targets, const int64_t* dev_offsets,
+                 const double* dev_prefix_score, const int64_t* dev_rollout_id, int32_t n_jobs, int32_t* dev_launch,
+                 int32_t* dev_victim_rank, void* stream);
 
 /* A forest of SearchTrees (tree.py:117-181) in flat device arrays: tree t owns
  * nodes [offsets[t], offsets[t+1]), its root first; parent[] holds forest

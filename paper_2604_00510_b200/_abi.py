@@ -12,7 +12,7 @@ import os
 
 TS_MAX_DEPTH = 32
 TS_MAX_WIDTH = 32
-TS_ABI_VERSION = 4
+TS_ABI_VERSION = 5
 
 TS_OK = 0
 TS_INVALID_ARGUMENT = 1
@@ -120,6 +120,12 @@ class TsInvariants(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class TsTraceRow(ctypes.Structure):
+    """ts_trace_row: one "allocation" record of a scheduler pass (simulator.py:314-330)."""
+    _fields_ = [("step", ctypes.c_int32), ("job", ctypes.c_int32), ("target", ctypes.c_int32),
+                ("active", ctypes.c_int32), ("score", ctypes.c_double)]
+
+
 # Every symbol include/treeserve_b200.h declares (checked by tests/test_abi.py).
 EXPORTED = (
     "ts_engine_create", "ts_engine_destroy", "ts_last_error", "ts_abi_version",
@@ -128,7 +134,8 @@ EXPORTED = (
     "ts_read_step_times", "ts_read_latencies", "ts_run_batch_host", "ts_tree_size", "ts_dump_tree", "ts_fill_problem",
     "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
     "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
-    "ts_generate_steps", "ts_engine_set_checks", "ts_read_invariants",
+    "ts_generate_steps", "ts_engine_set_checks", "ts_read_invariants", "ts_engine_set_trace", "ts_read_trace",
+    "ts_reconcile",
 )
 
 
@@ -281,6 +288,9 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_generate_steps": (ctypes.c_int, [vp, i32, vp, vp, i32, vp, vp, vp]),
         "ts_engine_set_checks": (ctypes.c_int, [vp, i32]),
         "ts_read_invariants": (ctypes.c_int, [vp, P(TsInvariants), vp]),
+        "ts_engine_set_trace": (ctypes.c_int, [vp, ctypes.c_int64]),
+        "ts_reconcile": (ctypes.c_int, [vp, vp, vp, vp, vp, i32, vp, vp, vp]),
+        "ts_read_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int64), vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

@@ -85,6 +85,8 @@ struct Counters {
   // current wave's Σ launched rollouts
   long long inv[8];
   long long inv_wave;
+  // ts_engine_set_trace: rows written / rows dropped (buffer full)
+  unsigned long long trace_n, trace_drop;
 };
 
 // Kernel-side view of one engine.
@@ -116,6 +118,8 @@ struct View {
   const double* log1p_tab; // log1p(k) computed by the host libm, k < log1p_n
   int32_t log1p_n;
   int32_t checks;          // ts_engine_set_checks: invariant kernels around every wave
+  ts_trace_row* trace;     // ts_engine_set_trace: allocation rows of every pass (null: off)
+  long long trace_cap;
   int32_t n_local, goff, n_global;
   unsigned long long* step_times;
   int32_t step_times_cap;
@@ -3868,6 +3872,33 @@ __global__ void __launch_bounds__(256) k_check_post(View v) {
   }
 }
 
+// ---- allocation trace (ts_engine_set_trace) -------------------------------------
+// One row per running search per scheduler pass, written between the pass and
+// the wave: the fields of the reference's per-pass "allocation" record
+// (simulator.py:314-330): parallelism_score at the pass (the same expressions
+// as the pass's records, scheduler.py:118-128), the target, and the active
+// rollouts (0: every wave ends with none in flight).  The host sorts the rows
+// into run-queue order and adds the "action" records reconcile() would emit.
+__global__ void __launch_bounds__(256) k_trace(View v) {
+  Counters* c = v.ctr;
+  const int nw = c->work_count, nh = c->heavy_count;
+  const int step = c->cur_step;
+  const ts_config& cf = v.cfg;
+  for (int i = threadIdx.x; i < nw + nh; i += blockDim.x) {
+    const int s = i < nw ? v.work[i] : v.work_heavy[i - nw];
+    const double ratio = v.st[s].job_best / cf.positive_exit_threshold;
+    ts_trace_row r;
+    r.step = step;
+    r.job = v.goff + s;
+    r.target = v.tgt[s];
+    r.active = 0;
+    r.score = v.log1p_tab[step - v.arrival[s]] + (ratio > cf.proximity ? cf.beta : 0.0);
+    const unsigned long long k = atomicAdd(&c->trace_n, 1ull);
+    if (k < (unsigned long long)v.trace_cap) v.trace[k] = r;
+    else atomicAdd(&c->trace_drop, 1ull);
+  }
+}
+
 }  // namespace
 
 // ============================================================================
@@ -3939,6 +3970,8 @@ struct ts_engine {
   View run_view;
   bool graph_failed = false;
   int checks = 0;        // ts_engine_set_checks
+  ts_trace_row* trace = nullptr;  // ts_engine_set_trace
+  long long trace_cap = 0;
   int graph_unroll = 3;  // scheduler passes + waves per iteration of the graph's while loop (TS_GRAPH_UNROLL)
 };
 
@@ -4005,6 +4038,8 @@ View make_view(ts_engine* e) {
   v.log1p_tab = e->log1p_tab;
   v.log1p_n = e->log1p_n;
   v.checks = e->checks;
+  v.trace = e->trace;
+  v.trace_cap = e->trace_cap;
   v.n_local = e->n_local;
   v.goff = e->goff;
   v.n_global = e->n_global;
@@ -4224,6 +4259,9 @@ int build_run_graph(ts_engine* e, const View& v) {
   kc2.func = (void*)k_check_post;
   kc2.gridDim = dim3(2 * e->sm_count);
   kc2.blockDim = dim3(256);
+  cudaKernelNodeParams kt = kc1;
+  kt.func = (void*)k_trace;
+  kt.blockDim = dim3(256);
   cudaGraphNode_t prev[2];
   int nprev = 0;
   for (int u = 0; u < e->graph_unroll; ++u) {
@@ -4233,6 +4271,11 @@ int build_run_graph(ts_engine* e, const View& v) {
       cudaGraphNode_t nc;
       TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nc, body, &n1, 1, &kc1));
       n1 = nc;
+    }
+    if (v.trace) {
+      cudaGraphNode_t nt;
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nt, body, &n1, 1, &kt));
+      n1 = nt;
     }
     TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
     prev[0] = n2;
@@ -4267,6 +4310,10 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   if (v.checks) {
     k_check_pre<<<1, 1024, 0, s>>>(v);
     TS_LAUNCH_CHECK(e, "k_check_pre");
+  }
+  if (v.trace) {
+    k_trace<<<1, 256, 0, s>>>(v);
+    TS_LAUNCH_CHECK(e, "k_trace");
   }
   cudaEventRecord(e->wave_ev[e->wave_ev_used], s);
   const int k = wave_index(e);
@@ -4367,7 +4414,7 @@ int ts_engine_destroy(ts_engine* e) {
   void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
-                  e->work_heavy, e->mt, e->tgt, e->nrec};
+                  e->work_heavy, e->mt, e->tgt, e->nrec, e->trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
@@ -4671,7 +4718,7 @@ static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cu
       // every iteration runs graph_unroll passes of {k_sched, k_wave[, k_heavy]}; the
       // last one contains the pass that ended the loop
       const long long iters = (c.step - step0) / e->graph_unroll + 1;
-      e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.checks ? 2 : 0));
+      e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.checks ? 2 : 0) + (v.trace ? 1 : 0));
     }
     step0 = c.step;
     if (c.finished >= e->n_local || c.step >= max_steps) break;
@@ -4823,6 +4870,38 @@ int ts_dump_tree(ts_engine* e, int32_t search, int32_t* parent, double* reward, 
 int ts_engine_set_checks(ts_engine* e, int32_t enable) {
   if (!e) return TS_INVALID_ARGUMENT;
   e->checks = enable ? 1 : 0;
+  return TS_OK;
+}
+
+int ts_engine_set_trace(ts_engine* e, int64_t capacity) {
+  if (!e || capacity < 0) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  if (e->trace) cudaFree(e->trace);
+  e->trace = nullptr;
+  e->trace_cap = 0;
+  if (capacity > 0) {
+    TS_CUDA_TRY(e, cudaSetDevice(e->device));
+    TS_CUDA_TRY(e, cudaMalloc((void**)&e->trace, sizeof(ts_trace_row) * (size_t)capacity));
+    e->trace_cap = capacity;
+  }
+  return TS_OK;
+}
+
+int ts_read_trace(ts_engine* e, ts_trace_row* host_out, int64_t cap, int64_t* n_out, int64_t* dropped,
+                  void* stream) {
+  if (!e || !n_out || cap < 0 || (cap > 0 && !host_out)) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  if (!e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  Counters c;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(&c, e->ctr, sizeof(c), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  TS_CUDA_TRY(e, cudaStreamSynchronize((cudaStream_t)stream));
+  const long long have = std::min<long long>((long long)c.trace_n, e->trace_cap);
+  *n_out = have;
+  if (dropped) *dropped = (int64_t)c.trace_drop;
+  const long long k = std::min<long long>(have, cap);
+  if (k > 0) {
+    TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, e->trace, sizeof(ts_trace_row) * (size_t)k, cudaMemcpyDeviceToHost,
+                                   (cudaStream_t)stream));
+    TS_CUDA_TRY(e, cudaStreamSynchronize((cudaStream_t)stream));
+  }
   return TS_OK;
 }
 

@@ -8,6 +8,8 @@
 //   ts_exit_policy         check_negative_exit  scoring.py:153-175
 //                          check_positive_exit  scoring.py:178-181
 //                          decide_exit          scoring.py:184-207
+//   ts_reconcile           reconcile            scheduler.py:199-214
+//                          choose_preemption_victims  scheduler.py:190-196
 //
 // Same numerics contract as engine.cu: compiled with -fmad=false, every
 // expression in the reference's order, log1p bit-identical to the host libm.
@@ -517,6 +519,48 @@ int workspace_for(int n, Workspace** out) {
   return TS_OK;
 }
 
+// ---- reconcile / choose_preemption_victims --------------------------------------
+// One warp per job.  gap = target - active (active = the job's in-flight
+// rollouts [off[j], off[j+1])): gap > 0 is LaunchAction(gap); gap < 0 ranks
+// the in-flight rollouts by (prefix_score, rollout_id) (sorted(...) with the
+// tuple key, scheduler.py:195) and the -gap lowest are the victims, emitted in
+// rank order.  A rollout's rank = # rollouts ordered before it (lanes stride
+// the segment; the comparisons of one rollout are a warp-wide count).
+// Non-running jobs produce no action.  Ties on both keys cannot occur for
+// distinct rollout ids; equal ids keep their input order.
+__global__ void __launch_bounds__(256) k_reconcile(int n, const int32_t* __restrict__ running,
+                                                   const int32_t* __restrict__ target,
+                                                   const int64_t* __restrict__ off,
+                                                   const double* __restrict__ score,
+                                                   const int64_t* __restrict__ rid, int32_t* __restrict__ launch,
+                                                   int32_t* __restrict__ victim_rank) {
+  const int lane = threadIdx.x & 31;
+  const int j = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  if (j >= n) return;
+  const long long a = off[j], b = off[j + 1];
+  const long long active = b - a;
+  const bool run = running == nullptr || running[j] != 0;
+  const long long gap = run ? (long long)target[j] - active : 0;
+  if (lane == 0) launch[j] = gap > 0 ? (int32_t)gap : 0;
+  const long long victims = gap < 0 ? -gap : 0;
+  for (long long r = a; r < b; ++r) {
+    int32_t out = -1;
+    if (victims > 0) {
+      const double sr = score[r];
+      const int64_t ir = rid[r];
+      unsigned cnt = 0;
+      for (long long q = a + lane; q < b; q += 32) {
+        const double sq = score[q];
+        const int64_t iq = rid[q];
+        cnt += (sq < sr || (sq == sr && (iq < ir || (iq == ir && q < r)))) ? 1u : 0u;
+      }
+      const long long rank = (long long)__reduce_add_sync(FULL, cnt);
+      if (rank < victims) out = (int32_t)rank;
+    }
+    if (lane == 0) victim_rank[r] = out;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -629,6 +673,20 @@ int ts_exit_policy(const ts_config* cfg, const ts_forest* f, int32_t* dev_kind, 
                                                    cfg->negative_exit, scheme_ok, pc, f->best_score, f->has_best,
                                                    f->completed, f->budget, f->exhausted, dev_kind, dev_ne);
   CK(cudaFreeAsync(pc, s));
+  CK(cudaGetLastError());
+  return TS_OK;
+}
+
+int ts_reconcile(const int32_t* dev_running, const int32_t* dev_targets, const int64_t* dev_offsets,
+                 const double* dev_prefix_score, const int64_t* dev_rollout_id, int32_t n_jobs, int32_t* dev_launch,
+                 int32_t* dev_victim_rank, void* stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && (!dev_targets || !dev_offsets || !dev_launch)))
+    return fail(TS_INVALID_ARGUMENT, "ts_reconcile: bad arguments");
+  if (n_jobs == 0) return TS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_reconcile<<<blocks((long long)n_jobs * 32, 256), 256, 0, s>>>(n_jobs, dev_running, dev_targets, dev_offsets,
+                                                                  dev_prefix_score, dev_rollout_id, dev_launch,
+                                                                  dev_victim_rank);
   CK(cudaGetLastError());
   return TS_OK;
 }

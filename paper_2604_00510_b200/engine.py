@@ -117,6 +117,28 @@ class Engine:
         self._check(self.lib.ts_read_invariants(self._h, ctypes.byref(inv), self.stream), "ts_read_invariants")
         return inv.as_dict()
 
+    def set_trace(self, capacity: int) -> None:
+        """Keep the per-pass allocation rows of the next runs (ts_engine_set_trace);
+        0 turns the trace off."""
+        self._check(self.lib.ts_engine_set_trace(self._h, int(capacity)), "ts_engine_set_trace")
+
+    def trace_rows(self) -> np.ndarray:
+        """The allocation rows since the last load, in run-queue order per step
+        (a structured array: step, job, target, active, score)."""
+        n, dropped = ctypes.c_int64(), ctypes.c_int64()
+        self._check(self.lib.ts_read_trace(self._h, None, 0, ctypes.byref(n), ctypes.byref(dropped), self.stream),
+                    "ts_read_trace")
+        if dropped.value:
+            from .tree import AccountingError
+
+            raise AccountingError(f"trace buffer too small: {dropped.value} rows dropped")
+        rows = (_abi.TsTraceRow * max(1, n.value))()
+        self._check(self.lib.ts_read_trace(self._h, rows, n.value, ctypes.byref(n), None, self.stream),
+                    "ts_read_trace")
+        dt = np.dtype([("step", "<i4"), ("job", "<i4"), ("target", "<i4"), ("active", "<i4"), ("score", "<f8")])
+        arr = np.frombuffer(bytes(rows)[: n.value * dt.itemsize], dtype=dt).copy()
+        return arr[np.lexsort((arr["job"], arr["step"]))]
+
     def outcomes(self, n: Optional[int] = None):
         n = self.n if n is None else n
         out = (TsOutcome * max(1, n))()

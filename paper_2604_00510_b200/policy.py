@@ -116,6 +116,32 @@ def parallelism_scores_arrays(arrival, best, now: float, positive_exit_threshold
     return out[:n]
 
 
+def reconcile_arrays(targets, offsets, prefix_score, rollout_id, running=None, device: int = 0, stream=None):
+    """reconcile + choose_preemption_victims (scheduler.py:190-214) over a run
+    queue as arrays: job j's in-flight rollouts are [offsets[j], offsets[j+1])
+    of ``prefix_score``/``rollout_id``.  Returns (launch int32[n_jobs],
+    victim_rank int32[n_rollouts]) device tensors (see ts_reconcile)."""
+    torch = _torch()
+    lib = load_library()
+    dev = torch.device("cuda", device)
+    with torch.cuda.device(dev), torch.cuda.stream(_torch_stream(stream, dev)):
+        tgt = _dev(targets, torch.int32, torch, dev)
+        off = _dev(offsets, torch.int64, torch, dev)
+        sc = _dev(prefix_score, torch.float64, torch, dev)
+        ids = _dev(rollout_id, torch.int64, torch, dev)
+        run = None if running is None else _dev(running, torch.int32, torch, dev)
+        n = int(tgt.numel())
+        if int(off.numel()) != n + 1 or int(sc.numel()) != int(ids.numel()):
+            raise ValueError("reconcile: offsets must have n_jobs + 1 entries, scores and ids one per rollout")
+        launch = torch.empty(max(1, n), dtype=torch.int32, device=dev)
+        rank = torch.empty(max(1, int(sc.numel())), dtype=torch.int32, device=dev)
+        rc = lib.ts_reconcile(_ptr(run), _ptr(tgt), _ptr(off), _ptr(sc), _ptr(ids), n, _ptr(launch), _ptr(rank),
+                              _stream(stream))
+    if rc != _abi.TS_OK:
+        raise_for_status(rc, "reconcile", _err())
+    return launch[:n], rank[: int(sc.numel())]
+
+
 # ---- forests of SearchTrees ------------------------------------------------------
 
 def _tree_columns(tree):

@@ -307,6 +307,35 @@ def gen_waves():
     dump("waves", cases)
 
 
+def gen_trace():
+    """The per-pass trace (simulator.py:314-341 allocation/action records, plus
+    job_finished events) of wave runs, as the JSONL text cli.py:263-265 writes."""
+    import json as _json
+
+    D7 = {d: (7, 7) for d in Difficulty}
+    c1 = make_workload(64, MIX, SEED, branching=4, depth_ranges=D7)
+    cli = make_workload(500, MIX, 20260810)
+    mixed = make_workload(97, (0.5, 0.3, 0.2), 77, branching=3,
+                          depth_ranges={Difficulty.EASY: (3, 9), Difficulty.HARD_SOLVABLE: (4, 10), Difficulty.UNSOLVABLE: (2, 6)},
+                          accept_threshold=0.35)
+    cases = []
+    for name, wl, probs, sch, budget, cap, width, pe, ne, scoring, arr, dt in (
+        ("c1_M256", "c1", c1, SchedulerConfig(max_concurrency=256), 32, 8, 4, True, True, None, None, 1.0),
+        ("c1_M48_admission", "c1", c1, SchedulerConfig(max_concurrency=48), 32, 8, 4, True, True, None, None, 1.0),
+        ("mixed_M200_obs3", "mixed_b3", mixed, SchedulerConfig(max_concurrency=200, beta=1.5, proximity=0.8, obs_threshold=3),
+         40, 9, 3, True, True, ScoringConfig(accept_threshold=0.35), None, 1.0),
+        ("cli_serving_pe_ne_boost", "cli_default", cli, SchedulerConfig(max_concurrency=16), 32, 16, 4, True, True, None,
+         serving_arrivals(500, 5.0, 20260810, 20.0), 1.0),
+    ):
+        tr = []
+        wave_ref.run_waves(probs, scoring=scoring, sched=sch, rollout_budget=budget, depth_cap=cap, expand_width=width,
+                           positive_exit=pe, negative_exit=ne, arrival_steps=arr, dt=dt, trace=tr)
+        jsonl = "".join(_json.dumps(e, sort_keys=True) + "\n" for e in tr)
+        print("trace", name, len(tr))
+        cases.append({"name": name, "wave_case": name, "dt": dt, "jsonl": jsonl})
+    dump("trace", cases)
+
+
 def gen_targets():
     """compute_targets (scheduler.py:143-187) on random pools, incl. equal-score lock-step pools."""
     r = random.Random(7)
@@ -649,6 +678,6 @@ def gen_arrivals():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps", "workload_json", "arrivals"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps", "workload_json", "arrivals", "trace"]
     for w in which:
         globals()["gen_" + w]()

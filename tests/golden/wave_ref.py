@@ -40,7 +40,10 @@ from treeserve.scheduler import (  # noqa: E402
     admit_jobs,
     compute_targets,
     on_rollout_complete,
+    parallelism_score,
+    reconcile,
 )
+from treeserve.scheduler import LaunchAction  # noqa: E402
 from treeserve.scoring import ExitKind, ScoringConfig, decide_exit  # noqa: E402
 from treeserve.search import _CountingBackend, finish_rollout, trajectory_index_path  # noqa: E402
 from treeserve.tree import (  # noqa: E402
@@ -67,7 +70,13 @@ def run_waves(
     dt: float = 1.0,
     max_steps: int = 1_000_000,
     keep_trees: bool = False,
+    trace=None,
 ):
+    """``trace``: a list that receives the per-pass records of the reference's
+    trace (simulator.py:314-341: "allocation" per running job, then the
+    "action" records of ``reconcile``), plus a "job_finished" record when a
+    job exits (the event record of simulator.py:240-249 without the heap's
+    ``seq``)."""
     scoring = scoring or ScoringConfig()
     selection = selection or SelectionParams()
     sched = sched or SchedulerConfig()
@@ -103,6 +112,16 @@ def run_waves(
             continue
         targets = compute_targets(state, sched, scoring.positive_exit_threshold)
         targets_trace.append([targets[j.job_id] for j in running])
+        if trace is not None:
+            now = state.now
+            for job in running:
+                trace.append({"time": round(now, 9), "kind": "allocation", "job": job.job_id,
+                              "score": round(parallelism_score(job, now, scoring.positive_exit_threshold, sched), 9),
+                              "target": targets[job.job_id], "active": len(job.active_rollouts)})
+            for action in reconcile(state, targets):
+                entry = ({"action": "launch", "count": action.count} if isinstance(action, LaunchAction)
+                         else {"action": "preempt", "rollout": action.rollout_id})
+                trace.append({"time": round(now, 9), "kind": "action", "job": action.job_id, **entry})
         for job in list(running):
             i = job.job_id
             tree = job.tree
@@ -121,6 +140,9 @@ def run_waves(
                         decisions[i] = d
                         exit_step[i] = step
                         finished = True
+                        if trace is not None:
+                            trace.append({"time": round(state.now, 9), "kind": "job_finished", "job": i,
+                                          "rollout": None})
                     break
                 terms.append(simulate_to_terminal(tree, leaf, backend, depth_cap))
             launched_total[i] += len(terms)
@@ -136,6 +158,9 @@ def run_waves(
                         cancelled_total[i] += 1
                     decisions[i] = d
                     exit_step[i] = step
+                    if trace is not None:
+                        trace.append({"time": round(state.now, 9), "kind": "job_finished", "job": i,
+                                      "rollout": None})
                     break
         step += 1
     out = []

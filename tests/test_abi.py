@@ -35,7 +35,7 @@ def test_header_and_mirror_agree():
 def test_library_exports_every_declared_symbol(lib):
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.ts_abi_version() == 4
+    assert lib.ts_abi_version() == 5
 
 
 def test_struct_layouts_match_header():
@@ -47,6 +47,9 @@ def test_struct_layouts_match_header():
     assert L.or_sizeof_config() == ctypes.sizeof(TsConfig)
     assert L.or_sizeof_outcome() == ctypes.sizeof(TsOutcome)
     assert ctypes.sizeof(TsSchedRecord) == 16
+    from paper_2604_00510_b200._abi import TsTraceRow
+
+    assert ctypes.sizeof(TsTraceRow) == 24
     from paper_2604_00510_b200._abi import TsForest, TsSchedParams, TsTargetsInfo
 
     assert ctypes.sizeof(TsSchedParams) == 40

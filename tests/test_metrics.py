@@ -73,3 +73,27 @@ def test_engine_tree_json_is_byte_identical_to_reference():
             eng.load(table([rec]))
             eng.run()
             assert eng.tree_json(0) == case["json"]
+
+
+def test_trace_assembly_reproduces_reference_trace():
+    """Host half of the trace (metrics.trace_entries/trace_to_jsonl) on CPU:
+    rows taken from the reference trace's own allocation records and the wave
+    fixture's exit steps rebuild the reference JSONL byte for byte."""
+    import json
+    from types import SimpleNamespace
+
+    import numpy as np
+
+    from paper_2604_00510_b200.metrics import trace_entries, trace_to_jsonl
+
+    for case in load("trace"):
+        wave = next(c for c in load("waves") if c["name"] == case["wave_case"])
+        entries = [json.loads(x) for x in case["jsonl"].splitlines()]
+        alloc = [e for e in entries if e["kind"] == "allocation"]
+        dt = np.dtype([("step", "<i4"), ("job", "<i4"), ("target", "<i4"), ("active", "<i4"), ("score", "<f8")])
+        rows = np.array([(round(e["time"] / case["dt"]), e["job"], e["target"], e["active"], e["score"])
+                         for e in alloc], dtype=dt)[::-1]
+        code = {"positive": 1, "negative": 2, "budget_exhausted": 3}
+        outs = [SimpleNamespace(exit_kind=code[o["exit_kind"]], exit_step=o["exit_step"]) for o in wave["outcomes"]]
+        rows = rows[np.lexsort((rows["job"], rows["step"]))]
+        assert trace_to_jsonl(trace_entries(rows, outs, case["dt"])) == case["jsonl"], case["name"]

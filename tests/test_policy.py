@@ -228,8 +228,9 @@ def test_admission_fifo_up_to_capacity():
     assert len(full.run_queue) == 4 and full.pending_queue[0].job_id == 99
 
 
+@pytest.mark.gpu
 def test_reconcile_and_victims():
-    """test_scheduler.py TestReconcile."""
+    """test_scheduler.py TestReconcile, on the device operator (ts_reconcile)."""
     def with_active(scores):
         job = make_job(0)
         job.active_rollouts = [InflightRollout(i, s) for i, s in enumerate(scores)]
@@ -544,3 +545,51 @@ def test_engine_exit_decisions_agree_with_forest_policy():
         exhausted = [o.exit_kind == 3 and o.rollouts_completed < budget for o in outs]
         got = decide_exits(trees, scoring, True, True, exhausted)
         assert [g.kind for g in got] == [kinds[o.exit_kind] for o in outs]
+
+
+@pytest.mark.gpu
+def test_preemption_victims_criterion_4():
+    """test_acceptance.py criterion 4: 200 seeded scenarios, victims == the
+    lowest-prefix-reward sort (ties to the earlier launch), on the device."""
+    rnd = random.Random(20260810 + 4)
+    for _ in range(200):
+        count = rnd.randrange(1, 12)
+        rollouts = [InflightRollout(rollout_id=i, prefix_score=round(rnd.uniform(0, 1), 3)) for i in range(count)]
+        rnd.shuffle(rollouts)
+        victims = rnd.randrange(0, count + 1)
+        assert choose_preemption_victims(rollouts, victims) == sorted(
+            rollouts, key=lambda r: (r.prefix_score, r.rollout_id))[:victims]
+
+
+@pytest.mark.gpu
+def test_reconcile_large_run_queue_vs_sort():
+    """ts_reconcile over 20,000 jobs (0-300 in-flight rollouts each, ties in the
+    scores, targets above and below): every action equals the reference
+    definition (scheduler.py:190-214) restated with sorted()."""
+    import numpy as np
+
+    from paper_2604_00510_b200.policy import reconcile_arrays
+
+    rng = np.random.default_rng(7)
+    n = 20000
+    active = rng.integers(0, 300, n)
+    active[rng.random(n) < 0.3] = 0
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(active)
+    m = int(off[-1])
+    scores = rng.choice([0.0, -0.0, 0.25, 0.5, 0.9], m) + (rng.random(m) < 0.5) * rng.random(m)
+    ids = rng.permutation(m).astype(np.int64)
+    targets = np.maximum(0, active + rng.integers(-320, 40, n)).astype(np.int32)
+    running = (rng.random(n) < 0.9).astype(np.int32)
+    launch, rank = reconcile_arrays(targets, off, scores, ids, running)
+    launch, rank = launch.cpu().numpy(), rank.cpu().numpy()
+    for j in range(n):
+        a, b = int(off[j]), int(off[j + 1])
+        gap = int(targets[j]) - (b - a) if running[j] else 0
+        assert launch[j] == max(gap, 0), j
+        want = [-1] * (b - a)
+        if gap < 0:
+            order = sorted(range(a, b), key=lambda r: (scores[r], ids[r]))
+            for pos, r in enumerate(order[:-gap]):
+                want[r - a] = pos
+        assert rank[a:b].tolist() == want, j
