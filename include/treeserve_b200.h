@@ -218,6 +218,24 @@ typedef struct ts_trace_row {
   int32_t active; /* len(job.active_rollouts) at the pass: 0 in the wave model */
   double score;   /* parallelism_score(job, now, θ_pos, config) (scheduler.py:118-128) */
 } ts_trace_row;
+/* ---- wave clock of the cost model ------------------------------
+ * The reference's simulated time (CostModel / service_time, backend.py:287-311,
+ * charged per generation request, simulator.py:443-463) restated on waves:
+ * every expansion of a launched rollout takes
+ *   ((max candidate token_count * per_token_latency) * contention) + reward_latency,
+ * contention = max(1, load / engine_capacity), load = the wave's in-flight
+ * candidates (sum over the wave's launched rollouts of the expansion width),
+ * accumulated onto the wave's start clock in expansion order; a search's wave
+ * ends with its last rollout and the clock advances to the latest end (idle
+ * steps take no time).  engine_capacity = 0 turns it off; otherwise the
+ * parameters are validated like CostModel (ValueError).  One engine only (the
+ * load is the whole run queue's). */
+int ts_engine_set_cost_model(ts_engine* eng, double per_token_latency, int32_t engine_capacity,
+                             double reward_latency);
+/* Per local search [0, n): simulated completion (the end of its exit wave, 0
+ * if not exited) and simulated arrival (the clock at its arrival step). */
+int ts_read_sim_times(ts_engine* eng, double* host_completion, double* host_arrival, int32_t n, void* stream);
+
 /* capacity = rows kept per run (0 frees the buffer and disables the trace);
  * rows past it are counted as dropped. */
 int ts_engine_set_trace(ts_engine* eng, int64_t capacity);

@@ -72,6 +72,11 @@ def lib() -> ctypes.CDLL:
         L.or_run_waves.restype = ctypes.c_void_p
         L.or_run_waves.argtypes = [P(TsProblem), i32, P(TsConfig), i32, i32, P(i32), ctypes.c_int64,
                                    P(ctypes.c_int64)]
+        L.or_run_waves_cost.restype = ctypes.c_void_p
+        L.or_run_waves_cost.argtypes = [P(TsProblem), i32, P(TsConfig), i32, i32, ctypes.c_double, i32,
+                                        ctypes.c_double]
+        L.or_run_sim_times.restype = None
+        L.or_run_sim_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.or_run_steps.restype = i32
         L.or_run_steps.argtypes = [ctypes.c_void_p]
         L.or_run_outcomes.restype = None
@@ -209,12 +214,20 @@ def beam_search(problem: TsProblem, cfg, out=None):
 class OracleRun:
     """Result of or_run_waves; owns the C trees until closed."""
 
-    def __init__(self, table, cfg: TsConfig, threads: int = 1, max_steps: int = 1 << 30, trace_cap: int = 0):
+    def __init__(self, table, cfg: TsConfig, threads: int = 1, max_steps: int = 1 << 30, trace_cap: int = 0,
+                 cost=None):
+        """``cost``: (per_token_latency, engine_capacity, reward_latency) runs
+        the wave clock of the cost model (or_run_waves_cost)."""
         self.n = len(table)
         self._trace = (ctypes.c_int32 * max(1, trace_cap))()
         tl = ctypes.c_int64(0)
-        self._h = lib().or_run_waves(table, self.n, ctypes.byref(cfg), threads, max_steps,
-                                     self._trace if trace_cap else None, trace_cap, ctypes.byref(tl))
+        if cost is not None:
+            pt, cap, rl = cost
+            self._h = lib().or_run_waves_cost(table, self.n, ctypes.byref(cfg), threads, max_steps, float(pt),
+                                              int(cap), float(rl))
+        else:
+            self._h = lib().or_run_waves(table, self.n, ctypes.byref(cfg), threads, max_steps,
+                                         self._trace if trace_cap else None, trace_cap, ctypes.byref(tl))
         self.trace_len = tl.value
         self.steps = lib().or_run_steps(self._h)
         self.outcomes = (TsOutcome * max(1, self.n))()
@@ -238,6 +251,15 @@ class OracleRun:
         order = ["parent", "reward", "prior", "N", "O", "W", "terminal", "depth", "step_ref"]
         lib().or_tree_dump(self._h, i, *[out[k].ctypes.data_as(ctypes.c_void_p) for k in order])
         return out
+
+    def sim_times(self):
+        """(completion, arrival) on the wave clock of the cost model, per job."""
+        import numpy as np
+
+        c = np.zeros(max(1, self.n), np.float64)
+        a = np.zeros(max(1, self.n), np.float64)
+        lib().or_run_sim_times(self._h, c.ctypes.data_as(ctypes.c_void_p), a.ctypes.data_as(ctypes.c_void_p))
+        return c[: self.n], a[: self.n]
 
     def latencies_s(self):
         import numpy as np

@@ -135,7 +135,7 @@ EXPORTED = (
     "ts_policy_last_error", "ts_parallelism_scores", "ts_compute_targets", "ts_exit_policy",
     "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
     "ts_generate_steps", "ts_engine_set_checks", "ts_read_invariants", "ts_engine_set_trace", "ts_read_trace",
-    "ts_reconcile",
+    "ts_reconcile", "ts_engine_set_cost_model", "ts_read_sim_times",
 )
 
 
@@ -290,6 +290,8 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_read_invariants": (ctypes.c_int, [vp, P(TsInvariants), vp]),
         "ts_engine_set_trace": (ctypes.c_int, [vp, ctypes.c_int64]),
         "ts_reconcile": (ctypes.c_int, [vp, vp, vp, vp, vp, i32, vp, vp, vp]),
+        "ts_engine_set_cost_model": (ctypes.c_int, [vp, ctypes.c_double, i32, ctypes.c_double]),
+        "ts_read_sim_times": (ctypes.c_int, [vp, vp, vp, i32, vp]),
         "ts_read_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int64), vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,

@@ -87,6 +87,13 @@ struct Counters {
   long long inv_wave;
   // ts_engine_set_trace: rows written / rows dropped (buffer full)
   unsigned long long trace_n, trace_drop;
+  // ts_engine_set_cost_model: the wave clock (s) at the current wave's start,
+  // the latest end of a search's wave so far (bits of a double >= 0), and the
+  // wave's in-flight candidate count
+  double clock;
+  unsigned long long clock_max;
+  long long cost_load;
+  long long clock_step1;  // 1 + the last step whose start clock was recorded (0: none)
 };
 
 // Kernel-side view of one engine.
@@ -120,6 +127,12 @@ struct View {
   int32_t checks;          // ts_engine_set_checks: invariant kernels around every wave
   ts_trace_row* trace;     // ts_engine_set_trace: allocation rows of every pass (null: off)
   long long trace_cap;
+  // ts_engine_set_cost_model (cost_cap 0: off)
+  double cost_pt, cost_rl;
+  int32_t cost_cap;
+  int2* cost_snap;         // (nodes, launched) of every search at its wave's start
+  double* sim_done;        // simulated completion time of every exited search
+  double* clock_at;        // wave clock at the start of every step (step_times_cap entries)
   int32_t n_local, goff, n_global;
   unsigned long long* step_times;
   int32_t step_times_cap;
@@ -273,6 +286,7 @@ __global__ void k_init(View v) {
   z.job_best = 0.0;
   z.t_exit = 0;
   v.st[s] = z;
+  if (v.sim_done) v.sim_done[s] = 0.0;
 }
 
 
@@ -3899,6 +3913,140 @@ __global__ void __launch_bounds__(256) k_trace(View v) {
   }
 }
 
+// ---- the wave clock of a cost model (ts_engine_set_cost_model) ---------------------
+// SURVEY §8(f4), a wave-level restatement of the reference's simulated time
+// (backend.py:287-311, simulator.py:443-463): every generation request of a
+// launched rollout (one expansion of its simulation) takes
+//     max(service_time(token_count, cost, load) for the candidates) + reward_latency
+//   = ((max_tokens * per_token_latency) * contention) + reward_latency,
+// contention = max(1, load / engine_capacity), accumulated onto the wave's
+// start clock in expansion order like the reference's event times.  load is
+// the wave's in-flight candidate count: sum over the wave's launched rollouts
+// of the expansion width.  A search's wave ends with its last rollout; the
+// clock advances to the latest end (idle steps take no time).  The wave
+// kernels are untouched: after the wave, the expansions are recovered from the
+// node pool (a wave's new nodes are its expansions in creation order, `width`
+// children each; an expansion continues the previous one's rollout iff its
+// parent is the previous expansion's greedy child, since a rollout stops only
+// at a terminal greedy child, which no later selection can expand) and their
+// token counts are redrawn from the keyed RNG (backend.py:261-263).
+
+// Between the pass and the wave: the clock of this step, per-search snapshots.
+__global__ void __launch_bounds__(256) k_cost_pre(View v) {
+  Counters* c = v.ctr;
+  const int nw = c->work_count, nh = c->heavy_count;
+  if (threadIdx.x == 0) {
+    const double cm = __longlong_as_double((long long)c->clock_max);
+    double clk = c->clock;
+    if (cm > clk) clk = cm;
+    c->clock = clk;
+    c->cost_load = 0;
+    // a pass after the batch has ended repeats the last step: keep its start
+    const int step = c->cur_step;
+    if (c->clock_step1 != (long long)step + 1) {
+      if (step < v.step_times_cap) v.clock_at[step] = clk;
+      c->clock_step1 = (long long)step + 1;
+    }
+  }
+  for (int i = threadIdx.x; i < nw + nh; i += blockDim.x) {
+    const int s = i < nw ? v.work[i] : v.work_heavy[i - nw];
+    v.cost_snap[s] = make_int2(v.st[s].nodes, v.st[s].launched);
+  }
+}
+
+__device__ __forceinline__ int cost_width(const View& v, int s) {
+  return min(v.cfg.expand_width, v.prob[s].branching);
+}
+
+// After the wave: load = sum of width x launched rollouts over the wave.
+__global__ void __launch_bounds__(1024) k_cost_load(View v) {
+  Counters* c = v.ctr;
+  const int nw = c->work_count, nh = c->heavy_count;
+  long long x = 0;
+  for (int i = threadIdx.x; i < nw + nh; i += blockDim.x) {
+    const int s = i < nw ? v.work[i] : v.work_heavy[i - nw];
+    x += (long long)cost_width(v, s) * (long long)(v.st[s].launched - v.cost_snap[s].y);
+  }
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+  if ((threadIdx.x & 31) == 0 && x) atomicAdd((unsigned long long*)&c->cost_load, (unsigned long long)x);
+}
+
+// After k_cost_load: one warp per search of the wave.  Lane k of a round of
+// 32 expansions recovers expansion g = 32*round + k (parent, greedy child, max
+// token count of its candidates); the warp then folds the round's durations
+// in expansion order.
+__global__ void __launch_bounds__(256) k_cost_wave(View v) {
+  Counters* c = v.ctr;
+  const int nw = c->work_count, nh = c->heavy_count;
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)((gridDim.x * (size_t)blockDim.x) >> 5);
+  const double clock = c->clock;
+  double cont = (double)c->cost_load / (double)v.cost_cap;  // inflight_load / engine_capacity
+  if (!(cont > 1.0)) cont = 1.0;                            // max(1.0, ...)
+  const double pt = v.cost_pt, rl = v.cost_rl;
+  const int step = c->cur_step;
+  for (int i = warp; i < nw + nh; i += nwarps) {
+    const int s = i < nw ? v.work[i] : v.work_heavy[i - nw];
+    const int w = cost_width(v, s);
+    const SearchState& S = v.st[s];
+    const int nb = v.cost_snap[s].x;
+    const int G = (S.nodes - nb) / w;
+    const size_t base = (size_t)s * (size_t)v.cap;
+    const int32_t* PA = v.parent + base;
+    const double* RW = v.reward + base;
+    const uint64_t* MF = v.mf + base;
+    const uint64_t seed = v.prob[s].seed;
+    double t = clock, end = clock;
+    int prev_greedy = -1;
+    for (int g0 = 0; g0 < G; g0 += 32) {
+      const int g = g0 + lane;
+      int par = -1, greedy = -1, mt = 0;
+      if (g < G) {
+        const int fc = nb + g * w;
+        par = PA[fc];
+        // greedy_child (tree.py:307-319): strict '>', first wins
+        greedy = fc;
+        double br = RW[fc];
+        for (int j = 1; j < w; ++j)
+          if (RW[fc + j] > br) { br = RW[fc + j]; greedy = fc + j; }
+        // the index path of the expanded node, root first
+        const uint32_t pm = (uint32_t)MF[par];
+        const int d = (int)(pm & M_DEPTH);
+        uint8_t refs[TS_MAX_DEPTH + 1];
+        int x = par;
+        for (int k = d - 1; k >= 0; --k) {
+          refs[k] = (uint8_t)((((uint32_t)MF[x]) >> SH_REF) & 31u);
+          x = PA[x];
+        }
+        // token counts: randint(40, 120, seed, 3, len(cp), *cp) (backend.py:261-263)
+        uint64_t h = sm64(MIX_INIT ^ seed);
+        h = sm64(h ^ 3ull);
+        h = sm64(h ^ (uint64_t)(d + 1));
+        for (int k = 0; k < d; ++k) h = sm64(h ^ (uint64_t)refs[k]);
+        for (int j = 0; j < w; ++j) {
+          const int tok = 40 + (int)(sm64(h ^ (uint64_t)j) % 81ull);
+          mt = tok > mt ? tok : mt;
+        }
+      }
+      const int m = min(32, G - g0);
+      for (int k = 0; k < m; ++k) {
+        const int pk = __shfl_sync(FULL, par, k);
+        const int gk = __shfl_sync(FULL, greedy, k);
+        const int tk = __shfl_sync(FULL, mt, k);
+        if (pk != prev_greedy) t = clock;  // a new rollout's first expansion
+        t = t + ((double)tk * pt * cont + rl);
+        if (t > end) end = t;
+        prev_greedy = gk;
+      }
+    }
+    if (lane == 0) {
+      atomicMax(&c->clock_max, (unsigned long long)__double_as_longlong(end));
+      if (S.state == ST_FINISHED && S.exit_step == step) v.sim_done[s] = end;
+    }
+  }
+}
+
 }  // namespace
 
 // ============================================================================
@@ -3972,6 +4120,12 @@ struct ts_engine {
   int checks = 0;        // ts_engine_set_checks
   ts_trace_row* trace = nullptr;  // ts_engine_set_trace
   long long trace_cap = 0;
+  double cost_pt = 0.0, cost_rl = 0.0;  // ts_engine_set_cost_model
+  int cost_cap = 0;
+  int2* cost_snap = nullptr;
+  double* sim_done = nullptr;
+  int cost_n = 0;
+  double* clock_at = nullptr;  // step_times_cap entries
   int graph_unroll = 3;  // scheduler passes + waves per iteration of the graph's while loop (TS_GRAPH_UNROLL)
 };
 
@@ -4040,6 +4194,14 @@ View make_view(ts_engine* e) {
   v.checks = e->checks;
   v.trace = e->trace;
   v.trace_cap = e->trace_cap;
+  if (e->cost_cap > 0 && e->cost_snap && e->cost_n >= e->n_local) {
+    v.cost_pt = e->cost_pt;
+    v.cost_rl = e->cost_rl;
+    v.cost_cap = e->cost_cap;
+    v.cost_snap = e->cost_snap;
+    v.sim_done = e->sim_done;
+  }
+  v.clock_at = e->clock_at;
   v.n_local = e->n_local;
   v.goff = e->goff;
   v.n_global = e->n_global;
@@ -4105,7 +4267,33 @@ int ensure_step_times(ts_engine* e, int need, cudaStream_t s) {
     cudaFree(e->step_times);
   }
   e->step_times = p;
+  double* ca = nullptr;  // the wave clock per step (cost model), same capacity
+  TS_CUDA_TRY(e, cudaMalloc((void**)&ca, sizeof(double) * n));
+  TS_CUDA_TRY(e, cudaMemsetAsync(ca, 0, sizeof(double) * n, s));
+  if (e->clock_at) {
+    TS_CUDA_TRY(e, cudaMemcpyAsync(ca, e->clock_at, sizeof(double) * e->step_times_cap, cudaMemcpyDeviceToDevice, s));
+    TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+    cudaFree(e->clock_at);
+  }
+  e->clock_at = ca;
   e->step_times_cap = n;
+  return TS_OK;
+}
+
+// Per-search buffers of the cost model's wave clock (ts_engine_set_cost_model).
+int ensure_cost(ts_engine* e) {
+  if (e->cost_cap <= 0) return TS_OK;
+  if (e->n_global != e->n_local)
+    return fail(e, TS_INVALID_ARGUMENT, "the cost model's wave clock needs the whole run queue on one engine");
+  if (e->n_local <= e->cost_n) return TS_OK;
+  if (e->cost_snap) cudaFree(e->cost_snap);
+  if (e->sim_done) cudaFree(e->sim_done);
+  e->cost_snap = nullptr;
+  e->sim_done = nullptr;
+  e->cost_n = 0;
+  TS_CUDA_TRY(e, cudaMalloc((void**)&e->cost_snap, sizeof(int2) * (size_t)e->n_local));
+  TS_CUDA_TRY(e, cudaMalloc((void**)&e->sim_done, sizeof(double) * (size_t)e->n_local));
+  e->cost_n = e->n_local;
   return TS_OK;
 }
 
@@ -4262,6 +4450,11 @@ int build_run_graph(ts_engine* e, const View& v) {
   cudaKernelNodeParams kt = kc1;
   kt.func = (void*)k_trace;
   kt.blockDim = dim3(256);
+  cudaKernelNodeParams kq1 = kt, kq2 = kc1, kq3 = kt;  // the cost model's wave clock
+  kq1.func = (void*)k_cost_pre;
+  kq2.func = (void*)k_cost_load;
+  kq3.func = (void*)k_cost_wave;
+  kq3.gridDim = dim3(2 * e->sm_count);
   cudaGraphNode_t prev[2];
   int nprev = 0;
   for (int u = 0; u < e->graph_unroll; ++u) {
@@ -4277,6 +4470,11 @@ int build_run_graph(ts_engine* e, const View& v) {
       TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nt, body, &n1, 1, &kt));
       n1 = nt;
     }
+    if (v.cost_cap) {
+      cudaGraphNode_t nq;
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nq, body, &n1, 1, &kq1));
+      n1 = nq;
+    }
     TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
     prev[0] = n2;
     nprev = 1;
@@ -4289,6 +4487,13 @@ int build_run_graph(ts_engine* e, const View& v) {
       cudaGraphNode_t nc;
       TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nc, body, prev, nprev, &kc2));
       prev[0] = nc;
+      nprev = 1;
+    }
+    if (v.cost_cap) {
+      cudaGraphNode_t nq2, nq3;
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nq2, body, prev, nprev, &kq2));
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nq3, body, &nq2, 1, &kq3));
+      prev[0] = nq3;
       nprev = 1;
     }
   }
@@ -4315,6 +4520,10 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
     k_trace<<<1, 256, 0, s>>>(v);
     TS_LAUNCH_CHECK(e, "k_trace");
   }
+  if (v.cost_cap) {
+    k_cost_pre<<<1, 256, 0, s>>>(v);
+    TS_LAUNCH_CHECK(e, "k_cost_pre");
+  }
   cudaEventRecord(e->wave_ev[e->wave_ev_used], s);
   const int k = wave_index(e);
   kWave[k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
@@ -4325,6 +4534,12 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   if (v.checks) {
     k_check_post<<<2 * e->sm_count, 256, 0, s>>>(v);
     TS_LAUNCH_CHECK(e, "k_check_post");
+  }
+  if (v.cost_cap) {
+    k_cost_load<<<1, 1024, 0, s>>>(v);
+    TS_LAUNCH_CHECK(e, "k_cost_load");
+    k_cost_wave<<<2 * e->sm_count, 256, 0, s>>>(v);
+    TS_LAUNCH_CHECK(e, "k_cost_wave");
   }
   return TS_OK;
 }
@@ -4414,7 +4629,8 @@ int ts_engine_destroy(ts_engine* e) {
   void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent, e->st, e->prob,
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
-                  e->work_heavy, e->mt, e->tgt, e->nrec, e->trace};
+                  e->work_heavy, e->mt, e->tgt, e->nrec, e->trace, e->cost_snap, e->sim_done,
+                  e->clock_at};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
@@ -4541,6 +4757,7 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   }
   if ((rc = ensure_log1p(e, 1024, s))) return rc;
   if ((rc = ensure_step_times(e, 4096, s))) return rc;
+  if ((rc = ensure_cost(e))) return rc;
   View v = make_view(e);
   e->launches = 0;
   e->wave_ev_used = 0;
@@ -4718,7 +4935,7 @@ static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cu
       // every iteration runs graph_unroll passes of {k_sched, k_wave[, k_heavy]}; the
       // last one contains the pass that ended the loop
       const long long iters = (c.step - step0) / e->graph_unroll + 1;
-      e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.checks ? 2 : 0) + (v.trace ? 1 : 0));
+      e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.checks ? 2 : 0) + (v.trace ? 1 : 0) + (v.cost_cap ? 3 : 0));
     }
     step0 = c.step;
     if (c.finished >= e->n_local || c.step >= max_steps) break;
@@ -4883,6 +5100,48 @@ int ts_engine_set_trace(ts_engine* e, int64_t capacity) {
     TS_CUDA_TRY(e, cudaMalloc((void**)&e->trace, sizeof(ts_trace_row) * (size_t)capacity));
     e->trace_cap = capacity;
   }
+  return TS_OK;
+}
+
+int ts_engine_set_cost_model(ts_engine* e, double per_token_latency, int32_t engine_capacity,
+                             double reward_latency) {
+  if (!e) return TS_INVALID_ARGUMENT;
+  if (engine_capacity == 0) {
+    e->cost_cap = 0;
+    return TS_OK;
+  }
+  // CostModel.__post_init__ (backend.py:299-301)
+  if (!(per_token_latency > 0) || engine_capacity < 1 || !(reward_latency >= 0))
+    return fail(e, TS_INVALID_ARGUMENT, "cost model parameters must be positive");
+  if (e->loaded && e->n_global != e->n_local)
+    return fail(e, TS_INVALID_ARGUMENT, "the cost model's wave clock needs the whole run queue on one engine");
+  e->cost_pt = per_token_latency;
+  e->cost_cap = engine_capacity;
+  e->cost_rl = reward_latency;
+  if (e->loaded) {
+    e->cost_n = 0;  // fresh buffers: sim_done is only zeroed by a load
+    int rc = ensure_cost(e);
+    if (rc) return rc;
+    TS_CUDA_TRY(e, cudaMemset(e->sim_done, 0, sizeof(double) * (size_t)e->n_local));
+  }
+  return TS_OK;
+}
+
+int ts_read_sim_times(ts_engine* e, double* host_completion, double* host_arrival, int32_t n, void* stream) {
+  if (!e || n < 0 || n > e->n_local) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  if (!e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (e->cost_cap <= 0 || !e->sim_done) return fail(e, TS_INVALID_ARGUMENT, "no cost model set");
+  if (n == 0) return TS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int32_t> arr(n);
+  std::vector<double> clk(e->step_times_cap);
+  TS_CUDA_TRY(e, cudaMemcpyAsync(arr.data(), e->arrival, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaMemcpyAsync(clk.data(), e->clock_at, sizeof(double) * clk.size(), cudaMemcpyDeviceToHost, s));
+  if (host_completion)
+    TS_CUDA_TRY(e, cudaMemcpyAsync(host_completion, e->sim_done, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  if (host_arrival)
+    for (int i = 0; i < n; ++i) host_arrival[i] = arr[i] >= 0 && arr[i] < (int)clk.size() ? clk[arr[i]] : 0.0;
   return TS_OK;
 }
 

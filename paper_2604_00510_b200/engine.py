@@ -117,6 +117,29 @@ class Engine:
         self._check(self.lib.ts_read_invariants(self._h, ctypes.byref(inv), self.stream), "ts_read_invariants")
         return inv.as_dict()
 
+    def set_cost_model(self, cost=None) -> None:
+        """Run the wave clock of a cost model (ts_engine_set_cost_model): a
+        ``CostModel``-like object (per_token_latency, engine_capacity,
+        reward_latency) or a 3-tuple; None turns it off."""
+        if cost is None:
+            pt, cap, rl = 0.0, 0, 0.0
+        elif isinstance(cost, tuple):
+            pt, cap, rl = cost
+        else:
+            pt, cap, rl = cost.per_token_latency, cost.engine_capacity, cost.reward_latency
+        self._check(self.lib.ts_engine_set_cost_model(self._h, float(pt), int(cap), float(rl)),
+                    "ts_engine_set_cost_model")
+
+    def sim_times(self, n: Optional[int] = None):
+        """(completion, arrival) of the local searches on the cost model's wave clock."""
+        n = self.n if n is None else n
+        c = np.zeros(max(1, n), np.float64)
+        a = np.zeros(max(1, n), np.float64)
+        self._check(self.lib.ts_read_sim_times(self._h, c.ctypes.data_as(ctypes.c_void_p),
+                                               a.ctypes.data_as(ctypes.c_void_p), n, self.stream),
+                    "ts_read_sim_times")
+        return c[:n], a[:n]
+
     def set_trace(self, capacity: int) -> None:
         """Keep the per-pass allocation rows of the next runs (ts_engine_set_trace);
         0 turns the trace off."""

@@ -336,6 +336,41 @@ def gen_trace():
     dump("trace", cases)
 
 
+def gen_cost():
+    """The wave clock of the reference cost model (wave_ref.run_waves(cost=...):
+    service_time and CostModel of backend.py:287-311, charged as
+    simulator.py:443-463) on the CLI serving workload, four presets."""
+    from treeserve.backend import CostModel
+
+    cli = make_workload(500, MIX, 20260810)
+    arr = serving_arrivals(500, 5.0, 20260810, 20.0)
+    mixed = make_workload(97, (0.5, 0.3, 0.2), 77, branching=3,
+                          depth_ranges={Difficulty.EASY: (3, 9), Difficulty.HARD_SOLVABLE: (4, 10), Difficulty.UNSOLVABLE: (2, 6)},
+                          accept_threshold=0.35)
+    cases = []
+    for name, wl, probs, arrivals, M, pe, ne, boost, cost in (
+        ("cli_vanilla", "cli_default", cli, arr, 16, False, False, False, CostModel()),
+        ("cli_pe", "cli_default", cli, arr, 16, True, False, False, CostModel()),
+        ("cli_pe_ne", "cli_default", cli, arr, 16, True, True, False, CostModel()),
+        ("cli_pe_ne_boost", "cli_default", cli, arr, 16, True, True, True, CostModel()),
+        ("mixed_M200_cost", "mixed_b3", mixed, None, 200, True, True, True,
+         CostModel(per_token_latency=0.0031, engine_capacity=7, reward_latency=0.02)),
+    ):
+        sch = SchedulerConfig(max_concurrency=M, boosting_enabled=boost)
+        out, info = wave_ref.run_waves(probs, sched=sch, rollout_budget=32, depth_cap=16, expand_width=4,
+                                       positive_exit=pe, negative_exit=ne, arrival_steps=arrivals, cost=cost)
+        cases.append({"name": name, "workload": wl, "n": len(probs), "arrival_steps": arrivals,
+                      "max_concurrency": M, "positive_exit": pe, "negative_exit": ne, "boosting_enabled": boost,
+                      "budget": 32, "depth_cap": 16, "expand_width": 4,
+                      "cost": [cost.per_token_latency, cost.engine_capacity, cost.reward_latency],
+                      "steps": info["steps"],
+                      "sim_arrival": [o["sim_arrival"] for o in out],
+                      "sim_completion": [o["sim_completion"] for o in out],
+                      "tokens": [o["tokens_generated"] for o in out]})
+        print("cost", name, info["steps"])
+    dump("cost", cases)
+
+
 def gen_targets():
     """compute_targets (scheduler.py:143-187) on random pools, incl. equal-score lock-step pools."""
     r = random.Random(7)
@@ -678,6 +713,6 @@ def gen_arrivals():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps", "workload_json", "arrivals", "trace"]
+    which = sys.argv[1:] or ["rng", "workloads", "steps", "serial", "deep", "waves", "targets", "policy", "beam", "metrics", "tree_json", "beam_steps", "workload_json", "arrivals", "trace", "cost"]
     for w in which:
         globals()["gen_" + w]()

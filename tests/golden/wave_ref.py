@@ -31,7 +31,7 @@ REF_SRC = "/root/reference/pkg/src"
 if REF_SRC not in sys.path:
     sys.path.insert(0, REF_SRC)
 
-from treeserve.backend import ProblemBackend  # noqa: E402
+from treeserve.backend import ProblemBackend, service_time  # noqa: E402
 from treeserve.scheduler import (  # noqa: E402
     Job,
     JobState,
@@ -71,12 +71,24 @@ def run_waves(
     max_steps: int = 1_000_000,
     keep_trees: bool = False,
     trace=None,
+    cost=None,
 ):
     """``trace``: a list that receives the per-pass records of the reference's
     trace (simulator.py:314-341: "allocation" per running job, then the
     "action" records of ``reconcile``), plus a "job_finished" record when a
     job exits (the event record of simulator.py:240-249 without the heap's
-    ``seq``)."""
+    ``seq``).
+
+    ``cost``: a reference ``CostModel`` (backend.py:287-311) drives the WAVE
+    CLOCK: each launched rollout's generation requests (its expansions, in
+    order) take ``max(service_time(c.token_count, cost, load) for c) +
+    cost.reward_latency`` each (simulator.py:443-463), accumulated onto the
+    wave's start clock like the reference's event times; ``load`` is the
+    wave's in-flight candidate count, sum over the wave's launched rollouts of
+    the expansion width; a job's wave ends with its last rollout, the clock
+    advances to the latest job's end (idle steps take no time).  A job's
+    simulated arrival is the clock at its arrival step, its completion the end
+    of its exit wave."""
     scoring = scoring or ScoringConfig()
     selection = selection or SelectionParams()
     sched = sched or SchedulerConfig()
@@ -97,12 +109,29 @@ def run_waves(
     targets_trace = []
     next_arrival = 0
     step = 0
+    clock = 0.0
+    clock_at = []
+    sim_done = [None] * n
+    rec_toks = None  # per launched rollout of the current job: max token count of each expansion
+
+    if cost is not None:
+        class _Rec:
+            def __init__(self, inner):
+                self.inner = inner
+
+            def candidates_for(self, tree, node_id):
+                cands = self.inner.candidates_for(tree, node_id)
+                rec_toks[-1].append([c.token_count for c in cands])
+                return cands
+
+        backends = [_Rec(b) for b in backends]
     while step < max_steps:
         while next_arrival < n and arrival_steps[next_arrival] <= step:
             state.pending_queue.append(jobs[next_arrival])
             next_arrival += 1
         if next_arrival >= n and not state.pending_queue and not state.run_queue:
             break
+        clock_at.append(clock)
         state.now = step * dt
         for job in admit_jobs(state, sched):
             admit_step[job.job_id] = step
@@ -122,10 +151,13 @@ def run_waves(
                 entry = ({"action": "launch", "count": action.count} if isinstance(action, LaunchAction)
                          else {"action": "preempt", "rollout": action.rollout_id})
                 trace.append({"time": round(now, 9), "kind": "action", "job": action.job_id, **entry})
+        wave_rollouts = {}  # job -> [[token counts of each expansion] per launched rollout]
+        finished_now = []
         for job in list(running):
             i = job.job_id
             tree = job.tree
             backend = backends[i]
+            rec_toks = wave_rollouts.setdefault(i, [])
             P = targets[i]
             count = min(P, tree.rollout_budget - tree.completed_rollouts)
             terms = []
@@ -140,10 +172,13 @@ def run_waves(
                         decisions[i] = d
                         exit_step[i] = step
                         finished = True
+                        finished_now.append(i)
                         if trace is not None:
                             trace.append({"time": round(state.now, 9), "kind": "job_finished", "job": i,
                                           "rollout": None})
                     break
+                if cost is not None:
+                    rec_toks.append([])
                 terms.append(simulate_to_terminal(tree, leaf, backend, depth_cap))
             launched_total[i] += len(terms)
             if finished:
@@ -158,10 +193,25 @@ def run_waves(
                         cancelled_total[i] += 1
                     decisions[i] = d
                     exit_step[i] = step
+                    finished_now.append(i)
                     if trace is not None:
                         trace.append({"time": round(state.now, 9), "kind": "job_finished", "job": i,
                                       "rollout": None})
                     break
+        if cost is not None:
+            load = sum(min(expand_width, problems[i].branching) * len(r) for i, r in wave_rollouts.items())
+            latest = clock
+            for i, rolls in wave_rollouts.items():
+                end = clock
+                for exps in rolls:
+                    t = clock
+                    for toks in exps:
+                        t = t + (max(service_time(tc, cost, load) for tc in toks) + cost.reward_latency)
+                    end = max(end, t)
+                if i in finished_now:
+                    sim_done[i] = end
+                latest = max(latest, end)
+            clock = latest
         step += 1
     out = []
     for i, (job, problem) in enumerate(zip(jobs, problems)):
@@ -174,7 +224,7 @@ def run_waves(
             "best_score": best.aggregate_score if best else 0.0,
             "best_path": list(best_path),
             "rollouts_completed": tree.completed_rollouts,
-            "tokens_generated": backends[i].tokens,
+            "tokens_generated": getattr(backends[i], "inner", backends[i]).tokens,
             "solved": problem.golden_path is not None and tuple(best_path) == problem.golden_path,
             "exit_step": exit_step[i],
             "admit_step": admit_step[i],
@@ -184,5 +234,8 @@ def run_waves(
         }
         if keep_trees:
             rec["tree"] = tree
+        if cost is not None:
+            rec["sim_arrival"] = clock_at[arrival_steps[i]]
+            rec["sim_completion"] = sim_done[i]
         out.append(rec)
     return out, {"steps": step, "targets_trace": targets_trace}

@@ -102,3 +102,11 @@ def assert_tree_equal(got: dict, want: dict, label: str = ""):
         w = np.asarray(want[k], dtype=g.dtype)
         bad = np.nonzero(g != w)[0]
         assert bad.size == 0, f"{label}: field {k} differs at node {bad[0]}: {g[bad[0]]!r} != {w[bad[0]]!r}"
+
+
+def cost_case_config(case) -> SearchConfig:
+    """SearchConfig of a tests/golden/cost.json.gz case (default scoring/selection)."""
+    return SearchConfig(
+        scheduler=SchedulerConfig(max_concurrency=case["max_concurrency"], boosting_enabled=case["boosting_enabled"]),
+        rollout_budget=case["budget"], depth_cap=case["depth_cap"], expand_width=case["expand_width"],
+        positive_exit=case["positive_exit"], negative_exit=case["negative_exit"])

@@ -133,3 +133,22 @@ def test_compute_targets_kats():
         comp = [j[1] for j in kat["jobs"]]
         best = [j[2] for j in kat["jobs"]]
         assert oracle.compute_targets(cfg, kat["now_step"], arr, comp, best) == kat["targets"]
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in load("cost")])
+def test_wave_clock_matches_reference(name):
+    """The oracle's wave clock of the cost model (or_run_waves_cost) equals the
+    reference-composed wave run charging service_time/reward_latency
+    (wave_ref.run_waves(cost=...)), every simulated time bit for bit."""
+    from golden_io import cost_case_config
+
+    case = next(c for c in load("cost") if c["name"] == name)
+    recs = load("workloads")[case["workload"]][: case["n"]]
+    r = oracle.OracleRun(table(recs, case["arrival_steps"]), cost_case_config(case).to_c(), threads=4,
+                         cost=case["cost"])
+    done, arr = r.sim_times()
+    assert r.steps == case["steps"]
+    assert [o.tokens_generated for o in r.outcomes[: case["n"]]] == case["tokens"]
+    assert done.tolist() == case["sim_completion"]
+    assert arr.tolist() == case["sim_arrival"]
+    r.close()
