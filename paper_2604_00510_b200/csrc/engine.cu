@@ -194,6 +194,37 @@ __device__ __forceinline__ uint64_t state_at(const uint64_t (&h)[NSLOT], int d) 
   constexpr int GS = 8 * NSLOT;
   return __shfl_sync(FULL, h[T % NSLOT], (T / NSLOT) * GS + d);
 }
+// The simulation keeps, per depth d it expands, the fold states of that depth:
+// lanes with lane % GS == d copy their slots at level d (`snap`).  The prior
+// (tag 2, len d) and token (tag 3, len d+1) draws of the w children are not on
+// greedy_child's critical path, so they are made in the lane-parallel
+// expansion batch instead (lane l = depth l), from these snapshots.
+template <int NSLOT>
+__device__ __forceinline__ void snap_take(uint64_t (&snap)[NSLOT], const uint64_t (&h)[NSLOT], int d) {
+  constexpr int GS = 8 * NSLOT;
+  if (((threadIdx.x & 31) % GS) == d) {
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) snap[k] = h[k];
+  }
+}
+template <int NSLOT>
+__device__ __forceinline__ void snap_prior_tokens(const uint64_t (&snap)[NSLOT], uint64_t& hp, uint64_t& hk) {
+  constexpr int GS = 8 * NSLOT;
+  const int l = (threadIdx.x & 31) % GS;
+  hp = __shfl_sync(FULL, snap[0 % NSLOT], (0 / NSLOT) * GS + l);
+  hk = __shfl_sync(FULL, snap[2 % NSLOT], ((2 / NSLOT) * GS + l) & 31);
+}
+template <int WT>
+__device__ __forceinline__ double pick_raw(const double (&rv)[WT ? WT : 1], const double* rawl, int i) {
+  if constexpr (WT > 0) return rv[i];
+  else return rawl[i];
+}
+// generate_steps (backend.py:248-263) for child j of a node whose prior/token
+// prefix folds are hp/hk: the raw prior 0.5 + uniform and the token count.
+__device__ __forceinline__ double draw_raw_prior(uint64_t hp, int j) { return 0.5 + u53(sm64(hp ^ (uint64_t)j)); }
+__device__ __forceinline__ long long draw_tokens(uint64_t hk, int j) {
+  return 40 + (long long)(sm64(hk ^ (uint64_t)j) % 81ull);
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -2287,14 +2318,16 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     // --- simulate_to_terminal (tree.py:322-349) with generate_steps replayed
     //     (backend.py:230-269); lane j = child j ---
     bool forced = false;
+    uint64_t snap[NSLOT];
+#pragma unroll
+    for (int k = 0; k < NSLOT; ++k) snap[k] = 0;
     while (true) {
       if (depth >= cf.depth_cap) { forced = true; break; }  // tree.py:340-343
       if (nnodes + width > v.cap) { status = TS_POOL_OVERFLOW; break; }
       const int d = depth;
       const int len = d + 1;
       const uint64_t hr = state_at<NSLOT, 1>(h, d);
-      const uint64_t hp = state_at<NSLOT, 0>(h, d);
-      const uint64_t hk = state_at<NSLOT, 2>(h, d);
+      snap_take<NSLOT>(snap, h, d);
       const double graw = __shfl_sync(FULL, grew, d);
       const int gnext = __shfl_sync(FULL, gstep, d);
       const bool gchild = golden && len <= glen && lane == gnext;
@@ -2318,15 +2351,8 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       }
       const bool vl = lane < width;
       const int j = warp_argmax(rew, vl, 0);  // greedy_child (tree.py:307-319)
-      // off the critical path: raw prior and token count of child `lane`
-      const double raw = 0.5 + u53(sm64(hp ^ jj));
-      const long long tok = 40 + (long long)(sm64(hk ^ jj) % 81ull);
       const unsigned tmask = __ballot_sync(FULL, vl && term);
-      if (vl) {
-        s_raw[d * WS + lane] = raw;
-        s_rew[d * WS + lane] = rew;
-        tok_acc += tok;
-      }
+      if (vl) s_rew[d * WS + lane] = rew;
       if (lane == d) lvl_term = tmask;
       const bool jterm = (tmask >> j) & 1u;
       node = nnodes + j;
@@ -2366,18 +2392,31 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     int live = 0;    // non-terminal children of this level
     int ne_cnt = 0;  // NE: check-relevant viable new leaves
     uint32_t meta_l = 0;
+    uint64_t hp, hk;
+    snap_prior_tokens<NSLOT>(snap, hp, hk);
     if (act) {
       const int l = lane;
       const int len = l + 1;
       const int fcl = fc0 + (l - d0) * width;
-      const double* rawl = s_raw + l * WS;
+      // raw priors and token counts of this level's children (generate_steps)
+      double rv[WT ? WT : 1];
+      double* rawl = s_raw + l * WS;
+#pragma unroll
+      for (int i = 0; i < WS; ++i) {
+        if (i >= width) break;
+        const double x = draw_raw_prior(hp, i);
+        if constexpr (WT > 0) rv[i] = x;
+        else rawl[i] = x;
+        tok_acc += draw_tokens(hk, i);
+      }
+#define rawv(i) pick_raw<WT>(rv, rawl, i)
       const double* rewl = s_rew + l * WS;
       // total = sum(raw_priors): CPython Neumaier sum in child order
-      double tot = rawl[0], cc = 0.0;
+      double tot = rawv(0), cc = 0.0;
 #pragma unroll
       for (int i = 1; i < WS; ++i) {
         if (i >= width) break;
-        const double x = rawl[i];
+        const double x = rawv(i);
         const double t = tot + x;
         if (fabs(tot) >= fabs(x)) cc += (tot - t) + x;
         else cc += (x - t) + tot;
@@ -2395,7 +2434,8 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
         const bool onpath = j == pj;
         NO[c] = onpath ? O_ONE : 0ull;
         Wv[c] = 0.0;
-        PR[c] = rawl[j] / tot;
+        PR[c] = rawv(j) / tot;
+#undef rawv
         RW[c] = rew;
         PA[c] = node_l;
         // the on-path child expanded at the next level gets its fc/meta from lane l+1
@@ -3209,14 +3249,16 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     const bool risky = jb.risky != 0;
     int depth = d0, nrel = 0, node = leaf;
     bool forced = false;
+    uint64_t snap[NSLOT];
+#pragma unroll
+    for (int q = 0; q < NSLOT; ++q) snap[q] = 0;
     // --- simulate_to_terminal, critical path (node ids relative to the commit base) ---
     while (true) {
       if (depth >= cf.depth_cap) { forced = true; break; }
       const int d = depth;
       const int len = d + 1;
       const uint64_t hr = state_at<NSLOT, 1>(h, d);
-      const uint64_t hp = state_at<NSLOT, 0>(h, d);
-      const uint64_t hk = state_at<NSLOT, 2>(h, d);
+      snap_take<NSLOT>(snap, h, d);
       const double graw = __shfl_sync(FULL, grew, d);
       const int gnext = __shfl_sync(FULL, gstep, d);
       const bool gchild = golden && len <= glen && lane == gnext;
@@ -3240,14 +3282,8 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
       }
       const bool vl = lane < width;
       const int j = warp_argmax(rew, vl, 0);
-      const double raw = 0.5 + u53(sm64(hp ^ jj));
-      const long long tok = 40 + (long long)(sm64(hk ^ jj) % 81ull);
       const unsigned tmask = __ballot_sync(FULL, vl && term);
-      if (vl) {
-        s_raw[d * WS + lane] = raw;
-        s_rew[d * WS + lane] = rew;
-        tok_acc += tok;
-      }
+      if (vl) s_rew[d * WS + lane] = rew;
       if (lane == d) lvl_term = tmask;
       const bool jterm = (tmask >> j) & 1u;
       node = nrel + j;  // relative id
@@ -3277,11 +3313,19 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     const bool act = lane >= d0 && lane < d0 + nlev;
     int live = 0, ne_cnt = 0;
     uint32_t meta_l = 0;  // word of path node l (expanded at depth l), minus the root's case
+    uint64_t hp, hk;
+    snap_prior_tokens<NSLOT>(snap, hp, hk);
     if (act) {
       const int l = lane;
       const int len = l + 1;
       double* rawl = s_raw + l * WS;
       const double* rewl = s_rew + l * WS;
+      // raw priors and token counts of this level's children (generate_steps)
+#pragma unroll
+      for (int i = 0; i < WS; ++i) {
+        rawl[i] = draw_raw_prior(hp, i);
+        tok_acc += draw_tokens(hk, i);
+      }
       double tot = rawl[0], cc = 0.0;
 #pragma unroll
       for (int i = 1; i < WS; ++i) {
@@ -3658,7 +3702,7 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
 }
 
 template <int NSLOT, int WT>
-__global__ void __launch_bounds__(HEAVY_THREADS) k_heavy(View v, int step) {
+__global__ void __launch_bounds__(HEAVY_THREADS, 2) k_heavy(View v, int step) {
   extern __shared__ double hsm[];
   __shared__ HeavyCtl ctl;
   __shared__ HeavyJob ring[HEAVY_RING];
