@@ -21,9 +21,11 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 5
+#define TS_ABI_VERSION 6
 #define TS_MAX_DEPTH 32 /* golden path / reward table length; base_depth <= 31 */
 #define TS_MAX_WIDTH 32 /* branching <= one warp                                */
+#define TS_MAX_PEERS 8  /* ranks of one node in ts_run_sharded                    */
+#define TS_IPC_HANDLE_BYTES 64
 
 /* Status codes, mapped to the reference's exception classes by the shim. */
 typedef enum ts_status {
@@ -180,6 +182,31 @@ int ts_step_wave(ts_engine* eng, int32_t step, void* stream);
 /* Whole batch on one GPU: the five calls above per step until every search
  * has exited (or max_steps).  stats_out may be NULL. */
 int ts_run(ts_engine* eng, int32_t max_steps, ts_run_stats* stats_out, void* stream);
+
+/* ---- multi-GPU: the sharded batch over peer memory ---------
+ * Replaces the per-wave all-gathers of ts_step_counts / ts_step_records plus
+ * a host round trip.  Each rank owns an exchange buffer (ts_xchg_bytes: a
+ * 512-byte header of flags and counts, then n_global scheduler records);
+ * every rank writes its counts and records straight into every rank's buffer
+ * (NVLink stores through CUDA IPC mappings, or device stores when several
+ * ranks share a device in one process) and raises a flag there, and waits on
+ * the flags in its own buffer.  Unequal shards are fine (each rank writes at
+ * its global offset).  Call order on every rank: ts_load_problems →
+ * ts_xchg_create (allocates and zeroes this rank's buffer; ipc_handle_out,
+ * TS_IPC_HANDLE_BYTES, may be NULL for in-process ranks) → exchange the
+ * handles (any host collective) and a barrier → ts_xchg_connect (ipc_handles:
+ * world × TS_IPC_HANDLE_BYTES, or dev_ptrs: world device pointers for ranks
+ * in this process; entry rank is ignored) → ts_run_sharded per batch (a
+ * collective: every rank the same number of times, with the same
+ * last_arrival_global = the largest arrival_step of the whole run queue).
+ * ts_run_sharded is ts_run's device-driven graph loop with the exchange
+ * inside; stats_out->steps is the global wave count.  A peer that stops
+ * signalling for 20 s fails the call with TS_CUDA instead of hanging. */
+int64_t ts_xchg_bytes(int32_t n_global);
+int ts_xchg_create(ts_engine* eng, int32_t world, int32_t rank, void** dev_ptr_out, uint8_t* ipc_handle_out);
+int ts_xchg_connect(ts_engine* eng, const uint8_t* ipc_handles, void* const* dev_ptrs);
+int ts_run_sharded(ts_engine* eng, int32_t max_steps, int32_t last_arrival_global, ts_run_stats* stats_out,
+                   void* stream);
 
 /* ---- run-time invariants (checked mode) ---------------------------------- */
 /* The reference asserts these while it runs (Engine._check_capacity and the

@@ -12,7 +12,7 @@ import os
 
 TS_MAX_DEPTH = 32
 TS_MAX_WIDTH = 32
-TS_ABI_VERSION = 5
+TS_ABI_VERSION = 6
 
 TS_OK = 0
 TS_INVALID_ARGUMENT = 1
@@ -136,7 +136,10 @@ EXPORTED = (
     "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
     "ts_generate_steps", "ts_engine_set_checks", "ts_read_invariants", "ts_engine_set_trace", "ts_read_trace",
     "ts_reconcile", "ts_engine_set_cost_model", "ts_read_sim_times",
+    "ts_xchg_bytes", "ts_xchg_create", "ts_xchg_connect", "ts_run_sharded",
 )
+TS_MAX_PEERS = 8
+TS_IPC_HANDLE_BYTES = 64
 
 
 class TsSchedParams(ctypes.Structure):
@@ -293,6 +296,10 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_engine_set_cost_model": (ctypes.c_int, [vp, ctypes.c_double, i32, ctypes.c_double]),
         "ts_read_sim_times": (ctypes.c_int, [vp, vp, vp, i32, vp]),
         "ts_read_trace": (ctypes.c_int, [vp, vp, ctypes.c_int64, P(ctypes.c_int64), P(ctypes.c_int64), vp]),
+        "ts_xchg_bytes": (ctypes.c_int64, [i32]),
+        "ts_xchg_create": (ctypes.c_int, [vp, i32, i32, P(vp), vp]),
+        "ts_xchg_connect": (ctypes.c_int, [vp, vp, vp]),
+        "ts_run_sharded": (ctypes.c_int, [vp, i32, i32, P(TsRunStats), vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

@@ -94,6 +94,10 @@ struct Counters {
   unsigned long long clock_max;
   long long cost_load;
   long long clock_step1;  // 1 + the last step whose start clock was recorded (0: none)
+  // ts_run_sharded: the batch has ended (every later kernel of the graph body
+  // returns at once), CTAs of k_px_records done this wave, a peer timed out
+  int px_done, px_blocks, px_err, px_gen;  // px_gen: the batch generation (epochs of the flags)
+  int px_last_arrival, _pad4;              // the run queue's last arrival step (admission exchange)
 };
 
 // Kernel-side view of one engine.
@@ -137,6 +141,11 @@ struct View {
   unsigned long long* step_times;
   int32_t step_times_cap;
   // targets-kernel scratch (global fallback when runs exceed shared memory)
+  // ts_run_sharded: every rank's exchange buffer (this process's mapping, px[prank]
+  // is this rank's own), the batch generation, and whether admission needs
+  // the counts exchange (capacity below the run queue) or up to which step
+  unsigned char* px[TS_MAX_PEERS];
+  int32_t pworld, prank, padm_all;
   double* g_runS;
   int32_t* g_runStart;
   long long* g_runWant;
@@ -386,6 +395,219 @@ __global__ void k_records(View v, int step, ts_sched_record* rec) {
     r._pad = (uint32_t)s->completed;
   }
   rec[i] = r;
+}
+
+// ---- the sharded wave loop over peer memory (ts_run_sharded) ----------------------
+//
+// Every rank owns an exchange buffer; a peer writes its scheduler inputs
+// straight into every other rank's buffer (NVLink stores through CUDA IPC
+// mappings; plain device stores when the ranks are emulated on one GPU) and
+// then sets its flag there to the wave's epoch.  A rank waits on the flags in
+// its own buffer, so each exchange is one round of peer stores plus one flag
+// wait — no collective library call, no host round trip — and the whole
+// sharded batch is one device-driven graph loop like ts_run's.
+struct XHdr {
+  unsigned long long fa[TS_MAX_PEERS];  // counts phase: epoch written by peer p
+  unsigned long long fb[TS_MAX_PEERS];  // records phase
+  long long cnt[TS_MAX_PEERS][4];       // peer p: {running, arrived-but-pending, unfinished, -} before admission
+  long long unf[TS_MAX_PEERS];          // peer p: unfinished searches when its records were written
+};
+constexpr size_t XHDR_BYTES = 512;
+constexpr int PX_MAX_WAVES = 1 << 20;  // the log1p table ts_xchg_connect sizes for the sharded loop
+static_assert(sizeof(XHdr) <= XHDR_BYTES, "exchange header");
+__host__ __device__ inline size_t xchg_bytes(long long n_global) {
+  return XHDR_BYTES + (size_t)n_global * sizeof(ts_sched_record);
+}
+__device__ __forceinline__ XHdr* xh(const View& v, int p) { return (XHdr*)v.px[p]; }
+__device__ __forceinline__ ts_sched_record* xrec(const View& v, int p) {
+  return (ts_sched_record*)(v.px[p] + XHDR_BYTES);
+}
+__device__ __forceinline__ unsigned long long px_epoch(const View& v, int step) {
+  return ((unsigned long long)(uint32_t)v.ctr->px_gen << 32) | (unsigned long long)(uint32_t)(step + 1);
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long x) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long x;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+  return x;
+}
+// wait until every peer's flag in this rank's buffer reached `epoch`; a peer
+// that stays silent for TS_PX_TIMEOUT_NS ends the batch with an error
+#ifndef TS_PX_TIMEOUT_NS
+#define TS_PX_TIMEOUT_NS 20000000000ull
+#endif
+__device__ bool px_wait(const View& v, const unsigned long long* flags, unsigned long long epoch) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < (unsigned)v.pworld) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(flags + threadIdx.x) < epoch) {
+      if (globaltimer() - t0 > TS_PX_TIMEOUT_NS) {
+        s_ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+__device__ __forceinline__ bool px_adm_active(const View& v, int step) {
+  return v.padm_all || step <= v.ctr->px_last_arrival;
+}
+// the batch ends: every later kernel of the graph returns at once and the
+// waves find empty work lists
+__device__ void px_finish(const View& v, cudaGraphConditionalHandle cond, int err) {
+  Counters* c = v.ctr;
+  c->px_done = 1;
+  if (err) c->px_err = err;
+  c->work_count = 0;
+  c->work_next = 0;
+  c->heavy_count = 0;
+  c->heavy_next = 0;
+  cudaGraphSetConditional(cond, 0);
+}
+
+__global__ void k_px_reset(Counters* c, int gen, int last_arrival) {
+  c->px_done = 0;
+  c->px_blocks = 0;
+  c->px_err = 0;
+  c->px_gen = gen;
+  c->px_last_arrival = last_arrival;
+}
+
+// counts phase: this rank's {running, pending, unfinished} into every peer's buffer
+__global__ void k_px_counts(View v) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  if (!px_adm_active(v, step)) return;
+  int lo = 0, hi = v.n_local;  // arrivals are non-decreasing: upper_bound(arrival, step)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v.arrival[mid] <= step) lo = mid + 1;
+    else hi = mid;
+  }
+  const long long run = c->running, pend = (long long)lo - c->head, unf = (long long)v.n_local - c->finished;
+  const int p = threadIdx.x;
+  if (p < v.pworld) {
+    long long* d = xh(v, p)->cnt[v.prank];
+    d[0] = run;
+    d[1] = pend;
+    d[2] = unf;
+    __threadfence_system();
+    st_release_sys(&xh(v, p)->fa[v.prank], px_epoch(v, step));
+  }
+}
+
+// admit_jobs (scheduler.py:131-140) over the global FIFO from every rank's
+// counts, and the loop test (no unfinished search on any rank)
+__global__ void k_px_admit(View v, cudaGraphConditionalHandle cond, int max_steps) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  if (step >= max_steps || step >= v.log1p_n) {
+    if (threadIdx.x == 0) px_finish(v, cond, 0);
+    return;
+  }
+  if (!px_adm_active(v, step)) {
+    if (threadIdx.x == 0) c->admit_lo = c->admit_hi = c->head;  // nobody can be pending
+    return;
+  }
+  const XHdr* x = xh(v, v.prank);
+  if (!px_wait(v, x->fa, px_epoch(v, step))) {
+    if (threadIdx.x == 0) px_finish(v, cond, 1);
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  long long run_g = 0, pend_g = 0, before = 0, unf_g = 0;
+  for (int r = 0; r < v.pworld; ++r) {
+    run_g += x->cnt[r][0];
+    pend_g += x->cnt[r][1];
+    unf_g += x->cnt[r][2];
+    if (r < v.prank) before += x->cnt[r][1];
+  }
+  if (unf_g == 0) {
+    px_finish(v, cond, 0);
+    return;
+  }
+  long long A = (long long)v.cfg.max_concurrency - run_g;
+  if (A > pend_g) A = pend_g;
+  if (A < 0) A = 0;
+  long long q = A - before;
+  if (q > x->cnt[v.prank][1]) q = x->cnt[v.prank][1];
+  if (q < 0) q = 0;
+  c->admit_lo = c->head;
+  c->admit_hi = c->head + q;
+  c->head += q;
+  c->running += q;
+}
+
+// parallelism_score (scheduler.py:118-128): this rank's records into every
+// peer's buffer at its global offset; the last CTA signals
+__global__ void k_px_records(View v) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < v.n_local) {
+    SearchState* s = v.st + i;
+    int state = s->state;
+    if (i >= c->admit_lo && i < c->admit_hi) {
+      state = ST_RUNNING;
+      s->state = ST_RUNNING;
+      s->admit_step = step;
+    }
+    ts_sched_record r;
+    r.score = 0.0;
+    r.flags = 0;
+    r._pad = 0;
+    if (state == ST_RUNNING) {
+      const ts_config& cf = v.cfg;
+      const double ratio = s->job_best / cf.positive_exit_threshold;
+      r.score = v.log1p_tab[step - v.arrival[i]] + (ratio > cf.proximity ? cf.beta : 0.0);
+      r.flags = 1u | (s->completed >= cf.obs_threshold ? 2u : 0u) | (ratio > cf.proximity ? 4u : 0u);
+      r._pad = (uint32_t)s->completed;
+    }
+    for (int p = 0; p < v.pworld; ++p) xrec(v, p)[v.goff + i] = r;
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(&c->px_blocks, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x == 0) c->px_blocks = 0;
+  const int p = threadIdx.x;
+  if (p < v.pworld) {
+    xh(v, p)->unf[v.prank] = (long long)v.n_local - c->finished;
+    __threadfence_system();
+    st_release_sys(&xh(v, p)->fb[v.prank], px_epoch(v, step));
+  }
+}
+
+// every rank's records are in: the loop test, and the step for the scheduler and the waves
+__global__ void k_px_wait(View v, cudaGraphConditionalHandle cond) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  const XHdr* x = xh(v, v.prank);
+  if (!px_wait(v, x->fb, px_epoch(v, step))) {
+    if (threadIdx.x == 0) px_finish(v, cond, 1);
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  long long unf_g = 0;
+  for (int r = 0; r < v.pworld; ++r) unf_g += x->unf[r];
+  if (unf_g == 0) {
+    px_finish(v, cond, 0);
+    return;
+  }
+  c->cur_step = step;
+  c->step = step + 1;
 }
 
 // ---- compute_targets (scheduler.py:143-187) in one CTA ------------------------
@@ -881,6 +1103,11 @@ __device__ __forceinline__ size_t targets_smem_dev() {
 __global__ void __launch_bounds__(SCHED_T) k_targets(View v, int step, const ts_sched_record* rec) {
   targets_block(v, step, rec, v.n_global, v.goff, v.goff + v.n_local, 0);
 }
+// ts_run_sharded: the one-CTA scheduler over the records in this rank's exchange buffer
+__global__ void __launch_bounds__(SCHED_T) k_px_targets(View v) {
+  if (v.ctr->px_done) return;
+  targets_block(v, v.ctr->cur_step, xrec(v, v.prank), v.n_global, v.goff, v.goff + v.n_local, 0);
+}
 
 // ---- compute_targets over many CTAs (multi-GPU runs: all n_global records) ----
 // The same algorithm as targets_block, with every cross-thread scan split into
@@ -1009,6 +1236,8 @@ __device__ void mt_scan_min2(double& a, double& b, double& ta, double& tb) {
 
 // phase 1: per-CTA counts, exact partial score sums, list minima
 __global__ void __launch_bounds__(MT_T) k_mt_count(View v, int step, const ts_sched_record* rec, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
+  if (step < 0) step = v.ctr->cur_step;
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int n = v.n_global;
@@ -1066,6 +1295,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_count(View v, int step, const ts_sc
 
 // phase 2 (one CTA): CTA offsets, the score sum T, the totals
 __global__ void __launch_bounds__(1024) k_mt_scan1(View v, const ts_sched_record* rec, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int n = v.n_global, G = mt_blocks(n);
@@ -1141,6 +1371,7 @@ __global__ void __launch_bounds__(1024) k_mt_scan1(View v, const ts_sched_record
 
 // phase 3: per-thread list positions and previous scores; runs of equal score
 __global__ void __launch_bounds__(MT_T) k_mt_runs(View v, const ts_sched_record* rec, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int n = v.n_global;
@@ -1187,6 +1418,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_runs(View v, const ts_sched_record*
 
 // phase 4 (one CTA): run offsets of the CTAs; run totals
 __global__ void __launch_bounds__(1024) k_mt_scan2(View v, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int G = mt_blocks(v.n_global);
@@ -1206,6 +1438,7 @@ __global__ void __launch_bounds__(1024) k_mt_scan2(View v, unsigned char* mt) {
 
 // phase 5: run records (score, start position) of the runs starting in each chunk
 __global__ void __launch_bounds__(MT_T) k_mt_write_runs(View v, const ts_sched_record* rec, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int n = v.n_global, G = gridDim.x;
@@ -1245,6 +1478,7 @@ __device__ __forceinline__ long long mt_want(double s, double T, long long M) {
 
 // phase 6: want per run and the per-CTA sums of cnt*(want-1) (one run per thread, both lists)
 __global__ void __launch_bounds__(MT_T) k_mt_want(View v, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int n = v.n_global, G3 = gridDim.x;
@@ -1278,6 +1512,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_want(View v, unsigned char* mt) {
 
 // phase 7 (one CTA): scan of the run-CTA sums; tw0, tw1
 __global__ void __launch_bounds__(1024) k_mt_scan3(View v, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int G3 = mt_run_blocks(v.n_global);
@@ -1309,6 +1544,7 @@ __global__ void __launch_bounds__(1024) k_mt_scan3(View v, unsigned char* mt) {
 // phase 8: targets of the local slice (closed-form clamp + round-robin, merge
 // rank by binary search in the other list's runs); pipelined-mode flags
 __global__ void __launch_bounds__(MT_T) k_mt_targets(View v, const ts_sched_record* rec, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   const int n = v.n_global, G3 = mt_run_blocks(n);
@@ -1395,6 +1631,8 @@ __global__ void __launch_bounds__(MT_T) k_mt_targets(View v, const ts_sched_reco
 
 // phase 9 (one CTA over the local slice): single-warp and pipelined work lists
 __global__ void __launch_bounds__(TT) k_mt_split(View v, int step, const ts_sched_record* rec, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
+  if (step < 0) step = v.ctr->cur_step;
   MtLayout L;
   mt_layout(mt, v.n_global, v.n_local, &L);
   __shared__ long long shl[264];
@@ -1430,6 +1668,8 @@ __global__ void __launch_bounds__(TT) k_mt_split(View v, int step, const ts_sche
 // records) fits on the device at once; the per-phase kernels above are the
 // fallback.
 __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sched_record* rec, unsigned char* mt) {
+  if (v.pworld && v.ctr->px_done) return;  // ts_run_sharded: the batch has ended
+  if (step < 0) step = v.ctr->cur_step;
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
 #ifdef TS_SCHED_PROF
@@ -4171,6 +4411,18 @@ struct ts_engine {
   int cost_n = 0;
   double* clock_at = nullptr;  // step_times_cap entries
   int graph_unroll = 3;  // scheduler passes + waves per iteration of the graph's while loop (TS_GRAPH_UNROLL)
+  // ts_run_sharded: this rank's exchange buffer and every rank's (IPC mappings
+  // of other processes' buffers, or in-process pointers), the batch generation
+  unsigned char* xbuf = nullptr;
+  size_t xbytes = 0;
+  int xworld = 0, xrank = 0, xgen = 0;
+  unsigned char* xpeer[TS_MAX_PEERS] = {};
+  bool xipc[TS_MAX_PEERS] = {};
+  bool xconnected = false;
+  cudaGraph_t px_graph = nullptr;
+  cudaGraphExec_t px_exec = nullptr;
+  View px_view;
+  int px_max_steps = -1;
 };
 
 namespace {
@@ -4588,6 +4840,127 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   return TS_OK;
 }
 
+void destroy_px_graph(ts_engine* e) {
+  if (e->px_exec) cudaGraphExecDestroy(e->px_exec);
+  if (e->px_graph) cudaGraphDestroy(e->px_graph);
+  e->px_exec = nullptr;
+  e->px_graph = nullptr;
+}
+
+void xchg_release(ts_engine* e) {
+  destroy_px_graph(e);
+  for (int p = 0; p < TS_MAX_PEERS; ++p) {
+    if (e->xipc[p] && e->xpeer[p]) cudaIpcCloseMemHandle(e->xpeer[p]);
+    e->xipc[p] = false;
+    e->xpeer[p] = nullptr;
+  }
+  if (e->xbuf) cudaFree(e->xbuf);
+  e->xbuf = nullptr;
+  e->xbytes = 0;
+  e->xconnected = false;
+}
+
+// while (cond) { counts -> admit -> records -> wait -> compute_targets -> waves }:
+// ts_run's loop with the scheduler's global terms exchanged over peer memory
+View px_make_view(ts_engine* e) {
+  View v = make_view(e);
+  for (int p = 0; p < e->xworld; ++p) v.px[p] = e->xpeer[p];
+  v.pworld = e->xworld;
+  v.prank = e->xrank;
+  v.padm_all = (long long)e->cfg.max_concurrency < (long long)e->n_global ? 1 : 0;
+  return v;
+}
+
+int build_px_graph(ts_engine* e, const View& v, int max_steps) {
+  destroy_px_graph(e);
+  int blocks = 0, rc;
+  if ((rc = wave_grid(e, blocks))) return rc;
+  cudaGraph_t g = nullptr;
+  TS_CUDA_TRY(e, cudaGraphCreate(&g, 0));
+  e->px_graph = g;
+  cudaGraphConditionalHandle h;
+  TS_CUDA_TRY(e, cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cn;
+  TS_CUDA_TRY(e, cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  View vv = v;
+  int ms = max_steps, stepm1 = -1;
+  const ts_sched_record* rec = (const ts_sched_record*)(e->xbuf + XHDR_BYTES);
+  unsigned char* mt = e->mt;
+  void* a_v[] = {(void*)&vv};
+  void* a_vc[] = {(void*)&vv, (void*)&h};
+  void* a_vcm[] = {(void*)&vv, (void*)&h, (void*)&ms};
+  void* a_st_rec_mt[] = {(void*)&vv, (void*)&stepm1, (void*)&rec, (void*)&mt};
+  void* a_rec_mt[] = {(void*)&vv, (void*)&rec, (void*)&mt};
+  void* a_mt[] = {(void*)&vv, (void*)&mt};
+  void* a_wave[] = {(void*)&vv, (void*)&stepm1};
+  auto kp = [](void* f, dim3 grid, dim3 block, size_t sm, void** args) {
+    cudaKernelNodeParams k;
+    memset(&k, 0, sizeof(k));
+    k.func = f;
+    k.gridDim = grid;
+    k.blockDim = block;
+    k.sharedMemBytes = (unsigned)sm;
+    k.kernelParams = args;
+    return k;
+  };
+  std::vector<cudaKernelNodeParams> chain;
+  chain.push_back(kp((void*)k_px_counts, dim3(1), dim3(32), 0, a_v));
+  chain.push_back(kp((void*)k_px_admit, dim3(1), dim3(32), 0, a_vcm));
+  chain.push_back(kp((void*)k_px_records, dim3((e->n_local + 255) / 256), dim3(256), 0, a_v));
+  chain.push_back(kp((void*)k_px_wait, dim3(1), dim3(32), 0, a_vc));
+  if (v.n_global <= e->mt_min) {
+    chain.push_back(kp((void*)k_px_targets, dim3(1), dim3(SCHED_T), targets_smem(), a_v));
+  } else {
+    const int G = mt_blocks(v.n_global), G3 = mt_run_blocks(v.n_global);
+    chain.push_back(kp((void*)k_mt_count, dim3(G), dim3(MT_T), 0, a_st_rec_mt));
+    chain.push_back(kp((void*)k_mt_scan1, dim3(1), dim3(1024), 0, a_rec_mt));
+    chain.push_back(kp((void*)k_mt_runs, dim3(G), dim3(MT_T), 0, a_rec_mt));
+    chain.push_back(kp((void*)k_mt_scan2, dim3(1), dim3(1024), 0, a_mt));
+    chain.push_back(kp((void*)k_mt_write_runs, dim3(G), dim3(MT_T), 0, a_rec_mt));
+    chain.push_back(kp((void*)k_mt_want, dim3(G3), dim3(MT_T), 0, a_mt));
+    chain.push_back(kp((void*)k_mt_scan3, dim3(1), dim3(1024), 0, a_mt));
+    chain.push_back(kp((void*)k_mt_targets, dim3(G), dim3(MT_T), 0, a_rec_mt));
+    chain.push_back(kp((void*)k_mt_split, dim3(1), dim3(TT), 0, a_st_rec_mt));
+  }
+  cudaKernelNodeParams kw = kp(wave_fn(e), dim3(blocks), dim3(WAVE_THREADS), wave_smem_of(e->wkind), a_wave);
+  cudaKernelNodeParams kh = kw;
+  if (v.heavy_on) {
+    int hb = 0;
+    if ((rc = heavy_grid(e, hb))) return rc;
+    kh = kp(heavy_fn(e), dim3(hb), dim3(HEAVY_THREADS), heavy_smem_of(e->wkind), a_wave);
+  }
+  cudaGraphNode_t prev[2];
+  int nprev = 0;
+  for (int u = 0; u < e->graph_unroll; ++u) {
+    for (const cudaKernelNodeParams& k : chain) {
+      cudaGraphNode_t n;
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n, body, nprev ? prev : nullptr, nprev, &k));
+      prev[0] = n;
+      nprev = 1;
+    }
+    const cudaGraphNode_t sched = prev[0];
+    cudaGraphNode_t n2, n3;
+    TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &sched, 1, &kw));
+    prev[0] = n2;
+    nprev = 1;
+    if (v.heavy_on) {
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n3, body, &sched, 1, &kh));
+      prev[1] = n3;
+      nprev = 2;
+    }
+  }
+  TS_CUDA_TRY(e, cudaGraphInstantiate(&e->px_exec, g, 0));
+  e->px_view = v;
+  e->px_max_steps = max_steps;
+  return TS_OK;
+}
+
 void host_stats(const Counters& c, ts_run_stats* o) {
   o->steps = (int32_t)(c.last_exit_step + 1);
   o->finished = (int32_t)c.finished;
@@ -4633,6 +5006,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     cr = cudaFuncSetAttribute(k_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   if (cr == cudaSuccess)
     cr = cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sched_smem());
+  if (cr == cudaSuccess)
+    cr = cudaFuncSetAttribute(k_px_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
       cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -4679,6 +5054,7 @@ int ts_engine_destroy(ts_engine* e) {
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
   destroy_run_graph(e);
+  xchg_release(e);
   if (e->pin) cudaFreeHost(e->pin);
   if (e->pin_out) cudaFreeHost(e->pin_out);
   if (e->pin_ctr) cudaFreeHost(e->pin_ctr);
@@ -5205,6 +5581,116 @@ int ts_read_trace(ts_engine* e, ts_trace_row* host_out, int64_t cap, int64_t* n_
                                    (cudaStream_t)stream));
     TS_CUDA_TRY(e, cudaStreamSynchronize((cudaStream_t)stream));
   }
+  return TS_OK;
+}
+
+int64_t ts_xchg_bytes(int32_t n_global) { return n_global < 0 ? -1 : (int64_t)xchg_bytes(n_global); }
+
+int ts_xchg_create(ts_engine* e, int32_t world, int32_t rank, void** dev_ptr_out, uint8_t* ipc_handle_out) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (world < 1 || world > TS_MAX_PEERS || rank < 0 || rank >= world || !dev_ptr_out)
+    return fail(e, TS_INVALID_ARGUMENT, "bad world/rank");
+  TS_CUDA_TRY(e, cudaSetDevice(e->device));
+  xchg_release(e);
+  e->xbytes = xchg_bytes(e->n_global);
+  TS_CUDA_TRY(e, cudaMalloc((void**)&e->xbuf, e->xbytes));
+  TS_CUDA_TRY(e, cudaMemset(e->xbuf, 0, e->xbytes));
+  TS_CUDA_TRY(e, cudaDeviceSynchronize());  // zeroed before any peer can write
+  e->xworld = world;
+  e->xrank = rank;
+  e->xgen = 0;
+  if (ipc_handle_out) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == TS_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    TS_CUDA_TRY(e, cudaIpcGetMemHandle(&h, e->xbuf));
+    memcpy(ipc_handle_out, &h, sizeof(h));
+  }
+  *dev_ptr_out = e->xbuf;
+  return TS_OK;
+}
+
+int ts_xchg_connect(ts_engine* e, const uint8_t* ipc_handles, void* const* dev_ptrs) {
+  if (!e || !e->xbuf) return fail(e, TS_INVALID_ARGUMENT, "ts_xchg_create first");
+  if (!ipc_handles && !dev_ptrs) return fail(e, TS_INVALID_ARGUMENT, "no peer buffers");
+  TS_CUDA_TRY(e, cudaSetDevice(e->device));
+  destroy_px_graph(e);
+  for (int p = 0; p < e->xworld; ++p) {
+    if (e->xipc[p] && e->xpeer[p]) cudaIpcCloseMemHandle(e->xpeer[p]);
+    e->xipc[p] = false;
+    e->xpeer[p] = nullptr;
+    if (p == e->xrank) {
+      e->xpeer[p] = e->xbuf;
+    } else if (dev_ptrs && dev_ptrs[p]) {
+      e->xpeer[p] = (unsigned char*)dev_ptrs[p];  // a rank emulated in this process
+    } else if (ipc_handles) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, ipc_handles + (size_t)p * TS_IPC_HANDLE_BYTES, sizeof(h));
+      void* q = nullptr;
+      TS_CUDA_TRY(e, cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess));
+      e->xpeer[p] = (unsigned char*)q;
+      e->xipc[p] = true;
+    } else {
+      return fail(e, TS_INVALID_ARGUMENT, "missing peer buffer");
+    }
+  }
+  // everything ts_run_sharded needs is allocated here: an allocation or free
+  // while another rank's loop spins on this rank's flags (several ranks on
+  // one device) would wait for that loop and never signal it
+  int rc;
+  cudaStream_t s0 = nullptr;
+  if ((rc = ensure_log1p(e, PX_MAX_WAVES, s0))) return rc;
+  if ((rc = ensure_step_times(e, e->log1p_n + 1, s0))) return rc;
+  if (!e->pin_ctr) TS_CUDA_TRY(e, cudaMallocHost((void**)&e->pin_ctr, sizeof(Counters)));
+  TS_CUDA_TRY(e, cudaDeviceSynchronize());
+  e->xconnected = true;
+  // the graph for the default max_steps, instantiated before any rank runs
+  if ((rc = build_px_graph(e, px_make_view(e), INT32_MAX)) != TS_OK) {
+    destroy_px_graph(e);
+    return rc;
+  }
+  return TS_OK;
+}
+
+int ts_run_sharded(ts_engine* e, int32_t max_steps, int32_t last_arrival_global, ts_run_stats* stats_out,
+                   void* stream) {
+  if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
+  if (!e->xconnected || e->xbytes != xchg_bytes(e->n_global))
+    return fail(e, TS_INVALID_ARGUMENT, "exchange not connected for this run queue (ts_xchg_create/connect)");
+  if (max_steps < 0) return fail(e, TS_INVALID_ARGUMENT, "max_steps must be >= 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  ++e->xgen;
+  Counters c;
+  long long step0 = 0;
+  {
+    k_px_reset<<<1, 1, 0, s>>>(e->ctr, e->xgen, last_arrival_global);
+    TS_LAUNCH_CHECK(e, "k_px_reset");
+    const View v = px_make_view(e);
+    if (!e->px_exec || e->px_max_steps != max_steps || memcmp(&v, &e->px_view, sizeof(View)) != 0) {
+      if ((rc = build_px_graph(e, v, max_steps)) != TS_OK) {
+        destroy_px_graph(e);
+        return rc;
+      }
+    }
+    TS_CUDA_TRY(e, cudaGraphLaunch(e->px_exec, s));
+    TS_CUDA_TRY(e, cudaMemcpyAsync(e->pin_ctr, e->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, s));
+    TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+    c = *e->pin_ctr;
+    const long long waves = c.step - step0;
+    e->launches += 1 + (waves / e->graph_unroll + 1) * e->graph_unroll *
+                           ((v.n_global <= e->mt_min ? 5 : 13) + (v.heavy_on ? 2 : 1));
+    step0 = c.step;
+    if (c.px_err) return fail(e, TS_CUDA, "a peer rank did not signal (peer exchange timed out)");
+    if (c.step < max_steps && c.step >= e->log1p_n && c.finished < e->n_local)
+      return fail(e, TS_INVALID_ARGUMENT, "ts_run_sharded: more than 2^20 waves");
+  }
+  if (stats_out) {
+    host_stats(c, stats_out);
+    stats_out->steps = (int32_t)c.step;  // waves of the global loop (the same on every rank)
+    stats_out->kernel_launches = e->launches;
+    stats_out->wave_ms = 0.0;
+  }
+  if (c.sched_error) return fail(e, TS_INVALID_ARGUMENT, "run queue scores not ordered by arrival");
   return TS_OK;
 }
 

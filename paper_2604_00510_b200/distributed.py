@@ -158,6 +158,59 @@ class ShardedRun:
         return max_steps
 
 
+class PeerShardedRun:
+    """The sharded batch of one rank as one device-driven graph loop
+    (``ts_run_sharded``): per wave every rank writes its admission counts and
+    scheduler records straight into every rank's exchange buffer over NVLink
+    (CUDA IPC mappings) and waits on flags in its own buffer — no collective
+    call and no host round trip per wave.  ``dist`` is used once, at set-up,
+    to exchange the 64-byte IPC handles and the last arrival step.  Shards may
+    differ in size."""
+
+    def __init__(self, engine, dist, group=None):
+        import torch
+
+        self.engine = engine
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        ptr, handle = engine.xchg_create(self.world, self.rank, ipc=self.world > 1)
+        handles = [handle]
+        if self.world > 1:
+            mine = torch.tensor(list(handle), dtype=torch.uint8)
+            out = [torch.zeros_like(mine) for _ in range(self.world)]
+            dist.all_gather(out, mine, group=group)
+            handles = [bytes(t.tolist()) for t in out]
+        engine.xchg_connect(handles=handles if self.world > 1 else None,
+                            dev_ptrs=None if self.world > 1 else [ptr])
+        table = getattr(engine, "_table", None)
+        local_max = max((int(p.arrival_step) for p in table), default=0) if table is not None else 0
+        t = torch.tensor([local_max], dtype=torch.int64)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            dist.barrier(group=group)  # every buffer is zeroed and mapped before any peer writes
+        self.last_arrival = int(t.item())
+
+    def run(self, max_steps: int = (1 << 31) - 1):
+        return self.engine.run_sharded(max_steps, self.last_arrival)
+
+
+def connect_in_process(engines) -> list:
+    """Ranks emulated in one process (one GPU): connect the engines' exchange
+    buffers by device pointer; returns the pointers."""
+    world = len(engines)
+    ptrs = []
+    for r, e in enumerate(engines):
+        p, _ = e.xchg_create(world, r, ipc=False)
+        ptrs.append(p)
+    for e in engines:
+        e.xchg_connect(dev_ptrs=ptrs)
+    return ptrs
+
+
+def last_arrival_of(tables) -> int:
+    return max((int(p.arrival_step) for t in tables for p in t), default=0)
+
+
 class _HostEvent:
     """Stand-in for a CUDA event when the exchange runs on CPU tensors."""
 

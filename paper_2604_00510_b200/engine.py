@@ -242,6 +242,37 @@ class Engine:
     def step_wave(self, step: int) -> None:
         self._check(self.lib.ts_step_wave(self._h, step, self.stream), "ts_step_wave")
 
+    # ---- the sharded batch over peer memory (multi-GPU) -----
+    def xchg_create(self, world: int, rank: int, ipc: bool = True):
+        """Allocate this rank's exchange buffer (after :meth:`load`); returns
+        (device pointer, 64-byte CUDA IPC handle or None)."""
+        from ._abi import TS_IPC_HANDLE_BYTES
+
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_uint8 * TS_IPC_HANDLE_BYTES)() if ipc else None
+        self._check(self.lib.ts_xchg_create(self._h, world, rank, ctypes.byref(ptr), handle), "ts_xchg_create")
+        return int(ptr.value or 0), (bytes(handle) if ipc else None)
+
+    def xchg_connect(self, handles=None, dev_ptrs=None) -> None:
+        """Map every rank's buffer: ``handles`` (list of 64-byte IPC handles,
+        other processes) or ``dev_ptrs`` (device pointers, ranks in this process)."""
+        h = None
+        if handles is not None:
+            h = (ctypes.c_uint8 * (64 * len(handles))).from_buffer_copy(b"".join(handles))
+        d = None
+        if dev_ptrs is not None:
+            d = (ctypes.c_void_p * len(dev_ptrs))(*[ctypes.c_void_p(x) for x in dev_ptrs])
+        self._check(self.lib.ts_xchg_connect(self._h, h, d), "ts_xchg_connect")
+
+    def run_sharded(self, max_steps: int = (1 << 31) - 1, last_arrival: int = 0) -> TsRunStats:
+        """The whole sharded batch as one device-driven graph loop (a collective
+        over the connected ranks); ``last_arrival`` = the largest arrival step
+        of the global run queue."""
+        st = TsRunStats()
+        self._check(self.lib.ts_run_sharded(self._h, max_steps, last_arrival, ctypes.byref(st), self.stream),
+                    "ts_run_sharded")
+        return st
+
     def read_targets(self, n: Optional[int] = None) -> list:
         n = self.n if n is None else n
         buf = (ctypes.c_int32 * max(1, n))()

@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "treeserve_b200.h")
 
 def _declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(ts_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|const char\*)\s+(ts_\w+)\s*\(", src, flags=re.M)))
 
 
 @pytest.fixture(scope="module")
@@ -35,7 +35,7 @@ def test_header_and_mirror_agree():
 def test_library_exports_every_declared_symbol(lib):
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.ts_abi_version() == 5
+    assert lib.ts_abi_version() == 6
 
 
 def test_struct_layouts_match_header():
