@@ -207,6 +207,10 @@ int ts_xchg_create(ts_engine* eng, int32_t world, int32_t rank, void** dev_ptr_o
 int ts_xchg_connect(ts_engine* eng, const uint8_t* ipc_handles, void* const* dev_ptrs);
 int ts_run_sharded(ts_engine* eng, int32_t max_steps, int32_t last_arrival_global, ts_run_stats* stats_out,
                    void* stream);
+/* Per wave of the last ts_run_sharded (first n waves, n <= 65536): three
+ * %globaltimer stamps (ns) — the counts phase starts (the previous wave's
+ * kernels are done), every rank's records are in, compute_targets is done. */
+int ts_read_px_times(ts_engine* eng, uint64_t* host_out, int32_t n, void* stream);
 
 /* ---- run-time invariants (checked mode) ---------------------------------- */
 /* The reference asserts these while it runs (Engine._check_capacity and the

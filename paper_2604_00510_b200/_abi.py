@@ -136,7 +136,7 @@ EXPORTED = (
     "ts_beam_search", "ts_beam_search_host", "ts_beam_expand", "ts_beam_prune",
     "ts_generate_steps", "ts_engine_set_checks", "ts_read_invariants", "ts_engine_set_trace", "ts_read_trace",
     "ts_reconcile", "ts_engine_set_cost_model", "ts_read_sim_times",
-    "ts_xchg_bytes", "ts_xchg_create", "ts_xchg_connect", "ts_run_sharded",
+    "ts_xchg_bytes", "ts_xchg_create", "ts_xchg_connect", "ts_run_sharded", "ts_read_px_times",
 )
 TS_MAX_PEERS = 8
 TS_IPC_HANDLE_BYTES = 64
@@ -300,6 +300,7 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         "ts_xchg_create": (ctypes.c_int, [vp, i32, i32, P(vp), vp]),
         "ts_xchg_connect": (ctypes.c_int, [vp, vp, vp]),
         "ts_run_sharded": (ctypes.c_int, [vp, i32, i32, P(TsRunStats), vp]),
+        "ts_read_px_times": (ctypes.c_int, [vp, P(ctypes.c_uint64), i32, vp]),
         "ts_fill_problem": (ctypes.c_int, [ctypes.c_uint64, i32, i32, i32, i32, ctypes.c_double,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, i32, i32,
                                            ctypes.c_double, ctypes.c_double, ctypes.c_double, P(TsProblem)]),

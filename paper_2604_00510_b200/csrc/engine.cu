@@ -95,7 +95,7 @@ struct Counters {
   long long cost_load;
   long long clock_step1;  // 1 + the last step whose start clock was recorded (0: none)
   // ts_run_sharded: the batch has ended (every later kernel of the graph body
-  // returns at once), CTAs of k_px_records done this wave, a peer timed out
+  // returns at once), (unused), a peer timed out (1) or the score sum needs the sequential loop (2)
   int px_done, px_blocks, px_err, px_gen;  // px_gen: the batch generation (epochs of the flags)
   int px_last_arrival, _pad4;              // the run queue's last arrival step (admission exchange)
 };
@@ -146,6 +146,8 @@ struct View {
   // the counts exchange (capacity below the run queue) or up to which step
   unsigned char* px[TS_MAX_PEERS];
   int32_t pworld, prank, padm_all;
+  unsigned long long* pstamp;  // per wave: counts phase start, every group table in, scheduler done (%globaltimer)
+  unsigned char* pscr;         // group scheduler scratch (px_scratch_bytes)
   double* g_runS;
   int32_t* g_runStart;
   long long* g_runWant;
@@ -395,219 +397,6 @@ __global__ void k_records(View v, int step, ts_sched_record* rec) {
     r._pad = (uint32_t)s->completed;
   }
   rec[i] = r;
-}
-
-// ---- the sharded wave loop over peer memory (ts_run_sharded) ----------------------
-//
-// Every rank owns an exchange buffer; a peer writes its scheduler inputs
-// straight into every other rank's buffer (NVLink stores through CUDA IPC
-// mappings; plain device stores when the ranks are emulated on one GPU) and
-// then sets its flag there to the wave's epoch.  A rank waits on the flags in
-// its own buffer, so each exchange is one round of peer stores plus one flag
-// wait — no collective library call, no host round trip — and the whole
-// sharded batch is one device-driven graph loop like ts_run's.
-struct XHdr {
-  unsigned long long fa[TS_MAX_PEERS];  // counts phase: epoch written by peer p
-  unsigned long long fb[TS_MAX_PEERS];  // records phase
-  long long cnt[TS_MAX_PEERS][4];       // peer p: {running, arrived-but-pending, unfinished, -} before admission
-  long long unf[TS_MAX_PEERS];          // peer p: unfinished searches when its records were written
-};
-constexpr size_t XHDR_BYTES = 512;
-constexpr int PX_MAX_WAVES = 1 << 20;  // the log1p table ts_xchg_connect sizes for the sharded loop
-static_assert(sizeof(XHdr) <= XHDR_BYTES, "exchange header");
-__host__ __device__ inline size_t xchg_bytes(long long n_global) {
-  return XHDR_BYTES + (size_t)n_global * sizeof(ts_sched_record);
-}
-__device__ __forceinline__ XHdr* xh(const View& v, int p) { return (XHdr*)v.px[p]; }
-__device__ __forceinline__ ts_sched_record* xrec(const View& v, int p) {
-  return (ts_sched_record*)(v.px[p] + XHDR_BYTES);
-}
-__device__ __forceinline__ unsigned long long px_epoch(const View& v, int step) {
-  return ((unsigned long long)(uint32_t)v.ctr->px_gen << 32) | (unsigned long long)(uint32_t)(step + 1);
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long x) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long x;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
-  return x;
-}
-// wait until every peer's flag in this rank's buffer reached `epoch`; a peer
-// that stays silent for TS_PX_TIMEOUT_NS ends the batch with an error
-#ifndef TS_PX_TIMEOUT_NS
-#define TS_PX_TIMEOUT_NS 20000000000ull
-#endif
-__device__ bool px_wait(const View& v, const unsigned long long* flags, unsigned long long epoch) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) s_ok = 1;
-  __syncthreads();
-  if (threadIdx.x < (unsigned)v.pworld) {
-    const unsigned long long t0 = globaltimer();
-    while (ld_acquire_sys(flags + threadIdx.x) < epoch) {
-      if (globaltimer() - t0 > TS_PX_TIMEOUT_NS) {
-        s_ok = 0;
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  __syncthreads();
-  return s_ok != 0;
-}
-__device__ __forceinline__ bool px_adm_active(const View& v, int step) {
-  return v.padm_all || step <= v.ctr->px_last_arrival;
-}
-// the batch ends: every later kernel of the graph returns at once and the
-// waves find empty work lists
-__device__ void px_finish(const View& v, cudaGraphConditionalHandle cond, int err) {
-  Counters* c = v.ctr;
-  c->px_done = 1;
-  if (err) c->px_err = err;
-  c->work_count = 0;
-  c->work_next = 0;
-  c->heavy_count = 0;
-  c->heavy_next = 0;
-  cudaGraphSetConditional(cond, 0);
-}
-
-__global__ void k_px_reset(Counters* c, int gen, int last_arrival) {
-  c->px_done = 0;
-  c->px_blocks = 0;
-  c->px_err = 0;
-  c->px_gen = gen;
-  c->px_last_arrival = last_arrival;
-}
-
-// counts phase: this rank's {running, pending, unfinished} into every peer's buffer
-__global__ void k_px_counts(View v) {
-  Counters* c = v.ctr;
-  if (c->px_done) return;
-  const int step = (int)c->step;
-  if (!px_adm_active(v, step)) return;
-  int lo = 0, hi = v.n_local;  // arrivals are non-decreasing: upper_bound(arrival, step)
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (v.arrival[mid] <= step) lo = mid + 1;
-    else hi = mid;
-  }
-  const long long run = c->running, pend = (long long)lo - c->head, unf = (long long)v.n_local - c->finished;
-  const int p = threadIdx.x;
-  if (p < v.pworld) {
-    long long* d = xh(v, p)->cnt[v.prank];
-    d[0] = run;
-    d[1] = pend;
-    d[2] = unf;
-    __threadfence_system();
-    st_release_sys(&xh(v, p)->fa[v.prank], px_epoch(v, step));
-  }
-}
-
-// admit_jobs (scheduler.py:131-140) over the global FIFO from every rank's
-// counts, and the loop test (no unfinished search on any rank)
-__global__ void k_px_admit(View v, cudaGraphConditionalHandle cond, int max_steps) {
-  Counters* c = v.ctr;
-  if (c->px_done) return;
-  const int step = (int)c->step;
-  if (step >= max_steps || step >= v.log1p_n) {
-    if (threadIdx.x == 0) px_finish(v, cond, 0);
-    return;
-  }
-  if (!px_adm_active(v, step)) {
-    if (threadIdx.x == 0) c->admit_lo = c->admit_hi = c->head;  // nobody can be pending
-    return;
-  }
-  const XHdr* x = xh(v, v.prank);
-  if (!px_wait(v, x->fa, px_epoch(v, step))) {
-    if (threadIdx.x == 0) px_finish(v, cond, 1);
-    return;
-  }
-  if (threadIdx.x != 0) return;
-  long long run_g = 0, pend_g = 0, before = 0, unf_g = 0;
-  for (int r = 0; r < v.pworld; ++r) {
-    run_g += x->cnt[r][0];
-    pend_g += x->cnt[r][1];
-    unf_g += x->cnt[r][2];
-    if (r < v.prank) before += x->cnt[r][1];
-  }
-  if (unf_g == 0) {
-    px_finish(v, cond, 0);
-    return;
-  }
-  long long A = (long long)v.cfg.max_concurrency - run_g;
-  if (A > pend_g) A = pend_g;
-  if (A < 0) A = 0;
-  long long q = A - before;
-  if (q > x->cnt[v.prank][1]) q = x->cnt[v.prank][1];
-  if (q < 0) q = 0;
-  c->admit_lo = c->head;
-  c->admit_hi = c->head + q;
-  c->head += q;
-  c->running += q;
-}
-
-// parallelism_score (scheduler.py:118-128): this rank's records into every
-// peer's buffer at its global offset; the last CTA signals
-__global__ void k_px_records(View v) {
-  Counters* c = v.ctr;
-  if (c->px_done) return;
-  const int step = (int)c->step;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < v.n_local) {
-    SearchState* s = v.st + i;
-    int state = s->state;
-    if (i >= c->admit_lo && i < c->admit_hi) {
-      state = ST_RUNNING;
-      s->state = ST_RUNNING;
-      s->admit_step = step;
-    }
-    ts_sched_record r;
-    r.score = 0.0;
-    r.flags = 0;
-    r._pad = 0;
-    if (state == ST_RUNNING) {
-      const ts_config& cf = v.cfg;
-      const double ratio = s->job_best / cf.positive_exit_threshold;
-      r.score = v.log1p_tab[step - v.arrival[i]] + (ratio > cf.proximity ? cf.beta : 0.0);
-      r.flags = 1u | (s->completed >= cf.obs_threshold ? 2u : 0u) | (ratio > cf.proximity ? 4u : 0u);
-      r._pad = (uint32_t)s->completed;
-    }
-    for (int p = 0; p < v.pworld; ++p) xrec(v, p)[v.goff + i] = r;
-  }
-  __threadfence_system();
-  __syncthreads();
-  __shared__ int s_last;
-  if (threadIdx.x == 0) s_last = atomicAdd(&c->px_blocks, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  if (threadIdx.x == 0) c->px_blocks = 0;
-  const int p = threadIdx.x;
-  if (p < v.pworld) {
-    xh(v, p)->unf[v.prank] = (long long)v.n_local - c->finished;
-    __threadfence_system();
-    st_release_sys(&xh(v, p)->fb[v.prank], px_epoch(v, step));
-  }
-}
-
-// every rank's records are in: the loop test, and the step for the scheduler and the waves
-__global__ void k_px_wait(View v, cudaGraphConditionalHandle cond) {
-  Counters* c = v.ctr;
-  if (c->px_done) return;
-  const int step = (int)c->step;
-  const XHdr* x = xh(v, v.prank);
-  if (!px_wait(v, x->fb, px_epoch(v, step))) {
-    if (threadIdx.x == 0) px_finish(v, cond, 1);
-    return;
-  }
-  if (threadIdx.x != 0) return;
-  long long unf_g = 0;
-  for (int r = 0; r < v.pworld; ++r) unf_g += x->unf[r];
-  if (unf_g == 0) {
-    px_finish(v, cond, 0);
-    return;
-  }
-  c->cur_step = step;
-  c->step = step + 1;
 }
 
 // ---- compute_targets (scheduler.py:143-187) in one CTA ------------------------
@@ -1103,10 +892,624 @@ __device__ __forceinline__ size_t targets_smem_dev() {
 __global__ void __launch_bounds__(SCHED_T) k_targets(View v, int step, const ts_sched_record* rec) {
   targets_block(v, step, rec, v.n_global, v.goff, v.goff + v.n_local, 0);
 }
-// ts_run_sharded: the one-CTA scheduler over the records in this rank's exchange buffer
-__global__ void __launch_bounds__(SCHED_T) k_px_targets(View v) {
-  if (v.ctr->px_done) return;
-  targets_block(v, v.ctr->cur_step, xrec(v, v.prank), v.n_global, v.goff, v.goff + v.n_local, 0);
+
+// ---- the sharded wave loop over peer memory (ts_run_sharded) ----------------------
+//
+// Every rank owns an exchange buffer; a peer writes its scheduler inputs
+// straight into every other rank's buffer (NVLink stores through CUDA IPC
+// mappings; plain device stores when the ranks are emulated on one GPU) and
+// then sets its flag there to the wave's epoch.  A rank waits on the flags in
+// its own buffer, so each exchange is one round of peer stores plus one flag
+// wait — no collective library call, no host round trip — and the whole
+// sharded batch is one device-driven graph loop like ts_run's.
+struct XHdr {
+  unsigned long long fa[TS_MAX_PEERS];  // counts phase: epoch written by peer p
+  unsigned long long fb[TS_MAX_PEERS];  // groups phase
+  long long cnt[TS_MAX_PEERS][4];       // peer p: {running, arrived-but-pending, unfinished, -} before admission
+  long long unf[TS_MAX_PEERS];          // peer p: unfinished searches when its groups were written
+  long long nent[TS_MAX_PEERS];         // peer p: entries of its group table
+  long long goff[TS_MAX_PEERS];         // peer p: its global offset (its table starts at entry goff)
+};
+constexpr size_t XHDR_BYTES = 1024;
+// One entry per distinct arrival step among a rank's running searches: the
+// running and the ungated (completed >= obs_threshold) counts of the
+// unboosted (0) and boosted (1) lists.  parallelism_score depends only on
+// (arrival, boosted) (scheduler.py:118-128), so these counts carry everything
+// compute_targets needs from the other ranks.
+struct PxEnt {
+  int a, nr0, nu0, nr1, nu1, _p0, _p1, _p2;
+};
+static_assert(sizeof(PxEnt) == 32, "group entry");
+constexpr int PX_MAX_WAVES = 1 << 20;  // the log1p table ts_xchg_connect sizes for the sharded loop
+constexpr int PX_STAMP_WAVES = 1 << 16;  // waves with timestamps (ts_read_px_times)
+__device__ __forceinline__ void px_stamp(const View& v, int step, int k) {
+  if (step < PX_STAMP_WAVES) v.pstamp[3 * step + k] = globaltimer();
+}
+static_assert(sizeof(XHdr) <= XHDR_BYTES, "exchange header");
+__host__ __device__ inline size_t xchg_bytes(long long n_global) {
+  return XHDR_BYTES + (size_t)n_global * sizeof(PxEnt);
+}
+__device__ __forceinline__ PxEnt* xent(const View& v, int p) { return (PxEnt*)(v.px[p] + XHDR_BYTES); }
+__device__ __forceinline__ XHdr* xh(const View& v, int p) { return (XHdr*)v.px[p]; }
+__device__ __forceinline__ unsigned long long px_epoch(const View& v, int step) {
+  return ((unsigned long long)(uint32_t)v.ctr->px_gen << 32) | (unsigned long long)(uint32_t)(step + 1);
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long x) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long x;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(p) : "memory");
+  return x;
+}
+// wait until every peer's flag in this rank's buffer reached `epoch`; a peer
+// that stays silent for TS_PX_TIMEOUT_NS ends the batch with an error
+#ifndef TS_PX_TIMEOUT_NS
+#define TS_PX_TIMEOUT_NS 20000000000ull
+#endif
+__device__ bool px_wait(const View& v, const unsigned long long* flags, unsigned long long epoch) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  if (threadIdx.x < (unsigned)v.pworld) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(flags + threadIdx.x) < epoch) {
+      if (globaltimer() - t0 > TS_PX_TIMEOUT_NS) {
+        s_ok = 0;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+__device__ __forceinline__ bool px_adm_active(const View& v, int step) {
+  return v.padm_all || step <= v.ctr->px_last_arrival;
+}
+// the batch ends: every later kernel of the graph returns at once and the
+// waves find empty work lists
+__device__ void px_finish(const View& v, cudaGraphConditionalHandle cond, int err) {
+  Counters* c = v.ctr;
+  c->px_done = 1;
+  if (err) c->px_err = err;
+  c->work_count = 0;
+  c->work_next = 0;
+  c->heavy_count = 0;
+  c->heavy_next = 0;
+  cudaGraphSetConditional(cond, 0);
+}
+
+__global__ void k_px_reset(Counters* c, int gen, int last_arrival) {
+  c->px_done = 0;
+  c->px_blocks = 0;
+  c->px_err = 0;
+  c->px_gen = gen;
+  c->px_last_arrival = last_arrival;
+}
+
+// counts phase: this rank's {running, pending, unfinished} into every peer's buffer
+__global__ void k_px_counts(View v) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  if (threadIdx.x == 0) px_stamp(v, step, 0);
+  if (!px_adm_active(v, step)) return;
+  int lo = 0, hi = v.n_local;  // arrivals are non-decreasing: upper_bound(arrival, step)
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v.arrival[mid] <= step) lo = mid + 1;
+    else hi = mid;
+  }
+  const long long run = c->running, pend = (long long)lo - c->head, unf = (long long)v.n_local - c->finished;
+  const int p = threadIdx.x;
+  if (p < v.pworld) {
+    long long* d = xh(v, p)->cnt[v.prank];
+    d[0] = run;
+    d[1] = pend;
+    d[2] = unf;
+    __threadfence_system();
+    st_release_sys(&xh(v, p)->fa[v.prank], px_epoch(v, step));
+  }
+}
+
+// admit_jobs (scheduler.py:131-140) over the global FIFO from every rank's
+// counts, and the loop test (no unfinished search on any rank)
+__global__ void k_px_admit(View v, cudaGraphConditionalHandle cond, int max_steps) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  if (step >= max_steps || step >= v.log1p_n) {
+    if (threadIdx.x == 0) px_finish(v, cond, 0);
+    return;
+  }
+  if (!px_adm_active(v, step)) {
+    if (threadIdx.x == 0) c->admit_lo = c->admit_hi = c->head;  // nobody can be pending
+    return;
+  }
+  const XHdr* x = xh(v, v.prank);
+  if (!px_wait(v, x->fa, px_epoch(v, step))) {
+    if (threadIdx.x == 0) px_finish(v, cond, 1);
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  long long run_g = 0, pend_g = 0, before = 0, unf_g = 0;
+  for (int r = 0; r < v.pworld; ++r) {
+    const long long c0 = __ldcg(&x->cnt[r][0]), c1 = __ldcg(&x->cnt[r][1]), c2 = __ldcg(&x->cnt[r][2]);
+    run_g += c0;
+    pend_g += c1;
+    unf_g += c2;
+    if (r < v.prank) before += c1;
+  }
+  if (unf_g == 0) {
+    px_finish(v, cond, 0);
+    return;
+  }
+  long long A = (long long)v.cfg.max_concurrency - run_g;
+  if (A > pend_g) A = pend_g;
+  if (A < 0) A = 0;
+  long long q = A - before;
+  if (q > __ldcg(&x->cnt[v.prank][1])) q = __ldcg(&x->cnt[v.prank][1]);
+  if (q < 0) q = 0;
+  c->admit_lo = c->head;
+  c->admit_hi = c->head + q;
+  c->head += q;
+  c->running += q;
+}
+
+// scratch of the group scheduler (k_px_groups / k_px_sched), carved from one buffer
+struct PxScr {
+  // per local search
+  unsigned char *code, *heavy;  // code: segment start | running << 1 | ungated << 2 | list << 3
+  int *segid, *jpre;            // arrival segment; exclusive prefix of the ungated of its list
+  int4* jq;                     // (entry, position among the ungated of its (entry, list) here, code, completed)
+  // per local arrival segment
+  int4 *segb, *sege;            // exclusive prefix (run0, ung0, run1, ung1) at its first job / inclusive at its last
+  int *sega, *segent;           // arrival; entry (-1: no running search)
+  // per entry of the concatenated global table, per merged entry, per run of each list
+  int* gm;                      // merged entry
+  int4* gp;                     // exclusive prefix (nr0, nu0, nr1, nu1) over the concatenated table
+  int* mfirst;                  // first concatenated entry of a merged entry
+  int2* mrun;                   // its run in list 0 / list 1 (-1: none)
+  double* rS[2];                // run score (non-increasing), arrival, ungated count, want, prefix U, prefix W
+  int *rA[2], *rC[2];
+  long long *rWant[2], *rU[2], *rW[2];
+};
+__host__ __device__ inline PxScr px_scr(unsigned char* base, long long nl, long long ng, size_t* bytes) {
+  PxScr X;
+  size_t o = 0;
+  auto take = [&](size_t b) -> unsigned char* {
+    unsigned char* q = base ? base + o : nullptr;
+    o += (b + 15) & ~(size_t)15;
+    return q;
+  };
+  X.code = take(nl);
+  X.heavy = take(nl);
+  X.segid = (int*)take(4 * nl);
+  X.jpre = (int*)take(4 * nl);
+  X.jq = (int4*)take(16 * nl);
+  X.segb = (int4*)take(16 * nl);
+  X.sege = (int4*)take(16 * nl);
+  X.sega = (int*)take(4 * nl);
+  X.segent = (int*)take(4 * nl);
+  X.gm = (int*)take(4 * ng);
+  X.gp = (int4*)take(16 * ng);
+  X.mfirst = (int*)take(4 * ng);
+  X.mrun = (int2*)take(8 * ng);
+  for (int b = 0; b < 2; ++b) {
+    X.rS[b] = (double*)take(8 * ng);
+    X.rA[b] = (int*)take(4 * ng);
+    X.rC[b] = (int*)take(4 * ng);
+    X.rWant[b] = (long long*)take(8 * ng);
+    X.rU[b] = (long long*)take(8 * ng);
+    X.rW[b] = (long long*)take(8 * ng);
+  }
+  if (bytes) *bytes = o;
+  return X;
+}
+
+constexpr int PXT = 1024;  // = SCHED_T (scan1_add's block size)
+
+// The groups phase: admission state (admit_jobs), then this rank's group
+// table — one PxEnt per distinct arrival among its running searches, in
+// arrival order — into every rank's buffer at this rank's global offset, and
+// each running search's entry and position within it for k_px_sched.
+__global__ void __launch_bounds__(PXT) k_px_groups(View v) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  const int tid = threadIdx.x;
+  __shared__ int sh[5 * 32];
+  const ts_config& cf = v.cfg;
+  const bool fold = cf.beta == 0.0;  // the boosted flag does not change the score: one list
+  const int n = v.n_local;
+  const PxScr X = px_scr(v.pscr, n, v.n_global, nullptr);
+  const int per = (n + PXT - 1) / PXT, lo = min(n, tid * per), hi = min(n, lo + per);
+  const long long alo = c->admit_lo, ahi = c->admit_hi;
+  int cnt[5] = {0, 0, 0, 0, 0};  // segment starts, run0, ung0, run1, ung1
+  for (int i = lo; i < hi; ++i) {
+    SearchState* st = v.st + i;
+    int state = st->state;
+    if (i >= alo && i < ahi) {
+      state = ST_RUNNING;
+      st->state = ST_RUNNING;
+      st->admit_step = step;
+    }
+    const int a = v.arrival[i];
+    const int ap = i > 0 ? v.arrival[i - 1] : a;
+    if (a < ap) c->sched_error = 1;
+    const bool start = i == 0 || a != ap;
+    unsigned code = start ? 1u : 0u;
+    int comp = 0;
+    if (state == ST_RUNNING) {
+      comp = st->completed;
+      const bool boosted = st->job_best / cf.positive_exit_threshold > cf.proximity;  // scheduler.py:126
+      const bool ung = comp >= cf.obs_threshold;
+      const int b = (boosted && !fold) ? 1 : 0;
+      code |= 2u | (ung ? 4u : 0u) | ((unsigned)b << 3);
+      cnt[1 + 2 * b] += 1;
+      if (ung) cnt[2 + 2 * b] += 1;
+    }
+    cnt[0] += start ? 1 : 0;
+    X.code[i] = (unsigned char)code;
+    X.jq[i] = make_int4(0, 0, 0, comp);
+  }
+  int tot[5];
+  scan1_add<5>(cnt, tot, sh);
+  {
+    int q[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) q[k] = cnt[k];
+    for (int i = lo; i < hi; ++i) {
+      const unsigned code = X.code[i];
+      if (code & 1u) {
+        X.segb[q[0]] = make_int4(q[1], q[2], q[3], q[4]);
+        X.sega[q[0]] = v.arrival[i];
+        ++q[0];
+      }
+      const int sg = q[0] - 1;
+      const int b = (code >> 3) & 1;
+      X.segid[i] = sg;
+      X.jpre[i] = q[2 + 2 * b];
+      if (code & 2u) {
+        q[1 + 2 * b] += 1;
+        if (code & 4u) q[2 + 2 * b] += 1;
+      }
+      if (i == n - 1 || v.arrival[i + 1] != v.arrival[i]) X.sege[sg] = make_int4(q[1], q[2], q[3], q[4]);
+    }
+  }
+  const int nseg = tot[0];
+  __syncthreads();
+  const int per2 = (nseg + PXT - 1) / PXT, s0 = min(nseg, tid * per2), s1 = min(nseg, s0 + per2);
+  int hr[1] = {0}, hrt[1];
+  for (int sg = s0; sg < s1; ++sg) {
+    const int4 b0 = X.segb[sg], b1 = X.sege[sg];
+    if (b1.x - b0.x + b1.z - b0.z > 0) ++hr[0];
+  }
+  scan1_add<1>(hr, hrt, sh);
+  {
+    int id = hr[0];
+    for (int sg = s0; sg < s1; ++sg) {
+      const int4 b0 = X.segb[sg], b1 = X.sege[sg];
+      if (b1.x - b0.x + b1.z - b0.z > 0) {
+        PxEnt en;
+        en.a = X.sega[sg];
+        en.nr0 = b1.x - b0.x;
+        en.nu0 = b1.y - b0.y;
+        en.nr1 = b1.z - b0.z;
+        en.nu1 = b1.w - b0.w;
+        en._p0 = en._p1 = en._p2 = 0;
+        for (int p = 0; p < v.pworld; ++p) xent(v, p)[v.goff + id] = en;
+        X.segent[sg] = id++;
+      } else {
+        X.segent[sg] = -1;
+      }
+    }
+  }
+  const int nent = hrt[0];
+  __syncthreads();
+  for (int i = lo; i < hi; ++i) {
+    const unsigned code = X.code[i];
+    int4 q = X.jq[i];
+    if (code & 2u) {
+      const int sg = X.segid[i];
+      const int4 sb = X.segb[sg];
+      q.x = X.segent[sg];
+      q.y = X.jpre[i] - ((code & 8u) ? sb.w : sb.y);
+    } else {
+      q.x = -1;
+      q.y = 0;
+    }
+    q.z = (int)code;
+    X.jq[i] = q;
+  }
+  __threadfence_system();
+  __syncthreads();
+  const int p = tid;
+  if (p < v.pworld) {
+    XHdr* h = xh(v, p);
+    h->nent[v.prank] = nent;
+    h->goff[v.prank] = v.goff;
+    h->unf[v.prank] = (long long)n - c->finished;
+    __threadfence_system();
+    st_release_sys(&h->fb[v.prank], px_epoch(v, step));
+  }
+}
+
+__device__ u128 block_sum_u128(u128 x, bool& bad) {
+  __shared__ u128 sq[32];
+  __shared__ int sb[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t h = __shfl_xor_sync(FULL, (uint64_t)(x >> 64), o);
+    const uint64_t l = __shfl_xor_sync(FULL, (uint64_t)x, o);
+    x += ((u128)h << 64) | l;
+  }
+  const bool wb = __any_sync(FULL, bad);
+  if (lane == 0) {
+    sq[wid] = x;
+    sb[wid] = wb;
+  }
+  __syncthreads();
+  u128 t = lane < (int)(blockDim.x >> 5) ? sq[lane] : (u128)0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t h = __shfl_xor_sync(FULL, (uint64_t)(t >> 64), o);
+    const uint64_t l = __shfl_xor_sync(FULL, (uint64_t)t, o);
+    t += ((u128)h << 64) | l;
+  }
+  bad = __any_sync(FULL, lane < (int)(blockDim.x >> 5) && sb[lane] != 0);
+  return t;
+}
+
+// compute_targets (scheduler.py:143-187) from every rank's group table.  The
+// reference sorts the ungated jobs by (-S, arrival, id); S depends only on
+// (arrival, boosted), and arrivals are non-decreasing in run-queue order, so
+// the sorted order is the merge of the unboosted and the boosted list, each a
+// sequence of runs = entries of one arrival (S non-increasing along it),
+// ordered inside a run by id.  A job's sorted position and the Σ(want-1)
+// before it are run prefix sums, its position inside its run (the run's
+// count on lower ranks plus its rank-local position), and a binary search in
+// the other list (equal scores there: the earlier arrival first).  The score
+// sum is the exact fixed-point sum of count × S (equal to CPython's Neumaier
+// sum under the check targets_block documents).  Then the closed forms of the
+// clamp and the round robin, and the two work lists, as targets_block.
+__global__ void __launch_bounds__(PXT) k_px_sched(View v, cudaGraphConditionalHandle cond) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int step = (int)c->step;
+  const int tid = threadIdx.x;
+  const XHdr* x = xh(v, v.prank);
+  if (!px_wait(v, x->fb, px_epoch(v, step))) {
+    if (tid == 0) px_finish(v, cond, 1);
+    return;
+  }
+  if (tid == 0) px_stamp(v, step, 1);
+  __shared__ int shi[5 * 32];
+  __shared__ long long shl[4 * 32];
+  const ts_config& cf = v.cfg;
+  const int W = v.pworld;
+  int off[TS_MAX_PEERS + 1];
+  long long gof[TS_MAX_PEERS];
+  long long unf_g = 0;
+  off[0] = 0;
+  for (int r = 0; r < W; ++r) {
+    unf_g += __ldcg(&x->unf[r]);
+    off[r + 1] = off[r] + (int)__ldcg(&x->nent[r]);
+    gof[r] = __ldcg(&x->goff[r]);
+  }
+  if (unf_g == 0) {
+    if (tid == 0) px_finish(v, cond, 0);
+    return;
+  }
+  const int G = off[W];
+  const PxEnt* tab = xent(v, v.prank);
+  // entries written by peers: read from L2 (ld.global.cg), never a stale L1 line
+  auto ent = [&](int g) -> PxEnt {
+    int r = 0;
+    while (r + 1 < W && off[r + 1] <= g) ++r;
+    const int4* e4 = (const int4*)(tab + gof[r] + (g - off[r]));
+    const int4 u = __ldcg(e4), w = __ldcg(e4 + 1);
+    PxEnt e;
+    e.a = u.x;
+    e.nr0 = u.y;
+    e.nu0 = u.z;
+    e.nr1 = u.w;
+    e.nu1 = w.x;
+    e._p0 = e._p1 = e._p2 = 0;
+    return e;
+  };
+  const PxScr X = px_scr(v.pscr, v.n_local, v.n_global, nullptr);
+  // 1. merged entries (equal arrivals at rank boundaries) and the exclusive
+  //    prefix of the counts over the concatenated table
+  const int pg = (G + PXT - 1) / PXT, g0 = min(G, tid * pg), g1 = min(G, g0 + pg);
+  int cg[5] = {0, 0, 0, 0, 0}, tg[5];
+  for (int g = g0; g < g1; ++g) {
+    const PxEnt e = ent(g);
+    cg[0] += (g == 0 || e.a != ent(g - 1).a) ? 1 : 0;
+    cg[1] += e.nr0;
+    cg[2] += e.nu0;
+    cg[3] += e.nr1;
+    cg[4] += e.nu1;
+  }
+  scan1_add<5>(cg, tg, shi);
+  for (int g = g0; g < g1; ++g) {
+    const PxEnt e = ent(g);
+    if (g == 0 || e.a != ent(g - 1).a) X.mfirst[cg[0]++] = g;
+    X.gm[g] = cg[0] - 1;
+    X.gp[g] = make_int4(cg[1], cg[2], cg[3], cg[4]);
+    cg[1] += e.nr0;
+    cg[2] += e.nu0;
+    cg[3] += e.nr1;
+    cg[4] += e.nu1;
+  }
+  const int Gm = tg[0];
+  const long long tot_run = (long long)tg[1] + tg[3], len0 = tg[2], len1 = tg[4];
+  const int4 ptot = make_int4(tg[1], tg[2], tg[3], tg[4]);
+  __syncthreads();
+  // 2. per merged entry: its counts and scores, the exact score sum, runs per list
+  const int pm = (Gm + PXT - 1) / PXT, m0 = min(Gm, tid * pm), m1 = min(Gm, m0 + pm);
+  auto mcounts = [&](int m, int& a, int4& k) {
+    const int ga = X.mfirst[m], gb = m + 1 < Gm ? X.mfirst[m + 1] : G;
+    const int4 pa = X.gp[ga], pb = gb < G ? X.gp[gb] : ptot;
+    k = make_int4(pb.x - pa.x, pb.y - pa.y, pb.z - pa.z, pb.w - pa.w);
+    a = ent(ga).a;
+  };
+  u128 fx = 0;
+  bool bad = false;
+  int cr[2] = {0, 0}, tr[2];
+  for (int m = m0; m < m1; ++m) {
+    int a;
+    int4 k;
+    mcounts(m, a, k);
+    // parallelism_score as the records phase writes it: log1p(waited) + boost
+    const double S0 = v.log1p_tab[step - a] + 0.0, S1 = v.log1p_tab[step - a] + cf.beta;
+    u128 q;
+    if (k.x > 0) {
+      if (to_fixed(S0, q)) fx += q * (u128)(unsigned)k.x;
+      else bad = true;
+    }
+    if (k.z > 0) {
+      if (to_fixed(S1, q)) fx += q * (u128)(unsigned)k.z;
+      else bad = true;
+    }
+    cr[0] += k.y > 0 ? 1 : 0;
+    cr[1] += k.w > 0 ? 1 : 0;
+  }
+  scan1_add<2>(cr, tr, shi);
+  const u128 fsum = block_sum_u128(fx, bad);
+  for (int m = m0; m < m1; ++m) {
+    int a;
+    int4 k;
+    mcounts(m, a, k);
+    const double S0 = v.log1p_tab[step - a] + 0.0, S1 = v.log1p_tab[step - a] + cf.beta;
+    int2 mr = make_int2(-1, -1);
+    if (k.y > 0) {
+      X.rS[0][cr[0]] = S0;
+      X.rA[0][cr[0]] = a;
+      X.rC[0][cr[0]] = k.y;
+      mr.x = cr[0]++;
+    }
+    if (k.w > 0) {
+      X.rS[1][cr[1]] = S1;
+      X.rA[1][cr[1]] = a;
+      X.rC[1][cr[1]] = k.w;
+      mr.y = cr[1]++;
+    }
+    X.mrun[m] = mr;
+  }
+  const int nrun[2] = {tr[0], tr[1]};
+  double T = fixed_to_double(fsum);
+  {
+    const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
+    if (bad || (double)tot_run * u2 >= 0x1p-10) {  // would need the sequential sum (targets_block)
+      if (tid == 0) px_finish(v, cond, 2);
+      return;
+    }
+  }
+  __syncthreads();
+  // 3. want per run, exclusive prefixes U (count) and W (count * (want-1)) per list
+  const long long M = cf.max_concurrency;
+  const long long R = M - tot_run;
+  const bool boost_on = cf.boosting_enabled != 0 && tot_run > 0 && R > 0 && len0 + len1 > 0;
+  long long tw[2] = {0, 0}, lenl[2] = {len0, len1};
+  if (boost_on) {
+    long long pre[4] = {0, 0, 0, 0}, tot4[4];
+    int a0[2], a1[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int pr = (nrun[b] + PXT - 1) / PXT;
+      a0[b] = min(nrun[b], tid * pr);
+      a1[b] = min(nrun[b], a0[b] + pr);
+      for (int k = a0[b]; k < a1[b]; ++k) {
+        long long want = 1;
+        if (T > 0.0) {
+          const double f = floor(X.rS[b][k] / T * (double)M);  // scheduler.py:173-175
+          want = f > 1.0 ? (long long)f : 1;
+        }
+        X.rWant[b][k] = want;
+        pre[2 * b] += X.rC[b][k];
+        pre[2 * b + 1] += (long long)X.rC[b][k] * (want - 1);
+      }
+    }
+    scan1_add<4>(pre, tot4, shl);
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      long long u = pre[2 * b], w = pre[2 * b + 1];
+      for (int k = a0[b]; k < a1[b]; ++k) {
+        X.rU[b][k] = u;
+        X.rW[b][k] = w;
+        u += X.rC[b][k];
+        w += (long long)X.rC[b][k] * (X.rWant[b][k] - 1);
+      }
+    }
+    tw[0] = tot4[1];
+    tw[1] = tot4[3];
+    __syncthreads();
+  }
+  // 4. targets of this rank's searches, and the two work lists in run-queue order
+  const long long U = len0 + len1;
+  long long Rp = R - (tw[0] + tw[1]);
+  if (Rp < 0) Rp = 0;
+  const long long rr_q = U > 0 ? Rp / U : 0, rr_r = U > 0 ? Rp % U : 0;
+  const int n = v.n_local, me = v.prank;
+  const int per = (n + PXT - 1) / PXT, lo = min(n, tid * per), hi = min(n, lo + per);
+  int nl2[2] = {0, 0}, tl2[2];
+  for (int i = lo; i < hi; ++i) {
+    const int4 q = X.jq[i];
+    const unsigned code = (unsigned)q.z;
+    unsigned char hv = 0;
+    if (!(code & 2u)) {
+      v.tgt[i] = 0;
+      X.heavy[i] = 2;  // not running
+      continue;
+    }
+    long long tgt = 1;
+    if ((code & 4u) && boost_on) {
+      const int b = (code >> 3) & 1, o = 1 - b;
+      const int g = off[me] + q.x, m = X.gm[g];
+      const int k = b ? X.mrun[m].y : X.mrun[m].x;
+      const int4 pg0 = X.gp[X.mfirst[m]], pgg = X.gp[g];
+      const long long qt = (long long)q.y + (b ? pgg.w - pg0.w : pgg.y - pg0.y);
+      const long long want = X.rWant[b][k];
+      const double S = X.rS[b][k];
+      const int a = X.rA[b][k];
+      long long pos = X.rU[b][k] + qt;
+      long long before = X.rW[b][k] + qt * (want - 1);
+      int kk = runs_lower(X.rS[o], nrun[o], S);  // other-list runs with a higher score
+      if (kk < nrun[o] && X.rS[o][kk] == S && X.rA[o][kk] < a) ++kk;  // equal score: earlier arrival first
+      pos += kk < nrun[o] ? X.rU[o][kk] : lenl[o];
+      before += kk < nrun[o] ? X.rW[o][kk] : tw[o];
+      long long extra = R - before;
+      if (extra < 0) extra = 0;
+      if (extra > want - 1) extra = want - 1;
+      tgt = 1 + extra + rr_q + (pos < rr_r ? 1 : 0);
+    }
+    v.tgt[i] = (int)tgt;
+    if (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - q.w)) >= HEAVY_P) hv = 1;
+    X.heavy[i] = hv;
+    ++nl2[hv ? 0 : 1];
+  }
+  scan1_add<2>(nl2, tl2, shi);
+  {
+    int ph = nl2[0], pl = nl2[1];
+    for (int i = lo; i < hi; ++i) {
+      const unsigned char hv = X.heavy[i];
+      if (hv == 2) continue;
+      if (hv) v.work_heavy[ph++] = i;
+      else v.work[pl++] = i;
+    }
+  }
+  if (tid == 0) {
+    c->work_count = tl2[1];
+    c->work_next = 0;
+    c->heavy_count = tl2[0];
+    c->heavy_next = 0;
+    c->cur_step = step;
+    c->step = step + 1;
+    px_stamp(v, step, 2);
+  }
 }
 
 // ---- compute_targets over many CTAs (multi-GPU runs: all n_global records) ----
@@ -4414,6 +4817,8 @@ struct ts_engine {
   // ts_run_sharded: this rank's exchange buffer and every rank's (IPC mappings
   // of other processes' buffers, or in-process pointers), the batch generation
   unsigned char* xbuf = nullptr;
+  unsigned long long* xstamp = nullptr;  // PX_STAMP_WAVES x 3 timestamps
+  unsigned char* xscr = nullptr;         // group scheduler scratch (px_scr)
   size_t xbytes = 0;
   int xworld = 0, xrank = 0, xgen = 0;
   unsigned char* xpeer[TS_MAX_PEERS] = {};
@@ -4855,7 +5260,11 @@ void xchg_release(ts_engine* e) {
     e->xpeer[p] = nullptr;
   }
   if (e->xbuf) cudaFree(e->xbuf);
+  if (e->xstamp) cudaFree(e->xstamp);
+  if (e->xscr) cudaFree(e->xscr);
   e->xbuf = nullptr;
+  e->xstamp = nullptr;
+  e->xscr = nullptr;
   e->xbytes = 0;
   e->xconnected = false;
 }
@@ -4868,6 +5277,8 @@ View px_make_view(ts_engine* e) {
   v.pworld = e->xworld;
   v.prank = e->xrank;
   v.padm_all = (long long)e->cfg.max_concurrency < (long long)e->n_global ? 1 : 0;
+  v.pstamp = e->xstamp;
+  v.pscr = e->xscr;
   return v;
 }
 
@@ -4890,14 +5301,9 @@ int build_px_graph(ts_engine* e, const View& v, int max_steps) {
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   View vv = v;
   int ms = max_steps, stepm1 = -1;
-  const ts_sched_record* rec = (const ts_sched_record*)(e->xbuf + XHDR_BYTES);
-  unsigned char* mt = e->mt;
   void* a_v[] = {(void*)&vv};
   void* a_vc[] = {(void*)&vv, (void*)&h};
   void* a_vcm[] = {(void*)&vv, (void*)&h, (void*)&ms};
-  void* a_st_rec_mt[] = {(void*)&vv, (void*)&stepm1, (void*)&rec, (void*)&mt};
-  void* a_rec_mt[] = {(void*)&vv, (void*)&rec, (void*)&mt};
-  void* a_mt[] = {(void*)&vv, (void*)&mt};
   void* a_wave[] = {(void*)&vv, (void*)&stepm1};
   auto kp = [](void* f, dim3 grid, dim3 block, size_t sm, void** args) {
     cudaKernelNodeParams k;
@@ -4912,22 +5318,8 @@ int build_px_graph(ts_engine* e, const View& v, int max_steps) {
   std::vector<cudaKernelNodeParams> chain;
   chain.push_back(kp((void*)k_px_counts, dim3(1), dim3(32), 0, a_v));
   chain.push_back(kp((void*)k_px_admit, dim3(1), dim3(32), 0, a_vcm));
-  chain.push_back(kp((void*)k_px_records, dim3((e->n_local + 255) / 256), dim3(256), 0, a_v));
-  chain.push_back(kp((void*)k_px_wait, dim3(1), dim3(32), 0, a_vc));
-  if (v.n_global <= e->mt_min) {
-    chain.push_back(kp((void*)k_px_targets, dim3(1), dim3(SCHED_T), targets_smem(), a_v));
-  } else {
-    const int G = mt_blocks(v.n_global), G3 = mt_run_blocks(v.n_global);
-    chain.push_back(kp((void*)k_mt_count, dim3(G), dim3(MT_T), 0, a_st_rec_mt));
-    chain.push_back(kp((void*)k_mt_scan1, dim3(1), dim3(1024), 0, a_rec_mt));
-    chain.push_back(kp((void*)k_mt_runs, dim3(G), dim3(MT_T), 0, a_rec_mt));
-    chain.push_back(kp((void*)k_mt_scan2, dim3(1), dim3(1024), 0, a_mt));
-    chain.push_back(kp((void*)k_mt_write_runs, dim3(G), dim3(MT_T), 0, a_rec_mt));
-    chain.push_back(kp((void*)k_mt_want, dim3(G3), dim3(MT_T), 0, a_mt));
-    chain.push_back(kp((void*)k_mt_scan3, dim3(1), dim3(1024), 0, a_mt));
-    chain.push_back(kp((void*)k_mt_targets, dim3(G), dim3(MT_T), 0, a_rec_mt));
-    chain.push_back(kp((void*)k_mt_split, dim3(1), dim3(TT), 0, a_st_rec_mt));
-  }
+  chain.push_back(kp((void*)k_px_groups, dim3(1), dim3(PXT), 0, a_v));
+  chain.push_back(kp((void*)k_px_sched, dim3(1), dim3(PXT), 0, a_vc));
   cudaKernelNodeParams kw = kp(wave_fn(e), dim3(blocks), dim3(WAVE_THREADS), wave_smem_of(e->wkind), a_wave);
   cudaKernelNodeParams kh = kw;
   if (v.heavy_on) {
@@ -5006,8 +5398,6 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     cr = cudaFuncSetAttribute(k_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   if (cr == cudaSuccess)
     cr = cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sched_smem());
-  if (cr == cudaSuccess)
-    cr = cudaFuncSetAttribute(k_px_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
       cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -5595,6 +5985,11 @@ int ts_xchg_create(ts_engine* e, int32_t world, int32_t rank, void** dev_ptr_out
   e->xbytes = xchg_bytes(e->n_global);
   TS_CUDA_TRY(e, cudaMalloc((void**)&e->xbuf, e->xbytes));
   TS_CUDA_TRY(e, cudaMemset(e->xbuf, 0, e->xbytes));
+  TS_CUDA_TRY(e, cudaMalloc((void**)&e->xstamp, sizeof(unsigned long long) * 3 * PX_STAMP_WAVES));
+  TS_CUDA_TRY(e, cudaMemset(e->xstamp, 0, sizeof(unsigned long long) * 3 * PX_STAMP_WAVES));
+  size_t scr = 0;
+  px_scr(nullptr, e->n_local, e->n_global, &scr);
+  TS_CUDA_TRY(e, cudaMalloc((void**)&e->xscr, scr));
   TS_CUDA_TRY(e, cudaDeviceSynchronize());  // zeroed before any peer can write
   e->xworld = world;
   e->xrank = rank;
@@ -5651,6 +6046,14 @@ int ts_xchg_connect(ts_engine* e, const uint8_t* ipc_handles, void* const* dev_p
   return TS_OK;
 }
 
+int ts_read_px_times(ts_engine* e, uint64_t* host_out, int32_t n, void* stream) {
+  if (!e || !e->xstamp || !host_out || n < 0 || n > PX_STAMP_WAVES) return fail(e, TS_INVALID_ARGUMENT, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  TS_CUDA_TRY(e, cudaMemcpyAsync(host_out, e->xstamp, sizeof(uint64_t) * 3 * (size_t)n, cudaMemcpyDeviceToHost, s));
+  TS_CUDA_TRY(e, cudaStreamSynchronize(s));
+  return TS_OK;
+}
+
 int ts_run_sharded(ts_engine* e, int32_t max_steps, int32_t last_arrival_global, ts_run_stats* stats_out,
                    void* stream) {
   if (!e || !e->loaded) return fail(e, TS_INVALID_ARGUMENT, "no problems loaded");
@@ -5677,8 +6080,7 @@ int ts_run_sharded(ts_engine* e, int32_t max_steps, int32_t last_arrival_global,
     TS_CUDA_TRY(e, cudaStreamSynchronize(s));
     c = *e->pin_ctr;
     const long long waves = c.step - step0;
-    e->launches += 1 + (waves / e->graph_unroll + 1) * e->graph_unroll *
-                           ((v.n_global <= e->mt_min ? 5 : 13) + (v.heavy_on ? 2 : 1));
+    e->launches += 1 + (waves / e->graph_unroll + 1) * e->graph_unroll * (4 + (v.heavy_on ? 2 : 1));
     step0 = c.step;
     if (c.px_err) return fail(e, TS_CUDA, "a peer rank did not signal (peer exchange timed out)");
     if (c.step < max_steps && c.step >= e->log1p_n && c.finished < e->n_local)

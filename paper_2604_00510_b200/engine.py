@@ -264,6 +264,14 @@ class Engine:
             d = (ctypes.c_void_p * len(dev_ptrs))(*[ctypes.c_void_p(x) for x in dev_ptrs])
         self._check(self.lib.ts_xchg_connect(self._h, h, d), "ts_xchg_connect")
 
+    def px_times(self, n: int) -> np.ndarray:
+        """[n, 3] ns stamps per wave of the last run_sharded: counts phase start,
+        all records in, compute_targets done."""
+        buf = np.zeros((max(1, n), 3), np.uint64)
+        self._check(self.lib.ts_read_px_times(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n,
+                                              self.stream), "ts_read_px_times")
+        return buf[:n]
+
     def run_sharded(self, max_steps: int = (1 << 31) - 1, last_arrival: int = 0) -> TsRunStats:
         """The whole sharded batch as one device-driven graph loop (a collective
         over the connected ranks); ``last_arrival`` = the largest arrival step
