@@ -148,6 +148,7 @@ struct View {
   int32_t pworld, prank, padm_all;
   unsigned long long* pstamp;  // per wave: counts phase start, every group table in, scheduler done (%globaltimer)
   unsigned char* pscr;         // group scheduler scratch (px_scratch_bytes)
+  int32_t pgwarp;              // k_px_step: one-warp scheduler up to this many table entries (<= 32)
   double* g_runS;
   int32_t* g_runStart;
   long long* g_runWant;
@@ -528,7 +529,7 @@ __device__ __forceinline__ void scan1_add(T (&x)[N], T (&tot)[N], T* sh) {
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < N; ++q) {
-    const T w = lane < SCHED_W ? sh[q * 32 + lane] : (T)0;
+    const T w = lane < (int)(blockDim.x >> 5) ? sh[q * 32 + lane] : (T)0;
     T wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1108,7 +1109,8 @@ __host__ __device__ inline PxScr px_scr(unsigned char* base, long long nl, long 
   return X;
 }
 
-constexpr int PXT = 1024;  // = SCHED_T (scan1_add's block size)
+constexpr int PXT = 1024;  // k_px_groups / k_px_sched block size
+constexpr int PXS = 512;   // k_px_step block size (128 registers per thread)
 
 // The groups phase: admission state (admit_jobs), then this rank's group
 // table — one PxEnt per distinct arrival among its running searches, in
@@ -1511,6 +1513,729 @@ __global__ void __launch_bounds__(PXT) k_px_sched(View v, cudaGraphConditionalHa
     px_stamp(v, step, 2);
   }
 }
+
+// ---- the fused sharded step (k_px_step): one CTA per rank per wave ----------------
+//
+// Admission (when a search can be pending), the group table, its exchange and
+// compute_targets in ONE kernel: jobs are processed in rounds of PXT (thread t
+// holds job r*PXT + t of round r, state in registers), arrival segments come
+// from a block-wide segmented scan, and the merged group tables live in shared
+// memory.  Rank shards up to PXT * 8 searches; larger shards use
+// k_px_groups + k_px_sched.
+constexpr int PX_GCAP = 768;  // concatenated group entries staged in shared memory
+struct PxTabs {
+  int *a, *gm, *mfirst;
+  unsigned long long *c0, *c1, *p0, *p1;  // counts (run | ungated << 32) of list 0/1; exclusive prefixes
+  int2* mrun;
+  double* rS[2];
+  int *rA[2], *rC[2];
+  long long *rWant[2], *rU[2], *rW[2];
+  int *l0, *l1;                   // per concatenated entry: ungated of list 0/1 earlier in its merged entry
+  long long *bp[2], *bb[2], *wn[2];  // per merged entry: its run's first sorted position, Σ(want-1) before, want
+};
+__host__ __device__ inline PxTabs px_tabs(unsigned char* base, long long cap, size_t* bytes) {
+  PxTabs t;
+  size_t o = 0;
+  auto take = [&](size_t b) -> unsigned char* {
+    unsigned char* q = base ? base + o : nullptr;
+    o += (b + 15) & ~(size_t)15;
+    return q;
+  };
+  t.a = (int*)take(4 * cap);
+  t.gm = (int*)take(4 * cap);
+  t.mfirst = (int*)take(4 * cap);
+  t.c0 = (unsigned long long*)take(8 * cap);
+  t.c1 = (unsigned long long*)take(8 * cap);
+  t.p0 = (unsigned long long*)take(8 * cap);
+  t.p1 = (unsigned long long*)take(8 * cap);
+  t.mrun = (int2*)take(8 * cap);
+  for (int b = 0; b < 2; ++b) {
+    t.rS[b] = (double*)take(8 * cap);
+    t.rA[b] = (int*)take(4 * cap);
+    t.rC[b] = (int*)take(4 * cap);
+    t.rWant[b] = (long long*)take(8 * cap);
+    t.rU[b] = (long long*)take(8 * cap);
+    t.rW[b] = (long long*)take(8 * cap);
+  }
+  t.l0 = (int*)take(4 * cap);
+  t.l1 = (int*)take(4 * cap);
+  for (int b = 0; b < 2; ++b) {
+    t.bp[b] = (long long*)take(8 * cap);
+    t.bb[b] = (long long*)take(8 * cap);
+    t.wn[b] = (long long*)take(8 * cap);
+  }
+  if (bytes) *bytes = o;
+  return t;
+}
+inline size_t px_step_smem() {
+  size_t b = 0;
+  px_tabs(nullptr, PX_GCAP, &b);
+  return b;
+}
+
+// Block-wide exclusive segmented scan (PXS threads, thread order): F = a
+// segment starts at this thread's element, X = its two packed counters.
+// Returns the sum since the last segment start before this thread (and
+// whether one occurred), and the block aggregate.
+__device__ void seg_scan_block(bool F, unsigned long long X0, unsigned long long X1, bool& Fex,
+                               unsigned long long& E0, unsigned long long& E1, bool& Ft, unsigned long long& T0,
+                               unsigned long long& T1) {
+  __shared__ unsigned long long sx0[32], sx1[32];
+  __shared__ int sf[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool f = F;
+  unsigned long long x0 = X0, x1 = X1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const bool fy = __shfl_up_sync(FULL, (int)f, o) != 0;
+    const unsigned long long y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
+    if (lane >= o) {
+      if (!f) { x0 += y0; x1 += y1; }
+      f = f || fy;
+    }
+  }
+  __syncthreads();  // the previous call's readers are done with sx/sf
+  if (lane == 31) {
+    sx0[wid] = x0;
+    sx1[wid] = x1;
+    sf[wid] = f;
+  }
+  __syncthreads();
+  // every warp scans the warp aggregates (lane j: warp j)
+  bool wf = lane < (PXS / 32) && sf[lane] != 0;
+  unsigned long long w0 = lane < (PXS / 32) ? sx0[lane] : 0ull, w1 = lane < (PXS / 32) ? sx1[lane] : 0ull;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const bool fy = __shfl_up_sync(FULL, (int)wf, o) != 0;
+    const unsigned long long y0 = __shfl_up_sync(FULL, w0, o), y1 = __shfl_up_sync(FULL, w1, o);
+    if (lane >= o) {
+      if (!wf) { w0 += y0; w1 += y1; }
+      wf = wf || fy;
+    }
+  }
+  Ft = __shfl_sync(FULL, (int)wf, 31) != 0;
+  T0 = __shfl_sync(FULL, w0, 31);
+  T1 = __shfl_sync(FULL, w1, 31);
+  // prefix of the warps before this one
+  // (every shuffle is executed by the whole warp; the lane / warp conditions apply after)
+  const int pfv = __shfl_sync(FULL, (int)wf, (wid + 31) & 31);
+  unsigned long long p0 = __shfl_sync(FULL, w0, (wid + 31) & 31), p1 = __shfl_sync(FULL, w1, (wid + 31) & 31);
+  const bool pf = wid > 0 && pfv != 0;
+  if (wid == 0) { p0 = 0; p1 = 0; }
+  // exclusive within the warp
+  const int lfv = __shfl_up_sync(FULL, (int)f, 1);
+  unsigned long long l0 = __shfl_up_sync(FULL, x0, 1), l1 = __shfl_up_sync(FULL, x1, 1);
+  const bool lf = lane > 0 && lfv != 0;
+  if (lane == 0) { l0 = 0; l1 = 0; }
+  Fex = pf || lf;
+  E0 = lf ? l0 : p0 + l0;
+  E1 = lf ? l1 : p1 + l1;
+}
+
+template <int JPT>
+__global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHandle cond, int max_steps) {
+  Counters* c = v.ctr;
+  if (c->px_done) return;
+  const int tid = threadIdx.x;
+  const int step = (int)c->step;
+  const ts_config& cf = v.cfg;
+  const int n = v.n_local, W = v.pworld, me = v.prank;
+  const unsigned long long epoch = px_epoch(v, step);
+  __shared__ int s_go;
+  __shared__ long long s_alo, s_ahi;
+  __shared__ int shi[5 * 32];
+  __shared__ long long shl[5 * 32];
+  if (tid == 0) px_stamp(v, step, 0);
+#ifdef TS_PX_PROF
+  unsigned long long pp_t = globaltimer();
+#define PX_MARK(slot)                                                   \
+  do {                                                                  \
+    __syncthreads();                                                    \
+    if (tid == 0) {                                                     \
+      const unsigned long long t_ = globaltimer();                      \
+      atomicAdd(&v.ctr->prof[slot], t_ - pp_t);                         \
+      pp_t = t_;                                                        \
+    }                                                                   \
+  } while (0)
+#else
+#define PX_MARK(slot) do { } while (0)
+#endif
+  if (step >= max_steps || step >= v.log1p_n) {
+    if (tid == 0) px_finish(v, cond, 0);
+    return;
+  }
+  // ---- admit_jobs (scheduler.py:131-140) over every rank's counts ----
+  if (px_adm_active(v, step)) {
+    if (tid == 0) {
+      int lo = 0, hi = n;  // arrivals are non-decreasing: upper_bound(arrival, step)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v.arrival[mid] <= step) lo = mid + 1;
+        else hi = mid;
+      }
+      const long long run = c->running, pend = (long long)lo - c->head, unf = (long long)n - c->finished;
+      for (int p = 0; p < W; ++p) {
+        long long* d = xh(v, p)->cnt[me];
+        d[0] = run;
+        d[1] = pend;
+        d[2] = unf;
+      }
+      for (int p = 0; p < W; ++p) st_release_sys(&xh(v, p)->fa[me], epoch);
+    }
+    const XHdr* x = xh(v, me);
+    if (!px_wait(v, x->fa, epoch)) {
+      if (tid == 0) px_finish(v, cond, 1);
+      return;
+    }
+    if (tid == 0) {
+      long long run_g = 0, pend_g = 0, before = 0, unf_g = 0;
+      for (int r = 0; r < W; ++r) {
+        const long long c0 = __ldcg(&x->cnt[r][0]), c1 = __ldcg(&x->cnt[r][1]), c2 = __ldcg(&x->cnt[r][2]);
+        run_g += c0;
+        pend_g += c1;
+        unf_g += c2;
+        if (r < me) before += c1;
+      }
+      s_go = unf_g > 0;
+      if (unf_g == 0) {
+        px_finish(v, cond, 0);
+      } else {
+        long long A = (long long)cf.max_concurrency - run_g;
+        if (A > pend_g) A = pend_g;
+        if (A < 0) A = 0;
+        long long q = A - before;
+        const long long mine = __ldcg(&x->cnt[me][1]);
+        if (q > mine) q = mine;
+        if (q < 0) q = 0;
+        s_alo = c->head;
+        s_ahi = c->head + q;
+        c->head += q;
+        c->running += q;
+      }
+    }
+    __syncthreads();
+    if (!s_go) return;
+  } else {
+    if (tid == 0) s_alo = s_ahi = c->head;
+    __syncthreads();
+  }
+  PX_MARK(0);
+  const long long alo = s_alo, ahi = s_ahi;
+  // ---- this rank's searches: thread t holds the contiguous jobs [t*JPT, t*JPT+JPT) ----
+  const bool fold = cf.beta == 0.0;  // the boosted flag does not change the score: one list
+  unsigned code[JPT];  // start | running << 1 | ungated << 2 | list << 3 | segment end << 4
+  int comp[JPT], arr[JPT], qv[JPT], ent[JPT];
+  const int lo = tid * JPT;
+  {
+    ulonglong2 w[JPT];
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      const int i = lo + u;
+      if (i < n) {
+        w[u] = *reinterpret_cast<const ulonglong2*>(v.st + i);  // state, completed, job_best
+        arr[u] = v.arrival[i];
+      }
+    }
+    const int aprev = (lo > 0 && lo - 1 < n) ? v.arrival[lo - 1] : 0;
+    const int anext = lo + JPT < n ? v.arrival[lo + JPT] : 0;
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      const int i = lo + u;
+      code[u] = 0;
+      comp[u] = 0;
+      if (i >= n) continue;
+      int state = (int)(uint32_t)w[u].x;
+      if (i >= alo && i < ahi) {
+        state = ST_RUNNING;
+        v.st[i].state = ST_RUNNING;
+        v.st[i].admit_step = step;
+      }
+      const int ap = u > 0 ? arr[u - 1] : (i > 0 ? aprev : arr[u]);
+      const int an = u + 1 < JPT ? arr[u + 1] : anext;
+      if (arr[u] < ap) c->sched_error = 1;
+      unsigned cd = (i == 0 || arr[u] != ap) ? 1u : 0u;
+      if (i == n - 1 || an != arr[u]) cd |= 16u;
+      if (state == ST_RUNNING) {
+        const int done = (int)(uint32_t)(w[u].x >> 32);
+        const double jb = __longlong_as_double((long long)w[u].y);
+        const bool boosted = jb / cf.positive_exit_threshold > cf.proximity;  // scheduler.py:126
+        cd |= 2u | (done >= cf.obs_threshold ? 4u : 0u) | ((boosted && !fold) ? 8u : 0u);
+        comp[u] = done;
+      }
+      code[u] = cd;
+    }
+  }
+  PX_MARK(1);
+  // arrival segments: (running | ungated << 16) of list 0 and of list 1, one
+  // block-wide segmented scan over the threads' aggregates
+  auto xv = [](unsigned cd, int b) -> unsigned long long {
+    if (!(cd & 2u) || (int)((cd >> 3) & 1u) != b) return 0ull;
+    return 1ull | ((cd & 4u) ? (1ull << 16) : 0ull);
+  };
+  bool fex;
+  unsigned long long e0, e1;
+  {
+    bool F = false, ft;
+    unsigned long long X0 = 0, X1 = 0, t0, t1;
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      if (code[u] & 1u) { F = true; X0 = X1 = 0; }
+      X0 += xv(code[u], 0);
+      X1 += xv(code[u], 1);
+    }
+    seg_scan_block(F, X0, X1, fex, e0, e1, ft, t0, t1);
+  }
+  PX_MARK(2);
+  // entries: segment ends with a running search, numbered in arrival order
+  int fl1[1] = {0}, tot1[1];
+  {
+    unsigned long long y0 = e0, y1 = e1;
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      const unsigned cd = code[u];
+      if (cd & 1u) y0 = y1 = 0;
+      y0 += xv(cd, 0);
+      y1 += xv(cd, 1);
+      if ((cd & 16u) && (((uint32_t)y0 & 0xFFFFu) + ((uint32_t)y1 & 0xFFFFu)) > 0) ++fl1[0];
+    }
+  }
+  scan1_add<1>(fl1, tot1, shi);
+  const int nent = tot1[0];
+  {
+    unsigned long long y0 = e0, y1 = e1;
+    int id = fl1[0];
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      const unsigned cd = code[u];
+      if (cd & 1u) y0 = y1 = 0;
+      qv[u] = (int)((((cd & 8u) ? y1 : y0) >> 16) & 0xFFFFu);  // ungated of its list before it in its segment
+      ent[u] = id;
+      y0 += xv(cd, 0);
+      y1 += xv(cd, 1);
+      if ((cd & 16u) && (((uint32_t)y0 & 0xFFFFu) + ((uint32_t)y1 & 0xFFFFu)) > 0) {
+        PxEnt en;
+        en.a = arr[u];
+        en.nr0 = (int)(y0 & 0xFFFFu);
+        en.nu0 = (int)((y0 >> 16) & 0xFFFFu);
+        en.nr1 = (int)(y1 & 0xFFFFu);
+        en.nu1 = (int)((y1 >> 16) & 0xFFFFu);
+        en._p0 = en._p1 = en._p2 = 0;
+        for (int p = 0; p < W; ++p) xent(v, p)[v.goff + id] = en;
+        ++id;
+      }
+    }
+  }
+  PX_MARK(3);
+  // every entry store above happens before the release below (bar.sync, then
+  // a cumulative st.release.sys per peer)
+  __syncthreads();
+  if (tid < W) {
+    XHdr* h = xh(v, tid);
+    h->nent[me] = nent;
+    h->goff[me] = v.goff;
+    h->unf[me] = (long long)n - c->finished;
+    st_release_sys(&h->fb[me], epoch);
+  }
+  const XHdr* x = xh(v, me);
+  if (!px_wait(v, x->fb, epoch)) {
+    if (tid == 0) px_finish(v, cond, 1);
+    return;
+  }
+  PX_MARK(4);
+  if (tid == 0) px_stamp(v, step, 1);
+  // ---- compute_targets (scheduler.py:143-187) from the merged group tables (see k_px_sched) ----
+  __shared__ int off[TS_MAX_PEERS + 1];
+  __shared__ long long gof[TS_MAX_PEERS], s_unf;
+  if (tid == 0) {
+    long long u = 0;
+    off[0] = 0;
+    for (int r = 0; r < W; ++r) {
+      u += __ldcg(&x->unf[r]);
+      off[r + 1] = off[r] + (int)__ldcg(&x->nent[r]);
+      gof[r] = __ldcg(&x->goff[r]);
+    }
+    s_unf = u;
+  }
+  __syncthreads();
+  const long long unf_g = s_unf;
+  if (unf_g == 0) {
+    if (tid == 0) px_finish(v, cond, 0);
+    return;
+  }
+  const int G = off[W];
+  const PxEnt* tab = xent(v, me);
+  // Outputs for the per-search pass: per concatenated entry its merged entry
+  // and the ungated of each list in that merged entry before it (lower
+  // ranks), per merged entry and list the sorted position and Σ(want-1) of
+  // its run's first job, and want.
+  __shared__ int w_gm[32], w_low0[32], w_low1[32];
+  __shared__ long long w_bp0[32], w_bp1[32], w_bb0[32], w_bb1[32], w_wn0[32], w_wn1[32];
+  __shared__ long long s_R, s_rrq, s_rrr;
+  __shared__ int s_boost, s_err;
+  extern __shared__ __align__(16) unsigned char psm[];
+  const PxTabs Tb = px_tabs(G <= PX_GCAP ? psm : v.pscr, G <= PX_GCAP ? PX_GCAP : v.n_global, nullptr);
+  const int *J_gm, *J_low0, *J_low1;
+  const long long *J_bp0, *J_bp1, *J_bb0, *J_bb1, *J_wn0, *J_wn1;
+  const long long M = cf.max_concurrency;
+  if (G <= v.pgwarp) {
+    // ---- one warp: every table entry in a lane ----
+    J_gm = w_gm; J_low0 = w_low0; J_low1 = w_low1;
+    J_bp0 = w_bp0; J_bp1 = w_bp1; J_bb0 = w_bb0; J_bb1 = w_bb1; J_wn0 = w_wn0; J_wn1 = w_wn1;
+    if (tid < 32) {
+      const int lane = tid, g = lane;
+      const bool has = g < G;
+      int ea = 0, nr0 = 0, nu0 = 0, nr1 = 0, nu1 = 0;
+      if (has) {
+        int r = 0;
+        while (r + 1 < W && off[r + 1] <= g) ++r;
+        const int4* e4 = (const int4*)(tab + gof[r] + (g - off[r]));
+        const int4 u4 = __ldcg(e4), w4 = __ldcg(e4 + 1);
+        ea = u4.x; nr0 = u4.y; nu0 = u4.z; nr1 = u4.w; nu1 = w4.x;
+      }
+      const int aprev = __shfl_up_sync(FULL, ea, 1);
+      const bool nw = has && (g == 0 || ea != aprev);
+      const unsigned nwb = __ballot_sync(FULL, nw);
+      const int Gm = __popc(nwb);
+      const int m = __popc(nwb & ((2u << g) - 1u)) - 1;  // merged entry of lane g
+      // segmented inclusive scans of the counts (reset where a merged entry starts)
+      int i0 = nr0, i1 = nu0, i2 = nr1, i3 = nu1;
+      bool f = nw;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y0 = __shfl_up_sync(FULL, i0, o), y1 = __shfl_up_sync(FULL, i1, o);
+        const int y2 = __shfl_up_sync(FULL, i2, o), y3 = __shfl_up_sync(FULL, i3, o);
+        const bool fy = __shfl_up_sync(FULL, (int)f, o) != 0;
+        if (lane >= o && !f) { i0 += y0; i1 += y1; i2 += y2; i3 += y3; }
+        if (lane >= o) f = f || fy;
+      }
+      if (has) {
+        w_gm[g] = m;
+        w_low0[g] = i1 - nu0;
+        w_low1[g] = i3 - nu1;
+      }
+      // lane mm: merged entry mm (its first and last concatenated entries)
+      const int mm = lane;
+      const bool mh = mm < Gm;
+      const int first = mh ? (int)__fns(nwb, 0, mm + 1) : 0;
+      const int last = mh ? ((mm + 1 < Gm ? (int)__fns(nwb, 0, mm + 2) : G) - 1) : 0;
+      const int ma = __shfl_sync(FULL, ea, first);
+      const int Mr0 = __shfl_sync(FULL, i0, last), Mu0 = __shfl_sync(FULL, i1, last);
+      const int Mr1 = __shfl_sync(FULL, i2, last), Mu1 = __shfl_sync(FULL, i3, last);
+      double S0 = 0.0, S1 = 0.0;
+      u128 fx = 0;
+      bool bad = false;
+      if (mh) {
+        S0 = v.log1p_tab[step - ma] + 0.0;  // parallelism_score (scheduler.py:118-128)
+        S1 = v.log1p_tab[step - ma] + cf.beta;
+        u128 q;
+        if (Mr0) { if (to_fixed(S0, q)) fx += q * (u128)(unsigned)Mr0; else bad = true; }
+        if (Mr1) { if (to_fixed(S1, q)) fx += q * (u128)(unsigned)Mr1; else bad = true; }
+      }
+      long long run = mh ? (long long)Mr0 + Mr1 : 0, l0 = mh ? Mu0 : 0, l1 = mh ? Mu1 : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t h = __shfl_xor_sync(FULL, (uint64_t)(fx >> 64), o);
+        const uint64_t l = __shfl_xor_sync(FULL, (uint64_t)fx, o);
+        fx += ((u128)h << 64) | l;
+        run += __shfl_xor_sync(FULL, run, o);
+        l0 += __shfl_xor_sync(FULL, l0, o);
+        l1 += __shfl_xor_sync(FULL, l1, o);
+      }
+      bad = __any_sync(FULL, bad);
+      const double T = fixed_to_double(fx);
+      const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
+      const bool err = bad || (double)run * u2 >= 0x1p-10;  // would need the sequential sum (targets_block)
+      const long long R = M - run;
+      const bool boost_on = cf.boosting_enabled != 0 && run > 0 && R > 0 && l0 + l1 > 0;
+      long long wn0 = 1, wn1 = 1;
+      if (T > 0.0) {
+        const double f0 = floor(S0 / T * (double)M), f1 = floor(S1 / T * (double)M);  // scheduler.py:173-175
+        wn0 = f0 > 1.0 ? (long long)f0 : 1;
+        wn1 = f1 > 1.0 ? (long long)f1 : 1;
+      }
+      const long long wv0 = mh ? (long long)Mu0 * (wn0 - 1) : 0, wv1 = mh ? (long long)Mu1 * (wn1 - 1) : 0;
+      // sorted position / Σ(want-1) of each run's first job: own-list runs of
+      // earlier arrival, other-list runs of higher score (equal: earlier arrival)
+      long long bp0 = 0, bb0 = 0, bp1 = 0, bb1 = 0, twt = 0;
+      for (int j = 0; j < Gm; ++j) {
+        const double T0 = __shfl_sync(FULL, S0, j), T1 = __shfl_sync(FULL, S1, j);
+        const int aj = __shfl_sync(FULL, ma, j);
+        const long long u0 = __shfl_sync(FULL, (long long)Mu0, j), u1 = __shfl_sync(FULL, (long long)Mu1, j);
+        const long long x0 = __shfl_sync(FULL, wv0, j), x1 = __shfl_sync(FULL, wv1, j);
+        twt += x0 + x1;
+        if (j < mm) { bp0 += u0; bb0 += x0; bp1 += u1; bb1 += x1; }
+        if (u1 > 0 && (T1 > S0 || (T1 == S0 && aj < ma))) { bp0 += u1; bb0 += x1; }
+        if (u0 > 0 && (T0 > S1 || (T0 == S1 && aj < ma))) { bp1 += u0; bb1 += x0; }
+      }
+      if (mh) {
+        w_bp0[mm] = bp0; w_bb0[mm] = bb0; w_wn0[mm] = wn0;
+        w_bp1[mm] = bp1; w_bb1[mm] = bb1; w_wn1[mm] = wn1;
+      }
+      if (lane == 0) {
+        const long long U = l0 + l1;
+        long long Rp = R - twt;
+        if (Rp < 0) Rp = 0;
+        s_R = R;
+        s_boost = boost_on;
+        s_rrq = U > 0 ? Rp / U : 0;
+        s_rrr = U > 0 ? Rp % U : 0;
+        s_err = err;
+      }
+    }
+    __syncthreads();
+  } else {
+    // ---- many entries: block-wide scans over the staged tables ----
+    J_gm = Tb.gm; J_low0 = Tb.l0; J_low1 = Tb.l1;
+    J_bp0 = Tb.bp[0]; J_bp1 = Tb.bp[1]; J_bb0 = Tb.bb[0]; J_bb1 = Tb.bb[1];
+    J_wn0 = Tb.wn[0]; J_wn1 = Tb.wn[1];
+    for (int g = tid; g < G; g += PXS) {
+      int r = 0;
+      while (r + 1 < W && off[r + 1] <= g) ++r;
+      const int4* e4 = (const int4*)(tab + gof[r] + (g - off[r]));
+      const int4 u = __ldcg(e4), w2 = __ldcg(e4 + 1);
+      Tb.a[g] = u.x;
+      Tb.c0[g] = (unsigned long long)(uint32_t)u.y | ((unsigned long long)(uint32_t)u.z << 32);
+      Tb.c1[g] = (unsigned long long)(uint32_t)u.w | ((unsigned long long)(uint32_t)w2.x << 32);
+    }
+    __syncthreads();
+    PX_MARK(5);
+    // merged entries and exclusive prefixes of the counts over the concatenated table
+    const int pg = (G + PXS - 1) / PXS, g0 = min(G, tid * pg), g1 = min(G, g0 + pg);
+    long long cg[5] = {0, 0, 0, 0, 0}, tg[5];  // new, run0, ung0, run1, ung1 — 64-bit sums of the 32-bit halves
+    {
+      long long acc[3] = {0, 0, 0};
+      for (int g = g0; g < g1; ++g) {
+        acc[0] += (g == 0 || Tb.a[g] != Tb.a[g - 1]) ? 1 : 0;
+        cg[1] += (uint32_t)Tb.c0[g];
+        cg[2] += (long long)(Tb.c0[g] >> 32);
+        cg[3] += (uint32_t)Tb.c1[g];
+        cg[4] += (long long)(Tb.c1[g] >> 32);
+      }
+      cg[0] = acc[0];
+    }
+    scan1_add<5>(cg, tg, shl);
+    for (int g = g0; g < g1; ++g) {
+      if (g == 0 || Tb.a[g] != Tb.a[g - 1]) Tb.mfirst[cg[0]++] = g;
+      Tb.gm[g] = (int)cg[0] - 1;
+      Tb.p0[g] = (unsigned long long)cg[1] | ((unsigned long long)cg[2] << 32);
+      Tb.p1[g] = (unsigned long long)cg[3] | ((unsigned long long)cg[4] << 32);
+      cg[1] += (uint32_t)Tb.c0[g];
+      cg[2] += (long long)(Tb.c0[g] >> 32);
+      cg[3] += (uint32_t)Tb.c1[g];
+      cg[4] += (long long)(Tb.c1[g] >> 32);
+    }
+    PX_MARK(6);
+    const int Gm = (int)tg[0];
+    const long long tot_run = tg[1] + tg[3], len0 = tg[2], len1 = tg[4];
+    const unsigned long long pt0 = (unsigned long long)tg[1] | ((unsigned long long)tg[2] << 32);
+    const unsigned long long pt1 = (unsigned long long)tg[3] | ((unsigned long long)tg[4] << 32);
+    __syncthreads();
+    const int pm = (Gm + PXS - 1) / PXS, m0 = min(Gm, tid * pm), m1 = min(Gm, m0 + pm);
+    auto mcount = [&](int m, int& a, unsigned long long& k0, unsigned long long& k1) {
+      const int ga = Tb.mfirst[m], gb = m + 1 < Gm ? Tb.mfirst[m + 1] : G;
+      k0 = (gb < G ? Tb.p0[gb] : pt0) - Tb.p0[ga];
+      k1 = (gb < G ? Tb.p1[gb] : pt1) - Tb.p1[ga];
+      a = Tb.a[ga];
+    };
+    u128 fx = 0;
+    bool bad = false;
+    int cr[2] = {0, 0}, tr[2];
+    for (int m = m0; m < m1; ++m) {
+      int a;
+      unsigned long long k0, k1;
+      mcount(m, a, k0, k1);
+      const double S0 = v.log1p_tab[step - a] + 0.0, S1 = v.log1p_tab[step - a] + cf.beta;
+      u128 q;
+      if ((uint32_t)k0) {
+        if (to_fixed(S0, q)) fx += q * (u128)(uint32_t)k0;
+        else bad = true;
+      }
+      if ((uint32_t)k1) {
+        if (to_fixed(S1, q)) fx += q * (u128)(uint32_t)k1;
+        else bad = true;
+      }
+      cr[0] += (k0 >> 32) ? 1 : 0;
+      cr[1] += (k1 >> 32) ? 1 : 0;
+    }
+    scan1_add<2>(cr, tr, shi);
+    const u128 fsum = block_sum_u128(fx, bad);
+    for (int m = m0; m < m1; ++m) {
+      int a;
+      unsigned long long k0, k1;
+      mcount(m, a, k0, k1);
+      const double S0 = v.log1p_tab[step - a] + 0.0, S1 = v.log1p_tab[step - a] + cf.beta;
+      int2 mr = make_int2(-1, -1);
+      if (k0 >> 32) {
+        Tb.rS[0][cr[0]] = S0;
+        Tb.rA[0][cr[0]] = a;
+        Tb.rC[0][cr[0]] = (int)(k0 >> 32);
+        mr.x = cr[0]++;
+      }
+      if (k1 >> 32) {
+        Tb.rS[1][cr[1]] = S1;
+        Tb.rA[1][cr[1]] = a;
+        Tb.rC[1][cr[1]] = (int)(k1 >> 32);
+        mr.y = cr[1]++;
+      }
+      Tb.mrun[m] = mr;
+    }
+    const int nrun0 = tr[0], nrun1 = tr[1];
+    const double T = fixed_to_double(fsum);
+    {
+      const double u2 = T > 0 ? ldexp(1.0, ilogb(2.0 * T) - 52) : 0.0;
+      if (bad || (double)tot_run * u2 >= 0x1p-10) {  // would need the sequential sum (targets_block)
+        if (tid == 0) px_finish(v, cond, 2);
+        return;  // block-uniform
+      }
+    }
+    __syncthreads();
+    PX_MARK(7);
+    const long long R = M - tot_run;
+    const bool boost_on = cf.boosting_enabled != 0 && tot_run > 0 && R > 0 && len0 + len1 > 0;
+    long long tw0 = 0, tw1 = 0;
+    if (boost_on) {
+      long long pre[4] = {0, 0, 0, 0}, tot4[4];
+      int a0[2], a1[2];
+  #pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int nr = b ? nrun1 : nrun0;
+        const int pr = (nr + PXS - 1) / PXS;
+        a0[b] = min(nr, tid * pr);
+        a1[b] = min(nr, a0[b] + pr);
+        for (int k = a0[b]; k < a1[b]; ++k) {
+          long long want = 1;
+          if (T > 0.0) {
+            const double f = floor(Tb.rS[b][k] / T * (double)M);  // scheduler.py:173-175
+            want = f > 1.0 ? (long long)f : 1;
+          }
+          Tb.rWant[b][k] = want;
+          pre[2 * b] += Tb.rC[b][k];
+          pre[2 * b + 1] += (long long)Tb.rC[b][k] * (want - 1);
+        }
+      }
+      __syncthreads();
+      scan1_add<4>(pre, tot4, shl);
+  #pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        long long u = pre[2 * b], w = pre[2 * b + 1];
+        for (int k = a0[b]; k < a1[b]; ++k) {
+          Tb.rU[b][k] = u;
+          Tb.rW[b][k] = w;
+          u += Tb.rC[b][k];
+          w += (long long)Tb.rC[b][k] * (Tb.rWant[b][k] - 1);
+        }
+      }
+      tw0 = tot4[1];
+      tw1 = tot4[3];
+      __syncthreads();
+    }
+    PX_MARK(8);
+    // per merged entry and list: the run's first job's sorted position and Σ(want-1)
+    for (int m = m0; m < m1; ++m) {
+      const int2 mr = Tb.mrun[m];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int kr = b ? mr.y : mr.x;
+        long long bp = 0, bb = 0, wn = 1;
+        if (kr >= 0 && boost_on) {
+          const double* oS = b ? Tb.rS[0] : Tb.rS[1];
+          const int* oA = b ? Tb.rA[0] : Tb.rA[1];
+          const long long* oU = b ? Tb.rU[0] : Tb.rU[1];
+          const long long* oW = b ? Tb.rW[0] : Tb.rW[1];
+          const int on = b ? nrun0 : nrun1;
+          const double S = (b ? Tb.rS[1] : Tb.rS[0])[kr];
+          const int a = (b ? Tb.rA[1] : Tb.rA[0])[kr];
+          wn = (b ? Tb.rWant[1] : Tb.rWant[0])[kr];
+          bp = (b ? Tb.rU[1] : Tb.rU[0])[kr];
+          bb = (b ? Tb.rW[1] : Tb.rW[0])[kr];
+          int kk = runs_lower(oS, on, S);  // other-list runs with a higher score
+          if (kk < on && oS[kk] == S && oA[kk] < a) ++kk;  // equal score: earlier arrival first
+          bp += kk < on ? oU[kk] : (b ? len0 : len1);
+          bb += kk < on ? oW[kk] : (b ? tw0 : tw1);
+        }
+        (b ? Tb.bp[1] : Tb.bp[0])[m] = bp;
+        (b ? Tb.bb[1] : Tb.bb[0])[m] = bb;
+        (b ? Tb.wn[1] : Tb.wn[0])[m] = wn;
+      }
+    }
+    for (int g = g0; g < g1; ++g) {
+      const int m = Tb.gm[g], f = Tb.mfirst[m];
+      Tb.l0[g] = (int)((Tb.p0[g] >> 32) - (Tb.p0[f] >> 32));
+      Tb.l1[g] = (int)((Tb.p1[g] >> 32) - (Tb.p1[f] >> 32));
+    }
+    if (tid == 0) {
+      const long long U = len0 + len1;
+      long long Rp = R - (tw0 + tw1);
+      if (Rp < 0) Rp = 0;
+      s_R = R;
+      s_boost = boost_on;
+      s_rrq = U > 0 ? Rp / U : 0;
+      s_rrr = U > 0 ? Rp % U : 0;
+      s_err = 0;
+    }
+    __syncthreads();
+  }
+  if (s_err) {
+    if (tid == 0) px_finish(v, cond, 2);
+    return;
+  }
+  PX_MARK(8);
+  const long long R = s_R, rr_q = s_rrq, rr_r = s_rrr;
+  const bool boost_on = s_boost != 0;
+  int nl2[2] = {0, 0}, tl2[2];
+  unsigned hv = 0;  // bit u: job lo+u is in the pipelined-mode list
+#pragma unroll
+  for (int u = 0; u < JPT; ++u) {
+    const int i = lo + u;
+    const unsigned cd = code[u];
+    if (i >= n) continue;
+    if (!(cd & 2u)) {
+      v.tgt[i] = 0;
+      continue;
+    }
+    long long tgt = 1;
+    if ((cd & 4u) && boost_on) {
+      const bool b = (cd & 8u) != 0;
+      const int g = off[me] + ent[u], m = J_gm[g];
+      const long long qt = (long long)qv[u] + (b ? J_low1 : J_low0)[g];
+      const long long want = (b ? J_wn1 : J_wn0)[m];
+      const long long pos = (b ? J_bp1 : J_bp0)[m] + qt;
+      const long long before = (b ? J_bb1 : J_bb0)[m] + qt * (want - 1);
+      long long extra = R - before;
+      if (extra < 0) extra = 0;
+      if (extra > want - 1) extra = want - 1;
+      tgt = 1 + extra + rr_q + (pos < rr_r ? 1 : 0);
+    }
+    v.tgt[i] = (int)tgt;
+    const bool h = v.heavy_on && min(tgt, (long long)(cf.rollout_budget - comp[u])) >= HEAVY_P;
+    if (h) hv |= 1u << u;
+    ++nl2[h ? 0 : 1];
+  }
+  PX_MARK(9);
+  // the two work lists in run-queue order (one scan: the chunks are contiguous)
+  scan1_add<2>(nl2, tl2, shi);
+  {
+    int ph = nl2[0], pl = nl2[1];
+#pragma unroll
+    for (int u = 0; u < JPT; ++u) {
+      const int i = lo + u;
+      if (i >= n || !(code[u] & 2u)) continue;
+      if ((hv >> u) & 1u) v.work_heavy[ph++] = i;
+      else v.work[pl++] = i;
+    }
+  }
+  PX_MARK(10);
+  if (tid == 0) {
+    c->work_count = tl2[1];
+    c->work_next = 0;
+    c->heavy_count = tl2[0];
+    c->heavy_next = 0;
+    c->cur_step = step;
+    c->step = step + 1;
+    px_stamp(v, step, 2);
+  }
+}
+#undef PX_MARK
 
 // ---- compute_targets over many CTAs (multi-GPU runs: all n_global records) ----
 // The same algorithm as targets_block, with every cross-thread scan split into
@@ -4828,6 +5553,8 @@ struct ts_engine {
   cudaGraphExec_t px_exec = nullptr;
   View px_view;
   int px_max_steps = -1;
+  bool px_two_kernels = false;  // TS_PX_TWO_KERNELS=1: k_px_groups + k_px_sched instead of k_px_step (diagnostics)
+  int px_gwarp = 32;            // TS_PX_GWARP: k_px_step's one-warp scheduler up to this many group entries
 };
 
 namespace {
@@ -5279,6 +6006,7 @@ View px_make_view(ts_engine* e) {
   v.padm_all = (long long)e->cfg.max_concurrency < (long long)e->n_global ? 1 : 0;
   v.pstamp = e->xstamp;
   v.pscr = e->xscr;
+  v.pgwarp = e->px_gwarp;
   return v;
 }
 
@@ -5318,8 +6046,17 @@ int build_px_graph(ts_engine* e, const View& v, int max_steps) {
   std::vector<cudaKernelNodeParams> chain;
   chain.push_back(kp((void*)k_px_counts, dim3(1), dim3(32), 0, a_v));
   chain.push_back(kp((void*)k_px_admit, dim3(1), dim3(32), 0, a_vcm));
-  chain.push_back(kp((void*)k_px_groups, dim3(1), dim3(PXT), 0, a_v));
-  chain.push_back(kp((void*)k_px_sched, dim3(1), dim3(PXT), 0, a_vc));
+  if (e->n_local <= 16 * PXS && !e->px_two_kernels) {
+    // the whole exchange and scheduler pass in one kernel
+    chain.clear();
+    const int jpt = (e->n_local + PXS - 1) / PXS;
+    void* f = jpt <= 1 ? (void*)k_px_step<1> : jpt <= 2 ? (void*)k_px_step<2> : jpt <= 4 ? (void*)k_px_step<4>
+            : jpt <= 8 ? (void*)k_px_step<8> : (void*)k_px_step<16>;
+    chain.push_back(kp(f, dim3(1), dim3(PXS), px_step_smem(), a_vcm));
+  } else {
+    chain.push_back(kp((void*)k_px_groups, dim3(1), dim3(PXT), 0, a_v));
+    chain.push_back(kp((void*)k_px_sched, dim3(1), dim3(PXT), 0, a_vc));
+  }
   cudaKernelNodeParams kw = kp(wave_fn(e), dim3(blocks), dim3(WAVE_THREADS), wave_smem_of(e->wkind), a_wave);
   cudaKernelNodeParams kh = kw;
   if (v.heavy_on) {
@@ -5398,6 +6135,12 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     cr = cudaFuncSetAttribute(k_targets, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)targets_smem());
   if (cr == cudaSuccess)
     cr = cudaFuncSetAttribute(k_sched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sched_smem());
+  {
+    void* fs[] = {(void*)k_px_step<1>, (void*)k_px_step<2>, (void*)k_px_step<4>, (void*)k_px_step<8>,
+                  (void*)k_px_step<16>};
+    for (void* f : fs)
+      if (cr == cudaSuccess) cr = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)px_step_smem());
+  }
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
       cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -5422,6 +6165,10 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     e->heavy_sync = env2 && env2[0] == '1';
     const char* env5 = getenv("TS_NO_GRAPH");  // host-driven stepping (diagnostics: ncu cannot see graph kernels)
     e->graph_failed = env5 && env5[0] == '1';
+    const char* env8 = getenv("TS_PX_TWO_KERNELS");
+    e->px_two_kernels = env8 && env8[0] == '1';
+    const char* env9 = getenv("TS_PX_GWARP");
+    if (env9) e->px_gwarp = std::max(0, std::min(32, atoi(env9)));
     const char* env6 = getenv("TS_GRAPH_UNROLL");
     if (env6) e->graph_unroll = std::max(1, std::min(8, atoi(env6)));
   }
@@ -5818,7 +6565,7 @@ int ts_read_targets(ts_engine* e, int32_t* host_out, int32_t n, void* stream) {
   return TS_OK;
 }
 
-#if defined(TS_HEAVY_PROF) || defined(TS_SCHED_PROF)
+#if defined(TS_HEAVY_PROF) || defined(TS_SCHED_PROF) || defined(TS_PX_PROF)
 // diagnostics build only (not part of the C-ABI): the phase counters
 int ts_debug_prof(ts_engine* e, uint64_t* host16) {
   Counters c;
@@ -5987,8 +6734,10 @@ int ts_xchg_create(ts_engine* e, int32_t world, int32_t rank, void** dev_ptr_out
   TS_CUDA_TRY(e, cudaMemset(e->xbuf, 0, e->xbytes));
   TS_CUDA_TRY(e, cudaMalloc((void**)&e->xstamp, sizeof(unsigned long long) * 3 * PX_STAMP_WAVES));
   TS_CUDA_TRY(e, cudaMemset(e->xstamp, 0, sizeof(unsigned long long) * 3 * PX_STAMP_WAVES));
-  size_t scr = 0;
+  size_t scr = 0, scr2 = 0;
   px_scr(nullptr, e->n_local, e->n_global, &scr);
+  px_tabs(nullptr, e->n_global, &scr2);
+  scr = std::max(scr, scr2);
   TS_CUDA_TRY(e, cudaMalloc((void**)&e->xscr, scr));
   TS_CUDA_TRY(e, cudaDeviceSynchronize());  // zeroed before any peer can write
   e->xworld = world;
@@ -6080,7 +6829,8 @@ int ts_run_sharded(ts_engine* e, int32_t max_steps, int32_t last_arrival_global,
     TS_CUDA_TRY(e, cudaStreamSynchronize(s));
     c = *e->pin_ctr;
     const long long waves = c.step - step0;
-    e->launches += 1 + (waves / e->graph_unroll + 1) * e->graph_unroll * (4 + (v.heavy_on ? 2 : 1));
+    e->launches += 1 + (waves / e->graph_unroll + 1) * e->graph_unroll *
+                           ((e->n_local <= 16 * PXS && !e->px_two_kernels ? 1 : 4) + (v.heavy_on ? 2 : 1));
     step0 = c.step;
     if (c.px_err) return fail(e, TS_CUDA, "a peer rank did not signal (peer exchange timed out)");
     if (c.step < max_steps && c.step >= e->log1p_n && c.finished < e->n_local)

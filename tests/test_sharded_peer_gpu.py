@@ -64,15 +64,23 @@ def _bounds(n, parts):
     return b[: parts + 1] if parts == 3 else [0, n]
 
 
-@pytest.mark.parametrize("name,multi_cta", [("c1_M48_admission", False), ("c1_M48_admission", True),
-                                             ("cli_serving_pe_ne_boost", False), ("cli_serving_pe_ne_boost", True),
-                                             ("c2_s512_M2048", False), ("c2_s512_M2048", True)])
-def test_peer_sharded_matches_reference_waves(name, multi_cta, monkeypatch):
+MODES = ["fused", "fused_block_tables", "two_kernels"]
+
+
+def _mode_env(monkeypatch, mode):
+    if mode == "fused_block_tables":  # k_px_step with the block-wide table path even for small tables
+        monkeypatch.setenv("TS_PX_GWARP", "0")
+    if mode == "two_kernels":  # k_px_groups + k_px_sched
+        monkeypatch.setenv("TS_PX_TWO_KERNELS", "1")
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("name", ["c1_M48_admission", "cli_serving_pe_ne_boost", "c2_s512_M2048"])
+def test_peer_sharded_matches_reference_waves(name, mode, monkeypatch):
     """3 unequal ranks over peer memory reproduce the reference-composed wave
-    oracle (FIFO admission across ranks, Poisson arrivals, boosting) with the
-    one-CTA or the many-CTA scheduler inside the graph loop."""
-    if multi_cta:
-        monkeypatch.setenv("TS_MT_MIN", "0")
+    oracle (FIFO admission across ranks, Poisson arrivals, boosting) with each
+    scheduler variant of the graph loop."""
+    _mode_env(monkeypatch, mode)
     case = next(c for c in load("waves") if c["name"] == name)
     recs = load("workloads")[case["workload"]][: len(case["outcomes"])]
     cfg = config_from_case(case)
@@ -94,11 +102,14 @@ def test_peer_sharded_matches_reference_waves(name, multi_cta, monkeypatch):
         e.close()
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("world", [1, 2, 5])
-def test_peer_sharded_matches_single_engine(world):
+def test_peer_sharded_matches_single_engine(world, mode, monkeypatch):
     """C2-shape batch (boosting, exits) sharded over `world` unequal ranks ==
     ts_run on one engine: every outcome field and the global wave count."""
     import torch
+
+    _mode_env(monkeypatch, mode)
 
     from paper_2604_00510_b200 import backend as B
     from paper_2604_00510_b200.config import SearchConfig
