@@ -188,6 +188,29 @@ def algorithmic_bytes(st) -> int:
             + B_PATH * st.path_nodes)
 
 
+def peer_exchange(eng, table, lo, n_total, d: Dist):
+    """The sharded loop over peer memory (PeerShardedRun: one device-driven
+    graph per batch, scheduler inputs written straight into every rank's
+    buffer over NVLink).  Validated with one batch; if any rank cannot set it
+    up (no CUDA IPC / peer access), every rank falls back to ShardedRun's
+    NCCL all-gathers together."""
+    import sys
+
+    from paper_2604_00510_b200.distributed import PeerShardedRun
+
+    peer, ok = None, 1.0
+    try:
+        eng.load(table, lo, n_total)
+        peer = PeerShardedRun(eng, d.pg)
+        peer.run()
+    except Exception as ex:  # reported; the whole job switches transport together
+        print(f"bench.py rank {d.rank}: peer exchange unavailable ({ex}); NCCL all-gather loop", file=sys.stderr)
+        ok = 0.0
+    if -d.max(-ok) < 1.0:
+        return None
+    return peer
+
+
 def profile_waves(eng, table, lo, n_total, d: Dist, sharded=None):
     """Σ wave-kernel time (CUDA events on the launch stream) and algorithmic
     bytes of one batch; for N ranks the bytes of all ranks over the slowest
@@ -245,16 +268,19 @@ def bench_ours(args, d: Dist):
     eng = Engine(cfg, d.local)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
-    sharded = None
+    sharded, peer = None, None
     if N > 1:
         from paper_2604_00510_b200.distributed import ShardedRun
 
         sharded = ShardedRun(eng, d.pg, PER_GPU, n_total, torch.device("cuda", d.local),
                              host_staging=d.backend != "nccl")
+        peer = peer_exchange(eng, table, lo, n_total, d)
 
     def one_step():
         if N == 1:
             eng.run()
+        elif peer is not None:
+            peer.run()
         else:
             sharded.run()
 
@@ -304,14 +330,16 @@ def bench_ours(args, d: Dist):
             d.barrier()
             t0 = time.perf_counter()
             eng.load(table, lo, n_total)  # H2D of this rank's problem table
-            sharded.run()
+            one_step()
             eng.outcomes()  # D2H of this rank's outcomes
             ts.append(d.max(time.perf_counter() - t0))
             ro = d.sum(eng.stats().rollouts)
         e2e = {"value": ro / statistics.median(ts), "unit": UNIT,
                "h2d_bytes_per_step": ctypes.sizeof(TsProblem) * n_total,
                "d2h_bytes_per_step": ctypes.sizeof(TsOutcome) * n_total,
-               "ms_per_step": 1e3 * statistics.median(ts), "api": "Engine.load + ShardedRun.run + Engine.outcomes"}
+               "ms_per_step": 1e3 * statistics.median(ts),
+               "api": "Engine.load + " + ("PeerShardedRun.run" if peer is not None else "ShardedRun.run")
+                      + " + Engine.outcomes"}
     if N == 1:
         from paper_2604_00510_b200._abi import TsOutcome, TsProblem
         from paper_2604_00510_b200.engine import pinned_array
@@ -396,6 +424,10 @@ def bench_ours(args, d: Dist):
                      "regime": "latency-bound: the boosted tail wave is sequential per search by definition"},
         "cpu_baseline": cpu, "clocks": clk, "variants": {"exits_off": variant, "c3_rollout_step": c3, **extra},
     }
+    if N > 1:
+        line["exchange"] = ("peer memory: ts_run_sharded (one device-driven graph per batch, counts and group "
+                            "tables written into every rank's buffer over NVLink)" if peer is not None else
+                            "NCCL all-gathers of counts and records per wave (ShardedRun, host-driven)")
     eng.close()
     return line
 
@@ -411,13 +443,19 @@ def c3_rollout_step(table, lo, n_total, d: Dist, flush, args) -> dict:
 
     N = d.world
     eng = Engine(search_config(4 * n_total, exits=False), d.local)
-    sharded = None
+    sharded, peer = None, None
     if N > 1:
         from paper_2604_00510_b200.distributed import ShardedRun
 
         sharded = ShardedRun(eng, d.pg, PER_GPU, n_total, torch.device("cuda", d.local),
                              host_staging=d.backend != "nccl")
-    run = (lambda: eng.run()) if N == 1 else (lambda: sharded.run())  # noqa: E731
+        peer = peer_exchange(eng, table, lo, n_total, d)
+    if N == 1:
+        run = lambda: eng.run()  # noqa: E731
+    elif peer is not None:
+        run = lambda: peer.run().steps  # noqa: E731
+    else:
+        run = lambda: sharded.run()  # noqa: E731
     eng.load(table, lo, n_total)
     run()
     stream = torch.cuda.current_stream()

@@ -1657,8 +1657,18 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
       pp_t = t_;                                                        \
     }                                                                   \
   } while (0)
+#define PX_WMARK(slot)                                                  \
+  do {                                                                  \
+    __syncwarp();                                                       \
+    if (tid == 0) {                                                     \
+      const unsigned long long t_ = globaltimer();                      \
+      atomicAdd(&v.ctr->prof[slot], t_ - pp_t);                         \
+      pp_t = t_;                                                        \
+    }                                                                   \
+  } while (0)
 #else
 #define PX_MARK(slot) do { } while (0)
+#define PX_WMARK(slot) do { } while (0)
 #endif
   if (step >= max_steps || step >= v.log1p_n) {
     if (tid == 0) px_finish(v, cond, 0);
@@ -1845,14 +1855,19 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
   if (tid == 0) px_stamp(v, step, 1);
   // ---- compute_targets (scheduler.py:143-187) from the merged group tables (see k_px_sched) ----
   __shared__ int off[TS_MAX_PEERS + 1];
-  __shared__ long long gof[TS_MAX_PEERS], s_unf;
+  __shared__ long long gof[TS_MAX_PEERS], s_unf, h_u[TS_MAX_PEERS], h_n[TS_MAX_PEERS];
+  if (tid < W) {  // every rank's header words at once
+    h_u[tid] = __ldcg(&x->unf[tid]);
+    h_n[tid] = __ldcg(&x->nent[tid]);
+    gof[tid] = __ldcg(&x->goff[tid]);
+  }
+  __syncthreads();
   if (tid == 0) {
     long long u = 0;
     off[0] = 0;
     for (int r = 0; r < W; ++r) {
-      u += __ldcg(&x->unf[r]);
-      off[r + 1] = off[r] + (int)__ldcg(&x->nent[r]);
-      gof[r] = __ldcg(&x->goff[r]);
+      u += h_u[r];
+      off[r + 1] = off[r] + (int)h_n[r];
     }
     s_unf = u;
   }
@@ -1881,6 +1896,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
     // ---- one warp: every table entry in a lane ----
     J_gm = w_gm; J_low0 = w_low0; J_low1 = w_low1;
     J_bp0 = w_bp0; J_bp1 = w_bp1; J_bb0 = w_bb0; J_bb1 = w_bb1; J_wn0 = w_wn0; J_wn1 = w_wn1;
+    PX_MARK(11);
     if (tid < 32) {
       const int lane = tid, g = lane;
       const bool has = g < G;
@@ -1892,6 +1908,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
         const int4 u4 = __ldcg(e4), w4 = __ldcg(e4 + 1);
         ea = u4.x; nr0 = u4.y; nu0 = u4.z; nr1 = u4.w; nu1 = w4.x;
       }
+      PX_WMARK(12);
       const int aprev = __shfl_up_sync(FULL, ea, 1);
       const bool nw = has && (g == 0 || ea != aprev);
       const unsigned nwb = __ballot_sync(FULL, nw);
@@ -1913,6 +1930,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
         w_low0[g] = i1 - nu0;
         w_low1[g] = i3 - nu1;
       }
+      PX_WMARK(13);
       // lane mm: merged entry mm (its first and last concatenated entries)
       const int mm = lane;
       const bool mh = mm < Gm;
@@ -1931,6 +1949,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
         if (Mr0) { if (to_fixed(S0, q)) fx += q * (u128)(unsigned)Mr0; else bad = true; }
         if (Mr1) { if (to_fixed(S1, q)) fx += q * (u128)(unsigned)Mr1; else bad = true; }
       }
+      PX_WMARK(14);
       long long run = mh ? (long long)Mr0 + Mr1 : 0, l0 = mh ? Mu0 : 0, l1 = mh ? Mu1 : 0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1954,6 +1973,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
         wn1 = f1 > 1.0 ? (long long)f1 : 1;
       }
       const long long wv0 = mh ? (long long)Mu0 * (wn0 - 1) : 0, wv1 = mh ? (long long)Mu1 * (wn1 - 1) : 0;
+      PX_WMARK(15);
       // sorted position / Σ(want-1) of each run's first job: own-list runs of
       // earlier arrival, other-list runs of higher score (equal: earlier arrival)
       long long bp0 = 0, bb0 = 0, bp1 = 0, bb1 = 0, twt = 0;
@@ -1967,6 +1987,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
         if (u1 > 0 && (T1 > S0 || (T1 == S0 && aj < ma))) { bp0 += u1; bb0 += x1; }
         if (u0 > 0 && (T0 > S1 || (T0 == S1 && aj < ma))) { bp1 += u0; bb1 += x0; }
       }
+      PX_WMARK(16);
       if (mh) {
         w_bp0[mm] = bp0; w_bb0[mm] = bb0; w_wn0[mm] = wn0;
         w_bp1[mm] = bp1; w_bb1[mm] = bb1; w_wn1[mm] = wn1;
@@ -2236,6 +2257,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
   }
 }
 #undef PX_MARK
+#undef PX_WMARK
 
 // ---- compute_targets over many CTAs (multi-GPU runs: all n_global records) ----
 // The same algorithm as targets_block, with every cross-thread scan split into

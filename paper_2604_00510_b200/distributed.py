@@ -175,16 +175,19 @@ class PeerShardedRun:
         self.rank = dist.get_rank(group)
         ptr, handle = engine.xchg_create(self.world, self.rank, ipc=self.world > 1)
         handles = [handle]
+        # host-side collectives once at set-up (NCCL needs device tensors)
+        dev = torch.device("cuda", torch.cuda.current_device()) if (
+            self.world > 1 and dist.get_backend(group) == "nccl") else torch.device("cpu")
         if self.world > 1:
-            mine = torch.tensor(list(handle), dtype=torch.uint8)
+            mine = torch.tensor(list(handle), dtype=torch.uint8, device=dev)
             out = [torch.zeros_like(mine) for _ in range(self.world)]
             dist.all_gather(out, mine, group=group)
-            handles = [bytes(t.tolist()) for t in out]
+            handles = [bytes(t.cpu().tolist()) for t in out]
         engine.xchg_connect(handles=handles if self.world > 1 else None,
                             dev_ptrs=None if self.world > 1 else [ptr])
         table = getattr(engine, "_table", None)
         local_max = max((int(p.arrival_step) for p in table), default=0) if table is not None else 0
-        t = torch.tensor([local_max], dtype=torch.int64)
+        t = torch.tensor([local_max], dtype=torch.int64, device=dev)
         if self.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
             dist.barrier(group=group)  # every buffer is zeroed and mapped before any peer writes

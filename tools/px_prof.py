@@ -32,6 +32,7 @@ r = peer_overhead.run(W, per, reps=1)
 p = captured[0]
 waves = r["waves"]
 names = ["admission", "load jobs", "segment scan", "entries", "publish+wait", "read headers+stage", "merge scan",
-         "runs+sum", "want scan", "per-job targets", "work lists"]
+         "runs+sum", "tables (to targets)", "per-job targets", "work lists", "(warp) headers", "(warp) entry loads",
+         "(warp) seg scan", "(warp) merged+scores", "(warp) sums+want", "(warp) run bases"]
 for i, nm in enumerate(names):
     print(f"{nm:20s} {p[i] / max(1, waves) / 1e3:8.2f} us/wave")
