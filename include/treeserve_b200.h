@@ -201,7 +201,9 @@ int ts_run(ts_engine* eng, int32_t max_steps, ts_run_stats* stats_out, void* str
  * last_arrival_global = the largest arrival_step of the whole run queue).
  * ts_run_sharded is ts_run's device-driven graph loop with the exchange
  * inside; stats_out->steps is the global wave count.  A peer that stops
- * signalling for 20 s fails the call with TS_CUDA instead of hanging. */
+ * signalling for 20 s fails the call with TS_CUDA instead of hanging.
+ * Checked mode, the trace and the cost-model clock are ts_run features
+ * (TS_INVALID_ARGUMENT here). */
 int64_t ts_xchg_bytes(int32_t n_global);
 int ts_xchg_create(ts_engine* eng, int32_t world, int32_t rank, void** dev_ptr_out, uint8_t* ipc_handle_out);
 int ts_xchg_connect(ts_engine* eng, const uint8_t* ipc_handles, void* const* dev_ptrs);

@@ -6831,6 +6831,10 @@ int ts_run_sharded(ts_engine* e, int32_t max_steps, int32_t last_arrival_global,
   if (!e->xconnected || e->xbytes != xchg_bytes(e->n_global))
     return fail(e, TS_INVALID_ARGUMENT, "exchange not connected for this run queue (ts_xchg_create/connect)");
   if (max_steps < 0) return fail(e, TS_INVALID_ARGUMENT, "max_steps must be >= 0");
+  if (e->checks || e->trace || e->cost_cap > 0)
+    return fail(e, TS_INVALID_ARGUMENT,
+                "ts_run_sharded: checked mode, the allocation trace and the cost-model clock are single-engine "
+                "features (ts_run)");
   cudaStream_t s = (cudaStream_t)stream;
   int rc;
   ++e->xgen;
