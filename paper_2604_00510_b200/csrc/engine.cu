@@ -98,6 +98,11 @@ struct Counters {
   // returns at once), (unused), a peer timed out (1) or the score sum needs the sequential loop (2)
   int px_done, px_blocks, px_err, px_gen;  // px_gen: the batch generation (epochs of the flags)
   int px_last_arrival, _pad4;              // the run queue's last arrival step (admission exchange)
+  // free-running waves (see k_sched): on for this pass, its first step, the
+  // waves it covers, the next (search, chunk) item; scheduler passes so far
+  int free_run, free_t0, free_rem, _pad5;
+  unsigned long long free_next;
+  long long passes;
 };
 
 // Kernel-side view of one engine.
@@ -129,6 +134,8 @@ struct View {
   const double* log1p_tab; // log1p(k) computed by the host libm, k < log1p_n
   int32_t log1p_n;
   int32_t checks;          // ts_engine_set_checks: invariant kernels around every wave
+  int32_t free_ok;         // free-running waves allowed (k_sched decides per pass); see k_sched
+  int32_t* fdone;          // free-running: chunks of a search's rollouts done
   ts_trace_row* trace;     // ts_engine_set_trace: allocation rows of every pass (null: off)
   long long trace_cap;
   // ts_engine_set_cost_model (cost_cap 0: off)
@@ -3391,6 +3398,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
       c->work_next = 0;
       c->heavy_count = 0;
       c->heavy_next = 0;
+      c->free_run = 0;
       if (use_cond) cudaGraphSetConditional(cond, 0);
 #ifdef TS_SCHED_PROF
       c->prof[30] = 1;
@@ -3496,28 +3504,67 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
     const int wt = lane < SCHED_W ? s_wcnt[lane] : 0;
     int pos = __reduce_add_sync(FULL, lane < wid ? wt : 0);
     const int total = __reduce_add_sync(FULL, wt);
+    __shared__ int s_cmin, s_cmax;
+    if (threadIdx.x == 0) { s_cmin = 0x7FFFFFFF; s_cmax = -1; }
+    __syncthreads();
+    int cmin = 0x7FFFFFFF, cmax = -1;
     for (int j0 = c0; j0 < c1; j0 += 32) {
       const int j = j0 + lane;
       const bool run = j < c1 && (srec[j].flags & 1u);
       const unsigned b = __ballot_sync(FULL, run);
-      if (run) v.work[pos + __popc(b & ((1u << lane) - 1u))] = wlo + j;
+      if (run) {
+        v.work[pos + __popc(b & ((1u << lane) - 1u))] = wlo + j;
+        const int done = (int)srec[j]._pad;  // completed_rollouts
+        cmin = min(cmin, done);
+        cmax = max(cmax, done);
+        if (v.free_ok) v.fdone[wlo + j] = 0;
+      }
       if (j < c1) v.tgt[wlo + j] = run ? 1 : 0;
       pos += __popc(b);
     }
+    cmin = __reduce_min_sync(FULL, cmin);
+    cmax = __reduce_max_sync(FULL, cmax);
+    if (lane == 0) {
+      atomicMin(&s_cmin, cmin);
+      atomicMax(&s_cmax, cmax);
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
       c->work_count = total;
       c->work_next = 0;
       c->heavy_count = 0;
       c->heavy_next = 0;
       c->cur_step = step;
+      // Free-running waves.  When every search is admitted, nobody can exit
+      // before its budget (no positive/negative exit; the trees are too deep
+      // to be exhausted within the budget, v.free_ok) and the next passes can
+      // only give P = 1 again (boosting off, or no free slot while every
+      // running search has the same remaining budget, so that nobody exits
+      // before the others), each search's remaining waves are one rollout each
+      // and independent of every other search: the wave kernel runs them back
+      // to back, each search's rollouts in wave order (step = t0 + r), without
+      // a scheduler pass or a grid-wide barrier per wave.
+      const int rem = cf.rollout_budget - s_cmin;
+      const bool freerun = v.free_ok && total > 0 && c->head == (long long)v.n_local && rem > 0 &&
+                           (cf.boosting_enabled == 0 ||
+                            ((long long)cf.max_concurrency - c->running <= 0 && s_cmin == s_cmax)) &&
+                           (long long)step + rem <= c->max_steps;
+      c->free_run = freerun ? 1 : 0;
+      if (freerun) {
+        c->free_t0 = step;
+        c->free_rem = rem;
+        c->free_next = 0;
+      }
     }
     SP_MARK(9, sp_t);
   } else {
+    if (threadIdx.x == 0) c->free_run = 0;
     targets_block(v, step, srec, nw, 0, nw, wlo);
   }
   if (threadIdx.x == 0) {
     c->win_lo = s_min;  // no running search below this index
-    c->step = step + 1;
+    c->step = c->free_run ? step + c->free_rem : step + 1;
+    c->passes += 1;
 #ifdef TS_SCHED_PROF
     c->prof[10] += 1;
     c->prof[20] = 0;
@@ -4025,6 +4072,47 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
 
 
 
+// Free-running waves (k_sched decides): items (search, chunk of FREE_C
+// rollouts) in chunk-major order; a warp runs an item's rollouts as single-
+// rollout waves at steps t0 + r after the search's previous chunk is done
+// (acquire), then publishes its own (release).  Items of one chunk level
+// outnumber the resident warps, so a predecessor has normally finished long
+// before its successor is taken.
+constexpr int FREE_C = 4;
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int x;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+  return x;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int x) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
+}
+template <int NSLOT, int WT>
+__device__ void free_run_waves(const View& v, WaveStats& ws, double* s_raw, double* s_rew) {
+  const int lane = threadIdx.x & 31;
+  Counters* c = v.ctr;
+  const int nw = c->work_count, t0 = c->free_t0, rem = c->free_rem;
+  const int nch = (rem + FREE_C - 1) / FREE_C;
+  const unsigned long long total = (unsigned long long)nw * (unsigned long long)nch;
+  for (;;) {
+    unsigned long long it = 0;
+    if (lane == 0) it = atomicAdd(&c->free_next, 1ull);
+    it = __shfl_sync(FULL, it, 0);
+    if (it >= total) break;
+    const int k = (int)(it / (unsigned long long)nw), s = v.work[it % (unsigned long long)nw];
+    if (lane == 0)
+      while (ld_acquire_gpu(v.fdone + s) < k) __nanosleep(64);
+    __syncwarp();
+    const int r1 = min(rem, (k + 1) * FREE_C);
+    for (int r = k * FREE_C; r < r1; ++r) {
+      if (v.st[s].state != ST_RUNNING) break;
+      search_wave<NSLOT, WT>(v, s, t0 + r, ws, s_raw, s_rew);
+      __syncwarp();
+    }
+    if (lane == 0) st_release_gpu(v.fdone + s, k + 1);
+  }
+}
+
 template <int NSLOT, int WT>
 #ifndef TS_WAVE_MINB
 #define TS_WAVE_MINB 4  // resident CTAs of 4 warps per SM the register budget is sized for
@@ -4039,6 +4127,9 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
 #ifdef TS_SCHED_PROF
   if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
 #endif
+  if (step < 0 && v.free_ok && v.ctr->free_run) {
+    free_run_waves<NSLOT, WT>(v, ws, s_raw, s_rew);
+  } else {
   const int count = v.ctr->work_count;
   if (step < 0) step = v.ctr->cur_step;
   // the first item of every warp is its global warp index (no burst of
@@ -4049,6 +4140,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
     search_wave<NSLOT, WT>(v, v.work[item], step, ws, s_raw, s_rew);
     if (lane == 0) item = nwarps + atomicAdd(&v.ctr->work_next, 1);
     item = __shfl_sync(FULL, item, 0);
+  }
   }
 #ifdef TS_SCHED_PROF
   if (lane == 0) atomicMax(&v.ctr->prof[20], globaltimer());
@@ -5575,6 +5667,10 @@ struct ts_engine {
   cudaGraphExec_t px_exec = nullptr;
   View px_view;
   int px_max_steps = -1;
+  bool free_ok = false;          // free-running waves allowed for the loaded batch (see k_sched)
+  bool free_off = false;         // TS_NO_FREE=1 (diagnostics)
+  int32_t* fdone = nullptr;      // n_local: chunks of a search's rollouts done (free-running waves)
+  int fdone_cap = 0;
   bool px_two_kernels = false;  // TS_PX_TWO_KERNELS=1: k_px_groups + k_px_sched instead of k_px_step (diagnostics)
   int px_gwarp = 32;            // TS_PX_GWARP: k_px_step's one-warp scheduler up to this many group entries
 };
@@ -5642,6 +5738,9 @@ View make_view(ts_engine* e) {
   v.log1p_tab = e->log1p_tab;
   v.log1p_n = e->log1p_n;
   v.checks = e->checks;
+  v.free_ok = (e->free_ok && !e->checks && !e->trace && !(e->cost_cap > 0 && e->cost_snap && e->cost_n >= e->n_local))
+                  ? 1 : 0;
+  v.fdone = e->fdone;
   v.trace = e->trace;
   v.trace_cap = e->trace_cap;
   if (e->cost_cap > 0 && e->cost_snap && e->cost_n >= e->n_local) {
@@ -6187,6 +6286,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     e->heavy_sync = env2 && env2[0] == '1';
     const char* env5 = getenv("TS_NO_GRAPH");  // host-driven stepping (diagnostics: ncu cannot see graph kernels)
     e->graph_failed = env5 && env5[0] == '1';
+    const char* envf = getenv("TS_NO_FREE");
+    e->free_off = envf && envf[0] == '1';
     const char* env8 = getenv("TS_PX_TWO_KERNELS");
     e->px_two_kernels = env8 && env8[0] == '1';
     const char* env9 = getenv("TS_PX_GWARP");
@@ -6208,7 +6309,7 @@ int ts_engine_destroy(ts_engine* e) {
                   e->arrival, e->ctr, e->work, e->sp, e->ss, e->sl, e->log1p_tab, e->step_times,
                   e->g_runS, e->g_runStart, e->g_runWant, e->g_runPW, e->counts, e->records, e->outcomes,
                   e->work_heavy, e->mt, e->tgt, e->nrec, e->trace, e->cost_snap, e->sim_done,
-                  e->clock_at};
+                  e->clock_at, e->fdone};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : e->wave_ev) cudaEventDestroy(ev);
@@ -6246,6 +6347,27 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   }
   e->max_arrival = prev_arr;
   e->nslot = max_len <= 8 ? 1 : max_len <= 16 ? 2 : 4;
+  {
+    // Exhausting a root needs every node of depth Dmin-1 = min(base_depth,
+    // depth_cap)-1 expanded (nodes above never become terminal or forced),
+    // one per rollout: impossible within the budget if budget < w^(Dmin-1).
+    int wmin = TS_MAX_WIDTH, dmin = TS_MAX_DEPTH;
+    for (int i = 0; i < n_local; ++i) {
+      wmin = std::min(wmin, std::min(c.expand_width, hp[i].branching));
+      dmin = std::min(dmin, std::min(c.depth_cap, hp[i].base_depth));
+    }
+    double need = 1.0;
+    for (int d = 1; d < dmin; ++d) need *= (double)wmin;
+    e->free_ok = !e->free_off && !c.positive_exit && !c.negative_exit && wmin >= 2 &&
+                 (double)c.rollout_budget < need && n_global == n_local;
+    if (e->fdone_cap < n_local) {
+      if (e->fdone) cudaFree(e->fdone);
+      e->fdone = nullptr;
+      e->fdone_cap = 0;
+      TS_CUDA_TRY(e, cudaMalloc((void**)&e->fdone, sizeof(int32_t) * (size_t)std::max(1, n_local)));
+      e->fdone_cap = n_local;
+    }
+  }
   {
     int w0 = std::min(c.expand_width, hp[0].branching);
     bool same = true;
@@ -6467,7 +6589,7 @@ static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cu
   if ((rc = ensure_log1p(e, 1 << 16, s))) return rc;
   if ((rc = ensure_step_times(e, e->log1p_n + 1, s))) return rc;
   Counters c;
-  long long step0 = 0;  // device step count before this graph launch
+  long long step0 = 0;  // device scheduler-pass count before this graph launch
   for (;;) {
     k_set_max_steps<<<1, 1, 0, s>>>(e->ctr, max_steps);
     TS_LAUNCH_CHECK(e, "k_set_max_steps");
@@ -6513,10 +6635,10 @@ static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cu
     if (graphed) {
       // every iteration runs graph_unroll passes of {k_sched, k_wave[, k_heavy]}; the
       // last one contains the pass that ended the loop
-      const long long iters = (c.step - step0) / e->graph_unroll + 1;
+      const long long iters = (c.passes - step0) / e->graph_unroll + 1;
       e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.checks ? 2 : 0) + (v.trace ? 1 : 0) + (v.cost_cap ? 3 : 0));
     }
-    step0 = c.step;
+    step0 = c.passes;
     if (c.finished >= e->n_local || c.step >= max_steps) break;
     // the log1p table bounds the device loop: grow it and continue
     if ((rc = ensure_log1p(e, e->log1p_n * 2, s))) return rc;

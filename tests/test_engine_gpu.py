@@ -531,3 +531,47 @@ def test_graph_loop_variants_match_oracle(unroll, no_graph, monkeypatch):
             _cmp_outcomes(eng.outcomes(), ref.outcomes, f"unroll{unroll}{'-nograph' if no_graph else ''}#{rep}")
             assert st.steps == ref.steps and st.rollouts == ref.stats.rollouts
     ref.close()
+
+
+@pytest.mark.parametrize("case", ["boost_on_full_queue", "boost_off_arrivals"])
+def test_free_running_waves(case, monkeypatch):
+    """Free-running waves (k_sched: every search admitted, no exit before the
+    budget, the next passes can only give P = 1) == the same batch with a
+    scheduler pass per wave (TS_NO_FREE=1) == the C oracle: every outcome field
+    (exit_step and admit_step included), the wave count, and trees node by node."""
+    from paper_2604_00510_b200 import backend as B
+    from paper_2604_00510_b200.config import SearchConfig
+    from paper_2604_00510_b200.scheduler import SchedulerConfig
+
+    n = 512
+    specs = B.make_workload(n, (0.6, 0.25, 0.15), 17, branching=4, depth_ranges={d: (15, 15) for d in B.Difficulty})
+    if case == "boost_on_full_queue":  # M = run queue: no free slot, every search advances in lockstep
+        cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=n), rollout_budget=64, depth_cap=16,
+                           expand_width=4, positive_exit=False, negative_exit=False)
+        t = B.problem_table(specs)
+    else:  # boosting off, staggered arrivals: free once the last search is admitted, unequal remaining budgets
+        cfg = SearchConfig(scheduler=SchedulerConfig(max_concurrency=4 * n, boosting_enabled=False),
+                           rollout_budget=48, depth_cap=16, expand_width=4, positive_exit=False,
+                           negative_exit=False)
+        t = B.problem_table(specs)
+        for i in range(n):
+            t[i].arrival_step = (i * 20) // n
+    runs = {}
+    for mode in ("free", "per_wave"):
+        if mode == "per_wave":
+            monkeypatch.setenv("TS_NO_FREE", "1")
+        with _engine(cfg) as eng:
+            eng.load(t)
+            st = eng.run()
+            runs[mode] = (st, eng.outcomes(), [eng.tree(i) for i in (0, n // 2, n - 1)])
+    (sf, of, tf), (sw, ow, tw) = runs["free"], runs["per_wave"]
+    assert sf.kernel_launches * 2 < sw.kernel_launches  # the free-running path was taken
+    assert (sf.steps, sf.rollouts, sf.nodes, sf.tokens) == (sw.steps, sw.rollouts, sw.nodes, sw.tokens)
+    _cmp_outcomes(of, ow, case)
+    for a, b in zip(tf, tw):
+        assert_tree_equal(a, b, case)
+    ref = oracle.OracleRun(t, cfg.to_c(), threads=8)
+    _cmp_outcomes(of, ref.outcomes, case)
+    assert sf.steps == ref.steps
+    assert_tree_equal(tf[1], ref.tree(n // 2), case)
+    ref.close()
