@@ -135,6 +135,7 @@ struct View {
   int32_t log1p_n;
   int32_t checks;          // ts_engine_set_checks: invariant kernels around every wave
   int32_t free_ok;         // free-running waves allowed (k_sched decides per pass); see k_sched
+  int32_t free_kernel;     // the graph runs them in k_wave_free (else k_wave does)
   int32_t* fdone;          // free-running: chunks of a search's rollouts done
   ts_trace_row* trace;     // ts_engine_set_trace: allocation rows of every pass (null: off)
   long long trace_cap;
@@ -3599,7 +3600,7 @@ constexpr int WAVE_WARPS = WAVE_THREADS / 32;
 // prefix aggregate, golden flag, chosen child index), so registration and a
 // single-rollout backup are pure stores, and subtree exhaustion propagates up
 // the path without loads.  WT = compile-time width (0: runtime, <= 32).
-template <int NSLOT, int WT>
+template <int NSLOT, int WT, bool SINGLE = false>
 __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, double* s_raw, double* s_rew) {
   constexpr int WS = WT ? WT : TS_MAX_WIDTH;  // shared-memory row stride
   const int lane = threadIdx.x & 31;
@@ -3641,8 +3642,10 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
   int launched = S->launched, cancelled = S->cancelled;
   int status = TS_OK;
   const int budget = cf.rollout_budget;
-  const int count = min(v.tgt[s], budget - completed);
-  const bool multi = count > 1;
+  // SINGLE: one rollout this wave (free-running waves), the multi-rollout
+  // bookkeeping compiled out
+  const int count = SINGLE ? min(1, budget - completed) : min(v.tgt[s], budget - completed);
+  const bool multi = !SINGLE && count > 1;
   int32_t* SPs = v.sp + (size_t)s * (size_t)budget * 32;
   double* SSs = v.ss + (size_t)s * budget;
   int32_t* SLs = v.sl + (size_t)s * budget;
@@ -4087,7 +4090,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void st_release_gpu(int* p, int x) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
 }
-template <int NSLOT, int WT>
+template <int NSLOT, int WT, bool SINGLE>
 __device__ void free_run_waves(const View& v, WaveStats& ws, double* s_raw, double* s_rew) {
   const int lane = threadIdx.x & 31;
   Counters* c = v.ctr;
@@ -4106,7 +4109,7 @@ __device__ void free_run_waves(const View& v, WaveStats& ws, double* s_raw, doub
     const int r1 = min(rem, (k + 1) * FREE_C);
     for (int r = k * FREE_C; r < r1; ++r) {
       if (v.st[s].state != ST_RUNNING) break;
-      search_wave<NSLOT, WT>(v, s, t0 + r, ws, s_raw, s_rew);
+      search_wave<NSLOT, WT, SINGLE>(v, s, t0 + r, ws, s_raw, s_rew);
       __syncwarp();
     }
     if (lane == 0) st_release_gpu(v.fdone + s, k + 1);
@@ -4128,7 +4131,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
   if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
 #endif
   if (step < 0 && v.free_ok && v.ctr->free_run) {
-    free_run_waves<NSLOT, WT>(v, ws, s_raw, s_rew);
+    if (!v.free_kernel) free_run_waves<NSLOT, WT, false>(v, ws, s_raw, s_rew);
   } else {
   const int count = v.ctr->work_count;
   if (step < 0) step = v.ctr->cur_step;
@@ -4154,6 +4157,40 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
     atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
   }
 }
+
+// Free-running waves get their own kernel: every wave is one rollout, so the
+// multi-rollout bookkeeping is compiled out (search_wave<..., SINGLE>) and 5
+// CTAs of 4 warps fit per SM (96 registers) where k_wave keeps 4.
+#ifndef TS_FREE_MINB
+#define TS_FREE_MINB 5
+#endif
+template <int NSLOT, int WT>
+__global__ void __launch_bounds__(WAVE_THREADS, TS_FREE_MINB) k_wave_free(View v) {
+  constexpr int WS = WT ? WT : TS_MAX_WIDTH;
+  extern __shared__ double wsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (!(v.free_ok && v.ctr->free_run)) return;
+  double* s_raw = wsm + (size_t)warp * 2 * 32 * WS;
+  double* s_rew = s_raw + 32 * WS;
+  WaveStats ws = {0, 0, 0, 0, 0, 0};
+  free_run_waves<NSLOT, WT, true>(v, ws, s_raw, s_rew);
+  if (lane == 0 && ws.launched) {
+    atomicAdd(&v.ctr->rollouts, ws.rollouts);
+    atomicAdd(&v.ctr->launched, ws.launched);
+    atomicAdd(&v.ctr->nodes, ws.nodes);
+    atomicAdd(&v.ctr->scored, ws.scored);
+    atomicAdd(&v.ctr->levels, ws.levels);
+    atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
+  }
+}
+static const void* kWaveFree[3][4] = {
+    {(const void*)k_wave_free<1, 2>, (const void*)k_wave_free<1, 4>, (const void*)k_wave_free<1, 8>,
+     (const void*)k_wave_free<1, 0>},
+    {(const void*)k_wave_free<2, 2>, (const void*)k_wave_free<2, 4>, (const void*)k_wave_free<2, 8>,
+     (const void*)k_wave_free<2, 0>},
+    {(const void*)k_wave_free<4, 2>, (const void*)k_wave_free<4, 4>, (const void*)k_wave_free<4, 8>,
+     (const void*)k_wave_free<4, 0>},
+};
 
 // kernel table: [nslot 1/2/4][width 2/4/8/runtime]
 typedef void (*wave_kernel_t)(View, int);
@@ -5669,6 +5706,7 @@ struct ts_engine {
   int px_max_steps = -1;
   bool free_ok = false;          // free-running waves allowed for the loaded batch (see k_sched)
   bool free_off = false;         // TS_NO_FREE=1 (diagnostics)
+  bool free_kernel_off = false;  // TS_NO_FREE_KERNEL=1: k_wave runs the free-running waves itself (diagnostics)
   int32_t* fdone = nullptr;      // n_local: chunks of a search's rollouts done (free-running waves)
   int fdone_cap = 0;
   bool px_two_kernels = false;  // TS_PX_TWO_KERNELS=1: k_px_groups + k_px_sched instead of k_px_step (diagnostics)
@@ -5741,6 +5779,7 @@ View make_view(ts_engine* e) {
   v.free_ok = (e->free_ok && !e->checks && !e->trace && !(e->cost_cap > 0 && e->cost_snap && e->cost_n >= e->n_local))
                   ? 1 : 0;
   v.fdone = e->fdone;
+  v.free_kernel = (v.free_ok && !e->graph_failed && !e->free_kernel_off) ? 1 : 0;
   v.trace = e->trace;
   v.trace_cap = e->trace_cap;
   if (e->cost_cap > 0 && e->cost_snap && e->cost_n >= e->n_local) {
@@ -5964,6 +6003,7 @@ int build_run_graph(ts_engine* e, const View& v) {
   k1.sharedMemBytes = (unsigned)sched_smem();
   k1.kernelParams = a1;
   void* a2[] = {(void*)&vv, (void*)&stepm1};
+  void* a4f[] = {(void*)&vv};
   cudaKernelNodeParams k2;
   memset(&k2, 0, sizeof(k2));
   k2.func = wave_fn(e);
@@ -5971,6 +6011,16 @@ int build_run_graph(ts_engine* e, const View& v) {
   k2.blockDim = dim3(WAVE_THREADS);
   k2.sharedMemBytes = (unsigned)wave_smem_of(e->wkind);
   k2.kernelParams = a2;
+  cudaKernelNodeParams kf = k2;
+  if (v.free_kernel) {
+    const int k = wave_index(e);
+    const void* f = kWaveFree[k / 4][k % 4];
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, WAVE_THREADS, wave_smem_of(e->wkind));
+    kf.func = (void*)f;
+    kf.gridDim = dim3(std::max(1, per) * e->sm_count);
+    kf.kernelParams = a4f;
+  }
   cudaKernelNodeParams k3 = k2;
   if (v.heavy_on) {
     int hb = 0;
@@ -6027,6 +6077,11 @@ int build_run_graph(ts_engine* e, const View& v) {
     TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n2, body, &n1, 1, &k2));
     prev[0] = n2;
     nprev = 1;
+    if (v.free_kernel) {
+      cudaGraphNode_t nf;
+      TS_CUDA_TRY(e, cudaGraphAddKernelNode(&nf, body, &n1, 1, &kf));
+      TS_CUDA_TRY(e, cudaGraphAddDependencies(body, &nf, &n2, 1));
+    }
     if (v.heavy_on) {
       TS_CUDA_TRY(e, cudaGraphAddKernelNode(&n3, body, &n1, 1, &k3));
       prev[1] = n3;
@@ -6264,6 +6319,10 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
   }
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
+      cr = cudaFuncSetAttribute(kWaveFree[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)wave_smem_of(b));
+  for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
+    for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
       cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)wave_smem_of(b));
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
@@ -6288,6 +6347,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
     e->graph_failed = env5 && env5[0] == '1';
     const char* envf = getenv("TS_NO_FREE");
     e->free_off = envf && envf[0] == '1';
+    const char* envk = getenv("TS_NO_FREE_KERNEL");
+    e->free_kernel_off = envk && envk[0] == '1';
     const char* env8 = getenv("TS_PX_TWO_KERNELS");
     e->px_two_kernels = env8 && env8[0] == '1';
     const char* env9 = getenv("TS_PX_GWARP");
@@ -6358,8 +6419,11 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
     }
     double need = 1.0;
     for (int d = 1; d < dmin; ++d) need *= (double)wmin;
+    // with boosting on, P = 1 for every running search needs no free slot: a
+    // run queue smaller than max_concurrency never free-runs
     e->free_ok = !e->free_off && !c.positive_exit && !c.negative_exit && wmin >= 2 &&
-                 (double)c.rollout_budget < need && n_global == n_local;
+                 (double)c.rollout_budget < need && n_global == n_local &&
+                 (!c.boosting_enabled || (long long)c.max_concurrency <= (long long)n_local);
     if (e->fdone_cap < n_local) {
       if (e->fdone) cudaFree(e->fdone);
       e->fdone = nullptr;
@@ -6636,7 +6700,8 @@ static int run_impl(ts_engine* e, int32_t max_steps, ts_run_stats* stats_out, cu
       // every iteration runs graph_unroll passes of {k_sched, k_wave[, k_heavy]}; the
       // last one contains the pass that ended the loop
       const long long iters = (c.passes - step0) / e->graph_unroll + 1;
-      e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.checks ? 2 : 0) + (v.trace ? 1 : 0) + (v.cost_cap ? 3 : 0));
+      e->launches += iters * e->graph_unroll * ((v.heavy_on ? 3 : 2) + (v.free_kernel ? 1 : 0) + (v.checks ? 2 : 0) +
+                                                (v.trace ? 1 : 0) + (v.cost_cap ? 3 : 0));
     }
     step0 = c.passes;
     if (c.finished >= e->n_local || c.step >= max_steps) break;

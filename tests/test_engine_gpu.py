@@ -557,19 +557,27 @@ def test_free_running_waves(case, monkeypatch):
         for i in range(n):
             t[i].arrival_step = (i * 20) // n
     runs = {}
-    for mode in ("free", "per_wave"):
-        if mode == "per_wave":
-            monkeypatch.setenv("TS_NO_FREE", "1")
+    # k_wave_free (single-rollout kernel), the same waves inside k_wave, host-driven passes, one pass per wave
+    envs = {"free": {}, "free_in_k_wave": {"TS_NO_FREE_KERNEL": "1"}, "host_driven": {"TS_NO_GRAPH": "1"},
+            "per_wave": {"TS_NO_FREE": "1"}}
+    for mode, env in envs.items():
+        for k in ("TS_NO_FREE_KERNEL", "TS_NO_GRAPH", "TS_NO_FREE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, val in env.items():
+            monkeypatch.setenv(k, val)
         with _engine(cfg) as eng:
             eng.load(t)
             st = eng.run()
             runs[mode] = (st, eng.outcomes(), [eng.tree(i) for i in (0, n // 2, n - 1)])
-    (sf, of, tf), (sw, ow, tw) = runs["free"], runs["per_wave"]
+    sf, of, tf = runs["free"]
+    sw = runs["per_wave"][0]
     assert sf.kernel_launches * 2 < sw.kernel_launches  # the free-running path was taken
-    assert (sf.steps, sf.rollouts, sf.nodes, sf.tokens) == (sw.steps, sw.rollouts, sw.nodes, sw.tokens)
-    _cmp_outcomes(of, ow, case)
-    for a, b in zip(tf, tw):
-        assert_tree_equal(a, b, case)
+    for mode in ("free_in_k_wave", "host_driven", "per_wave"):
+        so, oo, to = runs[mode]
+        assert (sf.steps, sf.rollouts, sf.nodes, sf.tokens) == (so.steps, so.rollouts, so.nodes, so.tokens), mode
+        _cmp_outcomes(of, oo, f"{case}/{mode}")
+        for a, b in zip(tf, to):
+            assert_tree_equal(a, b, f"{case}/{mode}")
     ref = oracle.OracleRun(t, cfg.to_c(), threads=8)
     _cmp_outcomes(of, ref.outcomes, case)
     assert sf.steps == ref.steps
