@@ -1656,6 +1656,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
   if (tid == 0) px_stamp(v, step, 0);
 #ifdef TS_PX_PROF
   unsigned long long pp_t = globaltimer();
+  long long pp_c = clock64();
 #define PX_MARK(slot)                                                   \
   do {                                                                  \
     __syncthreads();                                                    \
@@ -1669,9 +1670,9 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
   do {                                                                  \
     __syncwarp();                                                       \
     if (tid == 0) {                                                     \
-      const unsigned long long t_ = globaltimer();                      \
-      atomicAdd(&v.ctr->prof[slot], t_ - pp_t);                         \
-      pp_t = t_;                                                        \
+      const long long c_ = clock64();                                   \
+      if (slot > 11) atomicAdd(&v.ctr->prof[slot], (unsigned long long)(c_ - pp_c)); \
+      pp_c = c_;                                                        \
     }                                                                   \
   } while (0)
 #else

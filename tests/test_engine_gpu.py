@@ -101,13 +101,19 @@ def test_wave_goldens(name):
                 assert getattr(outs[i], k) == want[k], (name, i, k)
         for idx, tree in case["trees"].items():
             assert_tree_equal(eng.tree(int(idx)), tree, f"{name}[{idx}]")
-    # the one-call run path agrees with the stepwise one
+    # the one-call run path (the CUDA-graph loop the bench times) agrees with
+    # the reference on every per-wave field and on the trees too
     with _engine(cfg) as eng:
         eng.load(table(recs, case["arrival_steps"]))
         st = eng.run()
         assert st.steps == case["steps"]
+        outs = eng.outcomes()
         for i, want in enumerate(case["outcomes"]):
-            assert outcome_dict(eng.outcomes()[i]) == {k: want[k] for k in outcome_dict(eng.outcomes()[i])}
+            assert outcome_dict(outs[i]) == {k: want[k] for k in outcome_dict(outs[i])}
+            for k in WAVE_KEYS:
+                assert getattr(outs[i], k) == want[k], (name, "graph", i, k)
+        for idx, tree in case["trees"].items():
+            assert_tree_equal(eng.tree(int(idx)), tree, f"{name}[{idx}] graph")
 
 
 def test_compute_targets_kats():

@@ -35,4 +35,7 @@ names = ["admission", "load jobs", "segment scan", "entries", "publish+wait", "r
          "runs+sum", "tables (to targets)", "per-job targets", "work lists", "(warp) headers", "(warp) entry loads",
          "(warp) seg scan", "(warp) merged+scores", "(warp) sums+want", "(warp) run bases"]
 for i, nm in enumerate(names):
-    print(f"{nm:20s} {p[i] / max(1, waves) / 1e3:8.2f} us/wave")
+    if i < 12:
+        print(f"{nm:20s} {p[i] / max(1, waves) / 1e3:8.2f} us/wave")
+    else:  # the one-warp sub-phases are clock64 cycles
+        print(f"{nm:20s} {p[i] / max(1, waves):8.0f} cycles/wave")
