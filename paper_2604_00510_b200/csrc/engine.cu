@@ -3578,7 +3578,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
 
 // ---- the wave: one warp per running search ----------------------------------
 struct WaveStats {
-  unsigned long long rollouts, launched, nodes, scored, levels, path_nodes;
+  unsigned long long rollouts, launched, nodes, scored, levels, path_nodes, tokens;
 };
 
 constexpr int WAVE_THREADS = 128;
@@ -4048,7 +4048,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     S->best_term = best_term;
     S->best = best;
     S->tokens += tok_acc;
-    atomicAdd(&v.ctr->tokens, (unsigned long long)tok_acc);
+    ws.tokens += (unsigned long long)tok_acc;  // Counters::tokens once per warp at the kernel's end
     S->launched = launched;
     S->cancelled = cancelled;
     // on_rollout_complete (scheduler.py:217-233): refresh Job.best_score
@@ -4127,7 +4127,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* s_raw = wsm + (size_t)warp * 2 * 32 * WS;
   double* s_rew = s_raw + 32 * WS;
-  WaveStats ws = {0, 0, 0, 0, 0, 0};
+  WaveStats ws = {0, 0, 0, 0, 0, 0, 0};
 #ifdef TS_SCHED_PROF
   if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
 #endif
@@ -4156,6 +4156,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
     atomicAdd(&v.ctr->scored, ws.scored);
     atomicAdd(&v.ctr->levels, ws.levels);
     atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
+    if (ws.tokens) atomicAdd(&v.ctr->tokens, ws.tokens);
   }
 }
 
@@ -4173,7 +4174,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_FREE_MINB) k_wave_free(View v
   if (!(v.free_ok && v.ctr->free_run)) return;
   double* s_raw = wsm + (size_t)warp * 2 * 32 * WS;
   double* s_rew = s_raw + 32 * WS;
-  WaveStats ws = {0, 0, 0, 0, 0, 0};
+  WaveStats ws = {0, 0, 0, 0, 0, 0, 0};
   free_run_waves<NSLOT, WT, true>(v, ws, s_raw, s_rew);
   if (lane == 0 && ws.launched) {
     atomicAdd(&v.ctr->rollouts, ws.rollouts);
@@ -4182,6 +4183,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_FREE_MINB) k_wave_free(View v
     atomicAdd(&v.ctr->scored, ws.scored);
     atomicAdd(&v.ctr->levels, ws.levels);
     atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
+    if (ws.tokens) atomicAdd(&v.ctr->tokens, ws.tokens);
   }
 }
 static const void* kWaveFree[3][4] = {
@@ -5229,7 +5231,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 2) k_heavy(View v, int step) {
   __shared__ int s_item;
   __shared__ double sqt[SQRT_TAB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WaveStats ws = {0, 0, 0, 0, 0, 0};
+  WaveStats ws = {0, 0, 0, 0, 0, 0, 0};
   const int count_items = v.ctr->heavy_count;
   if (count_items == 0) return;  // most waves have no pipelined-mode search
   if (step < 0) step = v.ctr->cur_step;
@@ -5317,6 +5319,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 2) k_heavy(View v, int step) {
     atomicAdd(&v.ctr->scored, ws.scored);
     atomicAdd(&v.ctr->levels, ws.levels);
     atomicAdd(&v.ctr->path_nodes, ws.path_nodes);
+    if (ws.tokens) atomicAdd(&v.ctr->tokens, ws.tokens);
   }
 }
 
