@@ -4082,7 +4082,10 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
 // (acquire), then publishes its own (release).  Items of one chunk level
 // outnumber the resident warps, so a predecessor has normally finished long
 // before its successor is taken.
-constexpr int FREE_C = 4;
+#ifndef TS_FREE_C
+#define TS_FREE_C 4
+#endif
+constexpr int FREE_C = TS_FREE_C;
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int x;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
