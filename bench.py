@@ -188,6 +188,34 @@ def algorithmic_bytes(st) -> int:
             + B_PATH * st.path_nodes)
 
 
+def issue_roofline(rollouts_per_s: float, rollouts: int):
+    """The throughput regime's real bound: warp-instruction issue.  Instructions
+    per rollout from the newest ncu capture of the exits-off batch's
+    free-running kernel (one launch = the whole batch); peak = 4 schedulers x
+    SMs x the SM clock, one warp-instruction each per cycle."""
+    import torch
+
+    for rnd in ("r02",):
+        path = os.path.join(ROOT, "profiles", f"{rnd}_ncu_full_captures.json")
+        try:
+            with open(path) as f:
+                cap = json.load(f)["k_wave_free_exits_off"]["metrics"]
+        except Exception:
+            continue
+        instr = float(cap["Executed Instructions"].split()[0].replace(",", ""))
+        per = instr / 524288.0  # the captured launch ran the whole 4096 x 128-rollout batch
+        props = torch.cuda.get_device_properties(torch.cuda.current_device())
+        clk = float(cap["SM Frequency"].split()[0]) * 1e9
+        peak = 4.0 * props.multi_processor_count * clk
+        achieved = per * rollouts_per_s
+        return {"bound": "issue", "instr_per_rollout": per, "achieved_warp_instr_per_s": achieved,
+                "peak_warp_instr_per_s": peak, "frac": achieved / peak,
+                "ceiling_rollouts_per_s": peak / per,
+                "source": f"{os.path.relpath(path, ROOT)} (ncu --set full, k_wave_free, "
+                          f"issue slots busy {cap.get('Issue Slots Busy')})"}
+    return None
+
+
 def peer_exchange(eng, table, lo, n_total, d: Dist):
     """The sharded loop over peer memory (PeerShardedRun: one device-driven
     graph per batch, scheduler inputs written straight into every rank's
@@ -382,7 +410,8 @@ def bench_ours(args, d: Dist):
         variant = {"workload": "same 4096 searches, exits off (every search runs 128 rollouts)",
                    "value": st2.rollouts / (ms2 / 1e3), "unit": UNIT, "ms": ms2, "waves": st2.steps,
                    "wave_ms": wms2, "wave_kernel_GBs": b2 / (wms2 / 1e3) / 1e9,
-                   "wave_frac": b2 / (wms2 / 1e3) / 1e9 / hbm}
+                   "wave_frac": b2 / (wms2 / 1e3) / 1e9 / hbm,
+                   "issue_roofline": issue_roofline(st2.rollouts / (ms2 / 1e3), st2.rollouts)}
         eng2.close()
 
     c3 = c3_rollout_step(table, lo, n_total, d, flush, args)

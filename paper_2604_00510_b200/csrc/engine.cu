@@ -5786,7 +5786,7 @@ View make_view(ts_engine* e) {
   v.free_ok = (e->free_ok && !e->checks && !e->trace && !(e->cost_cap > 0 && e->cost_snap && e->cost_n >= e->n_local))
                   ? 1 : 0;
   v.fdone = e->fdone;
-  v.free_kernel = (v.free_ok && !e->graph_failed && !e->free_kernel_off) ? 1 : 0;
+  v.free_kernel = (v.free_ok && !e->free_kernel_off) ? 1 : 0;
   v.trace = e->trace;
   v.trace_cap = e->trace_cap;
   if (e->cost_cap > 0 && e->cost_snap && e->cost_n >= e->n_local) {
@@ -6139,6 +6139,16 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   const int k = wave_index(e);
   kWave[k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
   TS_LAUNCH_CHECK(e, "k_wave");
+  if (v.free_kernel && step < 0) {  // host-driven loop: the free-running waves' kernel (returns unless k_sched chose them)
+    const void* f = kWaveFree[k / 4][k % 4];
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, WAVE_THREADS, wave_smem_of(k % 4));
+    View vf = v;
+    void* args[] = {(void*)&vf};
+    TS_CUDA_TRY(e, cudaLaunchKernel(f, dim3(std::max(1, per) * e->sm_count), dim3(WAVE_THREADS), args,
+                                    wave_smem_of(k % 4), s));
+    TS_LAUNCH_CHECK(e, "k_wave_free");
+  }
   if ((rc = launch_heavy(e, v, step, s))) return rc;
   cudaEventRecord(e->wave_ev[e->wave_ev_used + 1], s);
   e->wave_ev_used += 2;
