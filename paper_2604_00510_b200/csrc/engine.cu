@@ -1746,12 +1746,15 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
   int comp[JPT], arr[JPT], qv[JPT], ent[JPT];
   const int lo = tid * JPT;
   {
-    ulonglong2 w[JPT];
+    // the record each search's wave wrote for this step (write_next_record:
+    // running, ungated, boosted, completed), contiguous 16-byte rows; the
+    // SearchState row only for a stale record or a search admitted now
+    ts_sched_record rr[JPT];
 #pragma unroll
     for (int u = 0; u < JPT; ++u) {
       const int i = lo + u;
       if (i < n) {
-        w[u] = *reinterpret_cast<const ulonglong2*>(v.st + i);  // state, completed, job_best
+        rr[u] = v.nrec[i];
         arr[u] = v.arrival[i];
       }
     }
@@ -1763,22 +1766,35 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
       code[u] = 0;
       comp[u] = 0;
       if (i >= n) continue;
-      int state = (int)(uint32_t)w[u].x;
-      if (i >= alo && i < ahi) {
-        state = ST_RUNNING;
-        v.st[i].state = ST_RUNNING;
-        v.st[i].admit_step = step;
+      const bool adm = i >= alo && i < ahi;
+      const uint32_t tag = rr[u].flags >> 8;
+      bool run, ung, boosted;
+      int done;
+      if (!adm && (tag == (uint32_t)step || tag == NREC_FINAL)) {
+        run = rr[u].flags & 1u;
+        ung = (rr[u].flags & 2u) != 0;
+        boosted = (rr[u].flags & 4u) != 0;
+        done = (int)rr[u]._pad;
+      } else {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(v.st + i);  // state, completed, job_best
+        int state = (int)(uint32_t)w.x;
+        if (adm) {
+          state = ST_RUNNING;
+          v.st[i].state = ST_RUNNING;
+          v.st[i].admit_step = step;
+        }
+        run = state == ST_RUNNING;
+        done = (int)(uint32_t)(w.x >> 32);
+        ung = done >= cf.obs_threshold;
+        boosted = __longlong_as_double((long long)w.y) / cf.positive_exit_threshold > cf.proximity;  // scheduler.py:126
       }
       const int ap = u > 0 ? arr[u - 1] : (i > 0 ? aprev : arr[u]);
       const int an = u + 1 < JPT ? arr[u + 1] : anext;
       if (arr[u] < ap) c->sched_error = 1;
       unsigned cd = (i == 0 || arr[u] != ap) ? 1u : 0u;
       if (i == n - 1 || an != arr[u]) cd |= 16u;
-      if (state == ST_RUNNING) {
-        const int done = (int)(uint32_t)(w[u].x >> 32);
-        const double jb = __longlong_as_double((long long)w[u].y);
-        const bool boosted = jb / cf.positive_exit_threshold > cf.proximity;  // scheduler.py:126
-        cd |= 2u | (done >= cf.obs_threshold ? 4u : 0u) | ((boosted && !fold) ? 8u : 0u);
+      if (run) {
+        cd |= 2u | (ung ? 4u : 0u) | ((boosted && !fold) ? 8u : 0u);
         comp[u] = done;
       }
       code[u] = cd;
