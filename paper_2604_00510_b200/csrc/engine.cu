@@ -3855,22 +3855,27 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       const int l = lane;
       const int len = l + 1;
       const int fcl = fc0 + (l - d0) * width;
-      // raw priors and token counts of this level's children (generate_steps)
-      double rv[WT ? WT : 1];
+      // raw priors and token counts of this level's children (generate_steps);
+      // widths up to 4 keep them in registers with the loops unrolled, wider
+      // levels stage them in shared memory with the loops unrolled by 2 (code
+      // size: config 4's width-8 kernel stalled on instruction fetch)
+      constexpr bool RREG = WT > 0 && WT <= 4;
+      constexpr int UR = RREG ? WT : 2;
+      double rv[RREG ? WT : 1];
       double* rawl = s_raw + l * WS;
-#pragma unroll
+#pragma unroll UR
       for (int i = 0; i < WS; ++i) {
         if (i >= width) break;
         const double x = draw_raw_prior(hp, i);
-        if constexpr (WT > 0) rv[i] = x;
+        if constexpr (RREG) rv[i] = x;
         else rawl[i] = x;
         tok_acc += draw_tokens(hk, i);
       }
-#define rawv(i) pick_raw<WT>(rv, rawl, i)
+#define rawv(i) pick_raw<RREG ? WT : 0>(rv, rawl, i)
       const double* rewl = s_rew + l * WS;
       // total = sum(raw_priors): CPython Neumaier sum in child order
       double tot = rawv(0), cc = 0.0;
-#pragma unroll
+#pragma unroll UR
       for (int i = 1; i < WS; ++i) {
         if (i >= width) break;
         const double x = rawv(i);
@@ -3882,7 +3887,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       if (cc != 0.0 && isfinite(cc)) tot += cc;
       const bool last = l == dend - 1;
       const bool rel_d1 = strict || d1r >= theta1;
-#pragma unroll
+#pragma unroll UR
       for (int j = 0; j < WS; ++j) {
         if (j >= width) break;
         const double rew = rewl[j];
