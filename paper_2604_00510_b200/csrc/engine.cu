@@ -3617,7 +3617,7 @@ constexpr int WAVE_WARPS = WAVE_THREADS / 32;
 // prefix aggregate, golden flag, chosen child index), so registration and a
 // single-rollout backup are pure stores, and subtree exhaustion propagates up
 // the path without loads.  WT = compile-time width (0: runtime, <= 32).
-template <int NSLOT, int WT, bool SINGLE = false>
+template <int NSLOT, int WT, bool SINGLE = false, bool PROD = false>
 __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, double* s_raw, double* s_rew) {
   constexpr int WS = WT ? WT : TS_MAX_WIDTH;  // shared-memory row stride
   const int lane = threadIdx.x & 31;
@@ -3759,7 +3759,12 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       nW = __shfl_sync(FULL, cw, j);
       nQ = __shfl_sync(FULL, cq, j);
       nfc = __shfl_sync(FULL, cfc, j);
-      agg.add(nrew, scheme);
+      if constexpr (PROD) {  // math.prod (scoring.py:113), the scheme fixed at compile time
+        agg.a = agg.a * nrew;
+        ++agg.n;
+      } else {
+        agg.add(nrew, scheme);
+      }
       if (depth == 1) d1r = nrew;
       golden = golden && depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
       if (lane == depth - 1) {
@@ -3780,7 +3785,9 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     for (int k = 0; k < NSLOT; ++k) snap[k] = 0;
     while (true) {
       if (depth >= cf.depth_cap) { forced = true; break; }  // tree.py:340-343
-      if (nnodes + width > v.cap) { status = TS_POOL_OVERFLOW; break; }
+      // (the pool holds every node a search's budget can create, ts_load_problems;
+      // the single-rollout build leaves the check out)
+      if (!SINGLE && nnodes + width > v.cap) { status = TS_POOL_OVERFLOW; break; }
       const int d = depth;
       const int len = d + 1;
       const uint64_t hr = state_at<NSLOT, 1>(h, d);
@@ -3817,7 +3824,12 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
       ++depth;
       nrew = __shfl_sync(FULL, rew, j);
       nmeta = (uint32_t)depth | ((uint32_t)j << SH_REF) | (jterm ? M_TERM : 0u);
-      agg.add(nrew, scheme);
+      if constexpr (PROD) {  // math.prod (scoring.py:113), the scheme fixed at compile time
+        agg.a = agg.a * nrew;
+        ++agg.n;
+      } else {
+        agg.add(nrew, scheme);
+      }
       if (depth == 1) d1r = nrew;
       golden = golden && depth <= glen && gnext == j;
       if (lane == depth - 1) {
@@ -3832,7 +3844,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     const int dend = depth;      // terminal (or force-terminated) node depth
     const int nlev = dend - d0;  // expansions happened at depths d0 .. dend-1
     plen = dend;
-    pscore = agg.value(scheme);
+    pscore = PROD ? agg.a : agg.value(scheme);
 
     // --- deferred expansion batch: lane l writes the children of depth l ---
     // values of path node l (the expanded node) come from lane l-1
@@ -3945,7 +3957,7 @@ __device__ void search_wave(const View& v, int s, int step, WaveStats& ws, doubl
     if (forced) {
       // NE: the force-terminated leaf leaves the leaf set
       const bool rel = strict || d1r >= theta1;
-      const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
+      const double bound = prefix_bound ? fmin(nrew, PROD ? agg.a : agg.value(scheme)) : nrew;
       if (rel && !(bound < tau)) --viable;
     }
     created += (unsigned long long)nlev * width;
@@ -4115,7 +4127,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void st_release_gpu(int* p, int x) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(x) : "memory");
 }
-template <int NSLOT, int WT, bool SINGLE>
+template <int NSLOT, int WT, bool SINGLE, bool PROD = false>
 __device__ void free_run_waves(const View& v, WaveStats& ws, double* s_raw, double* s_rew) {
   const int lane = threadIdx.x & 31;
   Counters* c = v.ctr;
@@ -4134,7 +4146,7 @@ __device__ void free_run_waves(const View& v, WaveStats& ws, double* s_raw, doub
     const int r1 = min(rem, (k + 1) * FREE_C);
     for (int r = k * FREE_C; r < r1; ++r) {
       if (v.st[s].state != ST_RUNNING) break;
-      search_wave<NSLOT, WT, SINGLE>(v, s, t0 + r, ws, s_raw, s_rew);
+      search_wave<NSLOT, WT, SINGLE, PROD>(v, s, t0 + r, ws, s_raw, s_rew);
       __syncwarp();
     }
     if (lane == 0) st_release_gpu(v.fdone + s, k + 1);
@@ -4190,7 +4202,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
 #ifndef TS_FREE_MINB
 #define TS_FREE_MINB 5
 #endif
-template <int NSLOT, int WT>
+template <int NSLOT, int WT, bool PROD>
 __global__ void __launch_bounds__(WAVE_THREADS, TS_FREE_MINB) k_wave_free(View v) {
   constexpr int WS = WT ? WT : TS_MAX_WIDTH;
   extern __shared__ double wsm[];
@@ -4199,7 +4211,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_FREE_MINB) k_wave_free(View v
   double* s_raw = wsm + (size_t)warp * 2 * 32 * WS;
   double* s_rew = s_raw + 32 * WS;
   WaveStats ws = {0, 0, 0, 0, 0, 0, 0};
-  free_run_waves<NSLOT, WT, true>(v, ws, s_raw, s_rew);
+  free_run_waves<NSLOT, WT, true, PROD>(v, ws, s_raw, s_rew);
   if (lane == 0 && ws.launched) {
     atomicAdd(&v.ctr->rollouts, ws.rollouts);
     atomicAdd(&v.ctr->launched, ws.launched);
@@ -4210,14 +4222,15 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_FREE_MINB) k_wave_free(View v
     if (ws.tokens) atomicAdd(&v.ctr->tokens, ws.tokens);
   }
 }
-static const void* kWaveFree[3][4] = {
-    {(const void*)k_wave_free<1, 2>, (const void*)k_wave_free<1, 4>, (const void*)k_wave_free<1, 8>,
-     (const void*)k_wave_free<1, 0>},
-    {(const void*)k_wave_free<2, 2>, (const void*)k_wave_free<2, 4>, (const void*)k_wave_free<2, 8>,
-     (const void*)k_wave_free<2, 0>},
-    {(const void*)k_wave_free<4, 2>, (const void*)k_wave_free<4, 4>, (const void*)k_wave_free<4, 8>,
-     (const void*)k_wave_free<4, 0>},
+// [scheme is product][nslot 1/2/4][width 2/4/8/runtime]
+#define TS_KWF(P, A)                                                                                   \
+  {(const void*)k_wave_free<A, 2, P>, (const void*)k_wave_free<A, 4, P>, (const void*)k_wave_free<A, 8, P>, \
+   (const void*)k_wave_free<A, 0, P>}
+static const void* kWaveFree[2][3][4] = {
+    {TS_KWF(false, 1), TS_KWF(false, 2), TS_KWF(false, 4)},
+    {TS_KWF(true, 1), TS_KWF(true, 2), TS_KWF(true, 4)},
 };
+#undef TS_KWF
 
 // kernel table: [nslot 1/2/4][width 2/4/8/runtime]
 typedef void (*wave_kernel_t)(View, int);
@@ -6042,7 +6055,7 @@ int build_run_graph(ts_engine* e, const View& v) {
   cudaKernelNodeParams kf = k2;
   if (v.free_kernel) {
     const int k = wave_index(e);
-    const void* f = kWaveFree[k / 4][k % 4];
+    const void* f = kWaveFree[e->cfg.scheme == TS_SCHEME_PRODUCT ? 1 : 0][k / 4][k % 4];
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, WAVE_THREADS, wave_smem_of(e->wkind));
     kf.func = (void*)f;
@@ -6161,7 +6174,7 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   kWave[k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
   TS_LAUNCH_CHECK(e, "k_wave");
   if (v.free_kernel && step < 0) {  // host-driven loop: the free-running waves' kernel (returns unless k_sched chose them)
-    const void* f = kWaveFree[k / 4][k % 4];
+    const void* f = kWaveFree[e->cfg.scheme == TS_SCHEME_PRODUCT ? 1 : 0][k / 4][k % 4];
     int per = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, WAVE_THREADS, wave_smem_of(k % 4));
     View vf = v;
@@ -6357,8 +6370,9 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
   }
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
-      cr = cudaFuncSetAttribute(kWaveFree[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)wave_smem_of(b));
+      for (int pr = 0; pr < 2 && cr == cudaSuccess; ++pr)
+        cr = cudaFuncSetAttribute(kWaveFree[pr][a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)wave_smem_of(b));
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
       cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
