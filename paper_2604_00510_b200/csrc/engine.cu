@@ -4153,7 +4153,9 @@ __device__ void free_run_waves(const View& v, WaveStats& ws, double* s_raw, doub
   }
 }
 
-template <int NSLOT, int WT>
+// PROD: the product aggregation scheme fixed at compile time (the default
+// ScoringConfig; no Neumaier compensation state along the path)
+template <int NSLOT, int WT, bool PROD>
 #ifndef TS_WAVE_MINB
 #define TS_WAVE_MINB 4  // resident CTAs of 4 warps per SM the register budget is sized for
 #endif
@@ -4168,7 +4170,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
   if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
 #endif
   if (step < 0 && v.free_ok && v.ctr->free_run) {
-    if (!v.free_kernel) free_run_waves<NSLOT, WT, false>(v, ws, s_raw, s_rew);
+    if (!v.free_kernel) free_run_waves<NSLOT, WT, false, PROD>(v, ws, s_raw, s_rew);
   } else {
   const int count = v.ctr->work_count;
   if (step < 0) step = v.ctr->cur_step;
@@ -4177,7 +4179,7 @@ __global__ void __launch_bounds__(WAVE_THREADS, TS_WAVE_MINB) k_wave(View v, int
   const int nwarps = gridDim.x * WAVE_WARPS;
   int item = blockIdx.x * WAVE_WARPS + warp;
   while (item < count) {
-    search_wave<NSLOT, WT>(v, v.work[item], step, ws, s_raw, s_rew);
+    search_wave<NSLOT, WT, false, PROD>(v, v.work[item], step, ws, s_raw, s_rew);
     if (lane == 0) item = nwarps + atomicAdd(&v.ctr->work_next, 1);
     item = __shfl_sync(FULL, item, 0);
   }
@@ -4235,10 +4237,13 @@ static const void* kWaveFree[2][3][4] = {
 // kernel table: [nslot 1/2/4][width 2/4/8/runtime]
 typedef void (*wave_kernel_t)(View, int);
 __device__ __host__ inline int wkind_of_width(int w) { return w == 2 ? 0 : w == 4 ? 1 : w == 8 ? 2 : 3; }
-static const wave_kernel_t kWave[3][4] = {
-    {k_wave<1, 2>, k_wave<1, 4>, k_wave<1, 8>, k_wave<1, 0>},
-    {k_wave<2, 2>, k_wave<2, 4>, k_wave<2, 8>, k_wave<2, 0>},
-    {k_wave<4, 2>, k_wave<4, 4>, k_wave<4, 8>, k_wave<4, 0>},
+static const wave_kernel_t kWave[2][3][4] = {
+    {{k_wave<1, 2, false>, k_wave<1, 4, false>, k_wave<1, 8, false>, k_wave<1, 0, false>},
+     {k_wave<2, 2, false>, k_wave<2, 4, false>, k_wave<2, 8, false>, k_wave<2, 0, false>},
+     {k_wave<4, 2, false>, k_wave<4, 4, false>, k_wave<4, 8, false>, k_wave<4, 0, false>}},
+    {{k_wave<1, 2, true>, k_wave<1, 4, true>, k_wave<1, 8, true>, k_wave<1, 0, true>},
+     {k_wave<2, 2, true>, k_wave<2, 4, true>, k_wave<2, 8, true>, k_wave<2, 0, true>},
+     {k_wave<4, 2, true>, k_wave<4, 4, true>, k_wave<4, 8, true>, k_wave<4, 0, true>}},
 };
 
 // ---- pipelined CTA mode for searches with many rollouts in one wave ----------
@@ -5963,7 +5968,7 @@ int wave_grid(ts_engine* e, int& blocks_out) {
   int blocks = e->wave_blocks[k];
   if (blocks <= 0) {
     int per = 0;
-    cudaError_t rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)kWave[k / 4][k % 4],
+    cudaError_t rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void*)kWave[0][k / 4][k % 4],
                                                                    WAVE_THREADS, wave_smem_of(k % 4));
     if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
     blocks = std::max(1, per) * e->sm_count;
@@ -5976,7 +5981,7 @@ int wave_grid(ts_engine* e, int& blocks_out) {
 
 void* wave_fn(ts_engine* e) {
   const int k = wave_index(e);
-  return (void*)kWave[k / 4][k % 4];
+  return (void*)kWave[e->cfg.scheme == TS_SCHEME_PRODUCT ? 1 : 0][k / 4][k % 4];
 }
 
 int heavy_grid(ts_engine* e, int& blocks_out) {
@@ -6171,7 +6176,7 @@ int launch_wave(ts_engine* e, const View& v, int step, cudaStream_t s) {
   }
   cudaEventRecord(e->wave_ev[e->wave_ev_used], s);
   const int k = wave_index(e);
-  kWave[k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
+  kWave[e->cfg.scheme == TS_SCHEME_PRODUCT ? 1 : 0][k / 4][k % 4]<<<blocks, WAVE_THREADS, wave_smem_of(k % 4), s>>>(v, step);
   TS_LAUNCH_CHECK(e, "k_wave");
   if (v.free_kernel && step < 0) {  // host-driven loop: the free-running waves' kernel (returns unless k_sched chose them)
     const void* f = kWaveFree[e->cfg.scheme == TS_SCHEME_PRODUCT ? 1 : 0][k / 4][k % 4];
@@ -6375,7 +6380,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
                                   (int)wave_smem_of(b));
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 4 && cr == cudaSuccess; ++b)
-      cr = cudaFuncSetAttribute((const void*)kWave[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+      for (int pr = 0; pr < 2 && cr == cudaSuccess; ++pr)
+        cr = cudaFuncSetAttribute((const void*)kWave[pr][a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)wave_smem_of(b));
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 3 && cr == cudaSuccess; ++b)
