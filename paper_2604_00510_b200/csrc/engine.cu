@@ -4735,7 +4735,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   ws.levels += levels;
 }
 
-template <int NSLOT, int WT>
+template <int NSLOT, int WT, bool PROD>
 __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, double* s_raw, double* s_rew,
                                int si) {
   constexpr int WS = WT;
@@ -4855,7 +4855,12 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
       ++depth;
       nrew = __shfl_sync(FULL, rew, j);
       const uint32_t nm = (uint32_t)depth | ((uint32_t)j << SH_REF) | (jterm ? M_TERM : 0u);
-      agg.add(nrew, scheme);
+      if constexpr (PROD) {
+        agg.a = agg.a * nrew;
+        ++agg.n;
+      } else {
+        agg.add(nrew, scheme);
+      }
       if (depth == 1) d1r = nrew;
       golden = golden && depth <= glen && gnext == j;
       if (lane == depth - 1) { pnode = node; pmeta = nm; prew = nrew; pagg = agg.a; pj = j; }
@@ -4866,7 +4871,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     __syncwarp();
     const int dend = depth;
     const int nlev = dend - d0;
-    const double pscore = agg.value(scheme);
+    const double pscore = PROD ? agg.a : agg.value(scheme);
     // --- everything that does not depend on the node ids, before the commit turn ---
     const double up_rew = __shfl_up_sync(FULL, prew, 1);
     const double up_agg = __shfl_up_sync(FULL, pagg, 1);
@@ -4927,7 +4932,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
     int dv = (int)__reduce_add_sync(FULL, (unsigned)(ne_cnt + 64)) - 64 * 32;
     if (forced) {
       const bool rel = strict || d1r >= theta1;
-      const double bound = prefix_bound ? fmin(nrew, agg.value(scheme)) : nrew;
+      const double bound = prefix_bound ? fmin(nrew, PROD ? agg.a : agg.value(scheme)) : nrew;
       if (rel && !(bound < tau)) --dv;
     }
     __syncwarp();
@@ -5265,7 +5270,7 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
   ws.path_nodes += pathn;
 }
 
-template <int NSLOT, int WT>
+template <int NSLOT, int WT, bool PROD>
 __global__ void __launch_bounds__(HEAVY_THREADS, 2) k_heavy(View v, int step) {
   extern __shared__ double hsm[];
   __shared__ HeavyCtl ctl;
@@ -5312,14 +5317,11 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 2) k_heavy(View v, int step) {
     double rW = 0.0;
     int decision = TS_EXIT_NONE;
     if (warp == 0) {
-      if (v.cfg.scheme == TS_SCHEME_PRODUCT)
-        heavy_select<NSLOT, WT, true>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
-      else
-        heavy_select<NSLOT, WT, false>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
+      heavy_select<NSLOT, WT, PROD>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
     } else if (warp != 4) {
       const int si = heavy_sim_of_warp(warp);
       double* s_raw = hsm + (size_t)si * 2 * 32 * WT;
-      heavy_simulate<NSLOT, WT>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, si);
+      heavy_simulate<NSLOT, WT, PROD>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, si);
     }
     __syncthreads();
 #ifdef TS_HEAVY_PROF
@@ -5365,10 +5367,13 @@ __global__ void __launch_bounds__(HEAVY_THREADS, 2) k_heavy(View v, int step) {
   }
 }
 
-static const wave_kernel_t kHeavy[3][3] = {
-    {k_heavy<1, 2>, k_heavy<1, 4>, k_heavy<1, 8>},
-    {k_heavy<2, 2>, k_heavy<2, 4>, k_heavy<2, 8>},
-    {k_heavy<4, 2>, k_heavy<4, 4>, k_heavy<4, 8>},
+static const wave_kernel_t kHeavy[2][3][3] = {
+    {{k_heavy<1, 2, false>, k_heavy<1, 4, false>, k_heavy<1, 8, false>},
+     {k_heavy<2, 2, false>, k_heavy<2, 4, false>, k_heavy<2, 8, false>},
+     {k_heavy<4, 2, false>, k_heavy<4, 4, false>, k_heavy<4, 8, false>}},
+    {{k_heavy<1, 2, true>, k_heavy<1, 4, true>, k_heavy<1, 8, true>},
+     {k_heavy<2, 2, true>, k_heavy<2, 4, true>, k_heavy<2, 8, true>},
+     {k_heavy<4, 2, true>, k_heavy<4, 4, true>, k_heavy<4, 8, true>}},
 };
 size_t heavy_smem_of(int wkind) {
   const int ws = wkind == 0 ? 2 : wkind == 1 ? 4 : 8;
@@ -5989,7 +5994,7 @@ int heavy_grid(ts_engine* e, int& blocks_out) {
     int per = 0;
     const int k = wave_index(e);
     cudaError_t rc = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per, (const void*)kHeavy[k / 4][std::min(k % 4, 2)], HEAVY_THREADS, heavy_smem_of(std::min(e->wkind, 2)));
+        &per, (const void*)kHeavy[0][k / 4][std::min(k % 4, 2)], HEAVY_THREADS, heavy_smem_of(std::min(e->wkind, 2)));
     if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
     e->heavy_blocks = std::max(1, per) * e->sm_count;
   }
@@ -5999,7 +6004,7 @@ int heavy_grid(ts_engine* e, int& blocks_out) {
 
 void* heavy_fn(ts_engine* e) {
   const int k = wave_index(e);
-  return (void*)kHeavy[k / 4][std::min(k % 4, 2)];
+  return (void*)kHeavy[e->cfg.scheme == TS_SCHEME_PRODUCT ? 1 : 0][k / 4][std::min(k % 4, 2)];
 }
 
 int launch_heavy(ts_engine* e, const View& v, int step, cudaStream_t s) {
@@ -6007,7 +6012,8 @@ int launch_heavy(ts_engine* e, const View& v, int step, cudaStream_t s) {
   int blocks = 0, rc;
   if ((rc = heavy_grid(e, blocks))) return rc;
   const int k = wave_index(e);
-  kHeavy[k / 4][std::min(k % 4, 2)]<<<blocks, HEAVY_THREADS, heavy_smem_of(std::min(e->wkind, 2)), s>>>(v, step);
+  kHeavy[e->cfg.scheme == TS_SCHEME_PRODUCT ? 1 : 0][k / 4][std::min(k % 4, 2)]<<<blocks, HEAVY_THREADS,
+                                                                                 heavy_smem_of(std::min(e->wkind, 2)), s>>>(v, step);
   TS_LAUNCH_CHECK(e, "k_heavy");
   return TS_OK;
 }
@@ -6385,7 +6391,8 @@ int ts_engine_create(const ts_config* cfg, int32_t device, ts_engine** out) {
                                 (int)wave_smem_of(b));
   for (int a = 0; a < 3 && cr == cudaSuccess; ++a)
     for (int b = 0; b < 3 && cr == cudaSuccess; ++b)
-      cr = cudaFuncSetAttribute((const void*)kHeavy[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+      for (int pr = 0; pr < 2 && cr == cudaSuccess; ++pr)
+        cr = cudaFuncSetAttribute((const void*)kHeavy[pr][a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)heavy_smem_of(b));
   {
     const char* env = getenv("TS_NO_PIPELINE");
