@@ -4367,8 +4367,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   const double rW = Wv[0];
   const long long rN = (long long)(uint32_t)rno;
   const double rq = rN == 0 ? 0.5 : QQ[0];  // the root's mean (constant during a wave)
-  uint64_t rmf = MF[0];
-  int root_seen = 0;  // commits of jobs below this index have been folded into rmf
+  uint64_t rmf = 0;  // the root's word, refreshed from ctl->root_mf per rollout
   int decision = TS_EXIT_NONE;
   int last_risky = -1;
   int lleaf = -1;  // lane l: leaf of job k-1-l
@@ -4389,18 +4388,11 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     // while this selection reads the tree (they are checked at every node entered)
     HPROF_T0(t_pro);
     const int cs = ld_acquire_cta(&ctl->committed);
-    {
-      // the root's word changes only when a committed job had the root as its
-      // leaf or was risky
-      bool stale = false;
-      for (int j = root_seen; j < cs; ++j) {
-        const HeavyJob& jb = ring[j % HEAVY_RING];
-        stale |= jb.leaf == 0 || jb.risky != 0;
-      }
-      root_seen = cs;
-      if (heavy_wait_inflight(ctl, lleaf, cs, k, 0)) stale = true;
-      if (stale) rmf = ctl->root_mf;
-    }
+    // the root's word changes only at the commit of a job that had the root as
+    // its leaf (waited for here) or was risky (waited for above); the
+    // committing simulator keeps it in shared memory
+    heavy_wait_inflight(ctl, lleaf, cs, k, 0);
+    rmf = ctl->root_mf;
     uint32_t nmeta = (uint32_t)rmf;
     if (!meta_expandable(nmeta)) {  // NoExpandableLeafError (tree.py:273-274)
       if (k == 0) decision = -1;
@@ -4641,15 +4633,6 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     HPROF_T0(t_g);
     if (k - ctl->committed >= HEAVY_RING) spin_until_ge(&ctl->committed, k - HEAVY_RING + 1);
     HPROF_ACC(p_ring, t_g);
-    if (root_seen <= k - HEAVY_RING) {  // fold commits whose ring slot is about to be reused
-      bool stale = false;
-      for (int j = root_seen; j <= k - HEAVY_RING; ++j) {
-        const HeavyJob& jb = ring[j % HEAVY_RING];
-        stale |= jb.leaf == 0 || jb.risky != 0;
-      }
-      root_seen = k - HEAVY_RING + 1;
-      if (stale) rmf = ctl->root_mf;
-    }
 #ifdef TS_HEAVY_PROF
     const long long e0 = clock64();
 #endif
