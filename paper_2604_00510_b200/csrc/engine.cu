@@ -4334,14 +4334,13 @@ __device__ __forceinline__ bool heavy_wait_inflight(HeavyCtl* ctl, int lleaf, in
 // memory round trip on the selection chain of every level.
 __device__ __forceinline__ uint64_t reload_u64(const uint64_t* p) { return *(const volatile uint64_t*)p; }
 
-constexpr int SQRT_TAB = 2048;  // sqrt(k) for k < SQRT_TAB in shared memory (IEEE sqrt is exact-rounded)
-// The table load is unconditional (no divergent branch around it, so the
-// shared-memory base is hoisted); IEEE sqrt only for the rare large counts.
-__device__ __forceinline__ double isqrt_tab(const double* sqt, long long n) {
-  const double t = sqt[n < SQRT_TAB ? n : 0];
-  if (__builtin_expect(n >= SQRT_TAB, 0)) return sqrt((double)n);
-  return t;
-}
+// sqrt(k) for k < SQRT_TAB in shared memory (IEEE sqrt is exact-rounded).
+// Every count the selector takes a root of is N + O of one node, and
+// N + O <= completed + in flight <= rollout_budget, so with the pipelined mode
+// enabled only for budgets below SQRT_TAB (ts_load) the lookup needs no range
+// check: a branch here stalled the selection chain on every scored node.
+constexpr int SQRT_TAB = 2048;
+__device__ __forceinline__ double isqrt_tab(const double* sqt, long long n) { return sqt[(int)n]; }
 
 template <int NSLOT, int WT, bool PROD>
 __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, const double* sqt, int count,
@@ -5801,7 +5800,8 @@ View make_view(ts_engine* e) {
   v.work_heavy = e->work_heavy;
   v.tgt = e->tgt;
   v.nrec = e->nrec;
-  v.heavy_on = (e->wkind != 3 && !e->heavy_off && e->n_local <= HBITS_WORDS * 32) ? 1 : 0;
+  v.heavy_on = (e->wkind != 3 && !e->heavy_off && e->n_local <= HBITS_WORDS * 32 &&
+                 e->cfg.rollout_budget < SQRT_TAB) ? 1 : 0;
   v.heavy_sync = e->heavy_sync ? 1 : 0;
   v.max_arrival = e->max_arrival;
   v.sp = e->sp;
