@@ -50,7 +50,8 @@ __host__ __device__ inline int meta_nexp(uint32_t m) { return (int)((m >> SH_NEX
 // _expandable (tree.py:175-181), maintained incrementally: a non-terminal
 // node is expandable iff it is a leaf or one of its children is.
 __host__ __device__ inline bool meta_expandable(uint32_t m) {
-  return !(m & M_TERM) && (!(m & M_KIDS) || meta_nexp(m) > 0);
+  // bitwise, so that no branch is emitted on the selection chain
+  return ((m & M_TERM) == 0) & (((m & M_KIDS) == 0) | ((m & (0x3Fu << SH_NEXP)) != 0));
 }
 
 enum { ST_PENDING = 0, ST_RUNNING = 1, ST_FINISHED = 2 };
@@ -4341,6 +4342,14 @@ __device__ __forceinline__ uint64_t reload_u64(const uint64_t* p) { return *(con
 // check: a branch here stalled the selection chain on every scored node.
 constexpr int SQRT_TAB = 2048;
 __device__ __forceinline__ double isqrt_tab(const double* sqt, long long n) { return sqt[(int)n]; }
+// the same lookup through a 32-bit shared-window address computed once per
+// search: a generic pointer costs a window conversion (S2UR of the CTA id) at
+// every use on the selection chain
+__device__ __forceinline__ double isqrt_s(uint32_t sqs, uint32_t n) {
+  double r;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(sqs + 8u * n));
+  return r;
+}
 
 template <int NSLOT, int WT, bool PROD>
 __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, const double* sqt, int count,
@@ -4366,6 +4375,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
   const double rW = Wv[0];
   const long long rN = (long long)(uint32_t)rno;
   const double rq = rN == 0 ? 0.5 : QQ[0];  // the root's mean (constant during a wave)
+  const uint32_t sqs = (uint32_t)__cvta_generic_to_shared(sqt);
   uint64_t rmf = 0;  // the root's word, refreshed from ctl->root_mf per rollout
   int decision = TS_EXIT_NONE;
   int last_risky = -1;
@@ -4380,18 +4390,22 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
 #endif
   for (; k < count; ++k) {
     HPROF_T0(t_r);
-    if (last_risky >= 0) spin_until_ge(&ctl->committed, last_risky + 1);
+    if (last_risky >= 0) {
+      spin_until_ge(&ctl->committed, last_risky + 1);
+      last_risky = -1;
+    }
     HPROF_ACC(p_risky, t_r);
-    if (ctl->status != TS_OK) break;
     // jobs < cs are committed and visible from here on; jobs [cs, k) may commit
     // while this selection reads the tree (they are checked at every node entered)
     HPROF_T0(t_pro);
     const int cs = ld_acquire_cta(&ctl->committed);
     // the root's word changes only at the commit of a job that had the root as
-    // its leaf (waited for here) or was risky (waited for above); the
-    // committing simulator keeps it in shared memory
-    heavy_wait_inflight(ctl, lleaf, cs, k, 0);
+    // its leaf (waited for below) or was risky (waited for above); the
+    // committing simulator keeps it in shared memory.  The three shared loads
+    // are issued back to back.
     rmf = ctl->root_mf;
+    if (ctl->status != TS_OK) break;
+    if (heavy_wait_inflight(ctl, lleaf, cs, k, 0)) rmf = ctl->root_mf;
     uint32_t nmeta = (uint32_t)rmf;
     if (!meta_expandable(nmeta)) {  // NoExpandableLeafError (tree.py:273-274)
       if (k == 0) decision = -1;
@@ -4401,7 +4415,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     HPROF_T0(t_desc);
     int node = 0, depth = 0, nfc = (int)(rmf >> 32);
     // the current node's mean W/N (0.5 unvisited) and sqrt(N+O), ready before its children are scored
-    double pq = rq, psq = isqrt_tab(sqt, rN + (long long)(rno >> 32));
+    double pq = rq, psq = isqrt_s(sqs, (uint32_t)(rN + (long long)(rno >> 32)));
     int pnode = -1, pj = 0;
     uint64_t pno = 0;
     double nrew = 1.0;
@@ -4450,19 +4464,14 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
       const int gj = l2lane ? (lane - WT) / WT : 0, gi = l2lane ? (lane - WT) % WT : 0;
       while (nmeta & M_KIDS) {
         const int fc = nfc;
-        uint64_t xno = 0, xmf = 0;
-        double xq = 0.0, xp = 0.0, xr = 0.0;
 #ifdef TS_HEAVY_PROF
         long long t_a = clock64();
 #endif
-        if (l1) {
-          const int c = fc + lane;
-          xno = NO[c];
-          xq = QQ[c];
-          xp = PR[c];
-          xmf = MF[c];
-          xr = RW[c];
-        }
+        // branch-free: every lane loads a real node (the other lanes the first
+        // child's record, the same lines), so no divergent branch sits on the chain
+        const int c1 = fc + (l1 ? lane : 0);
+        uint64_t xno = NO[c1], xmf = MF[c1];
+        double xq = QQ[c1], xp = PR[c1], xr = RW[c1];
         // the grandchild lanes read their parent child's record
         const int src = l1 ? lane : gj;
 #ifdef TS_HEAVY_PROF
@@ -4480,14 +4489,16 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         const uint64_t gpmf = __shfl_sync(FULL, xmf, src);
         const uint64_t gpno = __shfl_sync(FULL, xno, src);
         const double gpq = __shfl_sync(FULL, xq, src);
-        const bool l2 = l2lane && ((uint32_t)gpmf & M_KIDS);
-        if (l2) {
-          const int c = (int)(gpmf >> 32) + gi;
-          xno = NO[c];
-          xq = QQ[c];
-          xp = PR[c];
-          xmf = MF[c];
-          xr = RW[c];
+        const bool l2 = l2lane & (((uint32_t)gpmf & M_KIDS) != 0);
+        {
+          const int c2 = l2 ? (int)(gpmf >> 32) + gi : c1;
+          const uint64_t yno = NO[c2], ymf = MF[c2];
+          const double yq = QQ[c2], yp = PR[c2], yr = RW[c2];
+          xno = l2 ? yno : xno;
+          xmf = l2 ? ymf : xmf;
+          xq = l2 ? yq : xq;
+          xp = l2 ? yp : xp;
+          xr = l2 ? yr : xr;
         }
         // the scored node's parent terms: the current node for l1, the child for l2
 #ifdef TS_HEAVY_PROF
@@ -4504,15 +4515,19 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
 #endif
         const unsigned gN = (uint32_t)gpno, gO = (uint32_t)(gpno >> 32);
         const double ppq = l1 ? pq : (gN == 0 ? 0.5 : gpq);
-        const double ppsq = l1 ? psq : isqrt_tab(sqt, (long long)gN + gO);
-        const bool valid = (l1 || l2) && meta_expandable((uint32_t)xmf);
+        const double gsq = isqrt_s(sqs, gN + gO);
+        const double ppsq = l1 ? psq : gsq;
+        const bool valid = (l1 | l2) & meta_expandable((uint32_t)xmf);
         const unsigned xN = (uint32_t)xno, xO = (uint32_t)(xno >> 32);
         const double xnq = xN == 0 ? 0.5 : xq;
-        const double xnsq = isqrt_tab(sqt, (long long)xN + xO);
-        // _child_q (tree.py:235-239); wu_puct_score (tree.py:232)
+        const double xnsq = isqrt_s(sqs, xN + xO);
+        // _child_q (tree.py:235-239); wu_puct_score (tree.py:232); computed on
+        // every lane (finite inputs everywhere) and masked afterwards
         const double q = xN == 0 ? ppq : xq;
-        const double sc = valid ? q + c_puct * xp * ppsq / (double)(1u + xN + xO) : -INFINITY;
-        const bool bad = valid && (!(q >= 0.0 && q <= 1.0) || !(xp >= 0.0 && xp <= 1.0));
+        const double u = c_puct * xp * ppsq / (double)(1u + xN + xO);
+        const double sc = valid ? q + u : -INFINITY;
+        // non-short-circuit: four compares and no branch on the selection chain
+        const bool bad = valid & (!(q >= 0.0) | !(q <= 1.0) | !(xp >= 0.0) | !(xp <= 1.0));
 #ifdef TS_HEAVY_PROF
         {
           unsigned long long w_;
@@ -4630,7 +4645,7 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     }
     // hand the rollout to its simulator
     HPROF_T0(t_g);
-    if (k - ctl->committed >= HEAVY_RING) spin_until_ge(&ctl->committed, k - HEAVY_RING + 1);
+    if (k - cs >= HEAVY_RING && k - ctl->committed >= HEAVY_RING) spin_until_ge(&ctl->committed, k - HEAVY_RING + 1);
     HPROF_ACC(p_ring, t_g);
 #ifdef TS_HEAVY_PROF
     const long long e0 = clock64();
