@@ -4421,7 +4421,6 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
     double nrew = 1.0;
     Agg agg;
     agg.init();
-    bool golden = glen >= 0;
     double d1r = 1.0;
     int status = TS_OK;
     // per-lane record of a scored node; `take` moves the descent into the node scored by lane `src`
@@ -4443,7 +4442,6 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         agg.add(nrew, scheme);
       }
       if (depth == 1) d1r = nrew;
-      if (golden) golden = depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == child_index;
       if (lane == depth - 1) { pnode = node; pno = nno; pj = child_index; }
       // entering a leaf whose expansion may be in flight: its word and children
       // are only valid after that job's commit (acquired in the wait)
@@ -4623,7 +4621,6 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         agg.add(nrew, scheme);
       }
       if (depth == 1) d1r = nrew;
-      if (golden) golden = depth <= glen && __shfl_sync(FULL, gstep, depth - 1) == j;
       if (lane == depth - 1) { pnode = node; pno = nno; pj = j; }
       // entering a leaf whose expansion may be in flight: its word and children
       // are only valid after that job's commit (acquired in the wait)
@@ -4650,6 +4647,10 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
 #ifdef TS_HEAVY_PROF
     const long long e0 = clock64();
 #endif
+    // on the golden path iff every level's child is the golden step (lane
+    // l holds the child index chosen at depth l + 1); checked once per rollout
+    const bool on_golden = __all_sync(FULL, lane >= depth || pj == gstep);
+    const bool golden = glen >= 0 && depth <= glen && on_golden;
     HeavyJob& jb = ring[k % HEAVY_RING];
     jb.pnode[lane] = pnode;
     jb.pj[lane] = pj;
