@@ -4266,8 +4266,14 @@ static const wave_kernel_t kWave[2][3][4] = {
 // 8 warps: warp 0 selects; warp 4, which shares warp 0's SM sub-partition
 // (scheduler = warp id % 4), stays idle so the latency-bound selection chain
 // never competes for issue slots; the other 6 warps simulate.
-constexpr int HEAVY_SIM = 6;
-constexpr int HEAVY_WARPS = 8;
+#ifndef TS_HEAVY_WARPS
+#define TS_HEAVY_WARPS 8
+#endif
+#ifndef TS_HEAVY_MINB
+#define TS_HEAVY_MINB 2
+#endif
+constexpr int HEAVY_WARPS = TS_HEAVY_WARPS;
+constexpr int HEAVY_SIM = HEAVY_WARPS - 2;
 constexpr int HEAVY_THREADS = 32 * HEAVY_WARPS;
 __device__ __forceinline__ int heavy_sim_of_warp(int w) { return w < 4 ? w - 1 : w - 2; }
 constexpr int HEAVY_RING = 16;
@@ -4534,10 +4540,11 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         }
         t_c = clock64();
 #endif
-        // level 1
-        const unsigned vb1 = __ballot_sync(FULL, valid && l1);
-        if (__ballot_sync(FULL, bad && l1)) { status = TS_INVALID_ARGUMENT; break; }
-        if (!vb1) { status = TS_EXHAUSTED; break; }
+        // level 1; one ballot of each flag per round, the levels mask their lanes
+        constexpr unsigned L1M = (1u << WT) - 1u;
+        const unsigned vball = __ballot_sync(FULL, valid), bball = __ballot_sync(FULL, bad);
+        const unsigned vb1 = vball & L1M;
+        if ((bball & L1M) | (vb1 == 0u)) { status = (bball & L1M) ? TS_INVALID_ARGUMENT : TS_EXHAUSTED; break; }
         scored += __popc(vb1);
         ++levels;
         const int j1 = warp_argmax_nonneg(sc, valid && l1);
@@ -4555,9 +4562,9 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
         if (!(nmeta & M_KIDS)) break;
         // level 2, within the group of child j1
         const bool ing = l2lane && gj == j1;
-        const unsigned vb2 = __ballot_sync(FULL, valid && ing);
-        if (__ballot_sync(FULL, bad && ing)) { status = TS_INVALID_ARGUMENT; break; }
-        if (!vb2) { status = TS_EXHAUSTED; break; }
+        const unsigned gm = L1M << (WT + j1 * WT);
+        const unsigned vb2 = vball & gm;
+        if ((bball & gm) | (vb2 == 0u)) { status = (bball & gm) ? TS_INVALID_ARGUMENT : TS_EXHAUSTED; break; }
         scored += __popc(vb2);
         ++levels;
         const int s2 = warp_argmax_nonneg(sc, valid && ing);
@@ -5269,7 +5276,11 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
 }
 
 template <int NSLOT, int WT, bool PROD>
-__global__ void __launch_bounds__(HEAVY_THREADS, 2) k_heavy(View v, int step) {
+#ifdef TS_HEAVY_MAXNREG
+__global__ void __maxnreg__(TS_HEAVY_MAXNREG) k_heavy(View v, int step) {
+#else
+__global__ void __launch_bounds__(HEAVY_THREADS, TS_HEAVY_MINB) k_heavy(View v, int step) {
+#endif
   extern __shared__ double hsm[];
   __shared__ HeavyCtl ctl;
   __shared__ HeavyJob ring[HEAVY_RING];
