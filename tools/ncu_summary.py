@@ -56,11 +56,26 @@ def dram(path):
             for k, (n, r, w) in agg.items()}
 
 
-def details(rep):
-    """Key metrics of one `ncu --set full` capture (ncu -i <rep> --page details)."""
+def _page(rep, page):
+    """One page of a capture: from the .ncu-rep, or from the <rep>.<page>.csv[.gz] exported on the GPU box
+    (tools/ncu_export.sh; the reports themselves are too large to bring back)."""
+    import gzip
+    import os
     import subprocess
 
-    out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    base = rep[:-len(".ncu-rep")] if rep.endswith(".ncu-rep") else rep
+    for ext, op in ((".csv", open), (".csv.gz", gzip.open)):
+        if os.path.exists(f"{base}.{page}{ext}"):
+            with op(f"{base}.{page}{ext}", "rt") as f:
+                return f.read()
+    args = ["--page", "details", "--csv"] if page == "details" else ["--page", "source", "--csv",
+                                                                        "--print-source=cuda,sass"]
+    return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
+
+
+def details(rep):
+    """Key metrics of one `ncu --set full` capture (ncu -i <rep> --page details)."""
+    out = _page(rep, "details")
     r = list(csv.reader(out.splitlines()))
     hdr = r[0]
     keep = {"Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput", "Memory Throughput",
@@ -78,10 +93,7 @@ def details(rep):
 
 def stalls(rep):
     """Warp-stall reasons summed over the source page of one capture."""
-    import subprocess
-
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
-                         capture_output=True, text=True).stdout
+    out = _page(rep, "source")
     agg = collections.Counter()
     hdr = None
     for r in csv.reader(out.splitlines()):
