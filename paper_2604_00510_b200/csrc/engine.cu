@@ -6467,7 +6467,44 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   cudaStream_t s = (cudaStream_t)stream;
   TS_CUDA_TRY(e, cudaSetDevice(e->device));
   const ts_config& c = e->cfg;
+  int rc;
+  // The problem table's DMA is enqueued first and the host validates the
+  // table while it is in flight (one pass over the rows; a strided host pass
+  // costs about as much as the copy itself).  A table that fails validation
+  // leaves the engine unloaded.
+  if (n_local > e->cap_searches || !e->st) {
+    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0, h6 = 0, h7 = 0, h8 = 0;
+    e->loaded = false;
+    if ((rc = grow(e, e->st, n_local, h0, "search state")) ||
+        (rc = grow(e, e->prob, n_local, h1, "problem table")) ||
+        (rc = grow(e, e->arrival, n_local, h2, "arrivals")) ||
+        (rc = grow(e, e->work, n_local, h3, "work list")) ||
+        (rc = grow(e, e->work_heavy, n_local, h6, "work list")) ||
+        (rc = grow(e, e->tgt, n_local, h7, "targets")) ||
+        (rc = grow(e, e->nrec, n_local, h8, "records")) ||
+        (rc = grow(e, e->records, n_local, h4, "records")) ||
+        (rc = grow(e, e->outcomes, n_local, h5, "outcomes")))
+      return rc;
+    e->cap_searches = n_local;
+    e->outcomes_cap = n_local;
+  }
+  {
+    // one DMA at full PCIe rate: directly from pinned caller memory, else via pinned staging
+    const size_t bytes = sizeof(ts_problem) * (size_t)n_local;
+    e->loaded = false;
+    if (is_pinned(hp)) {
+      TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, hp, bytes, cudaMemcpyHostToDevice, s));
+    } else {
+      if ((rc = ensure_pinned(e, bytes))) return rc;
+      TS_CUDA_TRY(e, cudaStreamSynchronize(s));  // the staging buffer may still feed an earlier copy
+      memcpy(e->pin, hp, bytes);
+      TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, e->pin, bytes, cudaMemcpyHostToDevice, s));
+    }
+  }
   int max_len = 1, max_width = 1, prev_arr = 0;
+  int wmin = TS_MAX_WIDTH, dmin = TS_MAX_DEPTH;
+  const int w0 = std::min(c.expand_width, hp[0].branching);
+  bool same = true;
   for (int i = 0; i < n_local; ++i) {
     const ts_problem& p = hp[i];
     if (p.branching < 1 || p.branching > TS_MAX_WIDTH)
@@ -6478,8 +6515,12 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
     if (p.arrival_step < 0 || p.arrival_step < prev_arr)
       return fail(e, TS_INVALID_ARGUMENT, "arrival steps must be non-negative and non-decreasing");
     prev_arr = p.arrival_step;
+    const int w = std::min(c.expand_width, p.branching);
     max_len = std::max(max_len, std::min(c.depth_cap, p.base_depth + 1));
-    max_width = std::max(max_width, std::min(c.expand_width, p.branching));
+    max_width = std::max(max_width, w);
+    wmin = std::min(wmin, w);
+    dmin = std::min(dmin, std::min(c.depth_cap, p.base_depth));
+    same = same && w == w0;
   }
   e->max_arrival = prev_arr;
   e->nslot = max_len <= 8 ? 1 : max_len <= 16 ? 2 : 4;
@@ -6487,11 +6528,6 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
     // Exhausting a root needs every node of depth Dmin-1 = min(base_depth,
     // depth_cap)-1 expanded (nodes above never become terminal or forced),
     // one per rollout: impossible within the budget if budget < w^(Dmin-1).
-    int wmin = TS_MAX_WIDTH, dmin = TS_MAX_DEPTH;
-    for (int i = 0; i < n_local; ++i) {
-      wmin = std::min(wmin, std::min(c.expand_width, hp[i].branching));
-      dmin = std::min(dmin, std::min(c.depth_cap, hp[i].base_depth));
-    }
     double need = 1.0;
     for (int d = 1; d < dmin; ++d) need *= (double)wmin;
     // with boosting on, P = 1 for every running search needs no free slot: a
@@ -6507,17 +6543,10 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
       e->fdone_cap = n_local;
     }
   }
-  {
-    int w0 = std::min(c.expand_width, hp[0].branching);
-    bool same = true;
-    for (int i = 1; i < n_local && same; ++i) same = std::min(c.expand_width, hp[i].branching) == w0;
-    e->wkind = same ? wkind_of_width(w0) : 3;
-  }
+  e->wkind = same ? wkind_of_width(w0) : 3;
   // nodes a search can create: every launched rollout (<= budget) expands at
   // most min(depth_cap, base_depth+1) levels of `width` children
   const long long cap = 1 + (long long)c.rollout_budget * max_width * max_len;
-  size_t have;
-  int rc;
   const size_t pool = (size_t)cap * (size_t)n_local;
   if (pool > (size_t)e->pool_nodes || !e->no) {
     void* ptrs[] = {e->no, e->W, e->Q, e->prior, e->reward, e->mf, e->parent};
@@ -6536,21 +6565,6 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
     e->pool_nodes = (long long)pool;
   }
   e->cap = cap;
-  if (n_local > e->cap_searches || !e->st) {
-    size_t h0 = 0, h1 = 0, h2 = 0, h3 = 0, h4 = 0, h5 = 0, h6 = 0, h7 = 0, h8 = 0;
-    if ((rc = grow(e, e->st, n_local, h0, "search state")) ||
-        (rc = grow(e, e->prob, n_local, h1, "problem table")) ||
-        (rc = grow(e, e->arrival, n_local, h2, "arrivals")) ||
-        (rc = grow(e, e->work, n_local, h3, "work list")) ||
-        (rc = grow(e, e->work_heavy, n_local, h6, "work list")) ||
-        (rc = grow(e, e->tgt, n_local, h7, "targets")) ||
-        (rc = grow(e, e->nrec, n_local, h8, "records")) ||
-        (rc = grow(e, e->records, n_local, h4, "records")) ||
-        (rc = grow(e, e->outcomes, n_local, h5, "outcomes")))
-      return rc;
-    e->cap_searches = n_local;
-    e->outcomes_cap = n_local;
-  }
   const size_t rows = (size_t)n_local * (size_t)c.rollout_budget;
   if (rows > e->scratch_rows || !e->sp) {
     if (e->sp) cudaFree(e->sp);
@@ -6583,18 +6597,6 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   e->n_local = n_local;
   e->goff = global_offset;
   e->n_global = n_global;
-  {
-    // one DMA at full PCIe rate: directly from pinned caller memory, else via pinned staging
-    const size_t bytes = sizeof(ts_problem) * (size_t)n_local;
-    if (is_pinned(hp)) {
-      TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, hp, bytes, cudaMemcpyHostToDevice, s));
-    } else {
-      if ((rc = ensure_pinned(e, bytes))) return rc;
-      TS_CUDA_TRY(e, cudaStreamSynchronize(s));  // the staging buffer may still feed an earlier copy
-      memcpy(e->pin, hp, bytes);
-      TS_CUDA_TRY(e, cudaMemcpyAsync(e->prob, e->pin, bytes, cudaMemcpyHostToDevice, s));
-    }
-  }
   if ((rc = ensure_log1p(e, 1024, s))) return rc;
   if ((rc = ensure_step_times(e, 4096, s))) return rc;
   if ((rc = ensure_cost(e))) return rc;
@@ -6605,7 +6607,6 @@ int ts_load_problems(ts_engine* e, const ts_problem* hp, int32_t n_local, int32_
   k_init<<<(n_local + 63) / 64, 64, 0, s>>>(v);
   TS_LAUNCH_CHECK(e, "k_init");
   e->loaded = true;
-  (void)have;
   return TS_OK;
 }
 
