@@ -4358,7 +4358,7 @@ __device__ __forceinline__ double isqrt_s(uint32_t sqs, uint32_t n) {
 }
 
 template <int NSLOT, int WT, bool PROD>
-__device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, const double* sqt, int count,
+__device__ __forceinline__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, const double* sqt, int count,
                              WaveStats& ws, uint64_t& rno_out, double& rW_out, int& decision_out) {
   const int lane = threadIdx.x & 31;
   const ts_config& cf = v.cfg;
@@ -4741,8 +4741,8 @@ __device__ void heavy_select(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring
 }
 
 template <int NSLOT, int WT, bool PROD>
-__device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, double* s_raw, double* s_rew,
-                               int si) {
+__device__ __forceinline__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ring, double* s_raw, double* s_rew,
+                               int si, int nsim) {
   constexpr int WS = WT;
   const int lane = threadIdx.x & 31;
   const ts_config& cf = v.cfg;
@@ -4788,7 +4788,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
 #ifdef TS_HEAVY_PROF
   long long q_issue = 0, q_comp = 0, q_cwait = 0, q_commit = 0;
 #endif
-  for (int k = si;; k += HEAVY_SIM) {
+  for (int k = si;; k += nsim) {
     HPROF_T0(t_a);
     while (ld_acquire_cta(&ctl->issued) <= k && !ctl->done) __nanosleep(32);
     HPROF_ACC(q_issue, t_a);
@@ -5048,7 +5048,7 @@ __device__ void heavy_simulate(const View& v, int s, HeavyCtl* ctl, HeavyJob* ri
 
 // warp 0 after all commits: backups, exit decisions, cancellations (as the
 // single-warp mode's multi-rollout path) and the search-state write-back
-__device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int nl, uint64_t rno, double rW,
+__device__ __forceinline__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int nl, uint64_t rno, double rW,
                              int decision, WaveStats& ws) {
   const int lane = threadIdx.x & 31;
   const ts_config& cf = v.cfg;
@@ -5275,6 +5275,89 @@ __device__ void heavy_finish(const View& v, int s, int step, HeavyCtl* ctl, int 
   ws.path_nodes += pathn;
 }
 
+// One search's wave in the pipelined CTA mode, run by a unit of the CTA:
+// the whole CTA (8 warps: warp 0 selects, warp 4 idles on its scheduler
+// partition, 6 simulators), or, in the paired mode (DUAL), the 4 warps of one
+// parity (warp g selects, warps g+2, g+4, g+6 simulate), so that one CTA runs
+// two searches side by side with named barriers.
+template <bool DUAL>
+__device__ __forceinline__ void heavy_bar(int g) {
+  if constexpr (DUAL) asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+  else __syncthreads();
+}
+
+template <int NSLOT, int WT, bool PROD, bool DUAL>
+__device__ __forceinline__ void heavy_item(const View& v, int step, int item, HeavyCtl& ctl, HeavyJob* ring, const double* sqt,
+                           double* hsm, WaveStats& ws) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = DUAL ? (warp & 1) : 0;
+  const int gw = DUAL ? (warp >> 1) : warp;  // warp index in the unit
+  constexpr int UT = DUAL ? 128 : HEAVY_THREADS;
+  const int ut = gw * 32 + lane;
+  const int s = v.work_heavy[item];
+  const SearchState* S = v.st + s;
+  const int count = min(v.tgt[s], v.cfg.rollout_budget - S->completed);
+  if (ut == 0) {
+    ctl.issued = 0;
+    ctl.committed = 0;
+    ctl.done = 0;
+    ctl.zero_o = 0;
+    ctl.status = TS_OK;
+    ctl.nnodes = S->nodes;
+    ctl.viable = S->viable;
+    ctl.created = 0;
+    ctl.tokens = 0;
+    ctl.root_mf = v.mf[(size_t)s * (size_t)v.cap];
+  }
+  heavy_bar<DUAL>(g);
+  uint64_t rno = 0;
+  double rW = 0.0;
+  int decision = TS_EXIT_NONE;
+  if (gw == 0) {
+    heavy_select<NSLOT, WT, PROD>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
+  } else if (DUAL || gw != 4) {
+    const int si = DUAL ? gw - 1 : heavy_sim_of_warp(gw);
+    const int slot = DUAL ? g * 3 + si : si;  // staging rows of this simulator
+    double* s_raw = hsm + (size_t)slot * 2 * 32 * WT;
+    heavy_simulate<NSLOT, WT, PROD>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, si, DUAL ? 3 : HEAVY_SIM);
+  }
+  heavy_bar<DUAL>(g);
+#ifdef TS_HEAVY_PROF
+  long long t_fin = clock64();
+#endif
+  if (gw == 0) heavy_finish(v, s, step, &ctl, ctl.issued, rno, rW, decision, ws);
+  heavy_bar<DUAL>(g);
+  if (ctl.zero_o) {  // the cancellation of an exit: O back to 0 on every node but the root
+    uint64_t* NO = v.no + (size_t)s * (size_t)v.cap;
+    const int nn = ctl.nnodes;
+    // 8 independent loads in flight per thread, then the stores
+    constexpr int U = 8;
+    for (int i0 = 1 + ut; i0 < nn; i0 += U * UT) {
+      uint64_t w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * UT;
+        w[u] = i < nn ? NO[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * UT;
+        if (i < nn && (w[u] >> 32)) NO[i] = w[u] & 0xffffffffull;
+      }
+    }
+  }
+#ifdef TS_HEAVY_PROF
+  if (ut == 0) atomicMax(&v.ctr->prof[15], (unsigned long long)(clock64() - t_fin));
+#endif
+  heavy_bar<DUAL>(g);
+}
+
+// Work: items [0, n) of the wave's pipelined-mode list over G resident CTAs.
+// CTA b takes item b; when the wave has more items than CTAs (config 2's
+// third wave: 297 boosted searches for 296 CTAs), CTAs b < n - G also take
+// item G + b and run both side by side in the paired mode instead of one
+// after the other (the wave is as long as its longest CTA).  Items from 2G
+// on are claimed one at a time from a counter.
 template <int NSLOT, int WT, bool PROD>
 #ifdef TS_HEAVY_MAXNREG
 __global__ void __maxnreg__(TS_HEAVY_MAXNREG) k_heavy(View v, int step) {
@@ -5282,8 +5365,8 @@ __global__ void __maxnreg__(TS_HEAVY_MAXNREG) k_heavy(View v, int step) {
 __global__ void __launch_bounds__(HEAVY_THREADS, TS_HEAVY_MINB) k_heavy(View v, int step) {
 #endif
   extern __shared__ double hsm[];
-  __shared__ HeavyCtl ctl;
-  __shared__ HeavyJob ring[HEAVY_RING];
+  __shared__ HeavyCtl ctl[2];
+  __shared__ HeavyJob ring[2][HEAVY_RING];
   __shared__ int s_item;
   __shared__ double sqt[SQRT_TAB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -5291,81 +5374,33 @@ __global__ void __launch_bounds__(HEAVY_THREADS, TS_HEAVY_MINB) k_heavy(View v, 
   const int count_items = v.ctr->heavy_count;
   if (count_items == 0) return;  // most waves have no pipelined-mode search
   if (step < 0) step = v.ctr->cur_step;
-  if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
-  __syncthreads();
+  const int G = gridDim.x, b = blockIdx.x;
+  if (b >= count_items) return;  // no item for this CTA: skip the table set-up
 #ifdef TS_SCHED_PROF
   if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
 #endif
-  if (s_item >= count_items) return;  // no item for this CTA: skip the table set-up
   for (int i = threadIdx.x; i < SQRT_TAB; i += HEAVY_THREADS) sqt[i] = sqrt((double)i);
   __syncthreads();
-  for (bool first = true;; first = false) {
-    if (!first) {
-      if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
-      __syncthreads();
-    }
+  if (b < count_items - G) {
+    const int g = warp & 1;
+    heavy_item<NSLOT, WT, PROD, true>(v, step, g == 0 ? b : G + b, ctl[g], ring[g], sqt, hsm, ws);
+    __syncthreads();
+  } else {
+    heavy_item<NSLOT, WT, PROD, false>(v, step, b, ctl[0], ring[0], sqt, hsm, ws);
+  }
+  for (;;) {  // items from 2G on, one at a time
+    if (count_items <= 2 * G) break;
+    if (threadIdx.x == 0) s_item = 2 * G + atomicAdd(&v.ctr->heavy_next, 1);
+    __syncthreads();
     const int item = s_item;
+    __syncthreads();
     if (item >= count_items) break;
-    const int s = v.work_heavy[item];
-    const SearchState* S = v.st + s;
-    const int count = min(v.tgt[s], v.cfg.rollout_budget - S->completed);
-    if (threadIdx.x == 0) {
-      ctl.issued = 0;
-      ctl.committed = 0;
-      ctl.done = 0;
-      ctl.zero_o = 0;
-      ctl.status = TS_OK;
-      ctl.nnodes = S->nodes;
-      ctl.viable = S->viable;
-      ctl.created = 0;
-      ctl.tokens = 0;
-      ctl.root_mf = v.mf[(size_t)s * (size_t)v.cap];
-    }
-    __syncthreads();
-    uint64_t rno = 0;
-    double rW = 0.0;
-    int decision = TS_EXIT_NONE;
-    if (warp == 0) {
-      heavy_select<NSLOT, WT, PROD>(v, s, &ctl, ring, sqt, count, ws, rno, rW, decision);
-    } else if (warp != 4) {
-      const int si = heavy_sim_of_warp(warp);
-      double* s_raw = hsm + (size_t)si * 2 * 32 * WT;
-      heavy_simulate<NSLOT, WT, PROD>(v, s, &ctl, ring, s_raw, s_raw + 32 * WT, si);
-    }
-    __syncthreads();
-#ifdef TS_HEAVY_PROF
-    long long t_fin = clock64();
-#endif
-    if (warp == 0) heavy_finish(v, s, step, &ctl, ctl.issued, rno, rW, decision, ws);
-    __syncthreads();
-    if (ctl.zero_o) {  // the cancellation of an exit: O back to 0 on every node but the root
-      uint64_t* NO = v.no + (size_t)s * (size_t)v.cap;
-      const int nn = ctl.nnodes;
-      // 8 independent loads in flight per thread, then the stores
-      constexpr int U = 8;
-      for (int i0 = 1 + threadIdx.x; i0 < nn; i0 += U * HEAVY_THREADS) {
-        uint64_t w[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * HEAVY_THREADS;
-          w[u] = i < nn ? NO[i] : 0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * HEAVY_THREADS;
-          if (i < nn && (w[u] >> 32)) NO[i] = w[u] & 0xffffffffull;
-        }
-      }
-    }
-#ifdef TS_HEAVY_PROF
-    if (threadIdx.x == 0) atomicMax(&v.ctr->prof[15], (unsigned long long)(clock64() - t_fin));
-#endif
-    __syncthreads();
+    heavy_item<NSLOT, WT, PROD, false>(v, step, item, ctl[0], ring[0], sqt, hsm, ws);
   }
 #ifdef TS_SCHED_PROF
   if (threadIdx.x == 0) atomicMax(&v.ctr->prof[20], globaltimer());
 #endif
-  if (lane == 0 && warp == 0 && ws.launched) {
+  if (lane == 0 && ws.launched) {  // the selector warps' statistics
     atomicAdd(&v.ctr->rollouts, ws.rollouts);
     atomicAdd(&v.ctr->launched, ws.launched);
     atomicAdd(&v.ctr->nodes, ws.nodes);
@@ -6007,6 +6042,8 @@ int heavy_grid(ts_engine* e, int& blocks_out) {
         &per, (const void*)kHeavy[0][k / 4][std::min(k % 4, 2)], HEAVY_THREADS, heavy_smem_of(std::min(e->wkind, 2)));
     if (rc != cudaSuccess) return cuda_fail(e, rc, "occupancy");
     e->heavy_blocks = std::max(1, per) * e->sm_count;
+    const char* env = getenv("TS_HEAVY_BLOCKS");  // experiments: fewer resident pipelined-mode CTAs
+    if (env && atoi(env) > 0) e->heavy_blocks = std::min(e->heavy_blocks, atoi(env));
   }
   blocks_out = std::max(1, std::min(e->heavy_blocks, e->n_local));
   return TS_OK;
