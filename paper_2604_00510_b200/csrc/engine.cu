@@ -79,6 +79,7 @@ struct Counters {
   long long admit_lo, admit_hi;
   int work_count, work_next;
   int heavy_count, heavy_next;  // searches with >= HEAVY_P rollouts this wave (pipelined CTA mode)
+  int heavy_next2, _pad_h;      // k_heavy's claims beyond the first round
   int sum_fallbacks, sched_error;
   unsigned long long rollouts, launched, nodes, tokens, scored, levels, path_nodes, cancelled;
   unsigned long long prof[32];  // TS_HEAVY_PROF diagnostics (cycles), zero otherwise
@@ -889,7 +890,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     v.ctr->work_count = (int)tl2[1];
     v.ctr->work_next = 0;
     v.ctr->heavy_count = (int)tl2[0];
-    v.ctr->heavy_next = 0;
+    v.ctr->heavy_next = v.ctr->heavy_next2 = 0;
     v.ctr->cur_step = step;
   }
   SP_MARK(9, sp_t);
@@ -986,7 +987,7 @@ __device__ void px_finish(const View& v, cudaGraphConditionalHandle cond, int er
   c->work_count = 0;
   c->work_next = 0;
   c->heavy_count = 0;
-  c->heavy_next = 0;
+  c->heavy_next = c->heavy_next2 = 0;
   cudaGraphSetConditional(cond, 0);
 }
 
@@ -1516,7 +1517,7 @@ __global__ void __launch_bounds__(PXT) k_px_sched(View v, cudaGraphConditionalHa
     c->work_count = tl2[1];
     c->work_next = 0;
     c->heavy_count = tl2[0];
-    c->heavy_next = 0;
+    c->heavy_next = c->heavy_next2 = 0;
     c->cur_step = step;
     c->step = step + 1;
     px_stamp(v, step, 2);
@@ -2276,7 +2277,7 @@ __global__ void __launch_bounds__(PXS) k_px_step(View v, cudaGraphConditionalHan
     c->work_count = tl2[1];
     c->work_next = 0;
     c->heavy_count = tl2[0];
-    c->heavy_next = 0;
+    c->heavy_next = c->heavy_next2 = 0;
     c->cur_step = step;
     c->step = step + 1;
     px_stamp(v, step, 2);
@@ -2833,7 +2834,7 @@ __global__ void __launch_bounds__(TT) k_mt_split(View v, int step, const ts_sche
     v.ctr->work_count = (int)tt2[1];
     v.ctr->work_next = 0;
     v.ctr->heavy_count = (int)tt2[0];
-    v.ctr->heavy_next = 0;
+    v.ctr->heavy_next = v.ctr->heavy_next2 = 0;
     v.ctr->cur_step = step;
   }
 }
@@ -3279,7 +3280,7 @@ __global__ void __launch_bounds__(MT_T) k_mt_all(View v, int step, const ts_sche
         v.ctr->heavy_count = (int)(h + L.b1[b].nrun);
         v.ctr->work_count = (int)(l + L.b1[b].cnt0);
         v.ctr->work_next = 0;
-        v.ctr->heavy_next = 0;
+        v.ctr->heavy_next = v.ctr->heavy_next2 = 0;
         v.ctr->cur_step = step;
       }
     }
@@ -3332,7 +3333,7 @@ __global__ void __launch_bounds__(TT) k_set_targets(View v, int step, const int3
     v.ctr->work_count = (int)tt2[1];
     v.ctr->work_next = 0;
     v.ctr->heavy_count = (int)tt2[0];
-    v.ctr->heavy_next = 0;
+    v.ctr->heavy_next = v.ctr->heavy_next2 = 0;
     v.ctr->cur_step = step;
   }
 }
@@ -3416,7 +3417,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
       c->work_count = 0;
       c->work_next = 0;
       c->heavy_count = 0;
-      c->heavy_next = 0;
+      c->heavy_next = c->heavy_next2 = 0;
       c->free_run = 0;
       if (use_cond) cudaGraphSetConditional(cond, 0);
 #ifdef TS_SCHED_PROF
@@ -3552,7 +3553,7 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
       c->work_count = total;
       c->work_next = 0;
       c->heavy_count = 0;
-      c->heavy_next = 0;
+      c->heavy_next = c->heavy_next2 = 0;
       c->cur_step = step;
       // Free-running waves.  When every search is admitted, nobody can exit
       // before its budget (no positive/negative exit; the trees are too deep
@@ -4547,7 +4548,24 @@ __device__ __forceinline__ void heavy_select(const View& v, int s, HeavyCtl* ctl
         if ((bball & L1M) | (vb1 == 0u)) { status = (bball & L1M) ? TS_INVALID_ARGUMENT : TS_EXHAUSTED; break; }
         scored += __popc(vb1);
         ++levels;
+        // every group's level-2 argmax, issued with level 1's: a butterfly over
+        // the W lanes of each group (aligned), keys as in warp_argmax_nonneg,
+        // ties to the lower lane (the first child); read for group j1 below
+        int g2 = lane;
+        {
+          const uint64_t b = (uint64_t)__double_as_longlong(sc);
+          uint64_t key = valid ? ((b >> 63) ? ~b : (b | (1ull << 63))) : 0ull;
+#pragma unroll
+          for (int o = 1; o < WT; o <<= 1) {
+            const uint64_t pk = __shfl_xor_sync(FULL, key, o);
+            const int pl = __shfl_xor_sync(FULL, g2, o);
+            const bool tk = pk > key || (pk == key && pl < g2);
+            key = tk ? pk : key;
+            g2 = tk ? pl : g2;
+          }
+        }
         const int j1 = warp_argmax_nonneg(sc, valid && l1);
+        const int s2 = __shfl_sync(FULL, g2, WT + j1 * WT);
 #ifdef TS_HEAVY_PROF
         if (lane == 0) q_sc += clock64() - t_c;
         long long t_d = clock64();
@@ -4561,13 +4579,11 @@ __device__ __forceinline__ void heavy_select(const View& v, int s, HeavyCtl* ctl
         if (stale1) continue;  // the group is stale after a commit
         if (!(nmeta & M_KIDS)) break;
         // level 2, within the group of child j1
-        const bool ing = l2lane && gj == j1;
         const unsigned gm = L1M << (WT + j1 * WT);
         const unsigned vb2 = vball & gm;
         if ((bball & gm) | (vb2 == 0u)) { status = (bball & gm) ? TS_INVALID_ARGUMENT : TS_EXHAUSTED; break; }
         scored += __popc(vb2);
         ++levels;
-        const int s2 = warp_argmax_nonneg(sc, valid && ing);
         take(s2, (s2 - WT) % WT, nfc, xno, xmf, xr, xnq, xnsq);
 #ifdef TS_HEAVY_PROF
         if (lane == 0) q_l2t += clock64() - t_e + (nfc == -7 ? 1 : 0);
@@ -5353,11 +5369,14 @@ __device__ __forceinline__ void heavy_item(const View& v, int step, int item, He
 }
 
 // Work: items [0, n) of the wave's pipelined-mode list over G resident CTAs.
-// CTA b takes item b; when the wave has more items than CTAs (config 2's
-// third wave: 297 boosted searches for 296 CTAs), CTAs b < n - G also take
-// item G + b and run both side by side in the paired mode instead of one
-// after the other (the wave is as long as its longest CTA).  Items from 2G
-// on are claimed one at a time from a counter.
+// Each CTA claims c from a counter and takes item c (claim order: the first
+// CTAs to start, one per SM before a second on the same SM, as far as the
+// block scheduler spreads them); when the wave has more items than CTAs
+// (config 2's third wave: 297 boosted searches for 296 CTAs), claims c < n - G
+// also take item G + c and run both side by side in the paired mode instead
+// of one after the other (the wave is as long as its longest CTA).  Items
+// from 2G on are claimed one at a time from a second counter (a CTA that
+// starts late must still get its first-round claim).
 template <int NSLOT, int WT, bool PROD>
 #ifdef TS_HEAVY_MAXNREG
 __global__ void __maxnreg__(TS_HEAVY_MAXNREG) k_heavy(View v, int step) {
@@ -5374,7 +5393,10 @@ __global__ void __launch_bounds__(HEAVY_THREADS, TS_HEAVY_MINB) k_heavy(View v, 
   const int count_items = v.ctr->heavy_count;
   if (count_items == 0) return;  // most waves have no pipelined-mode search
   if (step < 0) step = v.ctr->cur_step;
-  const int G = gridDim.x, b = blockIdx.x;
+  const int G = gridDim.x;
+  if (threadIdx.x == 0) s_item = atomicAdd(&v.ctr->heavy_next, 1);
+  __syncthreads();
+  const int b = s_item;
   if (b >= count_items) return;  // no item for this CTA: skip the table set-up
 #ifdef TS_SCHED_PROF
   if (threadIdx.x == 0) atomicMin(&v.ctr->prof[21], globaltimer());
@@ -5390,7 +5412,7 @@ __global__ void __launch_bounds__(HEAVY_THREADS, TS_HEAVY_MINB) k_heavy(View v, 
   }
   for (;;) {  // items from 2G on, one at a time
     if (count_items <= 2 * G) break;
-    if (threadIdx.x == 0) s_item = 2 * G + atomicAdd(&v.ctr->heavy_next, 1);
+    if (threadIdx.x == 0) s_item = 2 * G + atomicAdd(&v.ctr->heavy_next2, 1);
     __syncthreads();
     const int item = s_item;
     __syncthreads();
