@@ -14,8 +14,11 @@ from paper_2604_00510_b200.engine import Engine  # noqa: E402
 table = problem_table(bench.workload(bench.PER_GPU))
 eng = Engine(bench.search_config(bench.PER_GPU), 0)
 tot = []
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH") else None
 for rep in range(12):
     eng.load(table)
+    if flush is not None:  # as bench.py: L2 flushed before every timed batch
+        bench.flush_l2(flush)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()

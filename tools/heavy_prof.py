@@ -15,8 +15,11 @@ from paper_2604_00510_b200.engine import Engine  # noqa: E402
 
 table = problem_table(bench.workload(bench.PER_GPU))
 eng = Engine(bench.search_config(bench.PER_GPU), 0)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if os.environ.get("FLUSH") else None
 for rep in range(2):
     eng.load(table)
+    if flush is not None:  # as bench.py: L2 flushed before every batch
+        bench.flush_l2(flush)
     st = eng.run()
 torch.cuda.synchronize()
 buf = (ctypes.c_uint64 * 32)()
