@@ -570,8 +570,10 @@ __device__ __forceinline__ void scan1_add(T (&x)[N], T (&tot)[N], T* sh) {
 // partition needs no barrier before the call.  Six barriers in all: the
 // counts/sum/min scan, the run-count scan, the run table, the want-prefix
 // scan, the run prefixes, the work-list scan.
+// cid: the records are a compacted run queue (running searches only, in
+// run-queue order) and record i's search is base + (flags >> 8)
 __device__ void targets_block(const View& v, int step, const ts_sched_record* rec, int n, int glo, int ghi,
-                              int base) {
+                              int base, bool cid = false) {
   extern __shared__ __align__(16) unsigned char smem[];
   long long* shA = (long long*)smem;                  // 96: scan scratch (even calls)
   long long* shB = shA + 96;                          // 96: scan scratch (odd calls)
@@ -818,7 +820,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
       const ts_sched_record r = rec[i];
       const bool local = i >= glo && i < ghi;
       if (!(r.flags & 1u)) {
-        if (local) v.tgt[base + i - glo] = 0;
+        if (local) v.tgt[cid ? base + (int)(r.flags >> 8) : base + i - glo] = 0;
         continue;
       }
       long long tgt = 1;
@@ -860,7 +862,7 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
         tgt = 1 + extra + rr_q + (spos < rr_r ? 1 : 0);
       }
       if (local) {
-        v.tgt[base + i - glo] = (int)tgt;
+        v.tgt[cid ? base + (int)(r.flags >> 8) : base + i - glo] = (int)tgt;
         // rollouts this wave = min(P_i, budget - completed); `_pad` carries completed
         if (v.heavy_on && min(tgt, (long long)(cf.rollout_budget - (int)r._pad)) >= HEAVY_P) {
           atomicOr(&hbits[(i - glo) >> 5], 1u << ((i - glo) & 31));
@@ -881,9 +883,11 @@ __device__ void targets_block(const View& v, int step, const ts_sched_record* re
     int ph = nl2[0], pl = nl2[1];
     const int loc_lo = max(lo, glo) - glo, loc_hi = max(loc_lo, min(hi, ghi) - glo);
     for (int i = loc_lo; i < loc_hi; ++i) {
-      if (!(rec[i + glo].flags & 1u)) continue;
-      if ((hbits[i >> 5] >> (i & 31)) & 1u) v.work_heavy[ph++] = base + i;
-      else v.work[pl++] = base + i;
+      const uint32_t fl = rec[i + glo].flags;
+      if (!(fl & 1u)) continue;
+      const int id = cid ? base + (int)(fl >> 8) : base + i;
+      if ((hbits[i >> 5] >> (i & 31)) & 1u) v.work_heavy[ph++] = id;
+      else v.work[pl++] = id;
     }
   }
   if (tid == 0) {
@@ -3579,7 +3583,48 @@ __global__ void __launch_bounds__(SCHED_T) k_sched(View v, ts_sched_record* rec,
     SP_MARK(9, sp_t);
   } else {
     if (threadIdx.x == 0) c->free_run = 0;
-    targets_block(v, step, srec, nw, 0, nw, wlo);
+    if (srec != rec) {
+      // the window's running searches compacted in place (shared memory, run-
+      // queue order kept, the window offset in flags bits 8+): compute_targets
+      // only sees running jobs, so the passes below touch the few still
+      // running (config 2's last waves: 297 and 39 of a 4096-search window)
+      // instead of the window.  srec is in shared memory only for nw <=
+      // SREC_MAX = 4 * SCHED_T, so a lane holds at most 4 records of its
+      // warp's chunk while every warp reads before any writes.
+      static_assert(SREC_MAX <= 4 * SCHED_T, "in-place compaction holds 4 records per lane");
+      __shared__ int s_ccnt[SCHED_W];
+      const int wid = threadIdx.x >> 5;
+      ts_sched_record rr[4];
+      unsigned bal[4];
+      int cnt = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = c0 + u * 32 + lane;
+        rr[u].flags = 0;
+        if (j < c1) rr[u] = srec[j];
+        bal[u] = __ballot_sync(FULL, j < c1 && (rr[u].flags & 1u));
+        cnt += __popc(bal[u]);
+        if (j < c1 && !(rr[u].flags & 1u)) v.tgt[wlo + j] = 0;
+      }
+      if (lane == 0) s_ccnt[wid] = cnt;
+      __syncthreads();
+      const int wt = lane < SCHED_W ? s_ccnt[lane] : 0;
+      int pos = __reduce_add_sync(FULL, lane < wid ? wt : 0);
+      const int nrun = __reduce_add_sync(FULL, wt);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if ((bal[u] >> lane) & 1u) {
+          ts_sched_record r = rr[u];
+          r.flags |= (uint32_t)(c0 + u * 32 + lane) << 8;
+          srec[pos + __popc(bal[u] & ((1u << lane) - 1u))] = r;
+        }
+        pos += __popc(bal[u]);
+      }
+      __syncthreads();
+      targets_block(v, step, srec, nrun, 0, nrun, wlo, true);
+    } else {
+      targets_block(v, step, srec, nw, 0, nw, wlo);
+    }
   }
   if (threadIdx.x == 0) {
     c->win_lo = s_min;  // no running search below this index
